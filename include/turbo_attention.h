@@ -1,0 +1,191 @@
+/*
+ * turbo_attention.h -- C-ABI of the B200 (sm_100a) TurboAttention hot path
+ * (arXiv 2412.08585: FlashQ block-progressive quantisation + SAS softmax).
+ *
+ * Citations: "P:n" = line n of the paper text with its section /
+ * algorithm; "R-n" = reading n in DESIGN.md §3 (where the paper is silent,
+ * ambiguous or garbled).
+ *
+ * Conventions for every entry point
+ *   * All tensor pointers are caller-owned DEVICE memory (e.g. torch tensors)
+ *     unless the argument says HOST.  The library never allocates or frees,
+ *     keeps no mutable global state, and never synchronises: work is enqueued
+ *     on `stream` (0 = legacy default stream) and completes asynchronously.
+ *   * Arguments are validated on the host before any launch.  Errors:
+ *       TURBO_ERR_INVALID_ARG  null pointer, non-positive size, bad enum value;
+ *       TURBO_ERR_UNSUPPORTED  head_dim not in {64,128}, block_kv != 64,
+ *                              block_q not in {64,128}, Hq % Hkv != 0,
+ *                              Hq/Hkv > 8 (decode), sas_nr not in [-30,-1];
+ *       TURBO_ERR_CAPACITY     an append/prefill would exceed cache->max_blocks;
+ *       TURBO_ERR_CUDA         a CUDA launch failed (cudaGetLastError).
+ *     On error nothing has been enqueued (except TURBO_ERR_CUDA, where earlier
+ *     kernels of the same call may have run).  No C++ exception crosses the ABI.
+ *   * Inputs must be contiguous in the documented layouts and 16-byte aligned.
+ *   * The product path has no CPU fallback: without an sm_100 device every
+ *     compute call returns TURBO_ERR_CUDA.
+ */
+#ifndef TURBO_ATTENTION_H
+#define TURBO_ATTENTION_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define TURBO_API __attribute__((visibility("default")))
+#else
+#define TURBO_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TURBO_OK = 0,
+  TURBO_ERR_INVALID_ARG = 1,
+  TURBO_ERR_UNSUPPORTED = 2,
+  TURBO_ERR_CAPACITY = 3,
+  TURBO_ERR_CUDA = 4
+} turbo_status_t;
+
+typedef void* turbo_stream_t; /* a cudaStream_t */
+
+/* Method parameters (paper defaults: B_r = B_c = n_b = 64, n_r = -6). */
+typedef struct {
+  int32_t head_dim;      /* d_H in {64, 128} (Eq. 1) */
+  int32_t block_q;       /* B_r in {64, 128}: Q stage-1 block rows and P-scale tile rows (Alg. 1) */
+  int32_t block_kv;      /* B_c = n_b = 64: K/V stage-1 block, Q2 group length, buffer size */
+  int32_t sas_nr;        /* n_r in [-30, -1]; SAS(x) = 0 for x - m < n_r */
+  int32_t alpha_mode;    /* 0: alpha = SAS(m_prev - m_new) literally (Alg. 1, R-15);
+                            1: alpha = 1 when the running max is unchanged */
+  float softmax_scale;   /* 1/sqrt(d_H) (Eq. 1; R-18) */
+  void* debug_tap;       /* NULL, or a turbo_debug_tap_t* (see below) */
+} turbo_params_t;
+
+/* Paged-free, caller-owned compressed KV cache for ONE layer (P:448-453,
+ * P:922-932).  slot = (b, kv_head, kind) with kind 0 = K, 1 = V.  All arrays
+ * are device memory sized by turbo_cache_sizes().
+ *
+ *   block_rec  uint8  [B][Hkv][2][max_blocks][rec_bytes]   one record per flushed
+ *              Q2 block: s_int u8[d] | z_int i8[d] | packed codes (see
+ *              DESIGN.md §6 "cache layout": K token-major, V channel-major with
+ *              a fixed token permutation; 2-bit records use the first half of
+ *              the code area).  rec_bytes = 2 d + B_c d / 2.
+ *   s_parent   f32    [B][Hkv][2][max_blocks]   first-stage scale of the block
+ *   buf        int8   [B][Hkv][2][B_c * d]      INT8 decode buffer (universal
+ *              scale): K token-major [t][c], V channel-major [c][t]
+ *   a_univ     f32    [B][Hkv][2]               universal max-abs (R-9)
+ *   counters   int32  [B][2]                    (n_blocks, n_buf) per sequence
+ *   bits       int32  [Hkv][2]  HOST and device copy: 2 or 4 per slot (head-wise
+ *              mixed precision P:430-436; R-8)
+ * n_tokens / max_blocks are HOST fields maintained by turbo_quantize_kv; all
+ * sequences of the batch have the same length. */
+typedef struct {
+  int32_t batch;
+  int32_t n_kv_heads;
+  int32_t head_dim;
+  int32_t block_kv;
+  int32_t max_blocks;
+  int64_t n_tokens;            /* HOST mirror of the cached length */
+  const int32_t* bits_host;    /* HOST [Hkv][2] */
+  const int32_t* bits_dev;     /* device [Hkv][2] */
+  uint8_t* block_rec;
+  float* s_parent;
+  int8_t* buf;
+  float* a_univ;
+  int32_t* counters;
+} turbo_kv_cache_t;
+
+/* Optional debug tap: records the exact-set intermediates of ONE tile so tests
+ * can compare them bit-for-bit with the oracle.  Prefill: query head `head`,
+ * 64-row Q block `i_block`, KV block `j_block`.  Decode: query head `head`,
+ * split 0, block `j_block` (-1 = buffer block).  All pointers device memory. */
+typedef struct {
+  int32_t batch, head, i_block, j_block;
+  int8_t* q1;        /* [64][d] prefill, [d] decode */
+  float* s_q;        /* [1] */
+  int32_t* s_int;    /* [64][64] prefill, [64] decode */
+  float* m_new;      /* [64] / [1] */
+  uint8_t* p_codes;  /* [64][64] / [64] */
+  float* s_p;        /* [1] */
+  int32_t* pv_int;   /* [64][d] / [d] */
+} turbo_debug_tap_t;
+
+/* Library version and the compiled target ("sm_100a"). */
+TURBO_API const char* turbo_version(void);
+
+/* Bytes of each cache array for the given geometry (HOST outputs, any may be NULL). */
+TURBO_API turbo_status_t turbo_cache_sizes(int32_t batch, int32_t n_kv_heads, int32_t head_dim, int32_t block_kv,
+                                 int32_t max_blocks, size_t* block_rec_bytes, size_t* s_parent_bytes,
+                                 size_t* buf_bytes, size_t* a_univ_bytes, size_t* counters_bytes);
+
+/* FlashQ quantisation of K and V into the cache (Alg. 1 P:907-932,
+ * Sec. 3.3).
+ *   mode 0 = PREFILL: k, v are FP16 [B][n_tokens][Hkv][d].  Resets the cache.
+ *     Every B_c block of each (b, kv_head) is quantised to symmetric INT8
+ *     (stage 1, s = max|x|/119, code = round_half_even(x * (119/max|x|)));
+ *     full blocks are progressively quantised (stage 2: channelwise asymmetric
+ *     INT4/INT2 at that slot's bits, integer only) into block records with the
+ *     stage-1 scale as parent scale; the n_tokens mod B_c tail is re-quantised
+ *     with the universal scale into the INT8 buffer.  The stage-1 operands of
+ *     turbo_attention_prefill are written to
+ *       k1_out   int8 [B][Hkv][n_tokens][d]
+ *       v1t_out  int8 [B][Hkv][T_c][d][B_c]   (each block transposed; tokens
+ *                past n_tokens are 0), T_c = ceil(n_tokens / B_c)
+ *       k1_scale_out, v1_scale_out  f32 [B][Hkv][T_c].
+ *   mode 1 = APPEND: k, v are FP16 [B][Hkv][d] (one new token per sequence,
+ *     n_tokens must be 1).  Quantised with the universal scale and clamped to
+ *     +-119 into the buffer; a full buffer (n_b = B_c tokens) is flushed to a
+ *     stage-2 block with parent scale a_univ/119.  The *_out pointers must be
+ *     NULL.  Updates cache->n_tokens (host) and the device counters. */
+TURBO_API turbo_status_t turbo_quantize_kv(const turbo_params_t* params, turbo_kv_cache_t* cache, const void* k,
+                                 const void* v, int32_t n_tokens, int32_t mode, int8_t* k1_out,
+                                 int8_t* v1t_out, float* k1_scale_out, float* v1_scale_out,
+                                 turbo_stream_t stream);
+
+/* Algorithm 1, TurboAttention prefill, tcgen05 INT8 MMA.
+ *   q       FP16 [B][N][Hq][d]; quantised per B_r x d block inside the kernel.
+ *   k1, v1t, k1_scale, v1_scale: the stage-1 operands from turbo_quantize_kv
+ *           (same B, N, Hkv, params).
+ *   causal  1 = key <= query (R-20), 0 = full.
+ *   o       FP16 [B][N][Hq][d] = O_i / l, round to nearest even.
+ *   lse     f32 [B][Hq][N] = m + ln l.
+ * Query head h reads kv head h / (Hq/Hkv) (GQA, R-22). */
+TURBO_API turbo_status_t turbo_attention_prefill(const turbo_params_t* params, int32_t B, int32_t N, int32_t Hq,
+                                       int32_t Hkv, int32_t causal, const void* q, const int8_t* k1,
+                                       const int8_t* v1t, const float* k1_scale, const float* v1_scale,
+                                       void* o, float* lse, turbo_stream_t stream);
+
+/* Workspace for turbo_attention_decode with n_splits splits (HOST result). */
+TURBO_API size_t turbo_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t head_dim, int32_t n_splits);
+
+/* Algorithm 2, TurboAttention decode of one new query per
+ * sequence against cache blocks [blk_begin, blk_end) (blk_end = -1: all
+ * flushed blocks) and, if with_buffer, the INT8 buffer block last.
+ * The block range is cut into n_splits contiguous sub-ranges of
+ * ceil(n / n_splits) blocks (the buffer joins the last one); each is one
+ * online-softmax pass (same order as Alg. 2) and the partial results are
+ * merged by the log-sum-exp combine (R-23).
+ *   q      FP16 [B][Hq][d]; quantised per (b, head) vector.
+ *   workspace  device, >= turbo_decode_workspace_bytes(B, Hq, d, n_splits).
+ *   o      FP16 [B][Hq][d] or NULL;  o_part f32 [B][Hq][d] (normalised) or
+ *          NULL -- at least one of them;  lse f32 [B][Hq] (required).
+ * Empty range with no buffer tokens: o = 0, lse = -inf. */
+TURBO_API turbo_status_t turbo_attention_decode(const turbo_params_t* params, const turbo_kv_cache_t* cache,
+                                      int32_t Hq, const void* q, int32_t blk_begin, int32_t blk_end,
+                                      int32_t with_buffer, int32_t n_splits, void* workspace,
+                                      size_t workspace_bytes, void* o, float* o_part, float* lse,
+                                      turbo_stream_t stream);
+
+/* Log-sum-exp combine of n_parts partial results, in ascending part order
+ * (R-23): L = max_s L_s + ln sum_s e^{L_s - max}, O = sum_s e^{L_s - L} O_s.
+ *   o_parts f32 [n_parts][rows][d], lse_parts f32 [n_parts][rows];
+ *   o FP16 [rows][d] (or NULL), o_f32 f32 [rows][d] (or NULL), lse f32 [rows]. */
+TURBO_API turbo_status_t turbo_combine_lse(int32_t n_parts, int32_t rows, int32_t d, const float* o_parts,
+                                 const float* lse_parts, void* o, float* o_f32, float* lse,
+                                 turbo_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TURBO_ATTENTION_H */

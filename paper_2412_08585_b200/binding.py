@@ -1,0 +1,229 @@
+"""Thin ctypes binding of libturboattn.so (include/turbo_attention.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA
+kernels behind the C-ABI.  PyTorch provides device memory and the stream.
+There is no CPU fallback -- if the library is missing or the GPU is not an
+sm_100 part, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+
+import torch
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libturboattn.so")
+
+TURBO_OK, TURBO_ERR_INVALID_ARG, TURBO_ERR_UNSUPPORTED, TURBO_ERR_CAPACITY, TURBO_ERR_CUDA = range(5)
+_ERR = {1: "TURBO_ERR_INVALID_ARG", 2: "TURBO_ERR_UNSUPPORTED", 3: "TURBO_ERR_CAPACITY", 4: "TURBO_ERR_CUDA"}
+
+EXPORTS = ("turbo_version", "turbo_cache_sizes", "turbo_quantize_kv", "turbo_attention_prefill",
+           "turbo_decode_workspace_bytes", "turbo_attention_decode", "turbo_combine_lse")
+
+
+class TurboError(RuntimeError):
+    def __init__(self, fn, code):
+        super().__init__(f"{fn} -> {_ERR.get(code, code)}")
+        self.code = code
+
+
+class TurboParams(C.Structure):
+    _fields_ = [("head_dim", C.c_int32), ("block_q", C.c_int32), ("block_kv", C.c_int32), ("sas_nr", C.c_int32),
+                ("alpha_mode", C.c_int32), ("softmax_scale", C.c_float), ("debug_tap", C.c_void_p)]
+
+
+class TurboKVCache(C.Structure):
+    _fields_ = [("batch", C.c_int32), ("n_kv_heads", C.c_int32), ("head_dim", C.c_int32), ("block_kv", C.c_int32),
+                ("max_blocks", C.c_int32), ("n_tokens", C.c_int64), ("bits_host", C.c_void_p),
+                ("bits_dev", C.c_void_p), ("block_rec", C.c_void_p), ("s_parent", C.c_void_p), ("buf", C.c_void_p),
+                ("a_univ", C.c_void_p), ("counters", C.c_void_p)]
+
+
+class TurboDebugTap(C.Structure):
+    _fields_ = [("batch", C.c_int32), ("head", C.c_int32), ("i_block", C.c_int32), ("j_block", C.c_int32),
+                ("q1", C.c_void_p), ("s_q", C.c_void_p), ("s_int", C.c_void_p), ("m_new", C.c_void_p),
+                ("p_codes", C.c_void_p), ("s_p", C.c_void_p), ("pv_int", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libturboattn.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2412_08585_b200.build`")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, sz = C.c_void_p, C.c_int32, C.c_size_t
+        L.turbo_version.restype = C.c_char_p
+        L.turbo_cache_sizes.argtypes = [i32, i32, i32, i32, i32] + [C.POINTER(sz)] * 5
+        L.turbo_quantize_kv.argtypes = [C.POINTER(TurboParams), C.POINTER(TurboKVCache), vp, vp, i32, i32, vp, vp,
+                                        vp, vp, vp]
+        L.turbo_attention_prefill.argtypes = [C.POINTER(TurboParams), i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp,
+                                              vp, vp]
+        L.turbo_decode_workspace_bytes.argtypes = [i32, i32, i32, i32]
+        L.turbo_decode_workspace_bytes.restype = sz
+        L.turbo_attention_decode.argtypes = [C.POINTER(TurboParams), C.POINTER(TurboKVCache), i32, vp, i32, i32, i32,
+                                             i32, vp, sz, vp, vp, vp, vp]
+        L.turbo_combine_lse.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp, vp]
+        for name in ("turbo_cache_sizes", "turbo_quantize_kv", "turbo_attention_prefill", "turbo_attention_decode",
+                     "turbo_combine_lse"):
+            getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(fn, code):
+    if code != TURBO_OK:
+        raise TurboError(fn, code)
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def params(head_dim=128, block_q=64, block_kv=64, sas_nr=-6, alpha_mode=0, softmax_scale=None, debug_tap=None):
+    """turbo_params_t with the paper's defaults."""
+    if softmax_scale is None:
+        softmax_scale = 1.0 / math.sqrt(head_dim)
+    p = TurboParams(head_dim, block_q, block_kv, sas_nr, alpha_mode, softmax_scale, None)
+    if debug_tap is not None:
+        p._tap = debug_tap  # keep alive
+        p.debug_tap = C.cast(C.pointer(debug_tap.c), C.c_void_p)
+    return p
+
+
+class KVCache:
+    """Caller-owned device memory for one layer's compressed cache (torch tensors)."""
+
+    def __init__(self, batch, n_kv_heads, head_dim, max_blocks, bits, block_kv=64, device="cuda"):
+        sizes = [C.c_size_t() for _ in range(5)]
+        _check("turbo_cache_sizes", lib().turbo_cache_sizes(batch, n_kv_heads, head_dim, block_kv, max_blocks,
+                                                            *[C.byref(s) for s in sizes]))
+        nrec, npar, nbuf, nau, ncnt = (s.value for s in sizes)
+        self.bits = torch.as_tensor(bits, dtype=torch.int32).reshape(n_kv_heads, 2).contiguous()
+        self.bits_dev = self.bits.to(device)
+        self.block_rec = torch.zeros(max(nrec, 16), dtype=torch.uint8, device=device)
+        self.s_parent = torch.zeros(max(npar // 4, 1), dtype=torch.float32, device=device)
+        self.buf = torch.zeros(nbuf, dtype=torch.int8, device=device)
+        self.a_univ = torch.zeros(nau // 4, dtype=torch.float32, device=device)
+        self.counters = torch.zeros(ncnt // 4, dtype=torch.int32, device=device)
+        self.c = TurboKVCache(batch, n_kv_heads, head_dim, block_kv, max_blocks, 0, self.bits.data_ptr(),
+                              self.bits_dev.data_ptr(), self.block_rec.data_ptr(), self.s_parent.data_ptr(),
+                              self.buf.data_ptr(), self.a_univ.data_ptr(), self.counters.data_ptr())
+        self.batch, self.n_kv_heads, self.head_dim, self.max_blocks, self.block_kv = (
+            batch, n_kv_heads, head_dim, max_blocks, block_kv)
+
+    @property
+    def n_tokens(self):
+        return self.c.n_tokens
+
+    def rec_bytes(self):
+        return 2 * self.head_dim + self.block_kv * self.head_dim // 2
+
+    def records(self):
+        """block_rec viewed as [B][Hkv][2][max_blocks][rec_bytes]."""
+        return self.block_rec[: self.batch * self.n_kv_heads * 2 * self.max_blocks * self.rec_bytes()].view(
+            self.batch, self.n_kv_heads, 2, self.max_blocks, self.rec_bytes())
+
+    def nbytes(self):
+        return sum(t.numel() * t.element_size() for t in (self.block_rec, self.s_parent, self.buf, self.a_univ,
+                                                          self.counters))
+
+
+def turbo_quantize_kv(p, cache: KVCache, k, v, mode=0, stream=None):
+    """mode 0 (PREFILL): k, v fp16 [B,N,Hkv,d] -> returns (k1, v1t, k1_scale, v1_scale);
+    mode 1 (APPEND): k, v fp16 [B,Hkv,d] -> returns None."""
+    assert k.dtype == torch.float16 and v.dtype == torch.float16 and k.is_contiguous() and v.is_contiguous()
+    if mode == 0:
+        B, N, H, d = k.shape
+        tc = -(-N // p.block_kv)
+        dev = k.device
+        k1 = torch.empty((B, H, N, d), dtype=torch.int8, device=dev)
+        v1t = torch.empty((B, H, tc, d, p.block_kv), dtype=torch.int8, device=dev)
+        k1s = torch.empty((B, H, tc), dtype=torch.float32, device=dev)
+        v1s = torch.empty((B, H, tc), dtype=torch.float32, device=dev)
+        _check("turbo_quantize_kv", lib().turbo_quantize_kv(C.byref(p), C.byref(cache.c), _ptr(k), _ptr(v), N, 0,
+                                                            _ptr(k1), _ptr(v1t), _ptr(k1s), _ptr(v1s),
+                                                            _stream(stream)))
+        return k1, v1t, k1s, v1s
+    _check("turbo_quantize_kv", lib().turbo_quantize_kv(C.byref(p), C.byref(cache.c), _ptr(k), _ptr(v), 1, 1, None,
+                                                        None, None, None, _stream(stream)))
+    return None
+
+
+def turbo_attention_prefill(p, q, k1, v1t, k1_scale, v1_scale, causal=True, o=None, lse=None, stream=None):
+    """q fp16 [B,N,Hq,d] -> (o fp16 [B,N,Hq,d], lse f32 [B,Hq,N])."""
+    assert q.dtype == torch.float16 and q.is_contiguous()
+    B, N, Hq, d = q.shape
+    Hkv = k1.shape[1]
+    if o is None:
+        o = torch.empty_like(q)
+    if lse is None:
+        lse = torch.empty((B, Hq, N), dtype=torch.float32, device=q.device)
+    _check("turbo_attention_prefill", lib().turbo_attention_prefill(
+        C.byref(p), B, N, Hq, Hkv, int(causal), _ptr(q), _ptr(k1), _ptr(v1t), _ptr(k1_scale), _ptr(v1_scale),
+        _ptr(o), _ptr(lse), _stream(stream)))
+    return o, lse
+
+
+def turbo_decode_workspace_bytes(B, Hq, head_dim, n_splits):
+    return lib().turbo_decode_workspace_bytes(B, Hq, head_dim, n_splits)
+
+
+def turbo_attention_decode(p, cache: KVCache, q, blk_begin=0, blk_end=-1, with_buffer=True, n_splits=1,
+                           workspace=None, o=None, o_part=None, lse=None, want_fp16=True, want_f32=False,
+                           stream=None):
+    """q fp16 [B,Hq,d] -> (o fp16 [B,Hq,d] or None, o_part f32 [B,Hq,d] or None, lse f32 [B,Hq])."""
+    assert q.dtype == torch.float16 and q.is_contiguous()
+    B, Hq, d = q.shape
+    dev = q.device
+    if want_fp16 and o is None:
+        o = torch.empty((B, Hq, d), dtype=torch.float16, device=dev)
+    if want_f32 and o_part is None:
+        o_part = torch.empty((B, Hq, d), dtype=torch.float32, device=dev)
+    if lse is None:
+        lse = torch.empty((B, Hq), dtype=torch.float32, device=dev)
+    wsb = turbo_decode_workspace_bytes(B, Hq, d, n_splits)
+    if wsb and workspace is None:
+        workspace = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    _check("turbo_attention_decode", lib().turbo_attention_decode(
+        C.byref(p), C.byref(cache.c), Hq, _ptr(q), blk_begin, blk_end, int(with_buffer), n_splits, _ptr(workspace),
+        wsb, _ptr(o), _ptr(o_part), _ptr(lse), _stream(stream)))
+    return o, o_part, lse
+
+
+def turbo_combine_lse(o_parts, lse_parts, o=None, o_f32=None, want_fp16=True, stream=None):
+    """o_parts f32 [S, rows, d], lse_parts f32 [S, rows] -> (o fp16 | None, o_f32 | None, lse [rows])."""
+    S, rows, d = o_parts.shape
+    if want_fp16 and o is None:
+        o = torch.empty((rows, d), dtype=torch.float16, device=o_parts.device)
+    lse = torch.empty((rows,), dtype=torch.float32, device=o_parts.device)
+    _check("turbo_combine_lse", lib().turbo_combine_lse(S, rows, d, _ptr(o_parts), _ptr(lse_parts), _ptr(o),
+                                                        _ptr(o_f32), _ptr(lse), _stream(stream)))
+    return o, o_f32, lse
+
+
+class DebugTap:
+    """Device buffers of a turbo_debug_tap_t (exact-set intermediates of one tile)."""
+
+    def __init__(self, batch, head, i_block, j_block, head_dim, decode=False, device="cuda"):
+        rows = 1 if decode else 64
+        z = lambda *s, dt: torch.zeros(s, dtype=dt, device=device)  # noqa: E731
+        self.q1 = z(rows, head_dim, dt=torch.int8)
+        self.s_q = z(1, dt=torch.float32)
+        self.s_int = z(rows, 64, dt=torch.int32)
+        self.m_new = z(rows, dt=torch.float32)
+        self.p_codes = z(rows, 64, dt=torch.uint8)
+        self.s_p = z(1, dt=torch.float32)
+        self.pv_int = z(rows, head_dim, dt=torch.int32)
+        self.c = TurboDebugTap(batch, head, i_block, j_block, *[t.data_ptr() for t in (
+            self.q1, self.s_q, self.s_int, self.m_new, self.p_codes, self.s_p, self.pv_int)])

@@ -1,0 +1,92 @@
+"""C-ABI library checks that need no GPU (-m "not gpu"): the shared library
+loads, exports every symbol include/turbo_attention.h declares, and its
+host-side validation rejects bad arguments before touching the device."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2412_08585_b200 import binding, build
+
+    build.build()
+    return binding.lib()
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "turbo_attention.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:TURBO_API\s+)?(?:const char\*|turbo_status_t|size_t)\s+(turbo_\w+)\(", src, re.M)))
+
+
+def test_header_declares_the_boundary():
+    syms = header_symbols()
+    for s in ("turbo_quantize_kv", "turbo_attention_prefill", "turbo_attention_decode", "turbo_combine_lse",
+              "turbo_decode_workspace_bytes", "turbo_cache_sizes", "turbo_version"):
+        assert s in syms
+
+
+def test_library_exports_every_header_symbol(L):
+    from paper_2412_08585_b200 import binding
+
+    for s in header_symbols():
+        assert hasattr(L, s), s
+    assert set(header_symbols()) == set(binding.EXPORTS)
+    assert b"sm_100a" in L.turbo_version()
+
+
+def test_cache_sizes(L):
+    from paper_2412_08585_b200 import binding
+
+    out = [C.c_size_t() for _ in range(5)]
+    assert L.turbo_cache_sizes(64, 10, 128, 64, 513, *[C.byref(o) for o in out]) == 0
+    rec, par, buf, au, cnt = (o.value for o in out)
+    assert rec == 64 * 10 * 2 * 513 * (2 * 128 + 64 * 128 // 2)
+    assert par == 64 * 10 * 2 * 513 * 4 and buf == 64 * 10 * 2 * 64 * 128 and au == 64 * 10 * 2 * 4
+    assert cnt == 64 * 2 * 4
+    assert L.turbo_cache_sizes(1, 1, 96, 64, 1, *[C.byref(o) for o in out]) == binding.TURBO_ERR_UNSUPPORTED
+    assert L.turbo_cache_sizes(0, 1, 64, 64, 1, *[C.byref(o) for o in out]) == binding.TURBO_ERR_INVALID_ARG
+
+
+def test_host_validation_without_gpu(L):
+    from paper_2412_08585_b200 import binding as b
+
+    p = b.params(head_dim=128)
+    # null / bad arguments are rejected before any CUDA call
+    assert L.turbo_attention_prefill(C.byref(p), 1, 64, 3, 2, 1, *[None] * 7, None) == b.TURBO_ERR_UNSUPPORTED
+    assert L.turbo_attention_prefill(C.byref(p), 1, 64, 2, 2, 1, *[None] * 7, None) == b.TURBO_ERR_INVALID_ARG
+    assert L.turbo_attention_prefill(None, 1, 64, 2, 2, 1, *[None] * 7, None) == b.TURBO_ERR_INVALID_ARG
+    bad = b.params(head_dim=128, block_kv=128)
+    assert L.turbo_attention_prefill(C.byref(bad), 1, 64, 2, 2, 1, *[None] * 7, None) == b.TURBO_ERR_UNSUPPORTED
+    bad = b.params(head_dim=128, sas_nr=0)
+    assert L.turbo_attention_prefill(C.byref(bad), 1, 64, 2, 2, 1, *[None] * 7, None) == b.TURBO_ERR_UNSUPPORTED
+    assert L.turbo_combine_lse(0, 1, 1, None, None, None, None, None, None) == b.TURBO_ERR_INVALID_ARG
+    assert L.turbo_decode_workspace_bytes(2, 8, 128, 1) == 0
+    assert L.turbo_decode_workspace_bytes(2, 8, 128, 4) == 4 * 2 * 8 * 129 * 4
+    # quantize_kv / decode with a malformed cache struct
+    cache = b.TurboKVCache()
+    assert L.turbo_quantize_kv(C.byref(p), C.byref(cache), None, None, 1, 0, None, None, None, None,
+                               None) == b.TURBO_ERR_INVALID_ARG
+    assert L.turbo_attention_decode(C.byref(p), C.byref(cache), 8, None, 0, -1, 1, 1, None, 0, None, None, None,
+                                    None) == b.TURBO_ERR_INVALID_ARG
+
+
+def test_sass_uses_tcgen05_and_tma():
+    """The prefill kernel's SASS contains tcgen05 MMA (UTC*MMA), TMEM loads
+    (LDTM) and TMA loads (UTMALDG); the decode kernel uses bulk copies."""
+    import shutil
+    import subprocess
+
+    from paper_2412_08585_b200 import build
+
+    lib = build.build()
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    sass = subprocess.run([tool, "-sass", lib], capture_output=True, text=True).stdout
+    assert re.search(r"UTC\w*MMA", sass)
+    assert "LDTM" in sass
+    assert "UTMALDG" in sass
+    assert "UBLKCP" in sass

@@ -1,0 +1,272 @@
+"""GPU parity: the CUDA path through the C-ABI vs the CPU oracle (-m gpu).
+
+Bar (BASELINE.json north_star): bit-exact codes, scales and INT32 S; the other
+exact-set values (m, P codes, s_P, PV_int) bit-exact too; FP16
+outputs within max-abs 2e-3 and rel-L2 1e-3 of the oracle's FP32 output.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2412_08585_b200 import synth
+from tests import cache_layout
+
+pytestmark = pytest.mark.gpu
+
+MAX_ABS, REL_L2 = 2e-3, 1e-3
+
+
+@pytest.fixture(scope="module")
+def ta():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2412_08585_b200 import binding
+
+    binding.lib()
+    return binding
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def assert_out_close(gpu_fp16, ref_f32, what=""):
+    g = gpu_fp16.astype(np.float32)
+    err = np.abs(g - ref_f32).max()
+    rl = rel_l2(g, ref_f32)
+    assert err <= MAX_ABS and rl <= REL_L2, f"{what}: max-abs {err:.3e} rel-L2 {rl:.3e}"
+
+
+CASES = [  # (B, N, Hq, Hkv, d, causal, block_q, alpha_mode)
+    (1, 128, 1, 1, 64, True, 64, 0),      # config 1 (BASELINE.json configs[0])
+    (2, 200, 8, 2, 128, True, 64, 0),     # GQA, ragged tail, several tiles
+    (1, 333, 4, 4, 128, False, 64, 1),    # non-causal, ragged, alpha mode 1
+    (1, 256, 2, 1, 64, True, 128, 0),     # B_r = 128
+]
+
+
+def _oracle_params(d, block_q, alpha_mode):
+    return O.params(d=d, block_q=block_q, block_kv=64, alpha_mode=alpha_mode)
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_quantize_kv_prefill_bit_exact(ta, case):
+    B, N, Hq, Hkv, d, causal, bq, am = case
+    q, k, v = synth.qkv(500 + N, B, N, Hq, Hkv, d)
+    bits = synth.head_bits_alternating(Hkv)
+    p = ta.params(head_dim=d, block_q=bq, alpha_mode=am)
+    cache = ta.KVCache(B, Hkv, d, max_blocks=8, bits=bits)
+    k1, v1t, k1s, v1s = ta.turbo_quantize_kv(p, cache, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    torch.cuda.synchronize()
+    ref = O.build_cache(_oracle_params(d, bq, am), k.astype(np.float32), v.astype(np.float32), bits, 8)
+    np.testing.assert_array_equal(k1.cpu().numpy(), ref["k1"])
+    np.testing.assert_array_equal(k1s.cpu().numpy(), ref["k1s"])
+    np.testing.assert_array_equal(v1s.cpu().numpy(), ref["v1s"])
+    tc = -(-N // 64)
+    v1 = v1t.cpu().numpy().transpose(0, 1, 2, 4, 3).reshape(B, Hkv, tc * 64, d)
+    np.testing.assert_array_equal(v1[:, :, :N], ref["v1"])
+    assert not v1[:, :, N:].any()
+    recs = cache.records().cpu().numpy()
+    spar = cache.s_parent[: B * Hkv * 2 * 8].view(B, Hkv, 2, 8).cpu().numpy()
+    buf = cache.buf.view(B, Hkv, 2, 64 * d).cpu().numpy()
+    a_univ = cache.a_univ.view(B, Hkv, 2).cpu().numpy()
+    cnt = cache.counters.view(B, 2).cpu().numpy()
+    for b in range(B):
+        for h in range(Hkv):
+            for kind, sl in enumerate(ref["slots"][b][h]):
+                assert cnt[b, 0] == sl.n_blocks and cnt[b, 1] == sl.n_buf
+                assert a_univ[b, h, kind] == sl.a_univ
+                for j in range(sl.n_blocks):
+                    codes, s_int, z_int = cache_layout.unpack_record(recs[b, h, kind, j], d, int(bits[h][kind]), kind)
+                    np.testing.assert_array_equal(codes, sl.codes[j])
+                    np.testing.assert_array_equal(s_int, sl.s_int[j])
+                    np.testing.assert_array_equal(z_int, sl.z_int[j])
+                    assert spar[b, h, kind, j] == sl.s_parent[j]
+                bb = buf[b, h, kind].reshape(64, d) if kind == 0 else buf[b, h, kind].reshape(d, 64).T
+                np.testing.assert_array_equal(bb[: sl.n_buf], sl.buf[: sl.n_buf])
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_prefill_parity(ta, case):
+    B, N, Hq, Hkv, d, causal, bq, am = case
+    q, k, v = synth.qkv(700 + N, B, N, Hq, Hkv, d)
+    bits = synth.head_bits_alternating(Hkv)
+    p = ta.params(head_dim=d, block_q=bq, alpha_mode=am)
+    cache = ta.KVCache(B, Hkv, d, max_blocks=8, bits=bits)
+    qt, kt, vt = (torch.from_numpy(x).cuda() for x in (q, k, v))
+    k1, v1t, k1s, v1s = ta.turbo_quantize_kv(p, cache, kt, vt)
+    o, lse = ta.turbo_attention_prefill(p, qt, k1, v1t, k1s, v1s, causal=causal)
+    torch.cuda.synchronize()
+    o, lse = o.cpu().numpy(), lse.cpu().numpy()
+    op = _oracle_params(d, bq, am)
+    G = Hq // Hkv
+    for b in range(B):
+        for h in range(Hq):
+            oref, lref = O.prefill_head(op, q[b, :, h], k[b, :, h // G], v[b, :, h // G], causal=causal)
+            assert_out_close(o[b, :, h], oref, f"b{b} h{h}")
+            np.testing.assert_allclose(lse[b, h], lref, atol=1e-4, rtol=1e-5)
+
+
+@pytest.mark.parametrize("case", CASES[:3])
+def test_prefill_exact_set_tap(ta, case):
+    """Bit-exact q1, s_Q, S_int, m_new, P codes, s_P and PV_int of chosen tiles."""
+    B, N, Hq, Hkv, d, causal, bq, am = case
+    q, k, v = synth.qkv(900 + N, B, N, Hq, Hkv, d)
+    bits = synth.head_bits_alternating(Hkv)
+    qt, kt, vt = (torch.from_numpy(x).cuda() for x in (q, k, v))
+    G = Hq // Hkv
+    op = _oracle_params(d, bq, am)
+    T = -(-N // 64)
+    for (b, h, i, j) in sorted({(B - 1, Hq - 1, T - 1, T - 1), (0, 0, 1, 0), (0, Hq // 2, T - 1, 0)}):
+        tap = ta.DebugTap(b, h, i, j, d)
+        p = ta.params(head_dim=d, block_q=bq, alpha_mode=am, debug_tap=tap)
+        cache = ta.KVCache(B, Hkv, d, max_blocks=8, bits=bits)
+        k1, v1t, k1s, v1s = ta.turbo_quantize_kv(p, cache, kt, vt)
+        ta.turbo_attention_prefill(p, qt, k1, v1t, k1s, v1s, causal=causal)
+        torch.cuda.synchronize()
+        _, _, rt = O.prefill_head(op, q[b, :, h], k[b, :, h // G], v[b, :, h // G], causal=causal, tap=(i, j))
+        assert rt["hit"]
+        rows = min(64, N - 64 * i)
+        np.testing.assert_array_equal(tap.q1.cpu().numpy()[:rows], rt["q1"][:rows])
+        assert tap.s_q.item() == rt["s_q"][0]
+        np.testing.assert_array_equal(tap.s_int.cpu().numpy()[:rows], rt["s_int"][:rows])
+        np.testing.assert_array_equal(tap.m_new.cpu().numpy()[:rows], rt["m_new"][:rows])
+        np.testing.assert_array_equal(tap.p_codes.cpu().numpy()[:rows], rt["p_codes"][:rows])
+        assert tap.s_p.item() == rt["s_p"][0]
+        np.testing.assert_array_equal(tap.pv_int.cpu().numpy()[:rows], rt["pv_int"][:rows])
+
+
+DEC_CASES = [  # (B, N_prefill, n_append, Hq, Hkv, d, n_splits, alpha_mode)
+    (1, 128, 64, 1, 1, 64, 1, 0),       # config 1 + 64 appends (one flush)
+    (2, 700, 70, 8, 2, 128, 1, 0),      # GQA, mixed 2/4 bit, buffer + flush
+    (2, 700, 5, 8, 2, 128, 3, 1),       # in-GPU split-KV + combine
+    (1, 64 * 9, 0, 4, 1, 128, 4, 0),    # G = 4, empty buffer
+]
+
+
+def _oracle_decode(op, q, slots, G, splits_bounds):
+    """Per q head: oracle decode over explicit split ranges + combine."""
+    Hq = q.shape[0]
+    outs, lses = np.zeros((Hq, op.d), np.float32), np.zeros(Hq, np.float32)
+    for h in range(Hq):
+        ks, vs = slots[h // G]
+        parts, ls = [], []
+        for s, (a, e) in enumerate(splits_bounds):
+            o, l = O.decode_head(op, q[h], ks, vs, a, e, s == len(splits_bounds) - 1)
+            parts.append(o)
+            ls.append(l)
+        if len(parts) == 1:
+            outs[h], lses[h] = parts[0], ls[0]
+        else:
+            outs[h], lses[h] = O.combine(np.stack(parts), np.array(ls))
+    return outs, lses
+
+
+@pytest.mark.parametrize("case", DEC_CASES)
+def test_append_and_decode_parity(ta, case):
+    B, N, n_app, Hq, Hkv, d, S, am = case
+    G = Hq // Hkv
+    q, k, v = synth.qkv(1300 + N, B, N, Hq, Hkv, d)
+    bits = synth.head_bits_alternating(Hkv)
+    maxb = (N + n_app) // 64 + 1
+    p = ta.params(head_dim=d, alpha_mode=am)
+    cache = ta.KVCache(B, Hkv, d, max_blocks=maxb, bits=bits)
+    ta.turbo_quantize_kv(p, cache, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    op = O.params(d=d, alpha_mode=am)
+    ref = O.build_cache(op, k.astype(np.float32), v.astype(np.float32), bits, maxb)
+    for t in range(n_app):
+        _, kt, vt = synth.decode_token(5000 + t, B, Hq, Hkv, d)
+        ta.turbo_quantize_kv(p, cache, torch.from_numpy(kt).cuda(), torch.from_numpy(vt).cuda(), mode=1)
+        for b in range(B):
+            for h in range(Hkv):
+                ref["slots"][b][h][0].append(kt[b, h].astype(np.float32))
+                ref["slots"][b][h][1].append(vt[b, h].astype(np.float32))
+    qd, _, _ = synth.decode_token(9000, B, Hq, Hkv, d)
+    o, _, lse = ta.turbo_attention_decode(p, cache, torch.from_numpy(qd).cuda(), n_splits=S)
+    torch.cuda.synchronize()
+    o, lse = o.cpu().numpy(), lse.cpu().numpy()
+    nb = ref["slots"][0][0][0].n_blocks
+    per = -(-nb // S)
+    bounds = [(min(s * per, nb), min(s * per + per, nb)) for s in range(S)]
+    # cache state after the appends is bit-exact
+    recs = cache.records().cpu().numpy()
+    cnt = cache.counters.view(B, 2).cpu().numpy()
+    for b in range(B):
+        for h in range(Hkv):
+            for kind, sl in enumerate(ref["slots"][b][h]):
+                assert tuple(cnt[b]) == (sl.n_blocks, sl.n_buf)
+                for j in range(sl.n_blocks):
+                    codes, s_int, z_int = cache_layout.unpack_record(recs[b, h, kind, j], d, int(bits[h][kind]), kind)
+                    np.testing.assert_array_equal(codes, sl.codes[j])
+                    np.testing.assert_array_equal(s_int, sl.s_int[j])
+                    np.testing.assert_array_equal(z_int, sl.z_int[j])
+        ro, rl = _oracle_decode(op, qd[b].astype(np.float32), ref["slots"][b], G, bounds)
+        assert_out_close(o[b], ro, f"decode b{b}")
+        np.testing.assert_allclose(lse[b], rl, atol=1e-4, rtol=1e-5)
+
+
+@pytest.mark.parametrize("j_block", [0, 3, -1])
+def test_decode_exact_set_tap(ta, j_block):
+    B, N, Hq, Hkv, d = 2, 64 * 5 + 37, 8, 2, 128
+    q, k, v = synth.qkv(77, B, N, Hq, Hkv, d)
+    bits = synth.head_bits_alternating(Hkv)
+    b, h = 1, 5
+    tap = ta.DebugTap(b, h, 0, j_block, d, decode=True)
+    p = ta.params(head_dim=d, debug_tap=tap)
+    cache = ta.KVCache(B, Hkv, d, max_blocks=8, bits=bits)
+    ta.turbo_quantize_kv(p, cache, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    qd, _, _ = synth.decode_token(31, B, Hq, Hkv, d)
+    ta.turbo_attention_decode(p, cache, torch.from_numpy(qd).cuda(), n_splits=1)
+    torch.cuda.synchronize()
+    op = O.params(d=d)
+    ref = O.build_cache(op, k.astype(np.float32), v.astype(np.float32), bits, 8)
+    ks, vs = ref["slots"][b][h // (Hq // Hkv)]
+    _, _, rt = O.decode_head(op, qd[b, h].astype(np.float32), ks, vs, tap=j_block)
+    assert rt["hit"]
+    np.testing.assert_array_equal(tap.q1.cpu().numpy()[0], rt["q1"])
+    assert tap.s_q.item() == rt["s_q"][0]
+    np.testing.assert_array_equal(tap.s_int.cpu().numpy()[0], rt["s_int"])
+    assert tap.m_new.item() == rt["m_new"][0]
+    np.testing.assert_array_equal(tap.p_codes.cpu().numpy()[0], rt["p_codes"])
+    assert tap.s_p.item() == rt["s_p"][0]
+    np.testing.assert_array_equal(tap.pv_int.cpu().numpy()[0], rt["pv_int"])
+
+
+def test_combine_lse_parity(ta):
+    rng = np.random.default_rng(0)
+    S, rows, d = 5, 37, 128
+    o_parts = rng.standard_normal((S, rows, d)).astype(np.float32)
+    lse_parts = (rng.standard_normal((S, rows)) * 3).astype(np.float32)
+    lse_parts[2, :5] = -np.inf
+    lse_parts[:, 7] = -np.inf
+    o16, _, lse = ta.turbo_combine_lse(torch.from_numpy(o_parts).cuda(), torch.from_numpy(lse_parts).cuda())
+    torch.cuda.synchronize()
+    for r in range(rows):
+        ro, rl = O.combine(o_parts[:, r], lse_parts[:, r])
+        np.testing.assert_allclose(o16[r].float().cpu().numpy(), ro, atol=2e-3, rtol=1e-3)
+        if np.isfinite(rl):
+            assert abs(lse[r].item() - rl) < 1e-5
+        else:
+            assert lse[r].item() == -np.inf
+
+
+def test_validation_errors(ta):
+    p = ta.params(head_dim=96)
+    cache_ok = ta.KVCache(1, 1, 64, 4, [[4, 4]])
+    with pytest.raises(ta.TurboError) as e:
+        ta.turbo_attention_prefill(p, torch.zeros(1, 64, 1, 96, dtype=torch.float16, device="cuda"),
+                                   torch.zeros(1, 1, 64, 96, dtype=torch.int8, device="cuda"),
+                                   torch.zeros(1, 1, 1, 96, 64, dtype=torch.int8, device="cuda"),
+                                   torch.zeros(1, 1, 1, device="cuda"), torch.zeros(1, 1, 1, device="cuda"))
+    assert e.value.code == ta.TURBO_ERR_UNSUPPORTED
+    p = ta.params(head_dim=64)
+    with pytest.raises(ta.TurboError) as e:  # decode on an empty cache
+        ta.turbo_attention_decode(p, cache_ok, torch.zeros(1, 1, 64, dtype=torch.float16, device="cuda"))
+    assert e.value.code == ta.TURBO_ERR_INVALID_ARG
+    with pytest.raises(ta.TurboError) as e:  # capacity
+        kk = torch.zeros(1, 64 * 5, 1, 64, dtype=torch.float16, device="cuda")
+        ta.turbo_quantize_kv(p, cache_ok, kk, kk)
+    assert e.value.code == ta.TURBO_ERR_CAPACITY
