@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""TurboAttention (arXiv 2412.08585) hot-path benchmark on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one pass of the whole hot path over one batch of the config
+BASELINE.json's metric is quoted on (configs[1]: Llama-3-8B attention shape,
+32 query / 8 KV heads, d = 128, prefill N = 4096, batch 8, causal):
+  turbo_quantize_kv(PREFILL)  stage-1 INT8 K/V + stage-2 INT4/INT2 cache   (a1, a2)
+  turbo_attention_prefill     tcgen05 INT8 QK^T / PV with SAS softmax     (a1 Q, a4-a8)
+  turbo_quantize_kv(APPEND)   one decode token into the INT8 buffer       (a3)
+  turbo_attention_decode      split-KV decode over the fresh cache + LSE  (a9, a10)
+`value` = prefill attention ops (4 d per unmasked (query, key) pair, 2 ops
+per MAC x 2 contractions) / step time, whole job over all ranks.  A second
+object `decode` measures configs[2] (Phi-3-medium shape, 40/10 heads, batch
+64 at 32k context, mixed INT4/INT2 cache): KV GB/s and tokens/s.
+
+Multi-GPU (torchrun): every rank runs its own batch (weak scaling, no data-path
+collective: the prefill is partitioned by (batch, KV head)).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASE_METRIC = "attention TOPS (prefill) and KV GB/s + tokens/s (decode) at 1/2/4/8 B200 vs roofline"
+CFG_PREFILL = dict(B=8, N=4096, Hq=32, Hkv=8, d=128)
+CFG_DECODE = dict(B=64, N=32768, Hq=40, Hkv=10, d=128)
+
+
+def prefill_ops(B, N, Hq, d, causal=True):
+    pairs = N * (N + 1) // 2 if causal else N * N
+    return 4.0 * d * pairs * B * Hq
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        m = json.load(open(path))
+        return dict(hbm=m["hbm_gbs"], bf16=m["bf16_tflops"], bf16_sus=m.get("bf16_tflops_sustained"),
+                    src="measured (MEASURED_PEAKS.json)")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback (B200_PROFILING.md)")
+
+
+class Clocks:
+    """nvidia-smi sampler over the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[3:7]))
+            except ValueError:
+                pass
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, x in enumerate(r) if x.lower() == "active"})
+        load = [s for s, _, _ in rows if s > 300] or [s for s, _, _ in rows]
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": max(m for _, m, _ in rows), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# --------------------------------------------------------------------------- ours
+def run_ours(args, rank, world, device):
+    import torch
+
+    from paper_2412_08585_b200 import binding as ta
+    from paper_2412_08585_b200 import synth
+
+    torch.cuda.set_device(device)
+    c = CFG_PREFILL
+    B, N, Hq, Hkv, d = c["B"], c["N"], c["Hq"], c["Hkv"], c["d"]
+    bits = synth.head_bits_alternating(Hkv)
+    p = ta.params(head_dim=d, block_q=64, alpha_mode=0)
+    q, k, v = synth.qkv_torch(1002 + 7919 * rank, B, N, Hq, Hkv, d, device=device)
+    qd, kd, vd = (x[:, 0].contiguous() for x in synth.qkv_torch(4002 + rank, B, 1, Hq, Hkv, d, device=device))
+    cache = ta.KVCache(B, Hkv, d, max_blocks=N // 64 + 2, bits=bits, device=device)
+    S = args.splits
+    ws = torch.empty(max(ta.turbo_decode_workspace_bytes(B, Hq, d, S), 16), dtype=torch.uint8, device=device)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=device)  # > 126 MB L2
+    st = torch.cuda.current_stream()
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step(qq, kk, vv, qdd, kdd, vdd, evs=None):
+        if evs:
+            evs[0].record(st)
+        k1, v1t, k1s, v1s = ta.turbo_quantize_kv(p, cache, kk, vv)
+        if evs:
+            evs[1].record(st)
+        o, lse = ta.turbo_attention_prefill(p, qq, k1, v1t, k1s, v1s, causal=True)
+        if evs:
+            evs[2].record(st)
+        ta.turbo_quantize_kv(p, cache, kdd, vdd, mode=1)
+        od, _, lsed = ta.turbo_attention_decode(p, cache, qdd, n_splits=S, workspace=ws)
+        if evs:
+            evs[3].record(st)
+        return o, lse, od, lsed
+
+    launches_per_step = 2 + 1 + 2 + (2 if S > 1 else 1)
+    for _ in range(args.warmup):
+        step(q, k, v, qd, kd, vd)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(device) if rank == 0 else None
+    evs = [[ev() for _ in range(4)] for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()  # L2 flush between timed steps (outside the events)
+        step(q, k, v, qd, kd, vd, evs[i])
+    torch.cuda.synchronize()
+    clocks = clk.stop() if clk else None
+    t_quant = [e[0].elapsed_time(e[1]) for e in evs]
+    t_prefill = [e[1].elapsed_time(e[2]) for e in evs]
+    t_dec = [e[2].elapsed_time(e[3]) for e in evs]
+    t_step = [e[0].elapsed_time(e[3]) for e in evs]
+    total_ms = sum(t_step)
+    if world > 1:
+        t = torch.tensor([total_ms], device=device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = t.item()
+    ms_step = total_ms / args.steps
+    ops = prefill_ops(B, N, Hq, d)
+    value = world * ops * args.steps / (total_ms * 1e-3) / 1e12
+
+    # ---- end to end through the public API: pinned host inputs -> device -> host result
+    hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
+    hqd, hkd, hvd = (x.cpu().pin_memory() for x in (qd, kd, vd))
+    ho = torch.empty(q.shape, dtype=torch.float16).pin_memory()
+    hlse = torch.empty((B, Hq, N), dtype=torch.float32).pin_memory()
+    hod = torch.empty(qd.shape, dtype=torch.float16).pin_memory()
+    dq, dk, dv, dqd, dkd, dvd = (torch.empty_like(x) for x in (q, k, v, qd, kd, vd))
+    e2e_steps = max(2, min(args.steps, 5))
+    e0, e1 = ev(), ev()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(e2e_steps):
+        for dst, src in ((dq, hq), (dk, hk), (dv, hv), (dqd, hqd), (dkd, hkd), (dvd, hvd)):
+            dst.copy_(src, non_blocking=True)
+        o, lse, od, _ = step(dq, dk, dv, dqd, dkd, dvd)
+        ho.copy_(o, non_blocking=True)
+        hlse.copy_(lse, non_blocking=True)
+        hod.copy_(od, non_blocking=True)
+    e1.record(st)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = t.item()
+    h2d = sum(x.numel() * x.element_size() for x in (hq, hk, hv, hqd, hkd, hvd))
+    d2h = sum(x.numel() * x.element_size() for x in (ho, hlse, hod))
+    e2e = {"value": world * ops * e2e_steps / (e2e_ms * 1e-3) / 1e12, "unit": "TOPS", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / e2e_steps}
+
+    pk = peaks()
+    int8_peak = 2.0 * pk["bf16"]  # dense int8 = 2 x dense bf16 (nominal 4.5 vs 2.25 PF), burst
+    pre_ms = statistics.mean(t_prefill)
+    achieved = ops / (pre_ms * 1e-3) / 1e12
+    roof = {"bound": "tensor", "kernel": "prefill_kernel<128> (turbo_attention_prefill)", "achieved": round(achieved, 1),
+            "peak": round(int8_peak, 1), "unit": "TFLOP/s", "frac": round(achieved / int8_peak, 4),
+            "traffic": None, "peak_source": f"2 x bf16 burst {pk['bf16']} TF/s, {pk['src']}",
+            "share_of_step": round(pre_ms / statistics.mean(t_step), 3)}
+    result = dict(value=value, ms_step=ms_step, e2e=e2e, roofline=roof, clocks=clocks,
+                  launches=launches_per_step * args.steps,
+                  breakdown_ms={"quantize_kv_prefill": round(statistics.mean(t_quant), 4),
+                                "attention_prefill": round(pre_ms, 4),
+                                "append+decode": round(statistics.mean(t_dec), 4)})
+    del hq, hk, hv, ho, hlse, dq, dk, dv, q, k, v, flush, cache
+    torch.cuda.empty_cache()
+    if not args.no_decode:
+        result["decode"] = bench_decode(args, rank, world, device, pk)
+    return result
+
+
+def decode_bytes(B, Hkv, d, nblk, nbuf, bits, Hq):
+    """Algorithmic HBM bytes of one decode step: block records (s_int, z_int,
+    packed codes), parent scales, buffer rows, q in, o/lse out."""
+    per_bh = 0
+    for h in range(Hkv):
+        for kind in range(2):
+            per_bh += nblk * (2 * d + 64 * d * int(bits[h][kind]) // 8 + 4) + nbuf * d + 4
+    return B * per_bh + B * Hq * d * 2 * 2 + B * Hq * 4
+
+
+def bench_decode(args, rank, world, device, pk):
+    import torch
+
+    from paper_2412_08585_b200 import binding as ta
+    from paper_2412_08585_b200 import synth
+
+    c = CFG_DECODE
+    B, N, Hq, Hkv, d = c["B"], c["N"], c["Hq"], c["Hkv"], c["d"]
+    bits = synth.head_bits_alternating(Hkv)
+    p = ta.params(head_dim=d, alpha_mode=0)
+    cache = ta.KVCache(B, Hkv, d, max_blocks=N // 64 + 4, bits=bits, device=device)
+    _, k, v = synth.qkv_torch(3003 + rank, B, N, Hkv, Hkv, d, device=device)
+    ta.turbo_quantize_kv(p, cache, k, v)  # builds the 32k-token compressed cache
+    del k, v
+    torch.cuda.empty_cache()
+    S = args.decode_splits
+    ws = torch.empty(max(ta.turbo_decode_workspace_bytes(B, Hq, d, S), 16), dtype=torch.uint8, device=device)
+    toks = [tuple(x[:, 0].contiguous() for x in synth.qkv_torch(6000 + i, B, 1, Hq, Hkv, d, device=device))
+            for i in range(args.warmup + args.steps)]
+    st = torch.cuda.current_stream()
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    for i in range(args.warmup):
+        qd, kd, vd = toks[i]
+        ta.turbo_quantize_kv(p, cache, kd, vd, mode=1)
+        ta.turbo_attention_decode(p, cache, qd, n_splits=S, workspace=ws)
+    torch.cuda.synchronize()
+    evs = [[ev() for _ in range(3)] for _ in range(args.steps)]
+    for i in range(args.steps):
+        qd, kd, vd = toks[args.warmup + i]
+        evs[i][0].record(st)
+        ta.turbo_quantize_kv(p, cache, kd, vd, mode=1)
+        evs[i][1].record(st)
+        ta.turbo_attention_decode(p, cache, qd, n_splits=S, workspace=ws)
+        evs[i][2].record(st)
+    torch.cuda.synchronize()
+    t_dec = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+    t_step = statistics.mean(e[0].elapsed_time(e[2]) for e in evs)
+    ntok = cache.n_tokens
+    nblk, nbuf = ntok // 64, ntok % 64
+    byt = decode_bytes(B, Hkv, d, nblk, nbuf, bits, Hq)
+    gbs = byt / (t_dec * 1e-3) / 1e9
+    return {"config": "Phi-3-medium attention (40 Q / 10 KV heads, d=128), batch 64, 32k context, mixed INT4/INT2",
+            "n_splits": S, "kv_bytes_per_step": byt, "decode_kernel_ms": round(t_dec, 4),
+            "step_ms_append_plus_decode": round(t_step, 4), "kv_gbs": round(gbs, 1),
+            "tokens_per_s": round(world * B / (t_step * 1e-3), 1),
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": pk["hbm"], "unit": "GB/s",
+                         "frac": round(gbs / pk["hbm"], 4), "peak_source": pk["src"]}}
+
+
+# --------------------------------------------------------------------------- reference (oracle)
+def cpu_sample_oracle(seconds_hint=True):
+    """The CPU oracle (oracle/, plain scalar C) on a bounded sample of the same
+    workload: K/V quantisation + cache build and Alg. 1 for ONE (batch, query
+    head) of configs[1] (N = 4096, d = 128, causal), single thread."""
+    import numpy as np
+
+    from oracle import oracle as O
+    from paper_2412_08585_b200 import synth
+
+    N, d = CFG_PREFILL["N"], CFG_PREFILL["d"]
+    q, k, v = synth.qkv(1002, 1, N, 1, 1, d)
+    q, k, v = (x[0, :, 0].astype(np.float32) for x in (q, k, v))
+    p = O.params(d=d)
+    t0 = time.perf_counter()
+    ks, vs = O.Slot(p, 4, N // 64 + 1), O.Slot(p, 2, N // 64 + 1)
+    ks.prefill(k)
+    vs.prefill(v)
+    O.prefill_head(p, q, k, v, causal=True)
+    dt = time.perf_counter() - t0
+    ops = prefill_ops(1, N, 1, d)
+    return {"value": ops / dt / 1e12, "unit": "TOPS", "cores": 1, "kind": "oracle",
+            "sample": f"1 of {CFG_PREFILL['B'] * CFG_PREFILL['Hq']} (batch, head) units of configs[1]: quantize + "
+                      f"cache build + Alg. 1, N={N}, d={d}, causal; {dt:.2f} s single-threaded",
+            "seconds": round(dt, 3)}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        pass  # the oracle has no warm-up state; one sample per step below
+    vals, secs = [], []
+    for _ in range(args.steps):
+        s = cpu_sample_oracle()
+        vals.append(s["value"])
+        secs.append(s["seconds"])
+    v = statistics.mean(vals)
+    s["value"] = v
+    line = {"metric": BASE_METRIC, "value": v, "unit": "TOPS", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(secs), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+            "impl": "reference", "config": workload_config(args),
+            "cpu_baseline": s, "e2e": {"value": v, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args):
+    c = CFG_PREFILL
+    return {"workload": "configs[1]: Llama-3-8B attention shape (32 Q / 8 KV heads GQA, d=128), prefill seq 4096, "
+                        "batch 8, causal, INT8 tcgen05; step = quantize_kv + prefill + append + split-KV decode",
+            "global_batch": c["B"] * args.gpus, "seq_len": c["N"], "n_q_heads": c["Hq"], "n_kv_heads": c["Hkv"],
+            "head_dim": c["d"], "block_q": 64, "block_kv": 64, "sas_nr": -6, "alpha_mode": 0,
+            "kv_bits": "half of the (kv_head, K/V) slots 2-bit, rest 4-bit", "decode_splits": args.splits,
+            "parallelism": f"(batch, kv-head) partition, {args.gpus} rank(s), no collective",
+            "l2": "flushed between timed steps (512 MB write)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--splits", type=int, default=4, help="split-KV count of the decode in the step")
+    ap.add_argument("--decode-splits", type=int, default=8)
+    ap.add_argument("--no-decode", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+
+    if world > 1:
+        torch.cuda.set_device(local)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2412_08585_b200 import build
+
+    build.build()
+    res = run_ours(args, rank, world, local)
+    cpu = cpu_sample_oracle() if rank == 0 and world == 1 else None
+    if rank == 0:
+        line = {"metric": BASE_METRIC, "value": round(res["value"], 2), "unit": "TOPS", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["ms_step"], 4),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
+                "data": "synthetic (seeded N(0,1) Q/K/V with outlier channels, DESIGN.md §4)",
+                "config": workload_config(args), "roofline": res["roofline"], "cpu_baseline": cpu,
+                "e2e": res["e2e"], "gpu_launches": res["launches"], "clocks": res["clocks"],
+                "breakdown_ms": res["breakdown_ms"], "decode": res.get("decode")}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
