@@ -21,11 +21,10 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
 cudaError_t launch_combine(int n_parts, int rows, int d, const float* o_parts, const float* lse_parts, __half* o,
                            float* o32, float* lse, cudaStream_t st);
 
-// LUT[i] = e^{-i} correctly rounded to binary32, 0 past |n_r|
-// (the Appendix B sentinel).
+// SAS threshold |n_r|; the LUT itself is ta::kExpNegBits.
 void fill_sas_const(ta::SasConst* sc, int32_t nr) {
-  for (int i = 0; i < 32; ++i) sc->lut[i] = i <= -nr ? (float)std::exp(-(double)i) : 0.0f;
   sc->nr_abs = (float)(-nr);
+  sc->nr_int = -nr;
 }
 }  // namespace ta_host
 

@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
   const size_t slotK = ((size_t)b * a.Hkv + kvh) * 2, slotV = slotK + 1;
   constexpr int REC = rec_bytes(HD);
   const uint32_t bytesK = 2 * HD + kBc * HD * bitsK / 8, bytesV = 2 * HD + kBc * HD * bitsV / 8;
-  const float lut_lane = a.sas.lut[lane];
+  const float lut_lane = sas_lut_lane(a.sas, lane);
   const int tap_row = a.has_tap && split == 0 && a.tap.batch == b && a.tap.head / G == kvh ? a.tap.head % G : -1;
 
   if (lane == 0) {
