@@ -251,7 +251,8 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
     const int kmax = row_ok ? (args.causal ? row : N - 1) : -1;  // last visible key of this row
 
     for (int j = 0; j <= nkv; ++j) {
-      float cpv = 0.f;
+      float cpv = 0.f, alpha_j = 0.f, sp_j = 0.f;
+      bool active_j = false;
       const bool tap_j = tap_row && args.tap.j_block == j;
       if (j < nkv) {
         const int sb = j & 1;
@@ -354,20 +355,9 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
         }
         fence_proxy_async();
         mbar_arrive(&sm.p_full[slot][sb]);
-        // Scaled-O bookkeeping: O_true = A * Ohat.  The alpha of tile j must
-        // hit the O of tile j-1 before tile j's PV lands, so rescale Ohat when
-        // A would underflow (or alpha == 0 resets the history).
-        if (active) {
-          const float An = A * alpha;
-          if (!(An >= 1e-30f)) {  // alpha == 0 or tiny product: fold A into Ohat
-#pragma unroll
-            for (int c = 0; c < HD; ++c) O[c] *= An;
-            A = 1.f;
-          } else {
-            A = An;
-          }
-          cpv = __fdiv_rn(__fmul_rn(s_p, args.v1s[bkv * Tc + j]), A);
-        }
+        alpha_j = alpha;
+        sp_j = s_p;
+        active_j = active;
       }
       // O += (s_P s_V / A) Q(P~) V^q1 for the previous tile
       if (j >= 1) {
@@ -386,6 +376,20 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
         }
         tc_fence_before();
         if (j < nkv) mbar_arrive(&sm.pv_free[slot]);
+      }
+      // Scaled-O bookkeeping, after PV(j-1) has landed in Ohat: O_true = A * Ohat,
+      // tile j's alpha multiplies everything accumulated so far; fold A
+      // into Ohat when it would underflow (alpha == 0 restarts the history).
+      if (j < nkv && active_j) {
+        const float An = A * alpha_j;
+        if (!(An >= 1e-30f)) {
+#pragma unroll
+          for (int c = 0; c < HD; ++c) O[c] *= An;
+          A = 1.f;
+        } else {
+          A = An;
+        }
+        cpv = __fdiv_rn(__fmul_rn(sp_j, args.v1s[bkv * Tc + j]), A);
       }
       cpv_p = cpv;
       tap_p = tap_j;
