@@ -46,7 +46,6 @@ struct DecodeArgs {
   int B, Hq, Hkv, G, max_blocks, blk_begin, blk_end, with_buffer, n_splits, alpha_mode;
   float scale;
   SasConst sas;
-  int has_tap;
   turbo_debug_tap_t tap;
 };
 
@@ -54,138 +53,119 @@ TA_DEV uint32_t byte_of(const uint4& v, int i) {
   const uint32_t w = i < 4 ? v.x : i < 8 ? v.y : i < 12 ? v.z : v.w;
   return (w >> (8 * (i & 3))) & 0xFFu;
 }
-TA_DEV int sbyte_of(const uint4& v, int i) { return (int)(int8_t)(uint8_t)byte_of(v, i); }
 
-TA_DEV int shfl_max_g(int v) {
-#pragma unroll
-  for (int o = 4; o < 32; o <<= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+// Shared-memory accessors on 32-bit shared addresses.
+TA_DEV uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
-TA_DEV float shfl_maxf_g(float v) {
+TA_DEV uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+TA_DEV uint32_t lds_u8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+TA_DEV int lds_s8(uint32_t a) {
+  int v;
+  asm volatile("ld.shared.s8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+TA_DEV void sts_u8(uint32_t a, uint32_t v) { asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
+
+// Reductions over the lanes that hold the same two query rows: general path
+// (rows 2q, 2q+1): lanes with equal q; packed path (rows 2(q&1), +1): equal q&1.
+template <bool PACK>
+TA_DEV float grp_maxf(float v) {
+  if (PACK) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 2));
 #pragma unroll
   for (int o = 4; o < 32; o <<= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
-TA_DEV float shfl_sumf_g(float v) {
+template <bool PACK>
+TA_DEV float grp_sumf(float v) {
+  if (PACK) v += __shfl_xor_sync(0xffffffffu, v, 2);
 #pragma unroll
   for (int o = 4; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-TA_DEV int shfl_sum_g(int v) {
+template <bool PACK>
+TA_DEV int grp_maxi(int v) {
+  if (PACK) v = max(v, __shfl_xor_sync(0xffffffffu, v, 2));
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+template <bool PACK>
+TA_DEV int grp_sumi(int v) {
+  if (PACK) v += __shfl_xor_sync(0xffffffffu, v, 2);
 #pragma unroll
   for (int o = 4; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 
-// Channel of the low k-slot m (0..3) of k-step j for lane quad q (layout.cuh):
-// the high slot is the next channel.
+// Channel of the low k-slot m (0..3) of k-step j inside a lane quad's channel
+// region of K codes (layout.cuh); the high slot is the next channel.
 template <int HD, int BITS>
-TA_DEV constexpr int k_chan(int q, int j, int m) {
-  return BITS == 4 ? q * (HD / 4) + 8 * j + 2 * m : q * (HD / 4) + 16 * (j >> 1) + 4 * m + 2 * (j & 1);
+TA_DEV constexpr int k_chan(int j, int m) {
+  return BITS == 4 ? 8 * j + 2 * m : 16 * (j >> 1) + 4 * m + 2 * (j & 1);
 }
 
-// Per-warp online-softmax state of the thread's two rows (2q, 2q+1) and its
-// O slice (channels 16 mt + g and 16 mt + g + 8, mt < HD/16).
-template <int HD>
-struct RowState {
-  float m[2], l[2];
-  float o[HD / 16][4];
+// Thread <-> data maps.  Lane = 4 g + q.
+//   General path (G <= 8): rows 2q+e; score values t = 2 mt + h at token
+//   16 mt + g + 8 h (NT = 8); O values c = 2 mt + h at channel 16 mt + g + 8 h.
+//   Packed path (G <= 4): the 4 spare MMA columns carry the lo half of the
+//   Eq. 5 fold, rows 2(q&1)+e; t = mt at token 16 mt + g + 8 (q>>1) (NT = 4);
+//   O values c = mt at channel 16 mt + g + 8 (q>>1).
+template <int HD, bool PACK>
+struct Map {
+  static constexpr int NT = PACK ? 4 : 8;
+  static constexpr int NC = PACK ? HD / 16 : HD / 8;
+  TA_DEV static int row(int q, int e) { return PACK ? 2 * (q & 1) + e : 2 * q + e; }
+  TA_DEV static int tok(int t, int g, int q) { return PACK ? 16 * t + g + 8 * (q >> 1) : 16 * (t >> 1) + g + 8 * (t & 1); }
+  TA_DEV static int chan(int c, int g, int q) { return PACK ? 16 * c + g + 8 * (q >> 1) : 16 * (c >> 1) + g + 8 * (c & 1); }
 };
 
-// One tile (64 keys) of Alg. 2 given S_int in C-fragment order.
-// s[mt][i]: token 16mt + g (+8 for i >= 2), row 2q + (i & 1).
-template <int HD>
-TA_DEV void softmax_tile(const DecodeArgs& a, RowState<HD>& st, int (&s)[4][4], int nvalid, const float (&cqk)[2],
-                         uint8_t (*pbuf)[kBc], float lut_lane, float (&alpha)[2], float (&s_p)[2], int (&sum_p)[2],
-                         bool tap, int tap_row, int g, int q) {
+// QK^T on a stage-2 block (Alg. 2, folded): S_int per thread value.
+template <int HD, int BK, bool PACK>
+TA_DEV void qk_block(uint32_t rec, const int (&qv)[HD / 4], const uint4 (&q1r)[HD / 64], int (&sv)[Map<HD, PACK>::NT][2],
+                     int g, int q) {
+  constexpr int R = HD / 4, KS = HD / 32;
+  uint4 s4[HD / 64];
 #pragma unroll
-  for (int e = 0; e < 2; ++e) {
-    int smax = INT_MIN;
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
-      if (16 * mt + g < nvalid) smax = max(smax, s[mt][e]);
-      if (16 * mt + g + 8 < nvalid) smax = max(smax, s[mt][2 + e]);
-    }
-    smax = shfl_max_g(smax);
-    const float m_prev = st.m[e];
-    const float m_new = fmaxf(m_prev, __fmul_rn((float)smax, cqk[e]));
-    // alpha = SAS(m_prev - m_new) (R-15); evaluated by every lane (shuffle LUT)
-    const float al_s = sas_eval(__fsub_rn(m_new, m_prev), lut_lane, a.sas.nr_abs);
-    const float al = m_prev == -INFINITY ? 0.f : (a.alpha_mode == 1 && m_new == m_prev) ? 1.f : al_s;
-    float pt[8], rs = 0.f, pm = 0.f;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int mt = i >> 1, hi = i & 1, tok = 16 * mt + g + 8 * hi;
-      const float x = __fmul_rn((float)s[mt][2 * hi + e], cqk[e]);
-      float p = sas_eval(__fsub_rn(m_new, x), lut_lane, a.sas.nr_abs);
-      p = tok < nvalid ? p : 0.f;
-      pt[i] = p;
-      rs += p;
-      pm = fmaxf(pm, p);
-    }
-    rs = shfl_sumf_g(rs);
-    pm = shfl_maxf_g(pm);
-    st.l[e] = al * st.l[e] + rs;
-    st.m[e] = m_new;
-    alpha[e] = al;
-    // per-row P scale (Alg. 2 P:976-977, R-17)
-    const float inv_p = pm > 0.f ? __fdiv_rn(kDiv, pm) : 0.f;
-    s_p[e] = __fdiv_rn(pm, kDiv);
-    int sp = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int mt = i >> 1, hi = i & 1, tok = 16 * mt + g + 8 * hi;
-      const int c = rint_prod(pt[i], inv_p);
-      sp += c;
-      pbuf[2 * q + e][tok] = (uint8_t)c;
-      if (tap && 2 * q + e == tap_row) a.tap.p_codes[tok] = (uint8_t)c;
-    }
-    sum_p[e] = shfl_sum_g(sp);
-    if (tap && 2 * q + e == tap_row && g == 0) {
-      a.tap.m_new[0] = m_new;
-      a.tap.s_p[0] = s_p[e];
-    }
-  }
-  __syncwarp();
-}
-
-template <int HD>
-TA_DEV void pv_update(RowState<HD>& st, const int (&acc)[HD / 16][4], const float (&alpha)[2], const float (&cpv)[2]) {
-#pragma unroll
-  for (int mt = 0; mt < HD / 16; ++mt)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) st.o[mt][i] = __fmaf_rn(alpha[i & 1], st.o[mt][i], cpv[i & 1] * (float)acc[mt][i]);
-}
-
-template <int HD, int BK>
-TA_DEV void qk_q2(const uint8_t* rec, const uint4 (&q1r)[HD / 64], int (&s)[4][4], int g, int q) {
-  // B fragments: hi/lo split of q1_c * s_c over the lane's channel region.
-  const int R = HD / 4;
-  uint4 sv[HD / 64];
-#pragma unroll
-  for (int i = 0; i < HD / 64; ++i) sv[i] = *reinterpret_cast<const uint4*>(rec + q * R + 16 * i);
-  constexpr int KS = HD / 32;
+  for (int i = 0; i < HD / 64; ++i) s4[i] = lds128(rec + q * R + 16 * i);
+  // B fragments from q1_c * s_c = 128 hi + lo.  Packed: column g < 4 holds hi of
+  // row g, column g >= 4 holds lo of row g - 4 (one MMA); general: two MMAs.
   uint32_t bhi[KS][2], blo[KS][2];
 #pragma unroll
   for (int j = 0; j < KS; ++j)
 #pragma unroll
     for (int h2 = 0; h2 < 2; ++h2) {
-      uint32_t vh = 0, vl = 0;
+      uint32_t ph[4], pl[4];
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
-        const int loc = k_chan<HD, BK>(0, j, m) + h2;  // channel offset inside the region
-        const int prod = sbyte_of(q1r[loc >> 4], loc & 15) * (int)byte_of(sv[loc >> 4], loc & 15);
-        vh |= (uint32_t)((prod >> 7) & 0xFF) << (8 * m);
-        vl |= (uint32_t)(prod & 0x7F) << (8 * m);
+        const int loc = k_chan<HD, BK>(j, m) + h2;
+        const int prod = qv[loc] * (int)byte_of(s4[loc >> 4], loc & 15);
+        ph[m] = (uint32_t)(prod >> 7);
+        pl[m] = (uint32_t)prod;
       }
-      bhi[j][h2] = vh;
-      blo[j][h2] = vl;
+      if (PACK) {
+        const bool lo = g >= 4;
+        bhi[j][h2] = lo ? (pack4_lo(pl[0], pl[1], pl[2], pl[3]) & 0x7F7F7F7Fu) : pack4_lo(ph[0], ph[1], ph[2], ph[3]);
+      } else {
+        bhi[j][h2] = pack4_lo(ph[0], ph[1], ph[2], ph[3]);
+        blo[j][h2] = pack4_lo(pl[0], pl[1], pl[2], pl[3]) & 0x7F7F7F7Fu;
+      }
     }
-  // z term: sum_c q1_c z_c (quad reduction), broadcast to the C-fragment rows.
+  // z term sum_c q1_c z_c of the lane-quad's row (dp4a, quad reduction).
   int zq = 0;
 #pragma unroll
   for (int i = 0; i < HD / 64; ++i) {
-    const uint4 zv = *reinterpret_cast<const uint4*>(rec + HD + q * R + 16 * i);
+    const uint4 zv = lds128(rec + HD + q * R + 16 * i);
     zq = __dp4a((int)zv.x, (int)q1r[i].x, zq);
     zq = __dp4a((int)zv.y, (int)q1r[i].y, zq);
     zq = __dp4a((int)zv.z, (int)q1r[i].z, zq);
@@ -193,22 +173,21 @@ TA_DEV void qk_q2(const uint8_t* rec, const uint4 (&q1r)[HD / 64], int (&s)[4][4
   }
   zq += __shfl_xor_sync(0xffffffffu, zq, 1);
   zq += __shfl_xor_sync(0xffffffffu, zq, 2);
-  const int z0 = __shfl_sync(0xffffffffu, zq, 8 * q), z1 = __shfl_sync(0xffffffffu, zq, 8 * q + 4);
-  // A fragments: raw codes of tokens 16 mt + g (+8), the lane's channel region.
-  const uint8_t* codes = rec + 2 * HD;
-  constexpr int TB = HD * BK / 8;   // bytes per token
-  constexpr int QB = TB / 4;        // bytes per lane region
+  const int rq = PACK ? (q & 1) : q;
+  const int z0 = __shfl_sync(0xffffffffu, zq, 8 * rq), z1 = __shfl_sync(0xffffffffu, zq, 8 * rq + 4);
+  // A fragments: raw codes of tokens 16 mt + g (+8) over the quad's channel region.
+  constexpr int TB = HD * BK / 8, QB = TB / 4;
+  const uint32_t codes = rec + 2 * HD;
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt) {
-    int ch[4] = {0, 0, 0, 0}, cl[4] = {0, 0, 0, 0};
     uint32_t w0[QB / 4], w1[QB / 4];
-    const uint8_t* t0 = codes + (16 * mt + g) * TB + q * QB;
-    const uint8_t* t1 = t0 + 8 * TB;
+    const uint32_t t0 = codes + (16 * mt + g) * TB + q * QB, t1 = t0 + 8 * TB;
 #pragma unroll
     for (int i = 0; i < QB / 4; ++i) {
-      w0[i] = reinterpret_cast<const uint32_t*>(t0)[i];
-      w1[i] = reinterpret_cast<const uint32_t*>(t1)[i];
+      w0[i] = lds32(t0 + 4 * i);
+      w1[i] = lds32(t1 + 4 * i);
     }
+    int ch[4] = {0, 0, 0, 0}, cl[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int j = 0; j < KS; ++j) {
       uint32_t af[4];
@@ -224,28 +203,143 @@ TA_DEV void qk_q2(const uint8_t* rec, const uint4 (&q1r)[HD / 64], int (&s)[4][4
         af[2] = (w0[j >> 1] >> (sh + 2)) & 0x03030303u;
         af[3] = (w1[j >> 1] >> (sh + 2)) & 0x03030303u;
       }
-      const uint32_t bh[2] = {bhi[j][0], bhi[j][1]}, bl[2] = {blo[j][0], blo[j][1]};
+      const uint32_t bh[2] = {bhi[j][0], bhi[j][1]};
       imma_u8s8(ch, af, bh);
-      imma_u8u8(cl, af, bl);
+      if (!PACK) {
+        const uint32_t bl[2] = {blo[j][0], blo[j][1]};
+        imma_u8u8(cl, af, bl);
+      }
     }
-    s[mt][0] = 128 * ch[0] + cl[0] + z0;
-    s[mt][1] = 128 * ch[1] + cl[1] + z1;
-    s[mt][2] = 128 * ch[2] + cl[2] + z0;
-    s[mt][3] = 128 * ch[3] + cl[3] + z1;
+    if (PACK) {
+      // exchange hi / lo halves between lane quads q and q ^ 2
+      const bool ql = q >= 2;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int own = ql ? ch[2 + e] : ch[e];
+        const int snd = ql ? ch[e] : ch[2 + e];
+        const int rcv = __shfl_xor_sync(0xffffffffu, snd, 2);
+        const int hi = ql ? rcv : own, lo = ql ? own : rcv;
+        sv[mt][e] = 128 * hi + lo + (e ? z1 : z0);
+      }
+    } else {
+      sv[2 * mt][0] = 128 * ch[0] + cl[0] + z0;
+      sv[2 * mt][1] = 128 * ch[1] + cl[1] + z1;
+      sv[2 * mt + 1][0] = 128 * ch[2] + cl[2] + z0;
+      sv[2 * mt + 1][1] = 128 * ch[3] + cl[3] + z1;
+    }
   }
 }
 
-template <int HD, int BV>
-TA_DEV void pv_q2(const uint8_t* rec, uint8_t (*pbuf)[kBc], const int (&sum_p)[2], int (&acc)[HD / 16][4], int g,
-                  int q) {
-  const uint8_t* codes = rec + 2 * HD;
-  constexpr int CB = kBc * BV / 8;  // bytes per channel
+// QK^T on the INT8 buffer block (token-major K, natural channels; s8 x s8).
+template <int HD, bool PACK>
+TA_DEV void qk_buffer(const int8_t* kb, uint32_t q1s, int (&sv)[Map<HD, PACK>::NT][2], int g, int q) {
+  const int rn = PACK ? (g & 3) : g;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) {
+    int c[4] = {0, 0, 0, 0};
+    const int t0 = 16 * mt + g, t1 = t0 + 8;
+#pragma unroll
+    for (int j = 0; j < HD / 32; ++j) {
+      uint32_t af[4];
+      af[0] = *reinterpret_cast<const uint32_t*>(kb + t0 * HD + 32 * j + 4 * q);
+      af[1] = *reinterpret_cast<const uint32_t*>(kb + t1 * HD + 32 * j + 4 * q);
+      af[2] = *reinterpret_cast<const uint32_t*>(kb + t0 * HD + 32 * j + 16 + 4 * q);
+      af[3] = *reinterpret_cast<const uint32_t*>(kb + t1 * HD + 32 * j + 16 + 4 * q);
+      const uint32_t bq[2] = {lds32(q1s + rn * HD + 32 * j + 4 * q), lds32(q1s + rn * HD + 32 * j + 16 + 4 * q)};
+      imma_s8s8(c, af, bq);
+    }
+    if (PACK) {
+      const bool ql = q >= 2;
+      sv[mt][0] = ql ? c[2] : c[0];
+      sv[mt][1] = ql ? c[3] : c[1];
+    } else {
+      sv[2 * mt][0] = c[0];
+      sv[2 * mt][1] = c[1];
+      sv[2 * mt + 1][0] = c[2];
+      sv[2 * mt + 1][1] = c[3];
+    }
+  }
+}
+
+template <int HD, bool PACK>
+struct RowState {
+  float m[2], l[2];
+  float o[Map<HD, PACK>::NC][2];
+};
+
+// One tile of Alg. 2 on the thread's score values: running max,
+// alpha, SAS, row sum, per-row P scale and codes (to smem rows).
+template <int HD, bool PACK, bool TAP>
+TA_DEV void softmax_tile(const DecodeArgs& a, RowState<HD, PACK>& st, int (&sv)[Map<HD, PACK>::NT][2], int nvalid,
+                         const float (&cqk)[2], uint32_t pbuf, float lut_lane, float (&alpha)[2], float (&s_p)[2],
+                         int (&sum_p)[2], bool tap, int tap_row, int g, int q) {
+  using M = Map<HD, PACK>;
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int row = M::row(q, e);
+    int smax = INT_MIN;
+#pragma unroll
+    for (int t = 0; t < M::NT; ++t)
+      if (M::tok(t, g, q) < nvalid) smax = max(smax, sv[t][e]);
+    smax = grp_maxi<PACK>(smax);
+    const float m_prev = st.m[e];
+    const float m_new = fmaxf(m_prev, __fmul_rn((float)smax, cqk[e]));
+    // alpha = SAS(m_prev - m_new) (R-15); every lane evaluates (shuffle LUT)
+    const float al_s = sas_eval(__fsub_rn(m_new, m_prev), lut_lane, a.sas.nr_abs);
+    const float al = m_prev == -INFINITY ? 0.f : (a.alpha_mode == 1 && m_new == m_prev) ? 1.f : al_s;
+    float pt[M::NT], rs = 0.f, pm = 0.f;
+#pragma unroll
+    for (int t = 0; t < M::NT; ++t) {
+      const float x = __fmul_rn((float)sv[t][e], cqk[e]);
+      float p = sas_eval(__fsub_rn(m_new, x), lut_lane, a.sas.nr_abs);
+      p = M::tok(t, g, q) < nvalid ? p : 0.f;
+      pt[t] = p;
+      rs += p;
+      pm = fmaxf(pm, p);
+    }
+    rs = grp_sumf<PACK>(rs);
+    pm = grp_maxf<PACK>(pm);
+    st.l[e] = al * st.l[e] + rs;
+    st.m[e] = m_new;
+    alpha[e] = al;
+    // per-row P scale (Alg. 2 P:976-977, R-17)
+    const float inv_p = pm > 0.f ? __fdiv_rn(kDiv, pm) : 0.f;
+    s_p[e] = __fdiv_rn(pm, kDiv);
+    int sp = 0;
+#pragma unroll
+    for (int t = 0; t < M::NT; ++t) {
+      const int c = rint_prod(pt[t], inv_p);
+      sp += c;
+      sts_u8(pbuf + row * kBc + M::tok(t, g, q), (uint32_t)c);
+      if (TAP && tap && row == tap_row) {
+        a.tap.p_codes[M::tok(t, g, q)] = (uint8_t)c;
+        a.tap.s_int[M::tok(t, g, q)] = M::tok(t, g, q) < nvalid ? sv[t][e] : 0;
+      }
+    }
+    sum_p[e] = grp_sumi<PACK>(sp);
+    if (TAP && tap && row == tap_row && g == 0 && (!PACK || q < 2)) {
+      a.tap.m_new[0] = m_new;
+      a.tap.s_p[0] = s_p[e];
+    }
+  }
+  __syncwarp();
+}
+
+// P V on a stage-2 block: raw V codes x P codes, then the exact per-channel
+// fixup s_c * acc + z_c * sum(P) (Eq. 5 fold).  Buffer block: INT8 V, no fixup.
+template <int HD, int BV, bool PACK, bool BUF>
+TA_DEV void pv_block(uint32_t rec, const int8_t* vb, uint32_t pbuf, const int (&sum_p)[2],
+                     int (&acc)[Map<HD, PACK>::NC][2], int g, int q) {
+  const int rn = PACK ? (g & 3) : g;
   uint32_t bf[2][2];
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
-    bf[j][0] = *reinterpret_cast<const uint32_t*>(&pbuf[g][32 * j + 4 * q]);
-    bf[j][1] = *reinterpret_cast<const uint32_t*>(&pbuf[g][32 * j + 16 + 4 * q]);
+    bf[j][0] = lds32(pbuf + rn * kBc + 32 * j + 4 * q);
+    bf[j][1] = lds32(pbuf + rn * kBc + 32 * j + 16 + 4 * q);
   }
+  constexpr int CB = kBc * BV / 8;  // bytes per channel of V codes
+  const uint32_t codes = rec + 2 * HD;
+  const bool ql = q >= 2;
 #pragma unroll
   for (int mt = 0; mt < HD / 16; ++mt) {
     const int c0 = 16 * mt + g, c1 = c0 + 8;
@@ -253,40 +347,58 @@ TA_DEV void pv_q2(const uint8_t* rec, uint8_t (*pbuf)[kBc], const int (&sum_p)[2
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       uint32_t af[4];
-      if (BV == 4) {
-        const uint32_t u0 = reinterpret_cast<const uint32_t*>(codes + c0 * CB)[4 * j + q];
-        const uint32_t u1 = reinterpret_cast<const uint32_t*>(codes + c1 * CB)[4 * j + q];
-        af[0] = u0 & 0x0F0F0F0Fu;
-        af[1] = u1 & 0x0F0F0F0Fu;
-        af[2] = (u0 >> 4) & 0x0F0F0F0Fu;
-        af[3] = (u1 >> 4) & 0x0F0F0F0Fu;
+      if (BUF) {
+        af[0] = *reinterpret_cast<const uint32_t*>(vb + c0 * kBc + 32 * j + 4 * q);
+        af[1] = *reinterpret_cast<const uint32_t*>(vb + c1 * kBc + 32 * j + 4 * q);
+        af[2] = *reinterpret_cast<const uint32_t*>(vb + c0 * kBc + 32 * j + 16 + 4 * q);
+        af[3] = *reinterpret_cast<const uint32_t*>(vb + c1 * kBc + 32 * j + 16 + 4 * q);
+        const uint32_t b2[2] = {bf[j][0], bf[j][1]};
+        imma_s8u8(c, af, b2);
       } else {
-        const uint32_t u0 = reinterpret_cast<const uint32_t*>(codes + c0 * CB)[q];
-        const uint32_t u1 = reinterpret_cast<const uint32_t*>(codes + c1 * CB)[q];
-        const int sh = 4 * j;
-        af[0] = (u0 >> sh) & 0x03030303u;
-        af[1] = (u1 >> sh) & 0x03030303u;
-        af[2] = (u0 >> (sh + 2)) & 0x03030303u;
-        af[3] = (u1 >> (sh + 2)) & 0x03030303u;
+        if (BV == 4) {
+          const uint32_t u0 = lds32(codes + c0 * CB + 4 * (4 * j + q));
+          const uint32_t u1 = lds32(codes + c1 * CB + 4 * (4 * j + q));
+          af[0] = u0 & 0x0F0F0F0Fu;
+          af[1] = u1 & 0x0F0F0F0Fu;
+          af[2] = (u0 >> 4) & 0x0F0F0F0Fu;
+          af[3] = (u1 >> 4) & 0x0F0F0F0Fu;
+        } else {
+          const uint32_t u0 = lds32(codes + c0 * CB + 4 * q);
+          const uint32_t u1 = lds32(codes + c1 * CB + 4 * q);
+          const int sh = 4 * j;
+          af[0] = (u0 >> sh) & 0x03030303u;
+          af[1] = (u1 >> sh) & 0x03030303u;
+          af[2] = (u0 >> (sh + 2)) & 0x03030303u;
+          af[3] = (u1 >> (sh + 2)) & 0x03030303u;
+        }
+        const uint32_t b2[2] = {bf[j][0], bf[j][1]};
+        imma_u8u8(c, af, b2);
       }
-      const uint32_t b[2] = {bf[j][0], bf[j][1]};
-      imma_u8u8(c, af, b);
     }
-    const int s0 = rec[c0], s1 = rec[c1];
-    const int z0 = (int)(int8_t)rec[HD + c0], z1 = (int)(int8_t)rec[HD + c1];
-    acc[mt][0] = s0 * c[0] + z0 * sum_p[0];
-    acc[mt][1] = s0 * c[1] + z0 * sum_p[1];
-    acc[mt][2] = s1 * c[2] + z1 * sum_p[0];
-    acc[mt][3] = s1 * c[3] + z1 * sum_p[1];
+#pragma unroll
+    for (int h = 0; h < (PACK ? 1 : 2); ++h) {
+      const int hh = PACK ? (ql ? 1 : 0) : h;  // which channel of the pair (c0 / c1)
+      const int ci = PACK ? mt : 2 * mt + h;
+      const int ch = c0 + 8 * hh;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int v = c[2 * hh + e];
+        if (BUF) {
+          acc[ci][e] = v;
+        } else {
+          acc[ci][e] = (int)lds_u8(rec + ch) * v + lds_s8(rec + HD + ch) * sum_p[e];
+        }
+      }
+    }
   }
 }
 
-template <int HD>
+template <int HD, bool PACK, bool TAP>
 __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_constant__ DecodeArgs a) {
-  extern __shared__ uint8_t smem_raw[];
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  using M = Map<HD, PACK>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
-  DecodeWarpSmem<HD>& sm = reinterpret_cast<DecodeWarpSmem<HD>*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127))[warp];
+  DecodeWarpSmem<HD>& sm = reinterpret_cast<DecodeWarpSmem<HD>*>(smem_raw)[warp];
   const int task = blockIdx.x * kWarpsPerCta + warp;
   if (task >= a.B * a.Hkv * a.n_splits) return;
   const int split = task % a.n_splits, bh = task / a.n_splits, b = bh / a.Hkv, kvh = bh % a.Hkv;
@@ -301,7 +413,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
   constexpr int REC = rec_bytes(HD);
   const uint32_t bytesK = 2 * HD + kBc * HD * bitsK / 8, bytesV = 2 * HD + kBc * HD * bitsV / 8;
   const float lut_lane = sas_lut_lane(a.sas, lane);
-  const int tap_row = a.has_tap && split == 0 && a.tap.batch == b && a.tap.head / G == kvh ? a.tap.head % G : -1;
+  const int tap_row = TAP && split == 0 && a.tap.batch == b && a.tap.head / G == kvh ? a.tap.head % G : -1;
+  const uint32_t pbuf = smem_u32(&sm.p[0][0]), q1s = smem_u32(&sm.q1[0][0]);
 
   if (lane == 0) {
     mbar_init(&sm.bar[0], 1);
@@ -319,12 +432,13 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
   if (j0 < j1) issue(j0, 0);
   if (j0 + 1 < j1) issue(j0 + 1, 1);
 
-  // q stage-1 quantisation per (b, head) vector (Alg. 2).
+  // q stage-1 quantisation per (b, head) vector (Alg. 2): lane quad g
+  // quantises row g (rows >= G are zero).
   float s_q_row = 0.f;
   {
-    const int R = HD / 4;
+    constexpr int R = HD / 4;
     float qa = 0.f;
-    float xv[HD / 4];
+    float xv[R];
     const __half* qp = a.q + ((size_t)b * a.Hq + kvh * G + g) * HD + q * R;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
@@ -336,62 +450,64 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
     const float inv = qa > 0.f ? __fdiv_rn(kDiv, qa) : 0.f;
     s_q_row = __fdiv_rn(qa, kDiv);
 #pragma unroll
-    for (int i = 0; i < R; ++i) sm.q1[g][q * R + i] = (int8_t)rint_prod(xv[i], inv);
-    if (g == tap_row) {
+    for (int i = 0; i < R; i += 4)
+      *reinterpret_cast<uint32_t*>(&sm.q1[g][q * R + i]) =
+          pack4_lo(rint_prod_bits(xv[i], inv), rint_prod_bits(xv[i + 1], inv), rint_prod_bits(xv[i + 2], inv),
+                   rint_prod_bits(xv[i + 3], inv));
+    if (TAP && g == tap_row) {
       for (int i = 0; i < R; ++i) a.tap.q1[q * R + i] = sm.q1[g][q * R + i];
       if (q == 0) a.tap.s_q[0] = s_q_row;
     }
   }
   __syncwarp();
-  uint4 q1r[HD / 64];  // the lane's channel region of row g
+  // The lane's K-channel region of its B-fragment row: row g (general) or row
+  // g & 3 (packed), as packed bytes (dp4a) and as ints (products).
+  const int brow = PACK ? (g & 3) : g;
+  uint4 q1r[HD / 64];
+  int qv[HD / 4];
 #pragma unroll
-  for (int i = 0; i < HD / 64; ++i) q1r[i] = *reinterpret_cast<const uint4*>(&sm.q1[g][q * (HD / 4) + 16 * i]);
-  const float sq2[2] = {__shfl_sync(0xffffffffu, s_q_row, 8 * q), __shfl_sync(0xffffffffu, s_q_row, 8 * q + 4)};
+  for (int i = 0; i < HD / 64; ++i) {
+    q1r[i] = lds128(q1s + brow * HD + q * (HD / 4) + 16 * i);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) qv[16 * i + e] = (int)(int8_t)(uint8_t)byte_of(q1r[i], e);
+  }
+  const int rq = PACK ? (q & 1) : q;
+  const float sq2[2] = {__shfl_sync(0xffffffffu, s_q_row, 8 * rq), __shfl_sync(0xffffffffu, s_q_row, 8 * rq + 4)};
 
-  RowState<HD> st;
+  RowState<HD, PACK> st;
   st.m[0] = st.m[1] = -INFINITY;
   st.l[0] = st.l[1] = 0.f;
 #pragma unroll
-  for (int mt = 0; mt < HD / 16; ++mt)
+  for (int c = 0; c < M::NC; ++c) st.o[c][0] = st.o[c][1] = 0.f;
+
+  auto update = [&](const int (&acc)[M::NC][2], const float (&alpha)[2], const float (&cpv)[2], bool tap) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) st.o[mt][i] = 0.f;
+    for (int c = 0; c < M::NC; ++c)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        st.o[c][e] = __fmaf_rn(alpha[e], st.o[c][e], cpv[e] * (float)acc[c][e]);
+        if (TAP && tap && M::row(q, e) == tap_row) a.tap.pv_int[M::chan(c, g, q)] = acc[c][e];
+      }
+  };
 
   for (int j = j0; j < j1; ++j) {
     const int stg = (j - j0) & 1;
     mbar_wait(&sm.bar[stg], ((j - j0) >> 1) & 1);
-    const uint8_t* recK = sm.rec[stg][0];
-    const uint8_t* recV = sm.rec[stg][1];
-    int s[4][4];
-    if (bitsK == 4) qk_q2<HD, 4>(recK, q1r, s, g, q);
-    else qk_q2<HD, 2>(recK, q1r, s, g, q);
+    const uint32_t recK = smem_u32(sm.rec[stg][0]), recV = smem_u32(sm.rec[stg][1]);
+    int sv[M::NT][2];
+    if (bitsK == 4) qk_block<HD, 4, PACK>(recK, qv, q1r, sv, g, q);
+    else qk_block<HD, 2, PACK>(recK, qv, q1r, sv, g, q);
     const float sK = a.s_parent[slotK * a.max_blocks + j], sV = a.s_parent[slotV * a.max_blocks + j];
     const float cqk[2] = {__fmul_rn(__fmul_rn(sq2[0], sK), a.scale), __fmul_rn(__fmul_rn(sq2[1], sK), a.scale)};
-    const bool tap = tap_row >= 0 && a.tap.j_block == j;
-    if (tap) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int mt = i >> 1, hi = i & 1;
-        const int e = tap_row - 2 * q;
-        if (e == 0 || e == 1) a.tap.s_int[16 * mt + g + 8 * hi] = s[mt][2 * hi + e];
-      }
-    }
+    const bool tap = TAP && tap_row >= 0 && a.tap.j_block == j;
     float alpha[2], s_p[2];
     int sum_p[2];
-    softmax_tile<HD>(a, st, s, kBc, cqk, sm.p, lut_lane, alpha, s_p, sum_p, tap, tap_row, g, q);
-    int acc[HD / 16][4];
-    if (bitsV == 4) pv_q2<HD, 4>(recV, sm.p, sum_p, acc, g, q);
-    else pv_q2<HD, 2>(recV, sm.p, sum_p, acc, g, q);
-    if (tap) {
-      const int e = tap_row - 2 * q;
-      if (e == 0 || e == 1)
-#pragma unroll
-        for (int mt = 0; mt < HD / 16; ++mt) {
-          a.tap.pv_int[16 * mt + g] = acc[mt][e];
-          a.tap.pv_int[16 * mt + g + 8] = acc[mt][2 + e];
-        }
-    }
+    softmax_tile<HD, PACK, TAP>(a, st, sv, kBc, cqk, pbuf, lut_lane, alpha, s_p, sum_p, tap, tap_row, g, q);
+    int acc[M::NC][2];
+    if (bitsV == 4) pv_block<HD, 4, PACK, false>(recV, nullptr, pbuf, sum_p, acc, g, q);
+    else pv_block<HD, 2, PACK, false>(recV, nullptr, pbuf, sum_p, acc, g, q);
     const float cpv[2] = {__fmul_rn(s_p[0], sV), __fmul_rn(s_p[1], sV)};
-    pv_update<HD>(st, acc, alpha, cpv);
+    update(acc, alpha, cpv, tap);
     __syncwarp();
     if (j + 2 < j1) issue(j + 2, stg);
   }
@@ -401,96 +517,37 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
     const int8_t* kb = a.buf + slotK * (size_t)(kBc * HD);
     const int8_t* vb = a.buf + slotV * (size_t)(kBc * HD);
     const float sK = __fdiv_rn(a.a_univ[slotK], kDiv), sV = __fdiv_rn(a.a_univ[slotV], kDiv);
-    int s[4][4];
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
-      int c[4] = {0, 0, 0, 0};
-#pragma unroll
-      for (int j = 0; j < HD / 32; ++j) {
-        const int t0 = 16 * mt + g, t1 = t0 + 8;
-        uint32_t af[4];
-        af[0] = *reinterpret_cast<const uint32_t*>(kb + t0 * HD + 32 * j + 4 * q);
-        af[1] = *reinterpret_cast<const uint32_t*>(kb + t1 * HD + 32 * j + 4 * q);
-        af[2] = *reinterpret_cast<const uint32_t*>(kb + t0 * HD + 32 * j + 16 + 4 * q);
-        af[3] = *reinterpret_cast<const uint32_t*>(kb + t1 * HD + 32 * j + 16 + 4 * q);
-        const uint32_t bq[2] = {*reinterpret_cast<const uint32_t*>(&sm.q1[g][32 * j + 4 * q]),
-                                *reinterpret_cast<const uint32_t*>(&sm.q1[g][32 * j + 16 + 4 * q])};
-        imma_s8s8(c, af, bq);
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) s[mt][i] = c[i];
-    }
+    int sv[M::NT][2];
+    qk_buffer<HD, PACK>(kb, q1s, sv, g, q);
     const float cqk[2] = {__fmul_rn(__fmul_rn(sq2[0], sK), a.scale), __fmul_rn(__fmul_rn(sq2[1], sK), a.scale)};
-    const bool tap = tap_row >= 0 && a.tap.j_block == -1;
-    if (tap) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int mt = i >> 1, hi = i & 1, e = tap_row - 2 * q, tok = 16 * mt + g + 8 * hi;
-        if (e == 0 || e == 1) a.tap.s_int[tok] = tok < nbuf ? s[mt][2 * hi + e] : 0;
-      }
-    }
+    const bool tap = TAP && tap_row >= 0 && a.tap.j_block == -1;
     float alpha[2], s_p[2];
     int sum_p[2];
-    softmax_tile<HD>(a, st, s, nbuf, cqk, sm.p, lut_lane, alpha, s_p, sum_p, tap, tap_row, g, q);
-    int acc[HD / 16][4];
-    uint32_t bf[2][2];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      bf[j][0] = *reinterpret_cast<const uint32_t*>(&sm.p[g][32 * j + 4 * q]);
-      bf[j][1] = *reinterpret_cast<const uint32_t*>(&sm.p[g][32 * j + 16 + 4 * q]);
-    }
-#pragma unroll
-    for (int mt = 0; mt < HD / 16; ++mt) {
-      const int c0 = 16 * mt + g, c1 = c0 + 8;
-      int c[4] = {0, 0, 0, 0};
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        uint32_t af[4];
-        af[0] = *reinterpret_cast<const uint32_t*>(vb + c0 * kBc + 32 * j + 4 * q);
-        af[1] = *reinterpret_cast<const uint32_t*>(vb + c1 * kBc + 32 * j + 4 * q);
-        af[2] = *reinterpret_cast<const uint32_t*>(vb + c0 * kBc + 32 * j + 16 + 4 * q);
-        af[3] = *reinterpret_cast<const uint32_t*>(vb + c1 * kBc + 32 * j + 16 + 4 * q);
-        const uint32_t b2[2] = {bf[j][0], bf[j][1]};
-        imma_s8u8(c, af, b2);
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) acc[mt][i] = c[i];
-    }
-    if (tap) {
-      const int e = tap_row - 2 * q;
-      if (e == 0 || e == 1)
-#pragma unroll
-        for (int mt = 0; mt < HD / 16; ++mt) {
-          a.tap.pv_int[16 * mt + g] = acc[mt][e];
-          a.tap.pv_int[16 * mt + g + 8] = acc[mt][2 + e];
-        }
-    }
+    softmax_tile<HD, PACK, TAP>(a, st, sv, nbuf, cqk, pbuf, lut_lane, alpha, s_p, sum_p, tap, tap_row, g, q);
+    int acc[M::NC][2];
+    pv_block<HD, 4, PACK, true>(0, vb, pbuf, sum_p, acc, g, q);
     const float cpv[2] = {__fmul_rn(s_p[0], sV), __fmul_rn(s_p[1], sV)};
-    pv_update<HD>(st, acc, alpha, cpv);
+    update(acc, alpha, cpv, tap);
   }
 
   // O = diag(l)^-1 O, L = m + log l; empty -> O = 0, L = -inf.
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
-    const int row = 2 * q + e;
+    const int row = M::row(q, e);
     if (row >= G) continue;
     const bool empty = st.l[e] == 0.f;
     const float inv_l = empty ? 0.f : 1.f / st.l[e];
     const size_t orow = (size_t)b * a.Hq + kvh * G + row;
     const size_t base = ((size_t)split * a.B * a.Hq + orow) * HD;
 #pragma unroll
-    for (int mt = 0; mt < HD / 16; ++mt) {
-      const float v0 = st.o[mt][e] * inv_l, v1 = st.o[mt][2 + e] * inv_l;
-      if (a.o_parts) {
-        a.o_parts[base + 16 * mt + g] = v0;
-        a.o_parts[base + 16 * mt + g + 8] = v1;
-      }
-      if (a.o16) {
-        a.o16[orow * HD + 16 * mt + g] = __float2half_rn(v0);
-        a.o16[orow * HD + 16 * mt + g + 8] = __float2half_rn(v1);
-      }
+    for (int c = 0; c < M::NC; ++c) {
+      const float v = st.o[c][e] * inv_l;
+      const int ch = M::chan(c, g, q);
+      if (a.o_parts) a.o_parts[base + ch] = v;
+      if (a.o16) a.o16[orow * HD + ch] = __float2half_rn(v);
     }
-    if (g == 0) a.lse_parts[(size_t)split * a.B * a.Hq + orow] = empty ? -INFINITY : st.m[e] + logf(st.l[e]);
+    if (g == 0 && (!PACK || q < 2))
+      a.lse_parts[(size_t)split * a.B * a.Hq + orow] = empty ? -INFINITY : st.m[e] + logf(st.l[e]);
   }
 }
 
@@ -552,8 +609,8 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
   a.alpha_mode = p->alpha_mode;
   a.scale = p->softmax_scale;
   fill_sas_const(&a.sas, p->sas_nr);
-  a.has_tap = p->debug_tap != nullptr;
-  if (a.has_tap) a.tap = *reinterpret_cast<const turbo_debug_tap_t*>(p->debug_tap);
+  const bool has_tap = p->debug_tap != nullptr;
+  if (has_tap) a.tap = *reinterpret_cast<const turbo_debug_tap_t*>(p->debug_tap);
   else memset(&a.tap, 0, sizeof(a.tap));
   if (S == 1) {
     a.o_parts = o_part;
@@ -566,15 +623,26 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
   }
   const int tasks = B * H * S;
   const dim3 grid((tasks + kWarpsPerCta - 1) / kWarpsPerCta);
-  if (HD == 128) {
-    const size_t smem = sizeof(DecodeWarpSmem<128>) * kWarpsPerCta + 128;
-    cudaFuncSetAttribute(decode_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    decode_kernel<128><<<grid, 32 * kWarpsPerCta, smem, st>>>(a);
-  } else {
-    const size_t smem = sizeof(DecodeWarpSmem<64>) * kWarpsPerCta + 128;
-    cudaFuncSetAttribute(decode_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    decode_kernel<64><<<grid, 32 * kWarpsPerCta, smem, st>>>(a);
+  const bool pack = a.G <= 4;
+#define TA_DEC(HDV, PK, TP)                                                                             \
+  {                                                                                                     \
+    const size_t smem = sizeof(DecodeWarpSmem<HDV>) * kWarpsPerCta;                                     \
+    cudaFuncSetAttribute(decode_kernel<HDV, PK, TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    decode_kernel<HDV, PK, TP><<<grid, 32 * kWarpsPerCta, smem, st>>>(a);                              \
   }
+#define TA_DEC2(HDV)                                                  \
+  if (pack) {                                                         \
+    if (has_tap) TA_DEC(HDV, true, true) else TA_DEC(HDV, true, false)  \
+  } else {                                                            \
+    if (has_tap) TA_DEC(HDV, false, true) else TA_DEC(HDV, false, false) \
+  }
+  if (HD == 128) {
+    TA_DEC2(128)
+  } else {
+    TA_DEC2(64)
+  }
+#undef TA_DEC2
+#undef TA_DEC
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || S == 1) return e;
   const int rows = B * Hq;

@@ -73,9 +73,10 @@ template <int HD, int NS, bool TAP>
 __global__ void __launch_bounds__(128 * (NS + 1), 1)
     prefill_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                    const __grid_constant__ PrefillArgs args) {
-  extern __shared__ uint8_t smem_raw[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
   using Smem = PrefillSmem<HD, NS>;
-  Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned (128B-swizzle atoms); pointer arithmetic keeps the shared address space.
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr uint32_t kTmemCols = NS == 2 ? 512 : 256;  // per slot: S0 [0,64) S1 [64,128) PV [128,128+d)
 
