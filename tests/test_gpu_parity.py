@@ -270,3 +270,51 @@ def test_validation_errors(ta):
         kk = torch.zeros(1, 64 * 5, 1, 64, dtype=torch.float16, device="cuda")
         ta.turbo_quantize_kv(p, cache_ok, kk, kk)
     assert e.value.code == ta.TURBO_ERR_CAPACITY
+
+
+def test_seq_sharded_decode_emulated_ranks(ta):
+    """configs[4]-style long-context decode on one GPU with W emulated ranks:
+    each shard's cache decodes with o_part (FP32, normalised) + L, the
+    partials merge with turbo_combine_lse in rank order."""
+    from paper_2412_08585_b200 import parallel
+
+    B, N, Hq, Hkv, d, W = 2, 64 * 11 + 9, 8, 2, 128, 3
+    G = Hq // Hkv
+    q, k, v = synth.qkv(4242, B, N, Hq, Hkv, d)
+    qd, _, _ = synth.decode_token(4243, B, Hq, Hkv, d)
+    bits = synth.head_bits_alternating(Hkv)
+    p = ta.params(head_dim=d, alpha_mode=1)
+    op = O.params(d=d, alpha_mode=1)
+    parts, lses, ref_parts, ref_lses = [], [], [], []
+    for r in range(W):
+        t0, t1 = parallel.seq_shard_tokens(N, W, r)
+        cache = ta.KVCache(B, Hkv, d, max_blocks=8, bits=bits)
+        ta.turbo_quantize_kv(p, cache, torch.from_numpy(np.ascontiguousarray(k[:, t0:t1])).cuda(),
+                             torch.from_numpy(np.ascontiguousarray(v[:, t0:t1])).cuda())
+        _, op32, l_ = ta.turbo_attention_decode(p, cache, torch.from_numpy(qd).cuda(), with_buffer=(r == W - 1),
+                                                n_splits=2, want_fp16=False, want_f32=True)
+        parts.append(op32.reshape(B * Hq, d))
+        lses.append(l_.reshape(B * Hq))
+        ref = O.build_cache(op, k[:, t0:t1].astype(np.float32), v[:, t0:t1].astype(np.float32), bits, 8)
+        rp, rl = np.zeros((B, Hq, d), np.float32), np.zeros((B, Hq), np.float32)
+        for b in range(B):
+            nb = ref["slots"][b][0][0].n_blocks
+            per = -(-nb // 2)
+            bounds = [(min(s * per, nb), min(s * per + per, nb)) for s in range(2)]
+            for h in range(Hq):
+                ks, vs = ref["slots"][b][h // G]
+                pp = [O.decode_head(op, qd[b, h].astype(np.float32), ks, vs, a_, e_, (s == 1) and (r == W - 1))
+                      for s, (a_, e_) in enumerate(bounds)]
+                rp[b, h], rl[b, h] = O.combine(np.stack([x for x, _ in pp]), np.array([y for _, y in pp]))
+        ref_parts.append(rp.reshape(B * Hq, d))
+        ref_lses.append(rl.reshape(B * Hq))
+    o16, _, L = ta.turbo_combine_lse(torch.stack(parts), torch.stack(lses))
+    torch.cuda.synchronize()
+    ref_p, ref_l = np.stack(ref_parts), np.stack(ref_lses)
+    for r in range(W):
+        np.testing.assert_allclose(parts[r].cpu().numpy(), ref_p[r], atol=2e-3, rtol=1e-3)
+        np.testing.assert_allclose(lses[r].cpu().numpy(), ref_l[r], atol=1e-4, rtol=1e-5)
+    for row in range(B * Hq):
+        ro, rl = O.combine(ref_p[:, row], ref_l[:, row])
+        assert np.abs(o16[row].float().cpu().numpy() - ro).max() <= MAX_ABS
+        assert abs(L[row].item() - rl) < 1e-4
