@@ -323,6 +323,115 @@ def workload_config(args):
             "l2": "flushed between timed steps (512 MB write)"}
 
 
+# --------------------------------------------------------------------------- secondary workloads
+CFG_70B = dict(B=1, N=32768, Hq=64, Hkv=8, d=128)
+CFG_LONG = dict(B=16, N=128 * 1024, Hq=32, Hkv=8, d=128)
+
+
+def _max_over_ranks(ms, world, device):
+    import torch
+
+    if world > 1:
+        t = torch.tensor([ms], device=device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = t.item()
+    return ms
+
+
+def run_prefill_70b(args, rank, world, device):
+    """configs[3]: Llama-3-70B attention (64 Q / 8 KV heads, d=128), prefill 32k,
+    batch 1; KV heads (with their query heads) partitioned over the ranks
+    (strong scaling, no collective)."""
+    import torch
+
+    from paper_2412_08585_b200 import binding as ta
+    from paper_2412_08585_b200 import parallel, synth
+
+    c = CFG_70B
+    (k0, k1), (h0, h1) = parallel.head_shard(c["Hq"], c["Hkv"], world, rank)
+    hkv, hq = k1 - k0, h1 - h0
+    B, N, d = c["B"], c["N"], c["d"]
+    p = ta.params(head_dim=d)
+    q, k, v = synth.qkv_torch(5005 + rank, B, N, hq, hkv, d, device=device)
+    cache = ta.KVCache(B, hkv, d, max_blocks=N // 64 + 1, bits=synth.head_bits_alternating(hkv), device=device)
+    st = torch.cuda.current_stream()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.warmup + args.steps):
+        if i >= args.warmup:
+            evs[i - args.warmup][0].record(st)
+        k1_, v1t, k1s, v1s = ta.turbo_quantize_kv(p, cache, k, v)
+        ta.turbo_attention_prefill(p, q, k1_, v1t, k1s, v1s, causal=True)
+        if i >= args.warmup:
+            evs[i - args.warmup][1].record(st)
+    torch.cuda.synchronize()
+    ms = _max_over_ranks(sum(a.elapsed_time(b) for a, b in evs), world, device) / args.steps
+    ops = prefill_ops(B, N, c["Hq"], d)
+    return {"value": ops / (ms * 1e-3) / 1e12, "unit": "TOPS", "ms_step": ms, "scaling": "strong",
+            "config": {"workload": "configs[3]: Llama-3-70B attention shape (64 Q / 8 KV heads, d=128), prefill 32k, "
+                                   "batch 1, causal; step = quantize_kv + prefill",
+                       "parallelism": f"KV heads partitioned over {world} rank(s), no collective",
+                       "per_rank_heads": [hq, hkv]}}
+
+
+def run_decode_long(args, rank, world, device):
+    """configs[4]: 128k-context decode, batch 16 (Llama-3-8B attention shape,
+    32/8 heads, mixed INT4/INT2), cache sequence-sharded over the ranks; per
+    step: append (last rank) + local split-KV decode + all-gather + LSE merge."""
+    import torch
+
+    from paper_2412_08585_b200 import binding as ta
+    from paper_2412_08585_b200 import parallel, synth
+
+    c = CFG_LONG
+    B, N, Hq, Hkv, d = c["B"], c["N"], c["Hq"], c["Hkv"], c["d"]
+    t0, t1 = parallel.seq_shard_tokens(N, world, rank)
+    n_loc = t1 - t0
+    bits = synth.head_bits_alternating(Hkv)
+    p = ta.params(head_dim=d, alpha_mode=1)
+    cache = ta.KVCache(B, Hkv, d, max_blocks=n_loc // 64 + 4, bits=bits, device=device)
+    _, k, v = synth.qkv_torch(9009 + rank, B, n_loc, Hkv, Hkv, d, device=device)
+    ta.turbo_quantize_kv(p, cache, k, v)
+    del k, v
+    torch.cuda.empty_cache()
+    last = rank == world - 1
+    toks = [tuple(x[:, 0].contiguous() for x in synth.qkv_torch(7000 + i, B, 1, Hq, Hkv, d, device=device))
+            for i in range(args.warmup + args.steps)]
+    group = torch.distributed.group.WORLD if world > 1 else None
+    st = torch.cuda.current_stream()
+
+    def step(i):
+        qd, kd, vd = toks[i]
+        if last:
+            ta.turbo_quantize_kv(p, cache, kd, vd, mode=1)
+        if world > 1:
+            return parallel.decode_seq_sharded(p, cache, qd, group, n_splits_local=args.decode_splits)
+        o, _, L = ta.turbo_attention_decode(p, cache, qd, n_splits=args.decode_splits)
+        return o, L
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for i in range(args.steps):
+        step(args.warmup + i)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = _max_over_ranks(e0.elapsed_time(e1), world, device) / args.steps
+    nblk = cache.n_tokens // 64
+    byt = decode_bytes(B, Hkv, d, nblk, cache.n_tokens % 64, bits, Hq)
+    total = _max_over_ranks(float(byt), world, device) * world  # shards are equal up to one block
+    return {"value": total / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms_step": ms, "scaling": "strong",
+            "tokens_per_s": B / (ms * 1e-3),
+            "config": {"workload": "configs[4]: decode 128k context, batch 16, Llama-3-8B attention shape "
+                                   "(32 Q / 8 KV heads, d=128), mixed INT4/INT2; step = append + split-KV decode "
+                                   "+ all-gather + LSE combine",
+                       "parallelism": f"sequence-sharded cache over {world} rank(s), NCCL all-gather of (O, L)",
+                       "decode_splits_per_rank": args.decode_splits}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -332,6 +441,8 @@ def main():
     ap.add_argument("--splits", type=int, default=4, help="split-KV count of the decode in the step")
     ap.add_argument("--decode-splits", type=int, default=8)
     ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--workload", default="step", choices=["step", "prefill_70b", "decode_long"],
+                    help="step = the default hot-path step (configs[1] + configs[2] decode)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -349,6 +460,21 @@ def main():
     from paper_2412_08585_b200 import build
 
     build.build()
+    if args.workload != "step":
+        fn = run_prefill_70b if args.workload == "prefill_70b" else run_decode_long
+        res = fn(args, rank, world, local)
+        if rank == 0:
+            line = {"metric": BASE_METRIC, "value": round(res["value"], 2), "unit": res["unit"], "n_gpus": world,
+                    "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["ms_step"], 4),
+                    "higher_is_better": True, "scaling": res["scaling"], "vs_baseline": None, "dtype": "int8",
+                    "data": "synthetic", "config": res["config"]}
+            if "tokens_per_s" in res:
+                line["tokens_per_s"] = round(res["tokens_per_s"], 1)
+            print(json.dumps(line), flush=True)
+        if world > 1:
+            torch.distributed.barrier()
+            torch.distributed.destroy_process_group()
+        return
     res = run_ours(args, rank, world, local)
     cpu = cpu_sample_oracle() if rank == 0 and world == 1 else None
     if rank == 0:
