@@ -232,6 +232,8 @@ def bench_decode(args, rank, world, device, pk):
     del k, v
     torch.cuda.empty_cache()
     S = args.decode_splits
+    if S is None:
+        S = ta.auto_splits(B, Hkv, cache.n_tokens // 64)
     ws = torch.empty(max(ta.turbo_decode_workspace_bytes(B, Hq, d, S), 16), dtype=torch.uint8, device=device)
     toks = [tuple(x[:, 0].contiguous() for x in synth.qkv_torch(6000 + i, B, 1, Hq, Hkv, d, device=device))
             for i in range(args.warmup + args.steps)]
@@ -439,7 +441,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--splits", type=int, default=4, help="split-KV count of the decode in the step")
-    ap.add_argument("--decode-splits", type=int, default=8)
+    ap.add_argument("--decode-splits", type=int, default=None, help="default: binding.auto_splits")
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--workload", default="step", choices=["step", "prefill_70b", "decode_long"],
                     help="step = the default hot-path step (configs[1] + configs[2] decode)")

@@ -179,12 +179,23 @@ def turbo_decode_workspace_bytes(B, Hq, head_dim, n_splits):
     return lib().turbo_decode_workspace_bytes(B, Hq, head_dim, n_splits)
 
 
+def auto_splits(batch, n_kv_heads, n_blocks, target_tasks=4096):
+    """Split count giving ~target_tasks warp tasks (>= 2 waves of the ~1800 resident
+    decode warps on 148 SMs), at least 8 blocks per split."""
+    s = -(-target_tasks // max(1, batch * n_kv_heads))
+    return max(1, min(s, n_blocks // 8))
+
+
 def turbo_attention_decode(p, cache: KVCache, q, blk_begin=0, blk_end=-1, with_buffer=True, n_splits=1,
                            workspace=None, o=None, o_part=None, lse=None, want_fp16=True, want_f32=False,
                            stream=None):
-    """q fp16 [B,Hq,d] -> (o fp16 [B,Hq,d] or None, o_part f32 [B,Hq,d] or None, lse f32 [B,Hq])."""
+    """q fp16 [B,Hq,d] -> (o fp16 [B,Hq,d] or None, o_part f32 [B,Hq,d] or None, lse f32 [B,Hq]).
+    n_splits=None picks auto_splits() for the cached length."""
     assert q.dtype == torch.float16 and q.is_contiguous()
     B, Hq, d = q.shape
+    if n_splits is None:
+        nb = (cache.n_tokens // cache.block_kv) if blk_end < 0 else blk_end
+        n_splits = auto_splits(B, cache.n_kv_heads, max(0, nb - blk_begin))
     dev = q.device
     if want_fp16 and o is None:
         o = torch.empty((B, Hq, d), dtype=torch.float16, device=dev)

@@ -108,12 +108,30 @@ TA_DEV int grp_sumi(int v) {
   return v;
 }
 
-// Channel of the low k-slot m (0..3) of k-step j inside a lane quad's channel
-// region of K codes (layout.cuh); the high slot is the next channel.
+// K codes are consumed without shifting them down: 4-bit codes as the masked
+// nibbles (w & 0x0F0F0F0F) and 16 x (w & 0xF0F0F0F0), 2-bit codes as
+// 4^s x ((w >> 2s) & 3) -- each "unit" (one scale) gets its own IMMA
+// accumulator and the exact sum is  sum_u acc_u >> (log2 scale_u).
+// Unit u, B register r (0: k-slots 4q+m, 1: k-slots 16+4q+m), slot m -> the
+// channel inside the lane quad's K region (layout.cuh: byte b of a token holds
+// channels b*8/bits ...), or -1 for a zero slot (d = 64, 2-bit).
 template <int HD, int BITS>
-TA_DEV constexpr int k_chan(int j, int m) {
-  return BITS == 4 ? 8 * j + 2 * m : 16 * (j >> 1) + 4 * m + 2 * (j & 1);
-}
+struct KUnits {
+  static constexpr int QB = HD * BITS / 32;             // bytes of a token's lane-quad region
+  static constexpr int NW = QB / 4;                     // 32-bit words per region
+  static constexpr int N = BITS == 4 ? NW : 4;          // units: 4-bit (word pair, lo/hi); 2-bit: s = 0..3
+  TA_DEV static constexpr int chan(int u, int r, int m) {
+    if (BITS == 4) {
+      const int pair = u >> 1, half = u & 1;
+      return 8 * (2 * pair + r) + 2 * m + half;
+    }
+    return (r == 1 && NW < 2) ? -1 : 16 * r + 4 * m + u;
+  }
+  TA_DEV static constexpr int shift(int u) { return BITS == 4 ? 4 * (u & 1) : 2 * u; }
+  TA_DEV static uint32_t mask(int u) { return BITS == 4 ? ((u & 1) ? 0xF0F0F0F0u : 0x0F0F0F0Fu) : (0x03030303u << (2 * u)); }
+  // word index (inside the region) feeding A register r of unit u
+  TA_DEV static constexpr int word(int u, int r) { return BITS == 4 ? 2 * (u >> 1) + r : r; }
+};
 
 // Thread <-> data maps.  Lane = 4 g + q.
 //   General path (G <= 8): rows 2q+e; score values t = 2 mt + h at token
@@ -134,32 +152,31 @@ struct Map {
 template <int HD, int BK, bool PACK>
 TA_DEV void qk_block(uint32_t rec, const int (&qv)[HD / 4], const uint4 (&q1r)[HD / 64], int (&sv)[Map<HD, PACK>::NT][2],
                      int g, int q) {
-  constexpr int R = HD / 4, KS = HD / 32;
+  using U = KUnits<HD, BK>;
+  constexpr int R = HD / 4;
   uint4 s4[HD / 64];
 #pragma unroll
   for (int i = 0; i < HD / 64; ++i) s4[i] = lds128(rec + q * R + 16 * i);
-  // B fragments from q1_c * s_c = 128 hi + lo.  Packed: column g < 4 holds hi of
-  // row g, column g >= 4 holds lo of row g - 4 (one MMA); general: two MMAs.
-  uint32_t bhi[KS][2], blo[KS][2];
+  // B fragments from q1_c * s_c = 128 hi + lo (hi in s8, lo in [0,127]).  Packed
+  // path: column g < 4 holds hi of row g, column g >= 4 holds lo of row g - 4
+  // (one IMMA); general path: separate hi and lo IMMAs.
+  const uint32_t sh = (PACK && g >= 4) ? 0u : 7u;
+  const uint32_t msk = (PACK && g >= 4) ? 0x7F7F7F7Fu : 0xFFFFFFFFu;
+  uint32_t bhi[U::N][2], blo[U::N][2];
 #pragma unroll
-  for (int j = 0; j < KS; ++j)
+  for (int u = 0; u < U::N; ++u)
 #pragma unroll
-    for (int h2 = 0; h2 < 2; ++h2) {
+    for (int r = 0; r < 2; ++r) {
       uint32_t ph[4], pl[4];
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
-        const int loc = k_chan<HD, BK>(j, m) + h2;
-        const int prod = qv[loc] * (int)byte_of(s4[loc >> 4], loc & 15);
-        ph[m] = (uint32_t)(prod >> 7);
+        const int loc = U::chan(u, r, m);
+        const int prod = loc < 0 ? 0 : qv[loc] * (int)byte_of(s4[loc >> 4], loc & 15);
+        ph[m] = PACK ? (uint32_t)(prod >> sh) : (uint32_t)(prod >> 7);
         pl[m] = (uint32_t)prod;
       }
-      if (PACK) {
-        const bool lo = g >= 4;
-        bhi[j][h2] = lo ? (pack4_lo(pl[0], pl[1], pl[2], pl[3]) & 0x7F7F7F7Fu) : pack4_lo(ph[0], ph[1], ph[2], ph[3]);
-      } else {
-        bhi[j][h2] = pack4_lo(ph[0], ph[1], ph[2], ph[3]);
-        blo[j][h2] = pack4_lo(pl[0], pl[1], pl[2], pl[3]) & 0x7F7F7F7Fu;
-      }
+      bhi[u][r] = pack4_lo(ph[0], ph[1], ph[2], ph[3]) & msk;
+      if (!PACK) blo[u][r] = pack4_lo(pl[0], pl[1], pl[2], pl[3]) & 0x7F7F7F7Fu;
     }
   // z term sum_c q1_c z_c of the lane-quad's row (dp4a, quad reduction).
   int zq = 0;
@@ -175,39 +192,38 @@ TA_DEV void qk_block(uint32_t rec, const int (&qv)[HD / 4], const uint4 (&q1r)[H
   zq += __shfl_xor_sync(0xffffffffu, zq, 2);
   const int rq = PACK ? (q & 1) : q;
   const int z0 = __shfl_sync(0xffffffffu, zq, 8 * rq), z1 = __shfl_sync(0xffffffffu, zq, 8 * rq + 4);
-  // A fragments: raw codes of tokens 16 mt + g (+8) over the quad's channel region.
-  constexpr int TB = HD * BK / 8, QB = TB / 4;
+  // A fragments: masked (unshifted) codes of tokens 16 mt + g (+8).
+  constexpr int TB = HD * BK / 8;
   const uint32_t codes = rec + 2 * HD;
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt) {
-    uint32_t w0[QB / 4], w1[QB / 4];
-    const uint32_t t0 = codes + (16 * mt + g) * TB + q * QB, t1 = t0 + 8 * TB;
+    uint32_t w0[U::NW], w1[U::NW];
+    const uint32_t t0 = codes + (16 * mt + g) * TB + q * U::QB, t1 = t0 + 8 * TB;
 #pragma unroll
-    for (int i = 0; i < QB / 4; ++i) {
+    for (int i = 0; i < U::NW; ++i) {
       w0[i] = lds32(t0 + 4 * i);
       w1[i] = lds32(t1 + 4 * i);
     }
     int ch[4] = {0, 0, 0, 0}, cl[4] = {0, 0, 0, 0};
 #pragma unroll
-    for (int j = 0; j < KS; ++j) {
+    for (int u = 0; u < U::N; ++u) {
+      int cu[4] = {0, 0, 0, 0}, cv[4] = {0, 0, 0, 0};
       uint32_t af[4];
-      if (BK == 4) {
-        af[0] = w0[j] & 0x0F0F0F0Fu;
-        af[1] = w1[j] & 0x0F0F0F0Fu;
-        af[2] = (w0[j] >> 4) & 0x0F0F0F0Fu;
-        af[3] = (w1[j] >> 4) & 0x0F0F0F0Fu;
-      } else {
-        const int sh = 4 * (j & 1);
-        af[0] = (w0[j >> 1] >> sh) & 0x03030303u;
-        af[1] = (w1[j >> 1] >> sh) & 0x03030303u;
-        af[2] = (w0[j >> 1] >> (sh + 2)) & 0x03030303u;
-        af[3] = (w1[j >> 1] >> (sh + 2)) & 0x03030303u;
-      }
-      const uint32_t bh[2] = {bhi[j][0], bhi[j][1]};
-      imma_u8s8(ch, af, bh);
+      const uint32_t mk = U::mask(u);
+      af[0] = w0[U::word(u, 0)] & mk;
+      af[1] = w1[U::word(u, 0)] & mk;
+      af[2] = U::chan(u, 1, 0) < 0 ? 0u : w0[U::word(u, 1) < U::NW ? U::word(u, 1) : 0] & mk;
+      af[3] = U::chan(u, 1, 0) < 0 ? 0u : w1[U::word(u, 1) < U::NW ? U::word(u, 1) : 0] & mk;
+      const uint32_t bh[2] = {bhi[u][0], bhi[u][1]};
+      imma_u8s8(cu, af, bh);
       if (!PACK) {
-        const uint32_t bl[2] = {blo[j][0], blo[j][1]};
-        imma_u8u8(cl, af, bl);
+        const uint32_t bl[2] = {blo[u][0], blo[u][1]};
+        imma_u8u8(cv, af, bl);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        ch[i] += cu[i] >> U::shift(u);  // exact: acc_u is a multiple of its scale
+        if (!PACK) cl[i] += cv[i] >> U::shift(u);
       }
     }
     if (PACK) {
@@ -356,12 +372,13 @@ TA_DEV void pv_block(uint32_t rec, const int8_t* vb, uint32_t pbuf, const int (&
         imma_s8u8(c, af, b2);
       } else {
         if (BV == 4) {
-          const uint32_t u0 = lds32(codes + c0 * CB + 4 * (4 * j + q));
-          const uint32_t u1 = lds32(codes + c1 * CB + 4 * (4 * j + q));
-          af[0] = u0 & 0x0F0F0F0Fu;
-          af[1] = u1 & 0x0F0F0F0Fu;
-          af[2] = (u0 >> 4) & 0x0F0F0F0Fu;
-          af[3] = (u1 >> 4) & 0x0F0F0F0Fu;
+          // unit j: j = 0 low nibbles (tokens 4q+e | 32+4q+e), j = 1 high nibbles x16
+          // (tokens 16+4q+e | 48+4q+e); word W = 4 j' + q holds both halves of k-step j'.
+          const uint32_t mk = j ? 0xF0F0F0F0u : 0x0F0F0F0Fu;
+          af[0] = lds32(codes + c0 * CB + 4 * q) & mk;
+          af[1] = lds32(codes + c1 * CB + 4 * q) & mk;
+          af[2] = lds32(codes + c0 * CB + 4 * (4 + q)) & mk;
+          af[3] = lds32(codes + c1 * CB + 4 * (4 + q)) & mk;
         } else {
           const uint32_t u0 = lds32(codes + c0 * CB + 4 * q);
           const uint32_t u1 = lds32(codes + c1 * CB + 4 * q);
@@ -371,8 +388,17 @@ TA_DEV void pv_block(uint32_t rec, const int8_t* vb, uint32_t pbuf, const int (&
           af[2] = (u0 >> (sh + 2)) & 0x03030303u;
           af[3] = (u1 >> (sh + 2)) & 0x03030303u;
         }
-        const uint32_t b2[2] = {bf[j][0], bf[j][1]};
-        imma_u8u8(c, af, b2);
+        if (BV == 4) {
+          // B rows of unit j: tokens (16 j + 4q..) and (32 + 16 j + 4q..)
+          const uint32_t b2[2] = {j ? bf[0][1] : bf[0][0], j ? bf[1][1] : bf[1][0]};
+          int cu[4] = {0, 0, 0, 0};
+          imma_u8u8(cu, af, b2);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) c[i] += cu[i] >> (4 * j);
+        } else {
+          const uint32_t b2[2] = {bf[j][0], bf[j][1]};
+          imma_u8u8(c, af, b2);
+        }
       }
     }
 #pragma unroll

@@ -1,0 +1,36 @@
+"""Sweep the split count of configs[2] / configs[4] decode (kernel time, GB/s)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2412_08585_b200 import binding as ta  # noqa: E402
+from paper_2412_08585_b200 import synth  # noqa: E402
+import bench  # noqa: E402
+
+for name, (B, N, Hq, Hkv, d), splits in (("cfg3", (64, 32768, 40, 10, 128), (4, 6, 8, 12, 16)),
+                                         ("cfg5", (16, 131072, 32, 8, 128), (8, 16, 24, 32, 48))):
+    bits = synth.head_bits_alternating(Hkv)
+    p = ta.params(head_dim=d)
+    cache = ta.KVCache(B, Hkv, d, max_blocks=N // 64 + 4, bits=bits)
+    _, k, v = synth.qkv_torch(3003, B, N, Hkv, Hkv, d)
+    ta.turbo_quantize_kv(p, cache, k, v)
+    del k, v
+    torch.cuda.empty_cache()
+    qd = synth.qkv_torch(7, B, 1, Hq, Hkv, d)[0][:, 0].contiguous()
+    byt = bench.decode_bytes(B, Hkv, d, N // 64, 0, bits, Hq)
+    for S in splits:
+        ws = torch.empty(max(ta.turbo_decode_workspace_bytes(B, Hq, d, S), 16), dtype=torch.uint8, device="cuda")
+        for _ in range(3):
+            ta.turbo_attention_decode(p, cache, qd, n_splits=S, workspace=ws)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(20):
+            ta.turbo_attention_decode(p, cache, qd, n_splits=S, workspace=ws)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 20
+        print(f"{name} S={S:3d} {ms * 1e3:8.1f} us  {byt / ms / 1e6:8.1f} GB/s", flush=True)
+    del cache
+    torch.cuda.empty_cache()
