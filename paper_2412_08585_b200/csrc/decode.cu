@@ -14,6 +14,7 @@
 //   PV[c]   = sum_t P_t (code_tc s_c + z_c) = s_c * sum_t P_t code_tc + z_c * sum_t P_t
 // with q1_c s_c = 128 hi + lo, hi in [-75, 74] (s8), lo in [0, 127] (u8), so the
 // tensor cores see only raw 4-bit / 2-bit codes.
+#include <algorithm>
 #include <climits>
 #include <cstring>
 
@@ -22,15 +23,25 @@
 
 namespace ta {
 
-constexpr int kWarpsPerCta = 4;
+constexpr int kWarpsPerCta = 5;
 
-template <int HD>
-struct DecodeWarpSmem {
-  uint8_t rec[2][2][rec_bytes(HD)];  // [stage][K,V][record]
-  int8_t q1[8][HD];
-  uint8_t p[8][kBc];
-  uint64_t bar[2];
+// Per-warp shared-memory region (runtime-sized): two stages of one K record
+// followed by the V record of the same (b, kv head, block) -- the stage holds
+// exactly this head's bytes, so mixed 4/2-bit plans need 2d+32d + 2d+16d --
+// then q^q1 rows [8][d], P codes [8][64] and two mbarriers.
+struct DecodeLayout {
+  uint32_t stage;   // bytes per stage (multiple of 128)
+  uint32_t q1, p, bar, size;
 };
+__host__ __device__ inline DecodeLayout decode_layout(int hd, uint32_t stage) {
+  DecodeLayout L;
+  L.stage = stage;
+  L.q1 = 2 * stage;
+  L.p = L.q1 + 8 * hd;
+  L.bar = L.p + 8 * kBc;
+  L.size = (L.bar + 16 + 127) & ~127u;
+  return L;
+}
 
 struct DecodeArgs {
   const __half* q;
@@ -44,6 +55,7 @@ struct DecodeArgs {
   float* lse_parts; // [S][B][Hq]
   __half* o16;      // final fp16 output when S == 1 (or NULL)
   int B, Hq, Hkv, G, max_blocks, blk_begin, blk_end, with_buffer, n_splits, alpha_mode;
+  uint32_t stage_bytes;
   float scale;
   SasConst sas;
   turbo_debug_tap_t tap;
@@ -420,11 +432,14 @@ TA_DEV void pv_block(uint32_t rec, const int8_t* vb, uint32_t pbuf, const int (&
 }
 
 template <int HD, bool PACK, bool TAP>
-__global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_constant__ DecodeArgs a) {
+__global__ void __launch_bounds__(32 * kWarpsPerCta, 3) decode_kernel(const __grid_constant__ DecodeArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   using M = Map<HD, PACK>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
-  DecodeWarpSmem<HD>& sm = reinterpret_cast<DecodeWarpSmem<HD>*>(smem_raw)[warp];
+  const DecodeLayout LY = decode_layout(HD, a.stage_bytes);
+  uint8_t* wbase = smem_raw + warp * LY.size;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wbase + LY.bar);
+  int8_t* q1p = reinterpret_cast<int8_t*>(wbase + LY.q1);
   const int task = blockIdx.x * kWarpsPerCta + warp;
   if (task >= a.B * a.Hkv * a.n_splits) return;
   const int split = task % a.n_splits, bh = task / a.n_splits, b = bh / a.Hkv, kvh = bh % a.Hkv;
@@ -440,19 +455,20 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
   const uint32_t bytesK = 2 * HD + kBc * HD * bitsK / 8, bytesV = 2 * HD + kBc * HD * bitsV / 8;
   const float lut_lane = sas_lut_lane(a.sas, lane);
   const int tap_row = TAP && split == 0 && a.tap.batch == b && a.tap.head / G == kvh ? a.tap.head % G : -1;
-  const uint32_t pbuf = smem_u32(&sm.p[0][0]), q1s = smem_u32(&sm.q1[0][0]);
+  const uint32_t pbuf = smem_u32(wbase + LY.p), q1s = smem_u32(q1p), stg0 = smem_u32(wbase);
 
   if (lane == 0) {
-    mbar_init(&sm.bar[0], 1);
-    mbar_init(&sm.bar[1], 1);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
     fence_barrier_init();
   }
   __syncwarp();
   auto issue = [&](int j, int stg) {
     if (lane == 0) {
-      mbar_expect_tx(&sm.bar[stg], bytesK + bytesV);
-      bulk_load(sm.rec[stg][0], a.block_rec + (slotK * a.max_blocks + j) * REC, bytesK, &sm.bar[stg]);
-      bulk_load(sm.rec[stg][1], a.block_rec + (slotV * a.max_blocks + j) * REC, bytesV, &sm.bar[stg]);
+      uint8_t* dst = wbase + stg * LY.stage;
+      mbar_expect_tx(&bar[stg], bytesK + bytesV);
+      bulk_load(dst, a.block_rec + (slotK * a.max_blocks + j) * REC, bytesK, &bar[stg]);
+      bulk_load(dst + bytesK, a.block_rec + (slotV * a.max_blocks + j) * REC, bytesV, &bar[stg]);
     }
   };
   if (j0 < j1) issue(j0, 0);
@@ -477,11 +493,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
     s_q_row = __fdiv_rn(qa, kDiv);
 #pragma unroll
     for (int i = 0; i < R; i += 4)
-      *reinterpret_cast<uint32_t*>(&sm.q1[g][q * R + i]) =
+      *reinterpret_cast<uint32_t*>(&q1p[g * HD + q * R + i]) =
           pack4_lo(rint_prod_bits(xv[i], inv), rint_prod_bits(xv[i + 1], inv), rint_prod_bits(xv[i + 2], inv),
                    rint_prod_bits(xv[i + 3], inv));
     if (TAP && g == tap_row) {
-      for (int i = 0; i < R; ++i) a.tap.q1[q * R + i] = sm.q1[g][q * R + i];
+      for (int i = 0; i < R; ++i) a.tap.q1[q * R + i] = q1p[g * HD + q * R + i];
       if (q == 0) a.tap.s_q[0] = s_q_row;
     }
   }
@@ -518,8 +534,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
 
   for (int j = j0; j < j1; ++j) {
     const int stg = (j - j0) & 1;
-    mbar_wait(&sm.bar[stg], ((j - j0) >> 1) & 1);
-    const uint32_t recK = smem_u32(sm.rec[stg][0]), recV = smem_u32(sm.rec[stg][1]);
+    mbar_wait(&bar[stg], ((j - j0) >> 1) & 1);
+    const uint32_t recK = stg0 + stg * LY.stage, recV = recK + bytesK;
     int sv[M::NT][2];
     if (bitsK == 4) qk_block<HD, 4, PACK>(recK, qv, q1r, sv, g, q);
     else qk_block<HD, 2, PACK>(recK, qv, q1r, sv, g, q);
@@ -647,12 +663,16 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
     a.lse_parts = a.o_parts + (size_t)S * B * Hq * HD;
     a.o16 = nullptr;
   }
+  uint32_t stage = 0;
+  for (int h = 0; h < H; ++h)
+    stage = std::max<uint32_t>(stage, 4 * HD + kBc * HD * (c->bits_host[2 * h] + c->bits_host[2 * h + 1]) / 8);
+  a.stage_bytes = (stage + 127) & ~127u;
   const int tasks = B * H * S;
   const dim3 grid((tasks + kWarpsPerCta - 1) / kWarpsPerCta);
   const bool pack = a.G <= 4;
 #define TA_DEC(HDV, PK, TP)                                                                             \
   {                                                                                                     \
-    const size_t smem = sizeof(DecodeWarpSmem<HDV>) * kWarpsPerCta;                                     \
+    const size_t smem = (size_t)decode_layout(HDV, a.stage_bytes).size * kWarpsPerCta;                 \
     cudaFuncSetAttribute(decode_kernel<HDV, PK, TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     decode_kernel<HDV, PK, TP><<<grid, 32 * kWarpsPerCta, smem, st>>>(a);                              \
   }
