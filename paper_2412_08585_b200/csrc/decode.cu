@@ -23,7 +23,7 @@
 
 namespace ta {
 
-constexpr int kWarpsPerCta = 5;
+constexpr int kWarpsPerCta = 4;
 
 // Per-warp shared-memory region (runtime-sized): two stages of one K record
 // followed by the V record of the same (b, kv head, block) -- the stage holds
@@ -216,10 +216,16 @@ TA_DEV void qk_block(uint32_t rec, const int (&qv)[HD / 4], const uint4 (&q1r)[H
       w0[i] = lds32(t0 + 4 * i);
       w1[i] = lds32(t1 + 4 * i);
     }
-    int ch[4] = {0, 0, 0, 0}, cl[4] = {0, 0, 0, 0};
+    // one IMMA accumulator per scale class (4-bit: lo / hi nibbles; 2-bit: s = 0..3)
+    constexpr int NCLS = BK == 4 ? 2 : 4;
+    int ah[NCLS][4], al[NCLS][4];
+#pragma unroll
+    for (int k = 0; k < NCLS; ++k)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) ah[k][i] = al[k][i] = 0;
 #pragma unroll
     for (int u = 0; u < U::N; ++u) {
-      int cu[4] = {0, 0, 0, 0}, cv[4] = {0, 0, 0, 0};
+      const int cls = BK == 4 ? (u & 1) : u;
       uint32_t af[4];
       const uint32_t mk = U::mask(u);
       af[0] = w0[U::word(u, 0)] & mk;
@@ -227,15 +233,21 @@ TA_DEV void qk_block(uint32_t rec, const int (&qv)[HD / 4], const uint4 (&q1r)[H
       af[2] = U::chan(u, 1, 0) < 0 ? 0u : w0[U::word(u, 1) < U::NW ? U::word(u, 1) : 0] & mk;
       af[3] = U::chan(u, 1, 0) < 0 ? 0u : w1[U::word(u, 1) < U::NW ? U::word(u, 1) : 0] & mk;
       const uint32_t bh[2] = {bhi[u][0], bhi[u][1]};
-      imma_u8s8(cu, af, bh);
+      imma_u8s8(ah[cls], af, bh);
       if (!PACK) {
         const uint32_t bl[2] = {blo[u][0], blo[u][1]};
-        imma_u8u8(cv, af, bl);
+        imma_u8u8(al[cls], af, bl);
       }
+    }
+    int ch[4], cl[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        ch[i] += cu[i] >> U::shift(u);  // exact: acc_u is a multiple of its scale
-        if (!PACK) cl[i] += cv[i] >> U::shift(u);
+    for (int i = 0; i < 4; ++i) {
+      ch[i] = ah[0][i];
+      cl[i] = al[0][i];
+#pragma unroll
+      for (int k = 1; k < NCLS; ++k) {  // exact: class k accumulates multiples of its scale
+        ch[i] += ah[k][i] >> U::shift(BK == 4 ? k : k);
+        if (!PACK) cl[i] += al[k][i] >> U::shift(BK == 4 ? k : k);
       }
     }
     if (PACK) {
@@ -297,7 +309,7 @@ struct RowState {
 
 // One tile of Alg. 2 on the thread's score values: running max,
 // alpha, SAS, row sum, per-row P scale and codes (to smem rows).
-template <int HD, bool PACK, bool TAP>
+template <int HD, bool PACK, bool TAP, bool FULL>
 TA_DEV void softmax_tile(const DecodeArgs& a, RowState<HD, PACK>& st, int (&sv)[Map<HD, PACK>::NT][2], int nvalid,
                          const float (&cqk)[2], uint32_t pbuf, float lut_lane, float (&alpha)[2], float (&s_p)[2],
                          int (&sum_p)[2], bool tap, int tap_row, int g, int q) {
@@ -308,7 +320,7 @@ TA_DEV void softmax_tile(const DecodeArgs& a, RowState<HD, PACK>& st, int (&sv)[
     int smax = INT_MIN;
 #pragma unroll
     for (int t = 0; t < M::NT; ++t)
-      if (M::tok(t, g, q) < nvalid) smax = max(smax, sv[t][e]);
+      if (FULL || M::tok(t, g, q) < nvalid) smax = max(smax, sv[t][e]);
     smax = grp_maxi<PACK>(smax);
     const float m_prev = st.m[e];
     const float m_new = fmaxf(m_prev, __fmul_rn((float)smax, cqk[e]));
@@ -320,7 +332,7 @@ TA_DEV void softmax_tile(const DecodeArgs& a, RowState<HD, PACK>& st, int (&sv)[
     for (int t = 0; t < M::NT; ++t) {
       const float x = __fmul_rn((float)sv[t][e], cqk[e]);
       float p = sas_eval(__fsub_rn(m_new, x), lut_lane, a.sas.nr_abs);
-      p = M::tok(t, g, q) < nvalid ? p : 0.f;
+      if (!FULL) p = M::tok(t, g, q) < nvalid ? p : 0.f;
       pt[t] = p;
       rs += p;
       pm = fmaxf(pm, p);
@@ -432,7 +444,7 @@ TA_DEV void pv_block(uint32_t rec, const int8_t* vb, uint32_t pbuf, const int (&
 }
 
 template <int HD, bool PACK, bool TAP>
-__global__ void __launch_bounds__(32 * kWarpsPerCta, 3) decode_kernel(const __grid_constant__ DecodeArgs a) {
+__global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_constant__ DecodeArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   using M = Map<HD, PACK>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
@@ -544,7 +556,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 3) decode_kernel(const __gr
     const bool tap = TAP && tap_row >= 0 && a.tap.j_block == j;
     float alpha[2], s_p[2];
     int sum_p[2];
-    softmax_tile<HD, PACK, TAP>(a, st, sv, kBc, cqk, pbuf, lut_lane, alpha, s_p, sum_p, tap, tap_row, g, q);
+    softmax_tile<HD, PACK, TAP, true>(a, st, sv, kBc, cqk, pbuf, lut_lane, alpha, s_p, sum_p, tap, tap_row, g, q);
     int acc[M::NC][2];
     if (bitsV == 4) pv_block<HD, 4, PACK, false>(recV, nullptr, pbuf, sum_p, acc, g, q);
     else pv_block<HD, 2, PACK, false>(recV, nullptr, pbuf, sum_p, acc, g, q);
@@ -565,7 +577,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 3) decode_kernel(const __gr
     const bool tap = TAP && tap_row >= 0 && a.tap.j_block == -1;
     float alpha[2], s_p[2];
     int sum_p[2];
-    softmax_tile<HD, PACK, TAP>(a, st, sv, nbuf, cqk, pbuf, lut_lane, alpha, s_p, sum_p, tap, tap_row, g, q);
+    softmax_tile<HD, PACK, TAP, false>(a, st, sv, nbuf, cqk, pbuf, lut_lane, alpha, s_p, sum_p, tap, tap_row, g, q);
     int acc[M::NC][2];
     pv_block<HD, 4, PACK, true>(0, vb, pbuf, sum_p, acc, g, q);
     const float cpv[2] = {__fmul_rn(s_p[0], sV), __fmul_rn(s_p[1], sV)};
