@@ -14,7 +14,7 @@ import os
 import torch
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libturboattn.so")
+LIB_PATH = os.environ.get("TURBO_LIB", os.path.join(PKG, "libturboattn.so"))
 
 TURBO_OK, TURBO_ERR_INVALID_ARG, TURBO_ERR_UNSUPPORTED, TURBO_ERR_CAPACITY, TURBO_ERR_CUDA = range(5)
 _ERR = {1: "TURBO_ERR_INVALID_ARG", 2: "TURBO_ERR_UNSUPPORTED", 3: "TURBO_ERR_CAPACITY", 4: "TURBO_ERR_CUDA"}

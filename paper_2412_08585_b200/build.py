@@ -28,16 +28,25 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, csrc: str = None, out: str = None) -> str:
+    """Compile csrc/*.cu into `out` (default: the in-tree libturboattn.so).
+    `csrc`/`out` let tools/ build A/B variants of the sources side by side."""
+    if csrc is not None or out is not None:
+        return _build(csrc or CSRC, out or LIB, verbose)
     if not force and not _stale():
         return LIB
-    objdir = os.path.join(PKG, "_obj")
+    return _build(CSRC, LIB, verbose)
+
+
+def _build(csrc: str, lib: str, verbose: bool) -> str:
+    objdir = os.path.join(PKG, "_obj", os.path.basename(lib).replace(".so", ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        flags = [f if f != CSRC else csrc for f in FLAGS]
+        cmd = [NVCC, *ARCH, *flags, "-c", os.path.join(csrc, src), "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
             print(" ".join(cmd), flush=True)
@@ -52,10 +61,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
             failed = True
     if failed:
         raise RuntimeError("nvcc failed")
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

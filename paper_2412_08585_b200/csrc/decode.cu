@@ -14,7 +14,6 @@
 //   PV[c]   = sum_t P_t (code_tc s_c + z_c) = s_c * sum_t P_t code_tc + z_c * sum_t P_t
 // with q1_c s_c = 128 hi + lo, hi in [-75, 74] (s8), lo in [0, 127] (u8), so the
 // tensor cores see only raw 4-bit / 2-bit codes.
-#include <algorithm>
 #include <climits>
 #include <cstring>
 
@@ -25,23 +24,13 @@ namespace ta {
 
 constexpr int kWarpsPerCta = 4;
 
-// Per-warp shared-memory region (runtime-sized): two stages of one K record
-// followed by the V record of the same (b, kv head, block) -- the stage holds
-// exactly this head's bytes, so mixed 4/2-bit plans need 2d+32d + 2d+16d --
-// then q^q1 rows [8][d], P codes [8][64] and two mbarriers.
-struct DecodeLayout {
-  uint32_t stage;   // bytes per stage (multiple of 128)
-  uint32_t q1, p, bar, size;
+template <int HD>
+struct DecodeWarpSmem {
+  uint8_t rec[2][2][rec_bytes(HD)];  // [stage][K,V][record]
+  int8_t q1[8][HD];
+  uint8_t p[8][kBc];
+  uint64_t bar[2];
 };
-__host__ __device__ inline DecodeLayout decode_layout(int hd, uint32_t stage) {
-  DecodeLayout L;
-  L.stage = stage;
-  L.q1 = 2 * stage;
-  L.p = L.q1 + 8 * hd;
-  L.bar = L.p + 8 * kBc;
-  L.size = (L.bar + 16 + 127) & ~127u;
-  return L;
-}
 
 struct DecodeArgs {
   const __half* q;
@@ -55,7 +44,6 @@ struct DecodeArgs {
   float* lse_parts; // [S][B][Hq]
   __half* o16;      // final fp16 output when S == 1 (or NULL)
   int B, Hq, Hkv, G, max_blocks, blk_begin, blk_end, with_buffer, n_splits, alpha_mode;
-  uint32_t stage_bytes;
   float scale;
   SasConst sas;
   turbo_debug_tap_t tap;
@@ -216,16 +204,10 @@ TA_DEV void qk_block(uint32_t rec, const int (&qv)[HD / 4], const uint4 (&q1r)[H
       w0[i] = lds32(t0 + 4 * i);
       w1[i] = lds32(t1 + 4 * i);
     }
-    // one IMMA accumulator per scale class (4-bit: lo / hi nibbles; 2-bit: s = 0..3)
-    constexpr int NCLS = BK == 4 ? 2 : 4;
-    int ah[NCLS][4], al[NCLS][4];
-#pragma unroll
-    for (int k = 0; k < NCLS; ++k)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) ah[k][i] = al[k][i] = 0;
+    int ch[4] = {0, 0, 0, 0}, cl[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int u = 0; u < U::N; ++u) {
-      const int cls = BK == 4 ? (u & 1) : u;
+      int cu[4] = {0, 0, 0, 0}, cv[4] = {0, 0, 0, 0};
       uint32_t af[4];
       const uint32_t mk = U::mask(u);
       af[0] = w0[U::word(u, 0)] & mk;
@@ -233,21 +215,15 @@ TA_DEV void qk_block(uint32_t rec, const int (&qv)[HD / 4], const uint4 (&q1r)[H
       af[2] = U::chan(u, 1, 0) < 0 ? 0u : w0[U::word(u, 1) < U::NW ? U::word(u, 1) : 0] & mk;
       af[3] = U::chan(u, 1, 0) < 0 ? 0u : w1[U::word(u, 1) < U::NW ? U::word(u, 1) : 0] & mk;
       const uint32_t bh[2] = {bhi[u][0], bhi[u][1]};
-      imma_u8s8(ah[cls], af, bh);
+      imma_u8s8(cu, af, bh);
       if (!PACK) {
         const uint32_t bl[2] = {blo[u][0], blo[u][1]};
-        imma_u8u8(al[cls], af, bl);
+        imma_u8u8(cv, af, bl);
       }
-    }
-    int ch[4], cl[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      ch[i] = ah[0][i];
-      cl[i] = al[0][i];
-#pragma unroll
-      for (int k = 1; k < NCLS; ++k) {  // exact: class k accumulates multiples of its scale
-        ch[i] += ah[k][i] >> U::shift(BK == 4 ? k : k);
-        if (!PACK) cl[i] += al[k][i] >> U::shift(BK == 4 ? k : k);
+      for (int i = 0; i < 4; ++i) {
+        ch[i] += cu[i] >> U::shift(u);  // exact: acc_u is a multiple of its scale
+        if (!PACK) cl[i] += cv[i] >> U::shift(u);
       }
     }
     if (PACK) {
@@ -448,10 +424,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
   extern __shared__ __align__(128) uint8_t smem_raw[];
   using M = Map<HD, PACK>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
-  const DecodeLayout LY = decode_layout(HD, a.stage_bytes);
-  uint8_t* wbase = smem_raw + warp * LY.size;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(wbase + LY.bar);
-  int8_t* q1p = reinterpret_cast<int8_t*>(wbase + LY.q1);
+  DecodeWarpSmem<HD>& sm = reinterpret_cast<DecodeWarpSmem<HD>*>(smem_raw)[warp];
   const int task = blockIdx.x * kWarpsPerCta + warp;
   if (task >= a.B * a.Hkv * a.n_splits) return;
   const int split = task % a.n_splits, bh = task / a.n_splits, b = bh / a.Hkv, kvh = bh % a.Hkv;
@@ -467,20 +440,19 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
   const uint32_t bytesK = 2 * HD + kBc * HD * bitsK / 8, bytesV = 2 * HD + kBc * HD * bitsV / 8;
   const float lut_lane = sas_lut_lane(a.sas, lane);
   const int tap_row = TAP && split == 0 && a.tap.batch == b && a.tap.head / G == kvh ? a.tap.head % G : -1;
-  const uint32_t pbuf = smem_u32(wbase + LY.p), q1s = smem_u32(q1p), stg0 = smem_u32(wbase);
+  const uint32_t pbuf = smem_u32(&sm.p[0][0]), q1s = smem_u32(&sm.q1[0][0]);
 
   if (lane == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    mbar_init(&sm.bar[0], 1);
+    mbar_init(&sm.bar[1], 1);
     fence_barrier_init();
   }
   __syncwarp();
   auto issue = [&](int j, int stg) {
     if (lane == 0) {
-      uint8_t* dst = wbase + stg * LY.stage;
-      mbar_expect_tx(&bar[stg], bytesK + bytesV);
-      bulk_load(dst, a.block_rec + (slotK * a.max_blocks + j) * REC, bytesK, &bar[stg]);
-      bulk_load(dst + bytesK, a.block_rec + (slotV * a.max_blocks + j) * REC, bytesV, &bar[stg]);
+      mbar_expect_tx(&sm.bar[stg], bytesK + bytesV);
+      bulk_load(sm.rec[stg][0], a.block_rec + (slotK * a.max_blocks + j) * REC, bytesK, &sm.bar[stg]);
+      bulk_load(sm.rec[stg][1], a.block_rec + (slotV * a.max_blocks + j) * REC, bytesV, &sm.bar[stg]);
     }
   };
   if (j0 < j1) issue(j0, 0);
@@ -505,11 +477,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
     s_q_row = __fdiv_rn(qa, kDiv);
 #pragma unroll
     for (int i = 0; i < R; i += 4)
-      *reinterpret_cast<uint32_t*>(&q1p[g * HD + q * R + i]) =
+      *reinterpret_cast<uint32_t*>(&sm.q1[g][q * R + i]) =
           pack4_lo(rint_prod_bits(xv[i], inv), rint_prod_bits(xv[i + 1], inv), rint_prod_bits(xv[i + 2], inv),
                    rint_prod_bits(xv[i + 3], inv));
     if (TAP && g == tap_row) {
-      for (int i = 0; i < R; ++i) a.tap.q1[q * R + i] = q1p[g * HD + q * R + i];
+      for (int i = 0; i < R; ++i) a.tap.q1[q * R + i] = sm.q1[g][q * R + i];
       if (q == 0) a.tap.s_q[0] = s_q_row;
     }
   }
@@ -546,8 +518,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
 
   for (int j = j0; j < j1; ++j) {
     const int stg = (j - j0) & 1;
-    mbar_wait(&bar[stg], ((j - j0) >> 1) & 1);
-    const uint32_t recK = stg0 + stg * LY.stage, recV = recK + bytesK;
+    mbar_wait(&sm.bar[stg], ((j - j0) >> 1) & 1);
+    const uint32_t recK = smem_u32(sm.rec[stg][0]), recV = smem_u32(sm.rec[stg][1]);
     int sv[M::NT][2];
     if (bitsK == 4) qk_block<HD, 4, PACK>(recK, qv, q1r, sv, g, q);
     else qk_block<HD, 2, PACK>(recK, qv, q1r, sv, g, q);
@@ -675,16 +647,12 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
     a.lse_parts = a.o_parts + (size_t)S * B * Hq * HD;
     a.o16 = nullptr;
   }
-  uint32_t stage = 0;
-  for (int h = 0; h < H; ++h)
-    stage = std::max<uint32_t>(stage, 4 * HD + kBc * HD * (c->bits_host[2 * h] + c->bits_host[2 * h + 1]) / 8);
-  a.stage_bytes = (stage + 127) & ~127u;
   const int tasks = B * H * S;
   const dim3 grid((tasks + kWarpsPerCta - 1) / kWarpsPerCta);
   const bool pack = a.G <= 4;
 #define TA_DEC(HDV, PK, TP)                                                                             \
   {                                                                                                     \
-    const size_t smem = (size_t)decode_layout(HDV, a.stage_bytes).size * kWarpsPerCta;                 \
+    const size_t smem = sizeof(DecodeWarpSmem<HDV>) * kWarpsPerCta;                                     \
     cudaFuncSetAttribute(decode_kernel<HDV, PK, TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     decode_kernel<HDV, PK, TP><<<grid, 32 * kWarpsPerCta, smem, st>>>(a);                              \
   }
