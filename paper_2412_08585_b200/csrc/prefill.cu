@@ -33,6 +33,7 @@ struct PrefillSmem {
   int8_t p[NS][2][kTileM * kBc];    // Q(P~) [128][64], SW64
   uint64_t kv_full[kStages], kv_empty[kStages];
   uint64_t s_full[NS][2], s_free[NS][2], p_full[NS][2], pv_full[NS], pv_free[NS], q_ready;
+  uint64_t pmax_bar[NS][2];  // per P-scale group: arrivals of its warps' partial max
   uint32_t tmem_base;
   float red_a[NS][4];
   float red_p[NS][2][4];
@@ -105,6 +106,7 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
       }
       mbar_init(&sm.pv_full[t], 1);
       mbar_init(&sm.pv_free[t], 128);
+      for (int g2 = 0; g2 < 2; ++g2) mbar_init(&sm.pmax_bar[t][g2], args.block_q / 32);
     }
     mbar_init(&sm.q_ready, 128 * NS);
     fence_barrier_init();
@@ -186,6 +188,7 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
     const int qd = warp & 3, r = qd * 32 + lane, row = it * kTileM + r;
     const bool row_ok = row < N;
     const int half = args.block_q == 64 ? (r >> 6) : 0;
+    const int grp = half;  // P-scale group (B_r rows)
     const uint32_t tbase = tmem + ((uint32_t)(qd * 32) << 16) + slot * 256;
     const float lut_lane = sas_lut_lane(args.sas, lane);
     const float nr_abs = args.sas.nr_abs;
@@ -320,11 +323,40 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
           l = alpha * l + rsum;  // l = SAS(m_prev - m_new) l + rowsum(P~)
           m = m_new;
         }
-        // P scale over the B_r x B_c tile
+        // P scale over the B_r x B_c tile: publish this warp's max
+        // now, pick the group max up after the previous tile's O update.
         pmax = warp_max(pmax);
-        if (lane == 0) red_p[sb * 4 + qd] = pmax;
+        if (lane == 0) {
+          red_p[sb * 4 + qd] = pmax;
+          mbar_arrive(&sm.pmax_bar[slot][grp]);
+        }
+        alpha_j = alpha;
+        active_j = active;
+      }
+      // O += (s_P s_V / A) Q(P~) V^q1 for the previous tile (P:920-921)
+      if (j >= 1) {
+        mbar_wait(&sm.pv_full[slot], (j - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int cc = 0; cc < HD / 16; ++cc) {
+          uint32_t pv[16];
+          TA_TMEM_LD16(tbase + 2 * kBc + cc * 16, pv);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) O[cc * 16 + e] = __fmaf_rn(cpv_p, (float)(int)pv[e], O[cc * 16 + e]);
+          if (tap_p) {
+            for (int e = 0; e < 16; ++e) args.tap.pv_int[(r & 63) * HD + cc * 16 + e] = (int)pv[e];
+          }
+        }
+        tc_fence_before();
+        if (j < nkv) mbar_arrive(&sm.pv_free[slot]);
+      }
+      if (j < nkv) {
+        const int sb = j & 1;
+        const uint32_t tS = tbase + sb * kBc;
+        constexpr int CW = 16;
         tmem_st_wait();
-        named_bar_sync(bar_id, 128);
+        mbar_wait(&sm.pmax_bar[slot][grp], j & 1);
         const float a_p = args.block_q == 64 ? fmaxf(red_p[sb * 4 + 2 * half], red_p[sb * 4 + 2 * half + 1])
                                              : fmaxf(fmaxf(red_p[sb * 4], red_p[sb * 4 + 1]),
                                                      fmaxf(red_p[sb * 4 + 2], red_p[sb * 4 + 3]));
@@ -356,27 +388,7 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
         }
         fence_proxy_async();
         mbar_arrive(&sm.p_full[slot][sb]);
-        alpha_j = alpha;
         sp_j = s_p;
-        active_j = active;
-      }
-      // O += (s_P s_V / A) Q(P~) V^q1 for the previous tile (P:920-921)
-      if (j >= 1) {
-        mbar_wait(&sm.pv_full[slot], (j - 1) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int cc = 0; cc < HD / 16; ++cc) {
-          uint32_t pv[16];
-          TA_TMEM_LD16(tbase + 2 * kBc + cc * 16, pv);
-          tmem_ld_wait();
-#pragma unroll
-          for (int e = 0; e < 16; ++e) O[cc * 16 + e] = __fmaf_rn(cpv_p, (float)(int)pv[e], O[cc * 16 + e]);
-          if (tap_p) {
-            for (int e = 0; e < 16; ++e) args.tap.pv_int[(r & 63) * HD + cc * 16 + e] = (int)pv[e];
-          }
-        }
-        tc_fence_before();
-        if (j < nkv) mbar_arrive(&sm.pv_free[slot]);
       }
       // Scaled-O bookkeeping, after PV(j-1) has landed in Ohat: O_true = A * Ohat,
       // tile j's alpha multiplies everything accumulated so far; fold A
