@@ -185,6 +185,20 @@ TURBO_API turbo_status_t turbo_combine_lse(int32_t n_parts, int32_t rows, int32_
                                  const float* lse_parts, void* o, float* o_f32, float* lse,
                                  turbo_stream_t stream);
 
+/* Head-wise mixed precision planner (Sec. 3.2; R-8).
+ * turbo_head_priority: for every slot (kv_head h, kind K=0 / V=1) over all
+ *   B x N prefill tokens of k, v (FP16 [B][N][Hkv][d]):
+ *   priority[h][kind] = (max_c max_t x - min_c min_t x) * std_c(max_t x_c - min_t x_c)
+ *   (population std over the d channel gaps), written as f64 to device memory.
+ *   workspace: device, >= turbo_priority_workspace_bytes(Hkv, d).
+ * turbo_plan_bits (HOST): the n_2bit lowest-priority slots get 2 bits, the
+ *   others 4; ties go to the lower slot index (slot = 2 h + kind). */
+TURBO_API size_t turbo_priority_workspace_bytes(int32_t n_kv_heads, int32_t head_dim);
+TURBO_API turbo_status_t turbo_head_priority(int32_t B, int32_t N, int32_t Hkv, int32_t head_dim, const void* k,
+                                             const void* v, void* workspace, size_t workspace_bytes,
+                                             double* priority, turbo_stream_t stream);
+TURBO_API turbo_status_t turbo_plan_bits(const double* priority, int32_t n_slots, int32_t n_2bit, int32_t* bits);
+
 #ifdef __cplusplus
 }
 #endif

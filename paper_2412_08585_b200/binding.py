@@ -20,7 +20,8 @@ TURBO_OK, TURBO_ERR_INVALID_ARG, TURBO_ERR_UNSUPPORTED, TURBO_ERR_CAPACITY, TURB
 _ERR = {1: "TURBO_ERR_INVALID_ARG", 2: "TURBO_ERR_UNSUPPORTED", 3: "TURBO_ERR_CAPACITY", 4: "TURBO_ERR_CUDA"}
 
 EXPORTS = ("turbo_version", "turbo_cache_sizes", "turbo_quantize_kv", "turbo_attention_prefill",
-           "turbo_decode_workspace_bytes", "turbo_attention_decode", "turbo_combine_lse")
+           "turbo_decode_workspace_bytes", "turbo_attention_decode", "turbo_combine_lse",
+           "turbo_priority_workspace_bytes", "turbo_head_priority", "turbo_plan_bits")
 
 
 class TurboError(RuntimeError):
@@ -69,8 +70,12 @@ def lib() -> C.CDLL:
         L.turbo_attention_decode.argtypes = [C.POINTER(TurboParams), C.POINTER(TurboKVCache), i32, vp, i32, i32, i32,
                                              i32, vp, sz, vp, vp, vp, vp]
         L.turbo_combine_lse.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp, vp]
+        L.turbo_priority_workspace_bytes.argtypes = [i32, i32]
+        L.turbo_priority_workspace_bytes.restype = sz
+        L.turbo_head_priority.argtypes = [i32, i32, i32, i32, vp, vp, vp, sz, vp, vp]
+        L.turbo_plan_bits.argtypes = [vp, i32, i32, vp]
         for name in ("turbo_cache_sizes", "turbo_quantize_kv", "turbo_attention_prefill", "turbo_attention_decode",
-                     "turbo_combine_lse"):
+                     "turbo_combine_lse", "turbo_head_priority", "turbo_plan_bits"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -238,3 +243,24 @@ class DebugTap:
         self.pv_int = z(rows, head_dim, dt=torch.int32)
         self.c = TurboDebugTap(batch, head, i_block, j_block, *[t.data_ptr() for t in (
             self.q1, self.s_q, self.s_int, self.m_new, self.p_codes, self.s_p, self.pv_int)])
+
+
+def turbo_head_priority(k, v, stream=None):
+    """Per (kv_head, K/V) slot priority over the prefill K, V fp16 [B,N,Hkv,d]
+     -> f64 tensor [Hkv, 2] on the device."""
+    assert k.dtype == torch.float16 and k.is_contiguous() and v.is_contiguous()
+    B, N, H, d = k.shape
+    ws = torch.empty(lib().turbo_priority_workspace_bytes(H, d), dtype=torch.uint8, device=k.device)
+    pr = torch.empty((H, 2), dtype=torch.float64, device=k.device)
+    _check("turbo_head_priority", lib().turbo_head_priority(B, N, H, d, _ptr(k), _ptr(v), _ptr(ws), ws.numel(),
+                                                            _ptr(pr), _stream(stream)))
+    return pr
+
+
+def turbo_plan_bits(priority, n_2bit):
+    """Host ranking: the n_2bit lowest-priority slots get 2 bits.
+    priority: [Hkv, 2] (any device) -> int32 [Hkv, 2] host tensor."""
+    pr = priority.detach().to("cpu", torch.float64).contiguous()
+    bits = torch.empty(pr.shape, dtype=torch.int32)
+    _check("turbo_plan_bits", lib().turbo_plan_bits(_ptr(pr), pr.numel(), n_2bit, _ptr(bits)))
+    return bits

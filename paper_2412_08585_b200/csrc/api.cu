@@ -21,6 +21,11 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
 cudaError_t launch_combine(int n_parts, int rows, int d, const float* o_parts, const float* lse_parts, __half* o,
                            float* o32, float* lse, cudaStream_t st);
 
+size_t priority_workspace(int Hkv, int HD);
+cudaError_t launch_priority(int B, int N, int Hkv, int HD, const __half* k, const __half* v, void* ws,
+                            double* priority, cudaStream_t st);
+void plan_bits(const double* priority, int n_slots, int n_2bit, int32_t* bits);
+
 // SAS threshold |n_r|; the LUT itself is ta::kExpNegBits.
 void fill_sas_const(ta::SasConst* sc, int32_t nr) {
   sc->nr_abs = (float)(-nr);
@@ -148,6 +153,27 @@ turbo_status_t turbo_combine_lse(int32_t n_parts, int32_t rows, int32_t d, const
     return TURBO_ERR_INVALID_ARG;
   return cuda_status(ta_host::launch_combine(n_parts, rows, d, o_parts, lse_parts, reinterpret_cast<__half*>(o), o_f32,
                                              lse, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+size_t turbo_priority_workspace_bytes(int32_t n_kv_heads, int32_t head_dim) {
+  if (n_kv_heads < 1 || (head_dim != 64 && head_dim != 128)) return 0;
+  return ta_host::priority_workspace(n_kv_heads, head_dim);
+}
+
+turbo_status_t turbo_head_priority(int32_t B, int32_t N, int32_t Hkv, int32_t head_dim, const void* k, const void* v,
+                                   void* workspace, size_t workspace_bytes, double* priority, turbo_stream_t stream) {
+  if (B < 1 || N < 1 || Hkv < 1 || !k || !v || !workspace || !priority) return TURBO_ERR_INVALID_ARG;
+  if (head_dim != 64 && head_dim != 128) return TURBO_ERR_UNSUPPORTED;
+  if (workspace_bytes < ta_host::priority_workspace(Hkv, head_dim)) return TURBO_ERR_INVALID_ARG;
+  return cuda_status(ta_host::launch_priority(B, N, Hkv, head_dim, reinterpret_cast<const __half*>(k),
+                                              reinterpret_cast<const __half*>(v), workspace, priority,
+                                              reinterpret_cast<cudaStream_t>(stream)));
+}
+
+turbo_status_t turbo_plan_bits(const double* priority, int32_t n_slots, int32_t n_2bit, int32_t* bits) {
+  if (!priority || !bits || n_slots < 1 || n_2bit < 0 || n_2bit > n_slots) return TURBO_ERR_INVALID_ARG;
+  ta_host::plan_bits(priority, n_slots, n_2bit, bits);
+  return TURBO_OK;
 }
 
 }  // extern "C"

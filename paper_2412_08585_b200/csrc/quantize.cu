@@ -22,10 +22,15 @@ TA_DEV void stage2_column(int8_t* tile, int ld, int c, int bits, uint8_t* s_out,
   const int levels = (1 << bits) - 1;
   int s = (mx - mn + levels - 1) / levels;
   s = max(s, 1);
+  // code = floor((2 (v - z) + s) / (2 s)) without an integer divide:
+  // fl(a * fl(1/(2s)) + 2^-10) truncated is exact for a <= 2*238+80, s <= 80
+  // (exhaustively verified, tests/test_quant_arith.py).
+  const float inv2s = __fdiv_rn(1.0f, (float)(2 * s));
 #pragma unroll 8
   for (int t = 0; t < kBc; ++t) {
-    int v = tile[t * ld + c];
-    tile[t * ld + c] = (int8_t)(uint8_t)((2 * (v - mn) + s) / (2 * s));
+    const int v = tile[t * ld + c];
+    const int code = __float2int_rz(__fmaf_rn((float)(2 * (v - mn) + s), inv2s, 0.0009765625f));
+    tile[t * ld + c] = (int8_t)(uint8_t)code;
   }
   *s_out = (uint8_t)s;
   *z_out = (int8_t)mn;

@@ -90,3 +90,17 @@ def test_sass_uses_tcgen05_and_tma():
     assert "LDTM" in sass
     assert "UTMALDG" in sass
     assert "UBLKCP" in sass
+
+
+def test_plan_bits_host_only(L):
+    """turbo_plan_bits is a host function: runs without a GPU."""
+    import numpy as np
+
+    from paper_2412_08585_b200 import binding as b
+
+    pr = np.array([3.0, 1.0, 1.0, 5.0, 0.5, 7.0], np.float64)
+    bits = np.zeros(6, np.int32)
+    assert L.turbo_plan_bits(pr.ctypes.data_as(C.c_void_p), 6, 3, bits.ctypes.data_as(C.c_void_p)) == 0
+    assert bits.tolist() == [4, 2, 2, 4, 2, 4]
+    assert L.turbo_plan_bits(pr.ctypes.data_as(C.c_void_p), 6, 7, bits.ctypes.data_as(C.c_void_p)) == \
+        b.TURBO_ERR_INVALID_ARG

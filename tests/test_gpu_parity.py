@@ -318,3 +318,22 @@ def test_seq_sharded_decode_emulated_ranks(ta):
         ro, rl = O.combine(ref_p[:, row], ref_l[:, row])
         assert np.abs(o16[row].float().cpu().numpy() - ro).max() <= MAX_ABS
         assert abs(L[row].item() - rl) < 1e-4
+
+
+@pytest.mark.parametrize("shape", [(2, 300, 8, 128), (1, 128, 1, 64)])
+def test_head_priority_planner_parity(ta, shape):
+    """NEXT-1: per-slot priority (gap x std of channel gaps)
+    bit-exact against the oracle; the plan (n_h lowest -> 2 bits) identical."""
+    B, N, Hkv, d = shape
+    _, k, v = synth.qkv(606 + N, B, N, Hkv, Hkv, d)
+    pr = ta.turbo_head_priority(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    torch.cuda.synchronize()
+    pr = pr.cpu().numpy()
+    ref = np.zeros((Hkv, 2))
+    for h in range(Hkv):
+        for kind, x in enumerate((k, v)):
+            ref[h, kind] = O.head_priority(x[:, :, h].reshape(B * N, d).astype(np.float32))
+    np.testing.assert_array_equal(pr, ref)
+    n2 = Hkv
+    bits = ta.turbo_plan_bits(torch.from_numpy(pr), n2).numpy()
+    np.testing.assert_array_equal(bits.reshape(-1), O.plan_bits(ref.reshape(-1), n2))
