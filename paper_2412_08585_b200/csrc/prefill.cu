@@ -269,12 +269,12 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
         // x = S s_Q s_K / sqrt(d) (R-18); masked keys -> -inf.
         // S -> x in place in TMEM, 32 columns at a time (keeps registers for O).
         const float cqk = __fmul_rn(__fmul_rn(s_q, args.k1s[bkv * Tc + j]), args.scale);
-        constexpr int CW = 16;  // TMEM chunk width (columns) -- bounds register pressure
+        constexpr int CW = 32;  // TMEM chunk width (columns) -- bounds register pressure
         float mt = -INFINITY;
 #pragma unroll 1
         for (int ch = 0; ch < kBc / CW; ++ch) {
           uint32_t v[CW];
-          TA_TMEM_LD16(tS + ch * CW, v);
+          TA_TMEM_LD32(tS + ch * CW, v);
           tmem_ld_wait();
           if (tap_j)
             for (int c = 0; c < CW; ++c)
@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
               v[c] = __float_as_uint(x);
             }
           }
-          TA_TMEM_ST16(tS + ch * CW, v);
+          TA_TMEM_ST32(tS + ch * CW, v);
         }
         // m_new, alpha = SAS(m_prev - m_new) (R-15)
         const float m_new = fmaxf(m, mt);
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
 #pragma unroll 1
         for (int ch = 0; ch < kBc / CW; ++ch) {
           uint32_t v[CW];
-          TA_TMEM_LD16(tS + ch * CW, v);
+          TA_TMEM_LD32(tS + ch * CW, v);
           tmem_ld_wait();
 #pragma unroll
           for (int c = 0; c < CW; ++c) {
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
             pmax = fmaxf(pmax, pt);
             v[c] = __float_as_uint(pt);
           }
-          TA_TMEM_ST16(tS + ch * CW, v);
+          TA_TMEM_ST32(tS + ch * CW, v);
         }
         if (active) {
           l = alpha * l + rsum;  // l = SAS(m_prev - m_new) l + rowsum(P~)
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
       if (j < nkv) {
         const int sb = j & 1;
         const uint32_t tS = tbase + sb * kBc;
-        constexpr int CW = 16;
+        constexpr int CW = 32;
         tmem_st_wait();
         mbar_wait(&sm.pmax_bar[slot][grp], j & 1);
         const float a_p = args.block_q == 64 ? fmaxf(red_p[sb * 4 + 2 * half], red_p[sb * 4 + 2 * half + 1])
@@ -367,18 +367,23 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
 #pragma unroll 1
         for (int ch = 0; ch < kBc / CW; ++ch) {
           uint32_t v[CW];
-          TA_TMEM_LD16(tS + ch * CW, v);
+          TA_TMEM_LD32(tS + ch * CW, v);
           tmem_ld_wait();
-          uint32_t w[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            w[e] = pack4_lo(rint_prod_bits(__uint_as_float(v[4 * e]), inv_p),
-                            rint_prod_bits(__uint_as_float(v[4 * e + 1]), inv_p),
-                            rint_prod_bits(__uint_as_float(v[4 * e + 2]), inv_p),
-                            rint_prod_bits(__uint_as_float(v[4 * e + 3]), inv_p));
-          *reinterpret_cast<uint4*>(prow + p_swz(r, ch)) = make_uint4(w[0], w[1], w[2], w[3]);
-          if (tap_j)
-            *reinterpret_cast<uint4*>(args.tap.p_codes + (r & 63) * kBc + ch * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+          for (int hh = 0; hh < CW / 16; ++hh) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              w[e] = pack4_lo(rint_prod_bits(__uint_as_float(v[16 * hh + 4 * e]), inv_p),
+                              rint_prod_bits(__uint_as_float(v[16 * hh + 4 * e + 1]), inv_p),
+                              rint_prod_bits(__uint_as_float(v[16 * hh + 4 * e + 2]), inv_p),
+                              rint_prod_bits(__uint_as_float(v[16 * hh + 4 * e + 3]), inv_p));
+            const int chunk = ch * (CW / 16) + hh;
+            *reinterpret_cast<uint4*>(prow + p_swz(r, chunk)) = make_uint4(w[0], w[1], w[2], w[3]);
+            if (tap_j)
+              *reinterpret_cast<uint4*>(args.tap.p_codes + (r & 63) * kBc + chunk * 16) =
+                  make_uint4(w[0], w[1], w[2], w[3]);
+          }
         }
         tc_fence_before();
         mbar_arrive(&sm.s_free[slot][sb]);

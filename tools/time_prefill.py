@@ -1,0 +1,29 @@
+"""Time turbo_attention_prefill on configs[1] (B=8, N=4096, 32/8 heads, d=128,
+causal) for the library in $TURBO_LIB (A/B of kernel variants)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2412_08585_b200 import binding as ta  # noqa: E402
+from paper_2412_08585_b200 import synth  # noqa: E402
+
+B, N, Hq, Hkv, d = 8, 4096, 32, 8, 128
+p = ta.params(head_dim=d)
+q, k, v = synth.qkv_torch(1002, B, N, Hq, Hkv, d)
+cache = ta.KVCache(B, Hkv, d, max_blocks=N // 64 + 2, bits=synth.head_bits_alternating(Hkv))
+k1, v1t, k1s, v1s = ta.turbo_quantize_kv(p, cache, k, v)
+o, lse = ta.turbo_attention_prefill(p, q, k1, v1t, k1s, v1s)
+for _ in range(3):
+    ta.turbo_attention_prefill(p, q, k1, v1t, k1s, v1s, o=o, lse=lse)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(20):
+    ta.turbo_attention_prefill(p, q, k1, v1t, k1s, v1s, o=o, lse=lse)
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / 20
+ops = 4.0 * d * N * (N + 1) / 2 * B * Hq
+print(f"{os.environ.get('TURBO_LIB', 'in-tree')}: {ms * 1e3:8.1f} us  {ops / ms / 1e9:7.1f} TOPS  "
+      f"checksum {o.float().abs().sum().item():.6e}")
