@@ -130,8 +130,9 @@ TURBO_API turbo_status_t turbo_cache_sizes(int32_t batch, int32_t n_kv_heads, in
  *     with the universal scale into the INT8 buffer.  The stage-1 operands of
  *     turbo_attention_prefill are written to
  *       k1_out   int8 [B][Hkv][n_tokens][d]
- *       v1t_out  int8 [B][Hkv][T_c][d][B_c]   (each block transposed; tokens
- *                past n_tokens are 0), T_c = ceil(n_tokens / B_c)
+ *       v1t_out  FP16 [B][Hkv][T_c][d][B_c]  the stage-1 V codes (integers in
+ *                [-119,119], exact in FP16), each block transposed; tokens past
+ *                n_tokens are 0; T_c = ceil(n_tokens / B_c)
  *       k1_scale_out, v1_scale_out  f32 [B][Hkv][T_c].
  *   mode 1 = APPEND: k, v are FP16 [B][Hkv][d] (one new token per sequence,
  *     n_tokens must be 1).  Quantised with the universal scale and clamped to
@@ -140,7 +141,7 @@ TURBO_API turbo_status_t turbo_cache_sizes(int32_t batch, int32_t n_kv_heads, in
  *     NULL.  Updates cache->n_tokens (host) and the device counters. */
 TURBO_API turbo_status_t turbo_quantize_kv(const turbo_params_t* params, turbo_kv_cache_t* cache, const void* k,
                                  const void* v, int32_t n_tokens, int32_t mode, int8_t* k1_out,
-                                 int8_t* v1t_out, float* k1_scale_out, float* v1_scale_out,
+                                 void* v1t_out, float* k1_scale_out, float* v1_scale_out,
                                  turbo_stream_t stream);
 
 /* Algorithm 1, TurboAttention prefill, tcgen05 INT8 MMA.
@@ -153,7 +154,7 @@ TURBO_API turbo_status_t turbo_quantize_kv(const turbo_params_t* params, turbo_k
  * Query head h reads kv head h / (Hq/Hkv) (GQA, R-22). */
 TURBO_API turbo_status_t turbo_attention_prefill(const turbo_params_t* params, int32_t B, int32_t N, int32_t Hq,
                                        int32_t Hkv, int32_t causal, const void* q, const int8_t* k1,
-                                       const int8_t* v1t, const float* k1_scale, const float* v1_scale,
+                                       const void* v1t, const float* k1_scale, const float* v1_scale,
                                        void* o, float* lse, turbo_stream_t stream);
 
 /* Workspace for turbo_attention_decode with n_splits splits (HOST result). */

@@ -153,7 +153,7 @@ def turbo_quantize_kv(p, cache: KVCache, k, v, mode=0, stream=None):
         tc = -(-N // p.block_kv)
         dev = k.device
         k1 = torch.empty((B, H, N, d), dtype=torch.int8, device=dev)
-        v1t = torch.empty((B, H, tc, d, p.block_kv), dtype=torch.int8, device=dev)
+        v1t = torch.empty((B, H, tc, d, p.block_kv), dtype=torch.float16, device=dev)
         k1s = torch.empty((B, H, tc), dtype=torch.float32, device=dev)
         v1s = torch.empty((B, H, tc), dtype=torch.float32, device=dev)
         _check("turbo_quantize_kv", lib().turbo_quantize_kv(C.byref(p), C.byref(cache.c), _ptr(k), _ptr(v), N, 0,

@@ -9,10 +9,10 @@
 
 namespace ta_host {
 cudaError_t launch_quant_prefill(const turbo_kv_cache_t* c, const __half* k, const __half* v, int N, int8_t* k1,
-                                 int8_t* v1t, float* k1s, float* v1s, cudaStream_t st);
+                                 __half* v1t, float* k1s, float* v1s, cudaStream_t st);
 cudaError_t launch_quant_append(const turbo_kv_cache_t* c, const __half* k, const __half* v, cudaStream_t st);
 cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Hq, int Hkv, int causal, const __half* q,
-                           const int8_t* k1, const int8_t* v1t, const float* k1s, const float* v1s, __half* o,
+                           const int8_t* k1, const __half* v1t, const float* k1s, const float* v1s, __half* o,
                            float* lse, cudaStream_t st);
 size_t decode_workspace(int B, int Hq, int HD, int S);
 cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, int Hq, const __half* q, int blk_begin,
@@ -79,7 +79,7 @@ turbo_status_t turbo_cache_sizes(int32_t batch, int32_t n_kv_heads, int32_t head
 }
 
 turbo_status_t turbo_quantize_kv(const turbo_params_t* params, turbo_kv_cache_t* cache, const void* k,
-                                 const void* v, int32_t n_tokens, int32_t mode, int8_t* k1_out, int8_t* v1t_out,
+                                 const void* v, int32_t n_tokens, int32_t mode, int8_t* k1_out, void* v1t_out,
                                  float* k1_scale_out, float* v1_scale_out, turbo_stream_t stream) {
   turbo_status_t s = check_params(params);
   if (s != TURBO_OK) return s;
@@ -90,7 +90,8 @@ turbo_status_t turbo_quantize_kv(const turbo_params_t* params, turbo_kv_cache_t*
     if (n_tokens < 1 || !k1_out || !v1t_out || !k1_scale_out || !v1_scale_out) return TURBO_ERR_INVALID_ARG;
     if (n_tokens / params->block_kv > cache->max_blocks) return TURBO_ERR_CAPACITY;
     s = cuda_status(ta_host::launch_quant_prefill(cache, reinterpret_cast<const __half*>(k),
-                                                  reinterpret_cast<const __half*>(v), n_tokens, k1_out, v1t_out,
+                                                  reinterpret_cast<const __half*>(v), n_tokens, k1_out,
+                                                  reinterpret_cast<__half*>(v1t_out),
                                                   k1_scale_out, v1_scale_out, st));
     if (s == TURBO_OK) cache->n_tokens = n_tokens;
     return s;
@@ -108,7 +109,7 @@ turbo_status_t turbo_quantize_kv(const turbo_params_t* params, turbo_kv_cache_t*
 }
 
 turbo_status_t turbo_attention_prefill(const turbo_params_t* params, int32_t B, int32_t N, int32_t Hq, int32_t Hkv,
-                                       int32_t causal, const void* q, const int8_t* k1, const int8_t* v1t,
+                                       int32_t causal, const void* q, const int8_t* k1, const void* v1t,
                                        const float* k1_scale, const float* v1_scale, void* o, float* lse,
                                        turbo_stream_t stream) {
   turbo_status_t s = check_params(params);
@@ -117,7 +118,7 @@ turbo_status_t turbo_attention_prefill(const turbo_params_t* params, int32_t B, 
   if (Hq % Hkv != 0) return TURBO_ERR_UNSUPPORTED;
   if (!q || !k1 || !v1t || !k1_scale || !v1_scale || !o || !lse) return TURBO_ERR_INVALID_ARG;
   return cuda_status(ta_host::launch_prefill(params, B, N, Hq, Hkv, causal, reinterpret_cast<const __half*>(q), k1,
-                                             v1t, k1_scale, v1_scale, reinterpret_cast<__half*>(o), lse,
+                                             reinterpret_cast<const __half*>(v1t), k1_scale, v1_scale, reinterpret_cast<__half*>(o), lse,
                                              reinterpret_cast<cudaStream_t>(stream)));
 }
 

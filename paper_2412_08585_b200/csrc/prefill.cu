@@ -29,8 +29,8 @@ template <int HD, int NS>
 struct PrefillSmem {
   int8_t q1[NS][kTileM * HD];       // Q^q1, K-major, swizzled rows of HD bytes
   int8_t k[kStages][kBc * HD];      // K_j^q1 [64][HD]
-  int8_t v[kStages][HD * kBc];      // V_j^q1 transposed [HD][64]
-  int8_t p[NS][2][kTileM * kBc];    // Q(P~) [128][64], SW64
+  __half v[kStages][HD * kBc];      // V_j^q1 codes as fp16, transposed [HD][64] (128-B rows, SW128)
+  __half p[NS][2][kTileM * kBc];    // Q(P~) codes as fp16 [128][64] (128-B rows, SW128)
   uint64_t kv_full[kStages], kv_empty[kStages];
   uint64_t s_full[NS][2], s_free[NS][2], p_full[NS][2], pv_full[NS], pv_free[NS], q_ready;
   uint64_t pmax_bar[NS][2];  // per P-scale group: arrivals of its warps' partial max
@@ -59,7 +59,7 @@ TA_DEV uint32_t q1_swz(int r, int chunk) {
   if (HD == 128) return r * 128 + ((chunk ^ (r & 7)) << 4);
   return r * 64 + ((chunk ^ ((r >> 1) & 3)) << 4);
 }
-TA_DEV uint32_t p_swz(int r, int chunk) { return r * 64 + ((chunk ^ ((r >> 1) & 3)) << 4); }
+TA_DEV uint32_t p_swz(int r, int chunk) { return r * 128 + ((chunk ^ (r & 7)) << 4); }  // SW128, 16-B chunk of 8 halves
 
 template <int NS>
 TA_DEV void reg_dealloc() {
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
         for (int j = 0; j < nkv; ++j) {
           const int st = j % kStages, n = j / kStages;
           if (n > 0) mbar_wait(&sm.kv_empty[st], (n - 1) & 1);
-          mbar_expect_tx(&sm.kv_full[st], 2 * kBc * HD);
+          mbar_expect_tx(&sm.kv_full[st], 3 * kBc * HD);  // K int8 + V fp16
           tma_load_3d(sm.k[st], &tm_k, &sm.kv_full[st], 0, j * kBc, (int)bkv);
           tma_load_3d(sm.v[st], &tm_v, &sm.kv_full[st], 0, 0, (int)(bkv * Tc + j));
         }
@@ -136,7 +136,9 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
       // ---------------------------------------------------------- MMA issuer
       constexpr uint32_t kLayQK = HD == 128 ? kSw128 : kSw64;
       constexpr uint32_t idesc_qk = idesc_i8(kTileM, kBc, true, true);
-      constexpr uint32_t idesc_pv = idesc_i8(kTileM, HD, false, true);
+      // P V runs as kind::f16: codes are small integers (exact in fp16) and every
+      // partial sum is an integer < 2^24, so the fp32 accumulator holds PV_int exactly.
+      constexpr uint32_t idesc_pv = idesc_f16(kTileM, HD);
       mbar_wait(&sm.q_ready, 0);
       tc_fence_after();
       for (int j = 0; j <= nkv; ++j) {
@@ -170,9 +172,9 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
             if (elect_one()) {
               const uint32_t pa = smem_u32(sm.p[t][pb]);
 #pragma unroll
-              for (int ks = 0; ks < kBc / 32; ++ks)
-                mma_i8_ss(tmem + t * 256 + 2 * kBc, smem_desc(pa + ks * 32, 512, kSw64),
-                          smem_desc(va + ks * 32, 512, kSw64), idesc_pv, ks > 0);
+              for (int ks = 0; ks < kBc / 16; ++ks)
+                mma_f16_ss(tmem + t * 256 + 2 * kBc, smem_desc(pa + ks * 32, 1024, kSw128),
+                           smem_desc(va + ks * 32, 1024, kSw128), idesc_pv, ks > 0);
               mma_commit(&sm.pv_full[t]);
               if (t == NS - 1) mma_commit(&sm.kv_empty[st]);
             }
@@ -343,9 +345,9 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
           TA_TMEM_LD16(tbase + 2 * kBc + cc * 16, pv);
           tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 16; ++e) O[cc * 16 + e] = __fmaf_rn(cpv_p, (float)(int)pv[e], O[cc * 16 + e]);
+          for (int e = 0; e < 16; ++e) O[cc * 16 + e] = __fmaf_rn(cpv_p, __uint_as_float(pv[e]), O[cc * 16 + e]);
           if (tap_p) {
-            for (int e = 0; e < 16; ++e) args.tap.pv_int[(r & 63) * HD + cc * 16 + e] = (int)pv[e];
+            for (int e = 0; e < 16; ++e) args.tap.pv_int[(r & 63) * HD + cc * 16 + e] = (int)__uint_as_float(pv[e]);
           }
         }
         tc_fence_before();
@@ -364,25 +366,32 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
         const float s_p = __fdiv_rn(a_p, kDiv);
         // Q(P~) codes in [0, 119] -> smem (A operand of the PV MMA)
         uint8_t* prow = reinterpret_cast<uint8_t*>(sm.p[slot][sb]);
+        constexpr float kMagicF16 = 12582912.0f + 25600.0f;  // 1.5*2^23 + 0x6400
 #pragma unroll 1
         for (int ch = 0; ch < kBc / CW; ++ch) {
           uint32_t v[CW];
           TA_TMEM_LD32(tS + ch * CW, v);
           tmem_ld_wait();
 #pragma unroll
-          for (int hh = 0; hh < CW / 16; ++hh) {
-            uint32_t w[4];
+          for (int hh = 0; hh < CW / 8; ++hh) {
+            // y = 1.5*2^23 + 0x6400 + code: its low half-word is the fp16 of 1024 + code
+            uint32_t y[8];
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
-              w[e] = pack4_lo(rint_prod_bits(__uint_as_float(v[16 * hh + 4 * e]), inv_p),
-                              rint_prod_bits(__uint_as_float(v[16 * hh + 4 * e + 1]), inv_p),
-                              rint_prod_bits(__uint_as_float(v[16 * hh + 4 * e + 2]), inv_p),
-                              rint_prod_bits(__uint_as_float(v[16 * hh + 4 * e + 3]), inv_p));
-            const int chunk = ch * (CW / 16) + hh;
+            for (int e = 0; e < 8; ++e)
+              y[e] = __float_as_uint(__fmaf_rn(__uint_as_float(v[8 * hh + e]), inv_p, kMagicF16));
+            uint32_t w[4];
+            const __half2 c1024 = __half2(__float2half_rn(1024.f), __float2half_rn(1024.f));
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const uint32_t hb = __byte_perm(y[2 * e], y[2 * e + 1], 0x5410);
+              const __half2 hv = __hsub2(*reinterpret_cast<const __half2*>(&hb), c1024);  // exact
+              w[e] = *reinterpret_cast<const uint32_t*>(&hv);
+            }
+            const int chunk = ch * (CW / 8) + hh;
             *reinterpret_cast<uint4*>(prow + p_swz(r, chunk)) = make_uint4(w[0], w[1], w[2], w[3]);
             if (tap_j)
-              *reinterpret_cast<uint4*>(args.tap.p_codes + (r & 63) * kBc + chunk * 16) =
-                  make_uint4(w[0], w[1], w[2], w[3]);
+              *reinterpret_cast<uint2*>(args.tap.p_codes + (r & 63) * kBc + chunk * 8) =
+                  make_uint2(pack4_lo(y[0], y[1], y[2], y[3]), pack4_lo(y[4], y[5], y[6], y[7]));
           }
         }
         tc_fence_before();
@@ -452,28 +461,29 @@ static EncodeTiledFn get_encode() {
 }
 
 static bool make_map_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
-                        uint64_t s2, uint32_t b0, uint32_t b1, CUtensorMapSwizzle swz) {
+                        uint64_t s2, uint32_t b0, uint32_t b1, CUtensorMapSwizzle swz,
+                        CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_UINT8) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[3] = {d0, d1, d2};
   cuuint64_t strides[2] = {s1, s2};
   cuuint32_t box[3] = {b0, b1, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
+  return enc(m, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Hq, int Hkv, int causal, const __half* q,
-                           const int8_t* k1, const int8_t* v1t, const float* k1s, const float* v1s, __half* o,
+                           const int8_t* k1, const __half* v1t, const float* k1s, const float* v1s, __half* o,
                            float* lse, cudaStream_t st) {
   const int HD = p->head_dim, Tc = (N + kBc - 1) / kBc;
   CUtensorMap tmk, tmv;
   const CUtensorMapSwizzle swk = HD == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
   if (!make_map_3d(&tmk, k1, HD, N, (uint64_t)B * Hkv, HD, (uint64_t)N * HD, HD, kBc, swk))
     return cudaErrorInvalidValue;
-  if (!make_map_3d(&tmv, v1t, kBc, HD, (uint64_t)B * Hkv * Tc, kBc, (uint64_t)HD * kBc, kBc, HD,
-                   CU_TENSOR_MAP_SWIZZLE_64B))
+  if (!make_map_3d(&tmv, v1t, kBc, HD, (uint64_t)B * Hkv * Tc, kBc * 2, (uint64_t)HD * kBc * 2, kBc, HD,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16))
     return cudaErrorInvalidValue;
   PrefillArgs a;
   a.q = q;

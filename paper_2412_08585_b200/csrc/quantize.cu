@@ -79,7 +79,7 @@ template <int HD>
 __global__ void __launch_bounds__(256) quant_prefill_kernel(
     const __half* __restrict__ k, const __half* __restrict__ v, int N, int Hkv, int max_blocks,
     const int32_t* __restrict__ bits_dev, uint8_t* __restrict__ block_rec, float* __restrict__ s_parent,
-    float* __restrict__ a_univ, int8_t* __restrict__ k1, int8_t* __restrict__ v1t, float* __restrict__ k1s,
+    float* __restrict__ a_univ, int8_t* __restrict__ k1, __half* __restrict__ v1t, float* __restrict__ k1s,
     float* __restrict__ v1s) {
   __shared__ __align__(16) int8_t tile[2][kBc * HD];
   __shared__ float red[2][8];
@@ -155,16 +155,15 @@ __global__ void __launch_bounds__(256) quant_prefill_kernel(
     atomicMax(reinterpret_cast<int*>(a_univ + bh * 2 + 1), __float_as_int(a[1]));
   }
   __syncthreads();
-  // v1t: the block transposed, [d][B_c] (tokens past N are 0 from the zero fill).
-  for (int w = tid; w < HD * (kBc / 16); w += 256) {
-    const int c = w / (kBc / 16), t0 = (w % (kBc / 16)) * 16;
+  // v1t: the block transposed, [d][B_c], codes as fp16 (exact) -- the B operand
+  // of the prefill's kind::f16 P V MMA; tokens past N are 0 (zero fill).
+  for (int w = tid; w < HD * (kBc / 8); w += 256) {
+    const int c = w / (kBc / 8), t0 = (w % (kBc / 8)) * 8;
     uint32_t u[4];
 #pragma unroll
-    for (int q4 = 0; q4 < 4; ++q4) {
-      uint32_t x = 0;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) x |= (uint32_t)(uint8_t)tile[1][(t0 + q4 * 4 + e) * HD + c] << (8 * e);
-      u[q4] = x;
+    for (int e = 0; e < 4; ++e) {
+      const __half2 hv = __floats2half2_rn((float)tile[1][(t0 + 2 * e) * HD + c], (float)tile[1][(t0 + 2 * e + 1) * HD + c]);
+      u[e] = *reinterpret_cast<const uint32_t*>(&hv);
     }
     *reinterpret_cast<uint4*>(v1t + ((bh * Tc + j) * HD + c) * kBc + t0) = make_uint4(u[0], u[1], u[2], u[3]);
   }
@@ -281,7 +280,7 @@ namespace ta_host {
 using namespace ta;
 
 cudaError_t launch_quant_prefill(const turbo_kv_cache_t* c, const __half* k, const __half* v, int N, int8_t* k1,
-                                 int8_t* v1t, float* k1s, float* v1s, cudaStream_t st) {
+                                 __half* v1t, float* k1s, float* v1s, cudaStream_t st) {
   const int B = c->batch, H = c->n_kv_heads, HD = c->head_dim;
   const int Tc = (N + kBc - 1) / kBc;
   cudaError_t e = cudaMemsetAsync(c->a_univ, 0, sizeof(float) * B * H * 2, st);

@@ -66,7 +66,9 @@ def test_quantize_kv_prefill_bit_exact(ta, case):
     np.testing.assert_array_equal(k1s.cpu().numpy(), ref["k1s"])
     np.testing.assert_array_equal(v1s.cpu().numpy(), ref["v1s"])
     tc = -(-N // 64)
-    v1 = v1t.cpu().numpy().transpose(0, 1, 2, 4, 3).reshape(B, Hkv, tc * 64, d)
+    v1t = v1t.float().cpu().numpy()
+    assert (v1t == np.rint(v1t)).all()  # integer codes carried exactly in FP16
+    v1 = v1t.astype(np.int8).transpose(0, 1, 2, 4, 3).reshape(B, Hkv, tc * 64, d)
     np.testing.assert_array_equal(v1[:, :, :N], ref["v1"])
     assert not v1[:, :, N:].any()
     recs = cache.records().cpu().numpy()
