@@ -17,15 +17,28 @@
 
 #include "common.cuh"
 
+#ifdef TURBO_PROFILE
+__device__ unsigned long long g_prof[32];
+#define PROF_T(var) const long long var = clock64()
+#define PROF_ADD(slot, a, b) \
+  if ((threadIdx.x & 31) == 0) atomicAdd(&g_prof[slot], (unsigned long long)((b) - (a)))
+#else
+#define PROF_T(var)
+#define PROF_ADD(slot, a, b)
+#endif
+
 namespace ta {
 
 constexpr int kStages = 3;
 constexpr int kTileM = 128;
+#ifndef TA_PREFILL_SPLIT
+#define TA_PREFILL_SPLIT 1  // softmax warps per 32-row quadrant (2 = column halves; measured slower)
+#endif
 
 // NS query tiles ("slots") per CTA share every K/V tile: NS = 2 pairs two
 // query heads of the same KV head (GQA) at the same rows, each with its own
 // softmax warpgroup, S/PV TMEM columns and P buffers.
-template <int HD, int NS>
+template <int HD, int NS, int SP>
 struct PrefillSmem {
   int8_t q1[NS][kTileM * HD];       // Q^q1, K-major, swizzled rows of HD bytes
   int8_t k[kStages][kBc * HD];      // K_j^q1 [64][HD]
@@ -35,8 +48,10 @@ struct PrefillSmem {
   uint64_t s_full[NS][2], s_free[NS][2], p_full[NS][2], pv_full[NS], pv_free[NS], q_ready;
   uint64_t pmax_bar[NS][2];  // per P-scale group: arrivals of its warps' partial max
   uint32_t tmem_base;
-  float red_a[NS][4];
-  float red_p[NS][2][4];
+  float red_a[NS][4][SP];
+  float red_p[NS][2][4 * SP];
+  float xmax[NS][2][SP][kTileM];  // per-half row max exchange (SP = 2)
+  float lsum[NS][SP][kTileM];     // per-half row sums (SP = 2)
 };
 
 struct PrefillArgs {
@@ -61,21 +76,26 @@ TA_DEV uint32_t q1_swz(int r, int chunk) {
 }
 TA_DEV uint32_t p_swz(int r, int chunk) { return r * 128 + ((chunk ^ (r & 7)) << 4); }  // SW128, 16-B chunk of 8 halves
 
-template <int NS>
+// Register split between the control warpgroup and the softmax warpgroups.
+// setmaxnreg.inc can only take registers released by setmaxnreg.dec of the
+// same CTA, so  128 * dec + 128 * NS * SP * inc <= threads * launch_regs.
+template <int NS, int SP>
 TA_DEV void reg_dealloc() {
-  if (NS == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+  if (NS * SP == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");  // 384 thr x 168
+  if (NS * SP == 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 24;\n" ::: "memory");  // 640 thr x 96
 }
-template <int NS>
+template <int NS, int SP>
 TA_DEV void reg_alloc() {
-  if (NS == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
+  if (NS * SP == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
+  if (NS * SP == 4) asm volatile("setmaxnreg.inc.sync.aligned.u32 112;\n" ::: "memory");
 }
 
-template <int HD, int NS, bool TAP>
-__global__ void __launch_bounds__(128 * (NS + 1), 1)
+template <int HD, int NS, int SP, bool TAP>
+__global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
     prefill_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                    const __grid_constant__ PrefillArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  using Smem = PrefillSmem<HD, NS>;
+  using Smem = PrefillSmem<HD, NS, SP>;
   // 1024-B aligned (128B-swizzle atoms); pointer arithmetic keeps the shared address space.
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -101,14 +121,14 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
     for (int t = 0; t < NS; ++t) {
       for (int s = 0; s < 2; ++s) {
         mbar_init(&sm.s_full[t][s], 1);
-        mbar_init(&sm.s_free[t][s], 128);
-        mbar_init(&sm.p_full[t][s], 128);
+        mbar_init(&sm.s_free[t][s], 128 * SP);
+        mbar_init(&sm.p_full[t][s], 128 * SP);
       }
       mbar_init(&sm.pv_full[t], 1);
-      mbar_init(&sm.pv_free[t], 128);
-      for (int g2 = 0; g2 < 2; ++g2) mbar_init(&sm.pmax_bar[t][g2], args.block_q / 32);
+      mbar_init(&sm.pv_free[t], 128 * SP);
+      for (int g2 = 0; g2 < 2; ++g2) mbar_init(&sm.pmax_bar[t][g2], (args.block_q / 32) * SP);
     }
-    mbar_init(&sm.q_ready, 128 * NS);
+    mbar_init(&sm.q_ready, 128 * NS * SP);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(&sm.tmem_base, kTmemCols);
@@ -118,7 +138,7 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
   const uint32_t tmem = sm.tmem_base;
 
   if (warp < 4) {
-    reg_dealloc<NS>();
+    reg_dealloc<NS, SP>();
     if (warp == 0) {
       // ---------------------------------------------------------- TMA producer
       if (elect_one()) {
@@ -126,7 +146,10 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
         tma_prefetch_desc(&tm_v);
         for (int j = 0; j < nkv; ++j) {
           const int st = j % kStages, n = j / kStages;
+          PROF_T(w0);
           if (n > 0) mbar_wait(&sm.kv_empty[st], (n - 1) & 1);
+          PROF_T(w1);
+          PROF_ADD(16, w0, w1);
           mbar_expect_tx(&sm.kv_full[st], 3 * kBc * HD);  // K int8 + V fp16
           tma_load_3d(sm.k[st], &tm_k, &sm.kv_full[st], 0, j * kBc, (int)bkv);
           tma_load_3d(sm.v[st], &tm_v, &sm.kv_full[st], 0, 0, (int)(bkv * Tc + j));
@@ -144,11 +167,17 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
       for (int j = 0; j <= nkv; ++j) {
         if (j < nkv) {
           const int st = j % kStages, sb = j & 1;
+          PROF_T(m0);
           mbar_wait(&sm.kv_full[st], (j / kStages) & 1);
+          PROF_T(m1);
+          PROF_ADD(10, m0, m1);
           const uint32_t ka = smem_u32(sm.k[st]);
 #pragma unroll
           for (int t = 0; t < NS; ++t) {
+            PROF_T(m2);
             if (j >= 2) mbar_wait(&sm.s_free[t][sb], ((j >> 1) - 1) & 1);
+            PROF_T(m3);
+            PROF_ADD(11, m2, m3);
             tc_fence_after();
             if (elect_one()) {
               const uint32_t q1a = smem_u32(sm.q1[t]);
@@ -166,8 +195,13 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
           const uint32_t va = smem_u32(sm.v[st]);
 #pragma unroll
           for (int t = 0; t < NS; ++t) {
+            PROF_T(m4);
             mbar_wait(&sm.p_full[t][pb], (jj >> 1) & 1);
+            PROF_T(m5);
             if (jj >= 1) mbar_wait(&sm.pv_free[t], (jj - 1) & 1);
+            PROF_T(m6);
+            PROF_ADD(12, m4, m5);
+            PROF_ADD(13, m5, m6);
             tc_fence_after();
             if (elect_one()) {
               const uint32_t pa = smem_u32(sm.p[t][pb]);
@@ -184,9 +218,14 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
       }
     }
   } else {
-    reg_alloc<NS>();
+    reg_alloc<NS, SP>();
     // ------------------------------------------------------------ softmax / correction
-    const int slot = (warp - 4) >> 2, h = h0 + slot;
+    // Thread = (slot, column half hc, row r = TMEM lane).  With SP = 2 two warps
+    // share each 32-row quadrant: hc owns S columns [hc SW, (hc+1) SW) and O
+    // columns [hc OW, (hc+1) OW); row max is exchanged per tile, partial row sums
+    // are added at the end (l is linear in the halves).
+    constexpr int SW = kBc / SP, OW = HD / SP, CW = SP == 2 ? 16 : 32;
+    const int widx = warp - 4, slot = widx / (4 * SP), hc = (widx >> 2) % SP, h = h0 + slot;
     const int qd = warp & 3, r = qd * 32 + lane, row = it * kTileM + r;
     const bool row_ok = row < N;
     const int half = args.block_q == 64 ? (r >> 6) : 0;
@@ -198,16 +237,18 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
                          (args.tap.i_block >> 1) == it;
     const bool tap_row = tap_cta && (args.tap.i_block & 1) == (r >> 6);
     float* red_p = &sm.red_p[slot][0][0];
-    const uint32_t bar_id = 1 + slot;
+    const uint32_t bar_slot = 1 + slot;                // 128*SP threads of the slot
+    const uint32_t bar_pair = 3 + slot * 4 + qd;       // the SP warps of one quadrant
 
-    // Q stage-1 quantisation (Alg. 1; per B_r x d block).
+    // Q stage-1 quantisation (Alg. 1; per B_r x d block): this thread
+    // quantises the channels [hc OW, (hc+1) OW) of its row.
     float s_q;
     {
-      uint4 qraw[HD / 8];
+      uint4 qraw[OW / 8];
       float qa = 0.f;
-      const __half* qrow = args.q + (((size_t)b * N + row) * args.Hq + h) * HD;
+      const __half* qrow = args.q + (((size_t)b * N + row) * args.Hq + h) * HD + hc * OW;
 #pragma unroll
-      for (int c = 0; c < HD / 8; ++c) {
+      for (int c = 0; c < OW / 8; ++c) {
         qraw[c] = row_ok ? reinterpret_cast<const uint4*>(qrow)[c] : make_uint4(0, 0, 0, 0);
         const __half2* hp = reinterpret_cast<const __half2*>(&qraw[c]);
 #pragma unroll
@@ -217,15 +258,18 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
         }
       }
       qa = warp_max(qa);
-      if (lane == 0) sm.red_a[slot][qd] = qa;
-      named_bar_sync(bar_id, 128);
-      const float* ra = sm.red_a[slot];
-      const float a_q = args.block_q == 64 ? fmaxf(ra[2 * half], ra[2 * half + 1])
-                                           : fmaxf(fmaxf(ra[0], ra[1]), fmaxf(ra[2], ra[3]));
+      if (lane == 0) sm.red_a[slot][qd][hc] = qa;
+      named_bar_sync(bar_slot, 128 * SP);
+      float a_q = 0.f;
+#pragma unroll
+      for (int x = 0; x < SP; ++x)
+        a_q = args.block_q == 64 ? fmaxf(a_q, fmaxf(sm.red_a[slot][2 * half][x], sm.red_a[slot][2 * half + 1][x]))
+                                 : fmaxf(a_q, fmaxf(fmaxf(sm.red_a[slot][0][x], sm.red_a[slot][1][x]),
+                                                    fmaxf(sm.red_a[slot][2][x], sm.red_a[slot][3][x])));
       const float inv_q = a_q > 0.f ? __fdiv_rn(kDiv, a_q) : 0.f;
       s_q = __fdiv_rn(a_q, kDiv);
 #pragma unroll
-      for (int c = 0; c < HD / 16; ++c) {
+      for (int c = 0; c < OW / 16; ++c) {
         uint32_t w[4];
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
@@ -237,20 +281,22 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
                                      rint_prod_bits(f1.x, inv_q), rint_prod_bits(f1.y, inv_q));
           }
         }
-        *reinterpret_cast<uint4*>(sm.q1[slot] + q1_swz<HD>(r, c)) = make_uint4(w[0], w[1], w[2], w[3]);
-        if (tap_row) *reinterpret_cast<uint4*>(args.tap.q1 + (r & 63) * HD + c * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+        const int chunk = hc * (OW / 16) + c;
+        *reinterpret_cast<uint4*>(sm.q1[slot] + q1_swz<HD>(r, chunk)) = make_uint4(w[0], w[1], w[2], w[3]);
+        if (tap_row)
+          *reinterpret_cast<uint4*>(args.tap.q1 + (r & 63) * HD + chunk * 16) = make_uint4(w[0], w[1], w[2], w[3]);
       }
-      if (tap_row && (r & 63) == 0) args.tap.s_q[0] = s_q;
+      if (tap_row && (r & 63) == 0 && hc == 0) args.tap.s_q[0] = s_q;
     }
     fence_proxy_async();
     mbar_arrive(&sm.q_ready);
 
     // Output accumulator in scaled form O_true = A * Ohat (A = product of the
     // alphas since the last renormalisation), so a tile costs one FFMA per
-    // element: Ohat += (s_P s_V / A) PV_int.  Rounding order of O is free (R-16).
-    float O[HD];
+    // element: Ohat += (s_P s_V / A) PV.  Rounding order of O is free (R-16).
+    float O[OW];
 #pragma unroll
-    for (int c = 0; c < HD; ++c) O[c] = 0.f;
+    for (int c = 0; c < OW; ++c) O[c] = 0.f;
     float m = -INFINITY, l = 0.f, A = 1.f;
     float cpv_p = 0.f;
     bool tap_p = false;
@@ -262,25 +308,27 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
       const bool tap_j = tap_row && args.tap.j_block == j;
       if (j < nkv) {
         const int sb = j & 1;
-        const uint32_t tS = tbase + sb * kBc;  // this tile's S columns (reused for x and P~)
+        const uint32_t tS = tbase + sb * kBc + hc * SW;  // this thread's S columns (reused for x, P~)
+        PROF_T(p0);
         mbar_wait(&sm.s_full[slot][sb], (j >> 1) & 1);
         tc_fence_after();
-        const int nvalid = max(0, min(kBc, kmax - j * kBc + 1));
+        PROF_T(p1);
+        PROF_ADD(0, p0, p1);
+        const int nvalid = max(0, min(kBc, kmax - j * kBc + 1));  // visible keys of the tile
+        const int nv = max(0, min(SW, nvalid - hc * SW));            // ... in this half
         const bool active = nvalid > 0;
-        const bool full = __all_sync(0xffffffffu, nvalid == kBc);
+        const bool full = __all_sync(0xffffffffu, nv == SW);
         // x = S s_Q s_K / sqrt(d) (R-18); masked keys -> -inf.
-        // S -> x in place in TMEM, 32 columns at a time (keeps registers for O).
         const float cqk = __fmul_rn(__fmul_rn(s_q, args.k1s[bkv * Tc + j]), args.scale);
-        constexpr int CW = 32;  // TMEM chunk width (columns) -- bounds register pressure
         float mt = -INFINITY;
 #pragma unroll 1
-        for (int ch = 0; ch < kBc / CW; ++ch) {
+        for (int ch = 0; ch < SW / CW; ++ch) {
           uint32_t v[CW];
-          TA_TMEM_LD32(tS + ch * CW, v);
+          TA_TMEM_LD(CW, tS + ch * CW, v);
           tmem_ld_wait();
           if (tap_j)
             for (int c = 0; c < CW; ++c)
-              args.tap.s_int[(r & 63) * kBc + ch * CW + c] = ch * CW + c < nvalid ? (int)v[c] : 0;
+              args.tap.s_int[(r & 63) * kBc + hc * SW + ch * CW + c] = ch * CW + c < nv ? (int)v[c] : 0;
           if (full) {
 #pragma unroll
             for (int c = 0; c < CW; ++c) {
@@ -291,13 +339,20 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
           } else {
 #pragma unroll
             for (int c = 0; c < CW; ++c) {
-              const float x = ch * CW + c < nvalid ? __fmul_rn((float)(int)v[c], cqk) : -INFINITY;
+              const float x = ch * CW + c < nv ? __fmul_rn((float)(int)v[c], cqk) : -INFINITY;
               mt = fmaxf(mt, x);
               v[c] = __float_as_uint(x);
             }
           }
-          TA_TMEM_ST32(tS + ch * CW, v);
+          TA_TMEM_ST(CW, tS + ch * CW, v);
         }
+        if (SP == 2) {  // row max over both halves
+          sm.xmax[slot][sb][hc][r] = mt;
+          named_bar_sync(bar_pair, 64);
+          mt = fmaxf(mt, sm.xmax[slot][sb][hc ^ 1][r]);
+        }
+        PROF_T(p2);
+        PROF_ADD(1, p1, p2);
         // m_new, alpha = SAS(m_prev - m_new) (R-15)
         const float m_new = fmaxf(m, mt);
         float alpha = sas_eval(__fsub_rn(m_new, m), lut_lane, nr_abs);
@@ -308,9 +363,9 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
         // P~ = SAS(x - m_new), in place in TMEM
         float rsum = 0.f, pmax = 0.f;
 #pragma unroll 1
-        for (int ch = 0; ch < kBc / CW; ++ch) {
+        for (int ch = 0; ch < SW / CW; ++ch) {
           uint32_t v[CW];
-          TA_TMEM_LD32(tS + ch * CW, v);
+          TA_TMEM_LD(CW, tS + ch * CW, v);
           tmem_ld_wait();
 #pragma unroll
           for (int c = 0; c < CW; ++c) {
@@ -319,17 +374,19 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
             pmax = fmaxf(pmax, pt);
             v[c] = __float_as_uint(pt);
           }
-          TA_TMEM_ST32(tS + ch * CW, v);
+          TA_TMEM_ST(CW, tS + ch * CW, v);
         }
         if (active) {
-          l = alpha * l + rsum;  // l = SAS(m_prev - m_new) l + rowsum(P~)
+          l = alpha * l + rsum;  // l = SAS(m_prev - m_new) l + rowsum(P~), this half's share
           m = m_new;
         }
+        PROF_T(p3);
+        PROF_ADD(2, p2, p3);
         // P scale over the B_r x B_c tile: publish this warp's max
         // now, pick the group max up after the previous tile's O update.
         pmax = warp_max(pmax);
         if (lane == 0) {
-          red_p[sb * 4 + qd] = pmax;
+          red_p[(sb * 4 + qd) * SP + hc] = pmax;
           mbar_arrive(&sm.pmax_bar[slot][grp]);
         }
         alpha_j = alpha;
@@ -337,40 +394,53 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
       }
       // O += (s_P s_V / A) Q(P~) V^q1 for the previous tile
       if (j >= 1) {
+        PROF_T(c0);
         mbar_wait(&sm.pv_full[slot], (j - 1) & 1);
         tc_fence_after();
+        PROF_T(c1);
+        PROF_ADD(3, c0, c1);
 #pragma unroll
-        for (int cc = 0; cc < HD / 16; ++cc) {
+        for (int cc = 0; cc < OW / 16; ++cc) {
           uint32_t pv[16];
-          TA_TMEM_LD16(tbase + 2 * kBc + cc * 16, pv);
+          TA_TMEM_LD16(tbase + 2 * kBc + hc * OW + cc * 16, pv);
           tmem_ld_wait();
 #pragma unroll
           for (int e = 0; e < 16; ++e) O[cc * 16 + e] = __fmaf_rn(cpv_p, __uint_as_float(pv[e]), O[cc * 16 + e]);
           if (tap_p) {
-            for (int e = 0; e < 16; ++e) args.tap.pv_int[(r & 63) * HD + cc * 16 + e] = (int)__uint_as_float(pv[e]);
+            for (int e = 0; e < 16; ++e)
+              args.tap.pv_int[(r & 63) * HD + hc * OW + cc * 16 + e] = (int)__uint_as_float(pv[e]);
           }
         }
         tc_fence_before();
         if (j < nkv) mbar_arrive(&sm.pv_free[slot]);
+        PROF_T(c2);
+        PROF_ADD(4, c1, c2);
       }
       if (j < nkv) {
         const int sb = j & 1;
-        const uint32_t tS = tbase + sb * kBc;
-        constexpr int CW = 32;
+        const uint32_t tS = tbase + sb * kBc + hc * SW;
         tmem_st_wait();
+        PROF_T(q0);
         mbar_wait(&sm.pmax_bar[slot][grp], j & 1);
-        const float a_p = args.block_q == 64 ? fmaxf(red_p[sb * 4 + 2 * half], red_p[sb * 4 + 2 * half + 1])
-                                             : fmaxf(fmaxf(red_p[sb * 4], red_p[sb * 4 + 1]),
-                                                     fmaxf(red_p[sb * 4 + 2], red_p[sb * 4 + 3]));
+        PROF_T(q1);
+        PROF_ADD(5, q0, q1);
+        float a_p = 0.f;
+#pragma unroll
+        for (int x = 0; x < SP; ++x)
+          a_p = args.block_q == 64
+                    ? fmaxf(a_p, fmaxf(red_p[(sb * 4 + 2 * half) * SP + x], red_p[(sb * 4 + 2 * half + 1) * SP + x]))
+                    : fmaxf(a_p, fmaxf(fmaxf(red_p[(sb * 4) * SP + x], red_p[(sb * 4 + 1) * SP + x]),
+                                       fmaxf(red_p[(sb * 4 + 2) * SP + x], red_p[(sb * 4 + 3) * SP + x])));
         const float inv_p = a_p > 0.f ? __fdiv_rn(kDiv, a_p) : 0.f;
         const float s_p = __fdiv_rn(a_p, kDiv);
-        // Q(P~) codes in [0, 119] -> smem (A operand of the PV MMA)
+        // Q(P~) codes in [0, 119] as fp16 -> smem (A operand of the PV MMA)
         uint8_t* prow = reinterpret_cast<uint8_t*>(sm.p[slot][sb]);
         constexpr float kMagicF16 = 12582912.0f + 25600.0f;  // 1.5*2^23 + 0x6400
+        const __half2 c1024 = __half2(__float2half_rn(1024.f), __float2half_rn(1024.f));
 #pragma unroll 1
-        for (int ch = 0; ch < kBc / CW; ++ch) {
+        for (int ch = 0; ch < SW / CW; ++ch) {
           uint32_t v[CW];
-          TA_TMEM_LD32(tS + ch * CW, v);
+          TA_TMEM_LD(CW, tS + ch * CW, v);
           tmem_ld_wait();
 #pragma unroll
           for (int hh = 0; hh < CW / 8; ++hh) {
@@ -380,14 +450,13 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
             for (int e = 0; e < 8; ++e)
               y[e] = __float_as_uint(__fmaf_rn(__uint_as_float(v[8 * hh + e]), inv_p, kMagicF16));
             uint32_t w[4];
-            const __half2 c1024 = __half2(__float2half_rn(1024.f), __float2half_rn(1024.f));
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const uint32_t hb = __byte_perm(y[2 * e], y[2 * e + 1], 0x5410);
               const __half2 hv = __hsub2(*reinterpret_cast<const __half2*>(&hb), c1024);  // exact
               w[e] = *reinterpret_cast<const uint32_t*>(&hv);
             }
-            const int chunk = ch * (CW / 8) + hh;
+            const int chunk = (hc * SW + ch * CW) / 8 + hh;
             *reinterpret_cast<uint4*>(prow + p_swz(r, chunk)) = make_uint4(w[0], w[1], w[2], w[3]);
             if (tap_j)
               *reinterpret_cast<uint2*>(args.tap.p_codes + (r & 63) * kBc + chunk * 8) =
@@ -396,13 +465,15 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
         }
         tc_fence_before();
         mbar_arrive(&sm.s_free[slot][sb]);
-        if (tap_j) {
+        if (tap_j && hc == 0) {
           args.tap.m_new[r & 63] = m;
           if ((r & 63) == 0) args.tap.s_p[0] = s_p;
         }
         fence_proxy_async();
         mbar_arrive(&sm.p_full[slot][sb]);
         sp_j = s_p;
+        PROF_T(q2);
+        PROF_ADD(6, q1, q2);
       }
       // Scaled-O bookkeeping, after PV(j-1) has landed in Ohat: O_true = A * Ohat,
       // tile j's alpha multiplies everything accumulated so far; fold A
@@ -411,7 +482,7 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
         const float An = A * alpha_j;
         if (!(An >= 1e-30f)) {
 #pragma unroll
-          for (int c = 0; c < HD; ++c) O[c] *= An;
+          for (int c = 0; c < OW; ++c) O[c] *= An;
           A = 1.f;
         } else {
           A = An;
@@ -421,18 +492,23 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
       cpv_p = cpv;
       tap_p = tap_j;
     }
+    if (SP == 2) {  // l = l_0 + l_1 (fixed order)
+      sm.lsum[slot][hc][r] = l;
+      named_bar_sync(bar_pair, 64);
+      l = sm.lsum[slot][0][r] + sm.lsum[slot][1][r];
+    }
     // Epilogue: O_i = diag(l)^-1 O, L_i = m + log l
     if (row_ok) {
       const float f = A / l;
-      __half* orow = args.o + (((size_t)b * N + row) * args.Hq + h) * HD;
+      __half* orow = args.o + (((size_t)b * N + row) * args.Hq + h) * HD + hc * OW;
 #pragma unroll
-      for (int c = 0; c < HD / 8; ++c) {
+      for (int c = 0; c < OW / 8; ++c) {
         __half2 hv[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) hv[e] = __floats2half2_rn(O[c * 8 + 2 * e] * f, O[c * 8 + 2 * e + 1] * f);
         reinterpret_cast<uint4*>(orow)[c] = *reinterpret_cast<uint4*>(hv);
       }
-      args.lse[((size_t)b * args.Hq + h) * N + row] = m + logf(l);
+      if (hc == 0) args.lse[((size_t)b * args.Hq + h) * N + row] = m + logf(l);
     }
   }
   tc_fence_before();
@@ -441,6 +517,12 @@ __global__ void __launch_bounds__(128 * (NS + 1), 1)
     tc_fence_after();
     tmem_dealloc(tmem, kTmemCols);
   }
+#ifdef TURBO_PROFILE
+  if (threadIdx.x == 0) {
+    atomicAdd(&g_prof[20], (unsigned long long)nkv);
+    atomicAdd(&g_prof[21], 1ull);
+  }
+#endif
 }
 
 }  // namespace ta
@@ -473,6 +555,16 @@ static bool make_map_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t 
              CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+
+#ifdef TURBO_PROFILE
+extern "C" TURBO_API void turbo_debug_prof(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_prof, sizeof(g_prof));
+  if (reset) {
+    unsigned long long z[32] = {0};
+    cudaMemcpyToSymbol(g_prof, z, sizeof(z));
+  }
+}
+#endif
 
 cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Hq, int Hkv, int causal, const __half* q,
                            const int8_t* k1, const __half* v1t, const float* k1s, const float* v1s, __half* o,
@@ -507,19 +599,19 @@ cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Hq, int Hk
   const int G = Hq / Hkv;
   const bool pair = (G % 2) == 0;
   const dim3 grid((unsigned)(a.n_qtiles * B * Hq / (pair ? 2 : 1)));
-#define TA_LAUNCH_T(HDV, NSV, TAPV)                                                                        \
+#define TA_LAUNCH_T(HDV, NSV, SPV, TAPV)                                                                  \
   {                                                                                                        \
-    const size_t smem = sizeof(PrefillSmem<HDV, NSV>) + 1024;                                              \
-    cudaFuncSetAttribute(prefill_kernel<HDV, NSV, TAPV>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+    const size_t smem = sizeof(PrefillSmem<HDV, NSV, SPV>) + 1024;                                         \
+    cudaFuncSetAttribute(prefill_kernel<HDV, NSV, SPV, TAPV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                          (int)smem);                                                                       \
-    prefill_kernel<HDV, NSV, TAPV><<<grid, 128 * (NSV + 1), smem, st>>>(tmk, tmv, a);                      \
+    prefill_kernel<HDV, NSV, SPV, TAPV><<<grid, 128 * (1 + NSV * SPV), smem, st>>>(tmk, tmv, a);           \
   }
-#define TA_LAUNCH(HDV, NSV) \
-  if (a.has_tap) TA_LAUNCH_T(HDV, NSV, true) else TA_LAUNCH_T(HDV, NSV, false)
+#define TA_LAUNCH(HDV, NSV, SPV) \
+  if (a.has_tap) TA_LAUNCH_T(HDV, NSV, SPV, true) else TA_LAUNCH_T(HDV, NSV, SPV, false)
   if (HD == 128) {
-    if (pair) TA_LAUNCH(128, 2) else TA_LAUNCH(128, 1)
+    if (pair) TA_LAUNCH(128, 2, TA_PREFILL_SPLIT) else TA_LAUNCH(128, 1, TA_PREFILL_SPLIT)
   } else {
-    if (pair) TA_LAUNCH(64, 2) else TA_LAUNCH(64, 1)
+    if (pair) TA_LAUNCH(64, 2, TA_PREFILL_SPLIT) else TA_LAUNCH(64, 1, TA_PREFILL_SPLIT)
   }
 #undef TA_LAUNCH
 #undef TA_LAUNCH_T
