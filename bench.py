@@ -62,7 +62,7 @@ class Clocks:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+                                       "-lms", "50"], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
 
@@ -128,13 +128,17 @@ def run_ours(args, rank, world, device):
         return o, lse, od, lsed
 
     launches_per_step = 2 + 1 + 2 + (2 if S > 1 else 1)
+    clk = Clocks(device) if rank == 0 else None  # sampler runs through the soak and the timed steps
     for _ in range(args.warmup):
         step(q, k, v, qd, kd, vd)
     torch.cuda.synchronize()
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < 0.7:  # untimed soak: clocks/power settle, sampler is live
+        step(q, k, v, qd, kd, vd)
+        torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    clk = Clocks(device) if rank == 0 else None
     evs = [[ev() for _ in range(4)] for _ in range(args.steps)]
     for i in range(args.steps):
         flush.zero_()  # L2 flush between timed steps (outside the events)
@@ -437,7 +441,7 @@ def run_decode_long(args, rank, world, device):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--splits", type=int, default=4, help="split-KV count of the decode in the step")

@@ -102,7 +102,8 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
   constexpr uint32_t kTmemCols = NS == 2 ? 512 : 256;  // per slot: S0 [0,64) S1 [64,128) PV [128,128+d)
 
   // Work item: (query tile, batch, kv head, head group of NS); heaviest
-  // (last) query tiles first for causal load balance.
+  // (last) query tiles first for causal load balance (a unit-major order that
+  // shares K/V in L2 measured 4% slower).
   const int G = args.Hq / args.Hkv, GS = G / NS;
   const int units = args.B * args.Hkv * GS;
   const int it = args.n_qtiles - 1 - (int)(blockIdx.x / units);
