@@ -330,19 +330,25 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
           if (tap_j)
             for (int c = 0; c < CW; ++c)
               args.tap.s_int[(r & 63) * kBc + hc * SW + ch * CW + c] = ch * CW + c < nv ? (int)v[c] : 0;
+          const f32x2 cq2 = pk2(cqk, cqk);
           if (full) {
 #pragma unroll
-            for (int c = 0; c < CW; ++c) {
-              const float x = __fmul_rn((float)(int)v[c], cqk);
-              mt = fmaxf(mt, x);
-              v[c] = __float_as_uint(x);
+            for (int c = 0; c < CW; c += 2) {
+              const f32x2 x2 = mul2(pk2((float)(int)v[c], (float)(int)v[c + 1]), cq2);
+              const float x0 = lo2(x2), x1 = hi2(x2);
+              mt = fmaxf(mt, fmaxf(x0, x1));
+              v[c] = __float_as_uint(x0);
+              v[c + 1] = __float_as_uint(x1);
             }
           } else {
 #pragma unroll
-            for (int c = 0; c < CW; ++c) {
-              const float x = ch * CW + c < nv ? __fmul_rn((float)(int)v[c], cqk) : -INFINITY;
-              mt = fmaxf(mt, x);
-              v[c] = __float_as_uint(x);
+            for (int c = 0; c < CW; c += 2) {
+              const f32x2 x2 = mul2(pk2((float)(int)v[c], (float)(int)v[c + 1]), cq2);
+              const float x0 = ch * CW + c < nv ? lo2(x2) : -INFINITY;
+              const float x1 = ch * CW + c + 1 < nv ? hi2(x2) : -INFINITY;
+              mt = fmaxf(mt, fmaxf(x0, x1));
+              v[c] = __float_as_uint(x0);
+              v[c + 1] = __float_as_uint(x1);
             }
           }
           TA_TMEM_ST(CW, tS + ch * CW, v);
@@ -361,22 +367,39 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
         else if (args.alpha_mode == 1 && m_new == m) alpha = 1.f;
         const float m_use = active ? m_new : 0.f;  // inactive row: every x = -inf -> P~ = 0
         tmem_st_wait();
-        // P~ = SAS(x - m_new), in place in TMEM
-        float rsum = 0.f, pmax = 0.f;
+        // P~ = SAS(x - m_new), in place in TMEM; two elements per
+        // FADD2 / FFMA2 / FMUL2, bit-identical to the scalar sas_eval.
+        float pmax = 0.f;
+        f32x2 rsum2 = pk2(0.f, 0.f);
+        {
+          const f32x2 m2 = pk2(m_use, m_use), mg2 = pk2(kMagic, kMagic);
+          const f32x2 c3 = pk2(-0.1025f, -0.1025f), c2 = pk2(0.4626f, 0.4626f), c1 = pk2(-0.9922f, -0.9922f),
+                      c0 = pk2(0.9996f, 0.9996f);
 #pragma unroll 1
-        for (int ch = 0; ch < SW / CW; ++ch) {
-          uint32_t v[CW];
-          TA_TMEM_LD(CW, tS + ch * CW, v);
-          tmem_ld_wait();
+          for (int ch = 0; ch < SW / CW; ++ch) {
+            uint32_t v[CW];
+            TA_TMEM_LD(CW, tS + ch * CW, v);
+            tmem_ld_wait();
 #pragma unroll
-          for (int c = 0; c < CW; ++c) {
-            const float pt = sas_eval(__fsub_rn(m_use, __uint_as_float(v[c])), lut_lane, nr_abs);
-            rsum += pt;
-            pmax = fmaxf(pmax, pt);
-            v[c] = __float_as_uint(pt);
+            for (int c = 0; c < CW; c += 2) {
+              const f32x2 d2 = sub2(m2, pk2(__uint_as_float(v[c]), __uint_as_float(v[c + 1])));
+              const f32x2 t2 = add2_rd(d2, mg2);           // kMagic + floor(d)
+              const f32x2 f2 = sub2(d2, sub2(t2, mg2));    // d - floor(d), exact
+              const float l0 = lut_shfl(lut_lane, __float_as_uint(lo2(t2)));
+              const float l1 = lut_shfl(lut_lane, __float_as_uint(hi2(t2)));
+              const f32x2 p2 = fma2(fma2(fma2(c3, f2, c2), f2, c1), f2, c0);
+              const f32x2 lp = mul2(pk2(l0, l1), p2);
+              const float pt0 = lo2(d2) > nr_abs ? 0.f : lo2(lp);
+              const float pt1 = hi2(d2) > nr_abs ? 0.f : hi2(lp);
+              rsum2 = add2(rsum2, pk2(pt0, pt1));
+              pmax = fmaxf(pmax, fmaxf(pt0, pt1));
+              v[c] = __float_as_uint(pt0);
+              v[c + 1] = __float_as_uint(pt1);
+            }
+            TA_TMEM_ST(CW, tS + ch * CW, v);
           }
-          TA_TMEM_ST(CW, tS + ch * CW, v);
         }
+        const float rsum = lo2(rsum2) + hi2(rsum2);
         if (active) {
           l = alpha * l + rsum;  // l = SAS(m_prev - m_new) l + rowsum(P~), this half's share
           m = m_new;
@@ -406,7 +429,12 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
           TA_TMEM_LD16(tbase + 2 * kBc + hc * OW + cc * 16, pv);
           tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 16; ++e) O[cc * 16 + e] = __fmaf_rn(cpv_p, __uint_as_float(pv[e]), O[cc * 16 + e]);
+          for (int e = 0; e < 16; e += 2) {
+            const f32x2 o2 = fma2(pk2(cpv_p, cpv_p), pk2(__uint_as_float(pv[e]), __uint_as_float(pv[e + 1])),
+                                  pk2(O[cc * 16 + e], O[cc * 16 + e + 1]));
+            O[cc * 16 + e] = lo2(o2);
+            O[cc * 16 + e + 1] = hi2(o2);
+          }
           if (tap_p) {
             for (int e = 0; e < 16; ++e)
               args.tap.pv_int[(r & 63) * HD + hc * OW + cc * 16 + e] = (int)__uint_as_float(pv[e]);
@@ -447,9 +475,13 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
           for (int hh = 0; hh < CW / 8; ++hh) {
             // y = 1.5*2^23 + 0x6400 + code: its low half-word is the fp16 of 1024 + code
             uint32_t y[8];
+            const f32x2 inv2 = pk2(inv_p, inv_p), mf2 = pk2(kMagicF16, kMagicF16);
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
-              y[e] = __float_as_uint(__fmaf_rn(__uint_as_float(v[8 * hh + e]), inv_p, kMagicF16));
+            for (int e = 0; e < 8; e += 2) {
+              const f32x2 y2 = fma2(pk2(__uint_as_float(v[8 * hh + e]), __uint_as_float(v[8 * hh + e + 1])), inv2, mf2);
+              y[e] = __float_as_uint(lo2(y2));
+              y[e + 1] = __float_as_uint(hi2(y2));
+            }
             uint32_t w[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
