@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
         const int sb = j & 1;
         const uint32_t tS = tbase + sb * kBc + hc * SW;  // this thread's S columns (reused for x, P~)
         PROF_T(p0);
-        mbar_wait(&sm.s_full[slot][sb], (j >> 1) & 1);
+        mbar_wait_spin(&sm.s_full[slot][sb], (j >> 1) & 1);
         tc_fence_after();
         PROF_T(p1);
         PROF_ADD(0, p0, p1);
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
       // O += (s_P s_V / A) Q(P~) V^q1 for the previous tile
       if (j >= 1) {
         PROF_T(c0);
-        mbar_wait(&sm.pv_full[slot], (j - 1) & 1);
+        mbar_wait_spin(&sm.pv_full[slot], (j - 1) & 1);
         tc_fence_after();
         PROF_T(c1);
         PROF_ADD(3, c0, c1);
@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
         const uint32_t tS = tbase + sb * kBc + hc * SW;
         tmem_st_wait();
         PROF_T(q0);
-        mbar_wait(&sm.pmax_bar[slot][grp], j & 1);
+        mbar_wait_spin(&sm.pmax_bar[slot][grp], j & 1);
         PROF_T(q1);
         PROF_ADD(5, q0, q1);
         float a_p = 0.f;
