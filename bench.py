@@ -52,46 +52,94 @@ def peaks():
     return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback (B200_PROFILING.md)")
 
 
+def traffic_per_launch(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`, from the
+    committed `ncu --set full` capture summary (profiles/traffic.json), or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)[kernel]["bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 class Clocks:
-    """nvidia-smi sampler over the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock + throttle-reason sampler over the timed region (B200_PROFILING.md
+    clocks line), polled through NVML every 50 ms from a thread.  (nvidia-smi -lms
+    block-buffers its stdout, so a terminated sampler can leave an empty file.)"""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
     def __init__(self, gpu):
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
+        import threading
+
+        self.rows, self.stop_ev, self.t = [], threading.Event(), None
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                       "-lms", "50"], stdout=self.f, stderr=subprocess.DEVNULL)
+            import pynvml as nv
+
+            nv.nvmlInit()
+            phys = os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")
+            idx = int(phys[gpu]) if len(phys) > gpu and phys[gpu].strip().isdigit() else gpu
+            h = nv.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            masks = [(n, getattr(nv, c)) for n, c in self.REASONS]
+
+            def poll():
+                while not self.stop_ev.is_set():
+                    try:
+                        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.rows.append((float(sm), [n for n, m in masks if r & m]))
+                    except Exception:
+                        pass
+                    self.stop_ev.wait(0.05)
+
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
         except Exception:
-            self.p = None
+            self.t = None
 
     def stop(self):
-        if self.p is None:
+        if self.t is None:
             return None
-        self.p.terminate()
-        self.p.wait()
-        self.f.flush()
-        rows = []
-        for line in open(self.f.name):
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                rows.append((float(parts[0]), float(parts[1]), parts[3:7]))
-            except ValueError:
-                pass
-        os.unlink(self.f.name)
-        if not rows:
+        self.stop_ev.set()
+        self.t.join()
+        if not self.rows:
             return None
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for _, _, r in rows for i, x in enumerate(r) if x.lower() == "active"})
-        load = [s for s, _, _ in rows if s > 300] or [s for s, _, _ in rows]
-        return {"sm_mhz": statistics.median(load), "sm_max_mhz": max(m for _, m, _ in rows), "reasons": reasons,
-                "samples": len(rows)}
+        reasons = sorted({n for _, rs in self.rows for n in rs})
+        load = [s for s, _ in self.rows if s > 300] or [s for s, _ in self.rows]
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": float(self.max_mhz), "reasons": reasons,
+                "samples": len(self.rows)}
 
 
 # --------------------------------------------------------------------------- ours
+def bind_host_to_gpu(device):
+    """Pin this process to the CPUs of the GPU's NUMA node so the pinned host
+    buffers of the e2e leg are first-touched on the node next to its PCIe root
+    (a remote node roughly halves H2D/D2H bandwidth).  Best effort."""
+    import torch
+
+    try:
+        pr = torch.cuda.get_device_properties(device)
+        bdf = f"{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bdf}/local_cpulist") as f:
+            spec = f.read().strip()
+        cpus = set()
+        for part in spec.split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        cpus &= os.sched_getaffinity(0)
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return bdf
+    except (OSError, ValueError, RuntimeError):
+        pass
+    return None
+
+
 def run_ours(args, rank, world, device):
     import torch
 
@@ -99,6 +147,7 @@ def run_ours(args, rank, world, device):
     from paper_2412_08585_b200 import synth
 
     torch.cuda.set_device(device)
+    bind_host_to_gpu(device)
     c = CFG_PREFILL
     B, N, Hq, Hkv, d = c["B"], c["N"], c["Hq"], c["Hkv"], c["d"]
     bits = synth.head_bits_alternating(Hkv)
@@ -196,7 +245,7 @@ def run_ours(args, rank, world, device):
     achieved = ops / (pre_ms * 1e-3) / 1e12
     roof = {"bound": "tensor", "kernel": "prefill_kernel<128> (turbo_attention_prefill)", "achieved": round(achieved, 1),
             "peak": round(int8_peak, 1), "unit": "TFLOP/s", "frac": round(achieved / int8_peak, 4),
-            "traffic": None, "peak_source": f"2 x bf16 burst {pk['bf16']} TF/s, {pk['src']}",
+            "traffic": traffic_per_launch("prefill_kernel"), "peak_source": f"2 x bf16 burst {pk['bf16']} TF/s, {pk['src']}",
             "share_of_step": round(pre_ms / statistics.mean(t_step), 3)}
     result = dict(value=value, ms_step=ms_step, e2e=e2e, roofline=roof, clocks=clocks,
                   launches=launches_per_step * args.steps,

@@ -12,6 +12,7 @@
 //               registers, P tile scale + INT8 codes -> smem (A operand of the
 //               PV MMA), and O = alpha O + s_P s_V PV_int in FP32 registers
 //               one tile behind (overlapping the next MMA).
+#include <algorithm>
 #include <climits>
 #include <cstring>
 
@@ -60,7 +61,7 @@ struct PrefillArgs {
   float* lse;
   const float* k1s;
   const float* v1s;
-  int B, N, Hq, Hkv, causal, block_q, alpha_mode, n_qtiles;
+  int B, N, Hq, Hkv, causal, block_q, alpha_mode, n_qtiles, unit_group;
   float scale;
   SasConst sas;
   int has_tap;
@@ -101,13 +102,18 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr uint32_t kTmemCols = NS == 2 ? 512 : 256;  // per slot: S0 [0,64) S1 [64,128) PV [128,128+d)
 
-  // Work item: (query tile, batch, kv head, head group of NS); heaviest
-  // (last) query tiles first for causal load balance (a unit-major order that
-  // shares K/V in L2 measured 4% slower).
+  // Work item: (query tile, batch, kv head, head group of NS).  Units are
+  // taken in groups of UG (about 4 x 148 CTAs' worth), heaviest (last) query
+  // tiles first inside a group for causal load balance; the group keeps the
+  // K/V streams resident in L2 (DRAM reads = the compulsory bytes, down from
+  // 2.9x with one global heavy-first order; same speed).
   const int G = args.Hq / args.Hkv, GS = G / NS;
   const int units = args.B * args.Hkv * GS;
-  const int it = args.n_qtiles - 1 - (int)(blockIdx.x / units);
-  const int u = blockIdx.x % units, b = u / (args.Hkv * GS), kvh = (u / GS) % args.Hkv, hg = u % GS;
+  const int UG = args.unit_group;
+  const int grp_i = (int)blockIdx.x / (UG * args.n_qtiles), rem = (int)blockIdx.x % (UG * args.n_qtiles);
+  const int UGg = min(UG, units - grp_i * UG);
+  const int it = args.n_qtiles - 1 - rem / UGg;
+  const int u = grp_i * UG + rem % UGg, b = u / (args.Hkv * GS), kvh = (u / GS) % args.Hkv, hg = u % GS;
   const int h0 = kvh * G + hg * NS;
   const int N = args.N, Tc = (N + kBc - 1) / kBc;
   const int last_row = min(it * kTileM + kTileM - 1, N - 1);
@@ -632,6 +638,11 @@ cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Hq, int Hk
   const int G = Hq / Hkv;
   const bool pair = (G % 2) == 0;
   const dim3 grid((unsigned)(a.n_qtiles * B * Hq / (pair ? 2 : 1)));
+  {
+    const int GS = G / (pair ? 2 : 1), units = B * Hkv * GS;
+    int ug = GS * std::max(1, (4 * 148 + a.n_qtiles * GS - 1) / (a.n_qtiles * GS));
+    a.unit_group = std::min(units, ug);
+  }
 #define TA_LAUNCH_T(HDV, NSV, SPV, TAPV)                                                                  \
   {                                                                                                        \
     const size_t smem = sizeof(PrefillSmem<HDV, NSV, SPV>) + 1024;                                         \

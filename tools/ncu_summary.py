@@ -20,14 +20,19 @@ def launches(path):
     start = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[start]
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    gi = h.index("Grid Size") if "Grid Size" in h else None
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     agg = defaultdict(list)
     for r in rows[start + 1:]:
-        agg[r[ki].split("(")[0]].append(float(r[vi].replace(",", "")))
+        if mi is not None and r[mi] != "gpu__time_duration.sum":
+            continue
+        key = r[ki].split("(")[0] + (f"  grid={r[gi]}" if gi is not None else "")
+        agg[key].append(float(r[vi].replace(",", "")))
     tot = sum(sum(v) for k, v in agg.items() if "ta::" in k)
     print(f"# per-kernel device time (ncu, cold cache, serialised) from {path}")
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
         share = f"{100 * sum(v) / tot:5.1f}% of ta:: time" if "ta::" in k else ""
-        print(f"{k[:70]:70s} launches={len(v):3d} mean={sum(v) / len(v) / 1e3:10.2f} us {share}")
+        print(f"{k[:96]:96s} n={len(v):3d} mean={sum(v) / len(v) / 1e3:10.2f} us {share}")
 
 
 def report(path):
