@@ -74,118 +74,180 @@ TA_DEV void pack_record(const int8_t* tile, int kind, int bits, uint8_t* rec_cod
 }
 
 // ---------------------------------------------------------------------------
-// PREFILL: one CTA per (block j, kv_head h, batch b); K and V of the block.
+// PREFILL: one CTA per (block j, kv_head h, batch b); thread = (kind, channel)
+// holds its channel's 64 tokens in registers, so the block max, stage-1 codes,
+// the stage-2 column statistics and the V record words need no shared-memory
+// round trips; only K's token-major outputs are transposed through smem.
+
+// 8 bytes, each < 16, -> one LSB-first 4-bit word.
+TA_DEV uint32_t pack_nib8(uint2 v) {
+  unsigned long long x = (unsigned long long)v.x | ((unsigned long long)v.y << 32);
+  x = (x | (x >> 4)) & 0x00FF00FF00FF00FFull;
+  x = (x | (x >> 8)) & 0x0000FFFF0000FFFFull;
+  return (uint32_t)(x | (x >> 16));
+}
+// 8 bytes, each < 4, -> one LSB-first 16-bit group of 2-bit codes.
+TA_DEV uint32_t pack_crumb8(uint2 v) {
+  unsigned long long x = (unsigned long long)v.x | ((unsigned long long)v.y << 32);
+  x = (x | (x >> 6)) & 0x000F000F000F000Full;
+  x = (x | (x >> 12)) & 0x000000FF000000FFull;
+  return (uint32_t)(x | (x >> 24)) & 0xFFFFu;
+}
+
 template <int HD>
-__global__ void __launch_bounds__(256) quant_prefill_kernel(
+__global__ void __launch_bounds__(2 * HD, 256 / HD) quant_prefill_kernel(
     const __half* __restrict__ k, const __half* __restrict__ v, int N, int Hkv, int max_blocks,
     const int32_t* __restrict__ bits_dev, uint8_t* __restrict__ block_rec, float* __restrict__ s_parent,
     float* __restrict__ a_univ, int8_t* __restrict__ k1, __half* __restrict__ v1t, float* __restrict__ k1s,
     float* __restrict__ v1s) {
-  __shared__ __align__(16) int8_t tile[2][kBc * HD];
-  __shared__ float red[2][8];
+  constexpr int NW = HD / 32;  // warps per kind
+  __shared__ __align__(16) uint8_t tile1[kBc * HD];  // K stage-1 codes [t][c]
+  __shared__ __align__(16) uint8_t tile2[kBc * HD];  // K stage-2 codes [t][c]
+  __shared__ float red[2][NW];
   const int j = blockIdx.x, h = blockIdx.y, b = blockIdx.z, tid = threadIdx.x;
+  const int kind = tid / HD, c = tid % HD;
   const int Tc = (N + kBc - 1) / kBc;
   const int rows = min(kBc, N - j * kBc);
-  constexpr int CPR = HD / 8;                 // 16-byte chunks per token row
-  constexpr int NCH = kBc * CPR / 256;        // chunks per thread (4 for HD=128)
-  uint4 raw[2][NCH];
-  float amax[2] = {0.f, 0.f};
-#pragma unroll
-  for (int kv = 0; kv < 2; ++kv) {
-    const __half* src = kv == 0 ? k : v;
-#pragma unroll
-    for (int i = 0; i < NCH; ++i) {
-      const int ch = tid + i * 256, t = ch / CPR, c8 = ch % CPR;
-      uint4 x = make_uint4(0, 0, 0, 0);
-      if (t < rows)
-        x = *reinterpret_cast<const uint4*>(src + (((size_t)b * N + (size_t)j * kBc + t) * Hkv + h) * HD + c8 * 8);
-      raw[kv][i] = x;
-      const __half2* hp = reinterpret_cast<const __half2*>(&x);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        float2 f = __half22float2(hp[e]);
-        amax[kv] = fmaxf(amax[kv], fmaxf(fabsf(f.x), fabsf(f.y)));
-      }
-    }
-    amax[kv] = warp_max(amax[kv]);
-  }
-  if ((tid & 31) == 0) {
-    red[0][tid >> 5] = amax[0];
-    red[1][tid >> 5] = amax[1];
-  }
-  __syncthreads();
-  float a[2], inv[2], sc[2];
-#pragma unroll
-  for (int kv = 0; kv < 2; ++kv) {
-    a[kv] = red[kv][0];
-#pragma unroll
-    for (int w = 1; w < 8; ++w) a[kv] = fmaxf(a[kv], red[kv][w]);
-    // s = max|x| / 119, codes = round_half_even(x * (119 / max|x|)) (Alg. 1; R-2, R-3, R-5)
-    inv[kv] = a[kv] > 0.f ? __fdiv_rn(kDiv, a[kv]) : 0.f;
-    sc[kv] = __fdiv_rn(a[kv], kDiv);
-  }
-  // Stage-1 codes: k1 row-major to global, both tiles to smem.
-#pragma unroll
-  for (int kv = 0; kv < 2; ++kv) {
-#pragma unroll
-    for (int i = 0; i < NCH; ++i) {
-      const int ch = tid + i * 256, t = ch / CPR, c8 = ch % CPR;
-      const __half2* hp = reinterpret_cast<const __half2*>(&raw[kv][i]);
-      uint32_t lo = 0, hi = 0;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        float2 f = __half22float2(hp[e]);
-        uint32_t c0 = (uint32_t)(rint_prod(f.x, inv[kv]) & 0xFF), c1 = (uint32_t)(rint_prod(f.y, inv[kv]) & 0xFF);
-        uint32_t pair = c0 | (c1 << 8);
-        if (e < 2) lo |= pair << (16 * e);
-        else hi |= pair << (16 * (e - 2));
-      }
-      *reinterpret_cast<uint2*>(&tile[kv][t * HD + c8 * 8]) = make_uint2(lo, hi);
-      if (kv == 0 && t < rows)
-        *reinterpret_cast<uint2*>(k1 + (((size_t)b * Hkv + h) * N + (size_t)j * kBc + t) * HD + c8 * 8) =
-            make_uint2(lo, hi);
-    }
-  }
   const size_t bh = (size_t)b * Hkv + h;
-  if (tid == 0) {
-    k1s[bh * Tc + j] = sc[0];
-    v1s[bh * Tc + j] = sc[1];
+  const __half* src = (kind ? v : k) + (((size_t)b * N + (size_t)j * kBc) * Hkv + h) * HD + c;
+  const size_t tstride = (size_t)Hkv * HD;
+
+  // the channel's 64 tokens as 32 half2
+  __half2 xh[kBc / 2];
+  __half2 amax2 = __float2half2_rn(0.f);
+#pragma unroll
+  for (int t = 0; t < kBc; t += 2) {
+    const __half z = __float2half_rn(0.f);
+    xh[t / 2] = __halves2half2(t < rows ? __ldcs(src + t * tstride) : z, t + 1 < rows ? __ldcs(src + (t + 1) * tstride) : z);
+    amax2 = __hmax2(amax2, __habs2(xh[t / 2]));
+  }
+  float amax = fmaxf(__low2float(amax2), __high2float(amax2));  // exact: max of fp16 magnitudes
+  amax = warp_max(amax);
+  if ((tid & 31) == 0) red[kind][c >> 5] = amax;
+  __syncthreads();
+  float a = red[kind][0];
+#pragma unroll
+  for (int w = 1; w < NW; ++w) a = fmaxf(a, red[kind][w]);
+  // s = max|x| / 119, codes = round_half_even(x * (119 / max|x|)) (Alg. 1; R-2, R-3, R-5)
+  const float inv = a > 0.f ? __fdiv_rn(kDiv, a) : 0.f;
+  const float sc = __fdiv_rn(a, kDiv);
+  // stage-1 code of token t, recomputed where needed (2 instructions) instead of held
+  auto q1 = [&](int t) -> int {
+    return rint_prod((t & 1) ? __high2float(xh[t >> 1]) : __low2float(xh[t >> 1]), inv);
+  };
+  if (c == 0) {
+    (kind ? v1s : k1s)[bh * Tc + j] = sc;
     // universal max-abs per (b, h, K/V) (R-9): non-negative floats order as ints
-    atomicMax(reinterpret_cast<int*>(a_univ + bh * 2 + 0), __float_as_int(a[0]));
-    atomicMax(reinterpret_cast<int*>(a_univ + bh * 2 + 1), __float_as_int(a[1]));
+    atomicMax(reinterpret_cast<int*>(a_univ + bh * 2 + kind), __float_as_int(a));
+    if (rows == kBc) s_parent[(bh * 2 + kind) * max_blocks + j] = sc;
+  }
+  if (kind == 0) {
+#pragma unroll
+    for (int t = 0; t < kBc; ++t) tile1[t * HD + c] = (uint8_t)q1(t);
+  } else {
+    // v1t: the block transposed, [d][B_c], codes as fp16 (exact) -- the B operand
+    // of the prefill's kind::f16 P V MMA; tokens past N are 0.
+    uint4* dst = reinterpret_cast<uint4*>(v1t + ((bh * Tc + j) * HD + c) * kBc);
+#pragma unroll
+    for (int t8 = 0; t8 < kBc / 8; ++t8) {
+      uint32_t u[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const __half2 hv = __halves2half2(__int2half_rn(q1(8 * t8 + 2 * e)), __int2half_rn(q1(8 * t8 + 2 * e + 1)));
+        u[e] = *reinterpret_cast<const uint32_t*>(&hv);
+      }
+      dst[t8] = make_uint4(u[0], u[1], u[2], u[3]);
+    }
+  }
+  const int bits = bits_dev[h * 2 + kind];
+  constexpr int REC = rec_bytes(HD);
+  uint8_t* rec = block_rec + ((bh * 2 + kind) * (size_t)max_blocks + j) * REC;
+  if (rows == kBc) {
+    // Stage 2 of this channel (integer only, R-6): z = min, s = max(1, ceil((max-min)/(2^b-1))),
+    // code = floor((2 (v - z) + s) / (2 s)) = fl((2(v-z)+s) * fl(1/(2s)) + 2^-10) truncated
+    // (exact for these ranges, tests/test_quant_arith.py).
+    int mn = q1(0), mx = mn;
+#pragma unroll
+    for (int t = 1; t < kBc; ++t) {
+      mn = min(mn, q1(t));
+      mx = max(mx, q1(t));
+    }
+    const int range = mx - mn;
+    const int sint = max(1, bits == 4 ? (range + 14) / 15 : (range + 2) / 3);
+    const float inv2s = __fdiv_rn(1.0f, (float)(2 * sint));
+    auto q = [&](int t) -> uint32_t {
+      return (uint32_t)__float2int_rz(__fmaf_rn((float)(2 * (q1(t) - mn) + sint), inv2s, 0.0009765625f));
+    };
+    rec[c] = (uint8_t)sint;
+    rec[HD + c] = (uint8_t)(int8_t)mn;
+    if (kind == 0) {
+#pragma unroll
+      for (int t = 0; t < kBc; ++t) tile2[t * HD + c] = (uint8_t)q(t);
+    } else if (bits == 4) {
+      // V, 4-bit: word W = 4jj + qd, byte e: token 32jj + 4qd + e (lo), + 16 (hi) (layout.cuh)
+      uint32_t w[8];
+#pragma unroll
+      for (int W = 0; W < 8; ++W) {
+        const int jj = W >> 2, qd = W & 3;
+        uint32_t acc = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          acc |= (q(32 * jj + 4 * qd + e) | (q(32 * jj + 16 + 4 * qd + e) << 4)) << (8 * e);
+        w[W] = acc;
+      }
+      uint4* dst = reinterpret_cast<uint4*>(rec + 2 * HD + c * (kBc / 2));
+      dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+      dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    } else {
+      // V, 2-bit: word qd, byte e, bits 2s: token 32(s>>1) + 16(s&1) + 4qd + e
+      uint32_t w[4];
+#pragma unroll
+      for (int qd = 0; qd < 4; ++qd) {
+        uint32_t acc = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+#pragma unroll
+          for (int s2 = 0; s2 < 4; ++s2)
+            acc |= q(32 * (s2 >> 1) + 16 * (s2 & 1) + 4 * qd + e) << (8 * e + 2 * s2);
+        w[qd] = acc;
+      }
+      *reinterpret_cast<uint4*>(rec + 2 * HD + c * (kBc / 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
   }
   __syncthreads();
-  // v1t: the block transposed, [d][B_c], codes as fp16 (exact) -- the B operand
-  // of the prefill's kind::f16 P V MMA; tokens past N are 0 (zero fill).
-  for (int w = tid; w < HD * (kBc / 8); w += 256) {
-    const int c = w / (kBc / 8), t0 = (w % (kBc / 8)) * 8;
-    uint32_t u[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const __half2 hv = __floats2half2_rn((float)tile[1][(t0 + 2 * e) * HD + c], (float)tile[1][(t0 + 2 * e + 1) * HD + c]);
-      u[e] = *reinterpret_cast<const uint32_t*>(&hv);
-    }
-    *reinterpret_cast<uint4*>(v1t + ((bh * Tc + j) * HD + c) * kBc + t0) = make_uint4(u[0], u[1], u[2], u[3]);
+  // k1 rows (token-major, natural channel order) from tile1
+  constexpr int CH16 = kBc * HD / 16;
+  for (int i = tid; i < CH16; i += 2 * HD) {
+    const int t = i / (HD / 16), c16 = i % (HD / 16);
+    if (t < rows)
+      *reinterpret_cast<uint4*>(k1 + (bh * N + (size_t)j * kBc + t) * HD + c16 * 16) =
+          *reinterpret_cast<const uint4*>(tile1 + t * HD + c16 * 16);
   }
   if (rows < kBc) return;  // partial tail block: goes to the buffer (tail kernel)
-  __syncthreads();
-  // Stage 2 (channelwise, integer only) of full blocks into the cache.
-  constexpr int REC = rec_bytes(HD);
-  uint8_t* rec[2];
+  // K record codes: token-major, natural channel order, LSB-first; one uint4 = 4 words per thread
+  const int kbits = bits_dev[h * 2];
+  uint8_t* krec = block_rec + ((bh * 2) * (size_t)max_blocks + j) * REC + 2 * HD;
+  if (kbits == 4) {
+    for (int i = tid; i < kBc * HD / 32; i += 2 * HD) {  // 32 channels (16 B of codes) per item
+      const int t = i / (HD / 32), c32 = i % (HD / 32);
+      const uint4 lo = *reinterpret_cast<const uint4*>(tile2 + t * HD + c32 * 32);
+      const uint4 hi = *reinterpret_cast<const uint4*>(tile2 + t * HD + c32 * 32 + 16);
+      *reinterpret_cast<uint4*>(krec + t * (HD / 2) + c32 * 16) =
+          make_uint4(pack_nib8(make_uint2(lo.x, lo.y)), pack_nib8(make_uint2(lo.z, lo.w)),
+                     pack_nib8(make_uint2(hi.x, hi.y)), pack_nib8(make_uint2(hi.z, hi.w)));
+    }
+  } else {
+    for (int i = tid; i < kBc * HD / 64; i += 2 * HD) {  // 64 channels (16 B of codes) per item
+      const int t = i / (HD / 64), c64 = i % (HD / 64);
+      uint32_t w[4];
 #pragma unroll
-  for (int kv = 0; kv < 2; ++kv) rec[kv] = block_rec + ((bh * 2 + kv) * (size_t)max_blocks + j) * REC;
-  if (tid < 2 * HD) {
-    const int kv = tid / HD, c = tid % HD;
-    uint8_t s;
-    int8_t z;
-    stage2_column(tile[kv], HD, c, bits_dev[h * 2 + kv], &s, &z);
-    rec[kv][c] = s;
-    rec[kv][HD + c] = (uint8_t)z;
+      for (int g = 0; g < 4; ++g) {
+        const uint4 u = *reinterpret_cast<const uint4*>(tile2 + t * HD + c64 * 64 + g * 16);
+        w[g] = pack_crumb8(make_uint2(u.x, u.y)) | (pack_crumb8(make_uint2(u.z, u.w)) << 16);
+      }
+      *reinterpret_cast<uint4*>(krec + t * (HD / 4) + c64 * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
   }
-  __syncthreads();
-#pragma unroll
-  for (int kv = 0; kv < 2; ++kv) pack_record<HD>(tile[kv], kv, bits_dev[h * 2 + kv], rec[kv] + 2 * HD, tid, 256);
-  if (tid < 2) s_parent[(bh * 2 + tid) * max_blocks + j] = sc[tid];
 }
 
 // Tail (N mod B_c tokens) -> INT8 buffer with the universal scale (R-11);
@@ -293,7 +355,7 @@ cudaError_t launch_quant_prefill(const turbo_kv_cache_t* c, const __half* k, con
                                                     c->s_parent, c->a_univ, k1, v1t, k1s, v1s);
     quant_tail_kernel<128><<<dim3(H, B), 256, 0, st>>>(k, v, N, H, c->a_univ, c->buf, c->counters);
   } else {
-    quant_prefill_kernel<64><<<grid, 256, 0, st>>>(k, v, N, H, c->max_blocks, c->bits_dev, c->block_rec,
+    quant_prefill_kernel<64><<<grid, 128, 0, st>>>(k, v, N, H, c->max_blocks, c->bits_dev, c->block_rec,
                                                    c->s_parent, c->a_univ, k1, v1t, k1s, v1s);
     quant_tail_kernel<64><<<dim3(H, B), 256, 0, st>>>(k, v, N, H, c->a_univ, c->buf, c->counters);
   }

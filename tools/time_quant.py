@@ -1,0 +1,31 @@
+"""Time turbo_quantize_kv on configs[1] (B=8, N=4096, 8 KV heads, d=128) for the
+library in $TURBO_LIB (A/B of kernel variants)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2412_08585_b200 import binding as ta  # noqa: E402
+from paper_2412_08585_b200 import synth  # noqa: E402
+
+B, N, Hq, Hkv, d = 8, 4096, 32, 8, 128
+p = ta.params(head_dim=d)
+q, k, v = synth.qkv_torch(1002, B, N, Hq, Hkv, d)
+cache = ta.KVCache(B, Hkv, d, max_blocks=N // 64 + 2, bits=synth.head_bits_alternating(Hkv))
+outs = ta.turbo_quantize_kv(p, cache, k, v)
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+ts = []
+for i in range(23):
+    flush.zero_()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    ta.turbo_quantize_kv(p, cache, k, v)
+    e1.record()
+    torch.cuda.synchronize()
+    if i >= 3:
+        ts.append(e0.elapsed_time(e1))
+ms = sorted(ts)[len(ts) // 2]
+nbytes = 2 * k.numel() * 2 + k.numel() + 2 * v.numel() + cache.records().numel()
+print(f"{os.environ.get('TURBO_LIB', 'in-tree')}: {ms * 1e3:8.1f} us  {nbytes / ms / 1e6:7.1f} GB/s  "
+      f"checksum {sum(int(x.double().abs().sum().item()) for x in outs[:2])} {int(cache.records().double().sum().item())}")
