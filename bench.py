@@ -317,6 +317,7 @@ def bench_decode(args, rank, world, device, pk):
             "step_ms_append_plus_decode": round(t_step, 4), "kv_gbs": round(gbs, 1),
             "tokens_per_s": round(world * B / (t_step * 1e-3), 1),
             "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": pk["hbm"], "unit": "GB/s",
+                         "traffic": traffic_per_launch("decode_kernel"),
                          "frac": round(gbs / pk["hbm"], 4), "peak_source": pk["src"]}}
 
 
