@@ -99,6 +99,8 @@ def _declare(L):
     L.tq_cache_append_slot.restype = i32
     L.tq_prefill_head.argtypes = [C.POINTER(Params), i32, i32, vp, vp, vp, vp, vp, vp]
     L.tq_prefill_head.restype = i32
+    L.tq_prefill_head_blocks.argtypes = [C.POINTER(Params), i32, i32, vp, vp, vp, i32, i32, vp, vp, vp]
+    L.tq_prefill_head_blocks.restype = i32
     L.tq_decode_head.argtypes = [C.POINTER(Params), vp, C.POINTER(_Slot), C.POINTER(_Slot), vp, vp, i32,
                                  i32, i32, i32, vp, vp, vp]
     L.tq_decode_head.restype = i32
@@ -229,11 +231,13 @@ def _tap_arrays(rows, bc, d):
                 s_p=np.zeros(1, np.float32), pv_int=np.zeros((rows, d), np.int32))
 
 
-def prefill_head(p: Params, q, k, v, causal=True, tap=None):
+def prefill_head(p: Params, q, k, v, causal=True, tap=None, blocks=None):
     """Alg. 1 for one (batch, head): q, k, v [N][d] (fp16-valued floats).
 
     Returns (O [N][d] f32, L [N] f32[, tap dict]).  ``tap=(i, j)`` records the
-    exact-set intermediates of B_r block i x KV block j.
+    exact-set intermediates of B_r block i x KV block j.  ``blocks=(i0, i1)``
+    runs only query blocks i0 <= i < i1 of the (independent) outer loop; the
+    other rows stay zero.
     """
     q, k, v = _f32(q), _f32(k), _f32(v)
     n = q.shape[0]
@@ -244,8 +248,9 @@ def prefill_head(p: Params, q, k, v, causal=True, tap=None):
         arrs = _tap_arrays(p.block_q, p.block_kv, p.d)
         t = _PrefillTap(tap[0], tap[1], 0, *[_p(arrs[k_]) for k_ in
                                              ("q1", "s_q", "s_int", "m_new", "p_tilde", "p_codes", "s_p", "pv_int")])
-    rc = lib().tq_prefill_head(C.byref(p), n, int(causal), _p(q), _p(k), _p(v), _p(o), _p(lse),
-                               C.byref(t) if t is not None else None)
+    i0, i1 = blocks if blocks is not None else (0, 2**31 - 1)
+    rc = lib().tq_prefill_head_blocks(C.byref(p), n, int(causal), _p(q), _p(k), _p(v), i0, i1, _p(o), _p(lse),
+                                      C.byref(t) if t is not None else None)
     if rc != 0:
         raise ValueError(f"tq_prefill_head -> {rc}")
     if tap is not None:

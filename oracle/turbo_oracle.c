@@ -243,9 +243,19 @@ static float quant_p(int64_t n, const float* pt, const uint8_t* use, int32_t wid
 int32_t tq_prefill_head(const tq_params* p, int32_t n, int32_t causal, const float* q,
                         const float* k, const float* v, float* o, float* lse,
                         tq_prefill_tap* tap) {
+  return tq_prefill_head_blocks(p, n, causal, q, k, v, 0, INT32_MAX, o, lse, tap);
+}
+
+/* Alg. 1's outer loop restricted to query blocks i in [i_begin, i_end): every
+ * iteration of that loop is independent, so this computes exactly
+ * the same rows as the full call; rows of other blocks are left untouched. */
+int32_t tq_prefill_head_blocks(const tq_params* p, int32_t n, int32_t causal, const float* q,
+                               const float* k, const float* v, int32_t i_begin, int32_t i_end,
+                               float* o, float* lse, tq_prefill_tap* tap) {
   const int32_t d = p->d, br = p->block_q, bc = p->block_kv;
-  if (n < 1) return -1;
+  if (n < 1 || i_begin < 0) return -1;
   const int32_t tr = (n + br - 1) / br, tc = (n + bc - 1) / bc;
+  if (i_end > tr) i_end = tr;
 
   /* Stage-1 K_j, V_j; done once per block instead of once per
    * (i, j) -- identical values (R-21). */
@@ -271,7 +281,7 @@ int32_t tq_prefill_head(const tq_params* p, int32_t n, int32_t causal, const flo
   float* m = (float*)malloc(sizeof(float) * br);
   uint8_t* active = (uint8_t*)malloc((size_t)br);
 
-  for (int32_t i = 0; i < tr; ++i) {             /* for 1 <= i <= T_r */
+  for (int32_t i = i_begin; i < i_end; ++i) {    /* for 1 <= i <= T_r */
     const int32_t r0 = i * br, nr = (r0 + br <= n) ? br : n - r0;
     float sq = 0.0f;
     if (p->quant) tq_quant_sym8(q + (int64_t)r0 * d, (int64_t)nr * d, q1, &sq);

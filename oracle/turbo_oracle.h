@@ -98,6 +98,9 @@ int32_t tq_cache_append_slot(const tq_params* p, const float* x /*[d]*/, tq_slot
 int32_t tq_prefill_head(const tq_params* p, int32_t n, int32_t causal, const float* q,
                         const float* k, const float* v, float* o, float* lse,
                         tq_prefill_tap* tap);
+int32_t tq_prefill_head_blocks(const tq_params* p, int32_t n, int32_t causal, const float* q,
+                               const float* k, const float* v, int32_t i_begin, int32_t i_end,
+                               float* o, float* lse, tq_prefill_tap* tap);
 int32_t tq_decode_head(const tq_params* p, const float* q, const tq_slot* ks, const tq_slot* vs,
                        const float* k_raw, const float* v_raw, int32_t n_raw,
                        int32_t blk_begin, int32_t blk_end, int32_t with_buffer,

@@ -401,3 +401,17 @@ def test_head_priority_planner(oracle):
     g = outl.max(0) - outl.min(0)
     assert abs(pr[1] - (outl.max() - outl.min()) * g.std()) < 1e-4 * pr[1]
     assert oracle.plan_bits([3.0, 1.0, 1.0, 5.0], 2).tolist() == [4, 2, 2, 4]
+
+
+def test_prefill_query_block_subset(oracle):
+    """Alg. 1's outer loop over query blocks is independent: running
+    only blocks [i0, i1) reproduces those rows of the full run bit-for-bit and
+    leaves the others untouched (used by the full-size sampled GPU parity)."""
+    for causal in (True, False):
+        q, k, v = synth.qkv(31, 1, 64 * 5 + 17, 1, 1, 64)
+        p = oracle.params(d=64)
+        full, lf = oracle.prefill_head(p, q[0, :, 0], k[0, :, 0], v[0, :, 0], causal=causal)
+        part, lp = oracle.prefill_head(p, q[0, :, 0], k[0, :, 0], v[0, :, 0], causal=causal, blocks=(2, 6))
+        np.testing.assert_array_equal(part[128:], full[128:])
+        np.testing.assert_array_equal(lp[128:], lf[128:])
+        assert not part[:128].any() and not lp[:128].any()
