@@ -200,6 +200,16 @@ TURBO_API turbo_status_t turbo_head_priority(int32_t B, int32_t N, int32_t Hkv, 
                                              double* priority, turbo_stream_t stream);
 TURBO_API turbo_status_t turbo_plan_bits(const double* priority, int32_t n_slots, int32_t n_2bit, int32_t* bits);
 
+/* Self-test (not on the hot path): compares the library's fast correctly
+ * rounded divisions used for the stage-1 and P scales (which = 0: a / 119,
+ * which = 1: 119 / a; Alg. 1, Alg. 2) with IEEE
+ * division for every binary32 bit pattern in [lo_bits, hi_bits].  Adds the
+ * number of mismatches to *mismatches (device u64) and lowers *first_bad
+ * (device u32) to the smallest mismatching pattern.  Async on the stream. */
+TURBO_API turbo_status_t turbo_selftest_div(int32_t which, uint32_t lo_bits, uint32_t hi_bits,
+                                            unsigned long long* mismatches, uint32_t* first_bad,
+                                            turbo_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,7 +21,7 @@ _ERR = {1: "TURBO_ERR_INVALID_ARG", 2: "TURBO_ERR_UNSUPPORTED", 3: "TURBO_ERR_CA
 
 EXPORTS = ("turbo_version", "turbo_cache_sizes", "turbo_quantize_kv", "turbo_attention_prefill",
            "turbo_decode_workspace_bytes", "turbo_attention_decode", "turbo_combine_lse",
-           "turbo_priority_workspace_bytes", "turbo_head_priority", "turbo_plan_bits")
+           "turbo_priority_workspace_bytes", "turbo_head_priority", "turbo_plan_bits", "turbo_selftest_div")
 
 
 class TurboError(RuntimeError):
@@ -74,6 +74,9 @@ def lib() -> C.CDLL:
         L.turbo_priority_workspace_bytes.restype = sz
         L.turbo_head_priority.argtypes = [i32, i32, i32, i32, vp, vp, vp, sz, vp, vp]
         L.turbo_plan_bits.argtypes = [vp, i32, i32, vp]
+        if hasattr(L, "turbo_selftest_div"):  # self-test entry (absent from older A/B builds in variants/)
+            L.turbo_selftest_div.argtypes = [i32, C.c_uint32, C.c_uint32, vp, vp, vp]
+            L.turbo_selftest_div.restype = C.c_int
         for name in ("turbo_cache_sizes", "turbo_quantize_kv", "turbo_attention_prefill", "turbo_attention_decode",
                      "turbo_combine_lse", "turbo_head_priority", "turbo_plan_bits"):
             getattr(L, name).restype = C.c_int
@@ -264,3 +267,14 @@ def turbo_plan_bits(priority, n_2bit):
     bits = torch.empty(pr.shape, dtype=torch.int32)
     _check("turbo_plan_bits", lib().turbo_plan_bits(_ptr(pr), pr.numel(), n_2bit, _ptr(bits)))
     return bits
+
+
+def turbo_selftest_div(which, lo_bits, hi_bits):
+    """Exhaustive check of the library's fast correctly rounded divisions
+    (which 0: a / 119, 1: 119 / a) against IEEE division over the binary32 bit
+    patterns [lo_bits, hi_bits]; returns (mismatches, first mismatching bits)."""
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    first = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+    _check("turbo_selftest_div", lib().turbo_selftest_div(which, lo_bits, hi_bits, _ptr(bad), _ptr(first), _stream()))
+    torch.cuda.synchronize()
+    return int(bad.item()), int(first.item()) & 0xFFFFFFFF

@@ -22,6 +22,8 @@ cudaError_t launch_combine(int n_parts, int rows, int d, const float* o_parts, c
                            float* o32, float* lse, cudaStream_t st);
 
 size_t priority_workspace(int Hkv, int HD);
+cudaError_t launch_selftest_div(int which, uint32_t lo, uint32_t hi, unsigned long long* bad, uint32_t* first,
+                                cudaStream_t st);
 cudaError_t launch_priority(int B, int N, int Hkv, int HD, const __half* k, const __half* v, void* ws,
                             double* priority, cudaStream_t st);
 void plan_bits(const double* priority, int n_slots, int n_2bit, int32_t* bits);
@@ -175,6 +177,13 @@ turbo_status_t turbo_plan_bits(const double* priority, int32_t n_slots, int32_t 
   if (!priority || !bits || n_slots < 1 || n_2bit < 0 || n_2bit > n_slots) return TURBO_ERR_INVALID_ARG;
   ta_host::plan_bits(priority, n_slots, n_2bit, bits);
   return TURBO_OK;
+}
+
+turbo_status_t turbo_selftest_div(int32_t which, uint32_t lo_bits, uint32_t hi_bits, unsigned long long* mismatches,
+                                  uint32_t* first_bad, turbo_stream_t stream) {
+  if ((which != 0 && which != 1) || lo_bits > hi_bits || !mismatches || !first_bad) return TURBO_ERR_INVALID_ARG;
+  return cuda_status(ta_host::launch_selftest_div(which, lo_bits, hi_bits, mismatches, first_bad,
+                                                  reinterpret_cast<cudaStream_t>(stream)));
 }
 
 }  // extern "C"

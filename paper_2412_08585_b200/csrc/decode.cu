@@ -319,8 +319,8 @@ TA_DEV void softmax_tile(const DecodeArgs& a, RowState<HD, PACK>& st, int (&sv)[
     st.m[e] = m_new;
     alpha[e] = al;
     // per-row P scale (Alg. 2, R-17)
-    const float inv_p = pm > 0.f ? __fdiv_rn(kDiv, pm) : 0.f;
-    s_p[e] = __fdiv_rn(pm, kDiv);
+    const float inv_p = pm > 0.f ? div_119_by(pm) : 0.f;
+    s_p[e] = div_by_119(pm);
     int sp = 0;
 #pragma unroll
     for (int t = 0; t < M::NT; ++t) {
@@ -473,8 +473,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
     }
     qa = fmaxf(qa, __shfl_xor_sync(0xffffffffu, qa, 1));
     qa = fmaxf(qa, __shfl_xor_sync(0xffffffffu, qa, 2));
-    const float inv = qa > 0.f ? __fdiv_rn(kDiv, qa) : 0.f;
-    s_q_row = __fdiv_rn(qa, kDiv);
+    const float inv = qa > 0.f ? div_119_by(qa) : 0.f;
+    s_q_row = div_by_119(qa);
 #pragma unroll
     for (int i = 0; i < R; i += 4)
       *reinterpret_cast<uint32_t*>(&sm.q1[g][q * R + i]) =
@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
     // Buffer block (INT8, universal scale, n_buf valid keys), last.
     const int8_t* kb = a.buf + slotK * (size_t)(kBc * HD);
     const int8_t* vb = a.buf + slotV * (size_t)(kBc * HD);
-    const float sK = __fdiv_rn(a.a_univ[slotK], kDiv), sV = __fdiv_rn(a.a_univ[slotV], kDiv);
+    const float sK = div_by_119(a.a_univ[slotK]), sV = div_by_119(a.a_univ[slotV]);
     int sv[M::NT][2];
     qk_buffer<HD, PACK>(kb, q1s, sv, g, q);
     const float cqk[2] = {__fmul_rn(__fmul_rn(sq2[0], sK), a.scale), __fmul_rn(__fmul_rn(sq2[1], sK), a.scale)};

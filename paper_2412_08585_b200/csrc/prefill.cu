@@ -20,9 +20,10 @@
 
 #ifdef TURBO_PROFILE
 __device__ unsigned long long g_prof[32];
+// per-thread register accumulators, flushed once per CTA (global atomics per
+// event would serialise the SMs and distort the timeline)
 #define PROF_T(var) const long long var = clock64()
-#define PROF_ADD(slot, a, b) \
-  if ((threadIdx.x & 31) == 0) atomicAdd(&g_prof[slot], (unsigned long long)((b) - (a)))
+#define PROF_ADD(slot, a, b) prof_acc[slot] += (uint32_t)((b) - (a))
 #else
 #define PROF_T(var)
 #define PROF_ADD(slot, a, b)
@@ -96,6 +97,10 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
     prefill_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                    const __grid_constant__ PrefillArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+#ifdef TURBO_PROFILE
+  const long long t_cta0 = clock64();
+  uint32_t prof_acc[17] = {0};
+#endif
   using Smem = PrefillSmem<HD, NS, SP>;
   // 1024-B aligned (128B-swizzle atoms); pointer arithmetic keeps the shared address space.
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
@@ -226,6 +231,7 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
     }
   } else {
     reg_alloc<NS, SP>();
+    PROF_T(pro0);
     // ------------------------------------------------------------ softmax / correction
     // Thread = (slot, column half hc, row r = TMEM lane).  With SP = 2 two warps
     // share each 32-row quadrant: hc owns S columns [hc SW, (hc+1) SW) and O
@@ -273,8 +279,8 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
         a_q = args.block_q == 64 ? fmaxf(a_q, fmaxf(sm.red_a[slot][2 * half][x], sm.red_a[slot][2 * half + 1][x]))
                                  : fmaxf(a_q, fmaxf(fmaxf(sm.red_a[slot][0][x], sm.red_a[slot][1][x]),
                                                     fmaxf(sm.red_a[slot][2][x], sm.red_a[slot][3][x])));
-      const float inv_q = a_q > 0.f ? __fdiv_rn(kDiv, a_q) : 0.f;
-      s_q = __fdiv_rn(a_q, kDiv);
+      const float inv_q = a_q > 0.f ? div_119_by(a_q) : 0.f;
+      s_q = div_by_119(a_q);
 #pragma unroll
       for (int c = 0; c < OW / 16; ++c) {
         uint32_t w[4];
@@ -297,6 +303,8 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
     }
     fence_proxy_async();
     mbar_arrive(&sm.q_ready);
+    PROF_T(pro1);
+    PROF_ADD(7, pro0, pro1);
 
     // Output accumulator in scaled form O_true = A * Ohat (A = product of the
     // alphas since the last renormalisation), so a tile costs one FFMA per
@@ -466,8 +474,8 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
                     ? fmaxf(a_p, fmaxf(red_p[(sb * 4 + 2 * half) * SP + x], red_p[(sb * 4 + 2 * half + 1) * SP + x]))
                     : fmaxf(a_p, fmaxf(fmaxf(red_p[(sb * 4) * SP + x], red_p[(sb * 4 + 1) * SP + x]),
                                        fmaxf(red_p[(sb * 4 + 2) * SP + x], red_p[(sb * 4 + 3) * SP + x])));
-        const float inv_p = a_p > 0.f ? __fdiv_rn(kDiv, a_p) : 0.f;
-        const float s_p = __fdiv_rn(a_p, kDiv);
+        const float inv_p = a_p > 0.f ? div_119_by(a_p) : 0.f;
+        const float s_p = div_by_119(a_p);
         // Q(P~) codes in [0, 119] as fp16 -> smem (A operand of the PV MMA)
         uint8_t* prow = reinterpret_cast<uint8_t*>(sm.p[slot][sb]);
         constexpr float kMagicF16 = 12582912.0f + 25600.0f;  // 1.5*2^23 + 0x6400
@@ -526,11 +534,12 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
         } else {
           A = An;
         }
-        cpv = __fdiv_rn(__fmul_rn(sp_j, args.v1s[bkv * Tc + j]), A);
+        cpv = __fdividef(__fmul_rn(sp_j, args.v1s[bkv * Tc + j]), A);  // tolerance set (R-16): ~2 ulp is fine
       }
       cpv_p = cpv;
       tap_p = tap_j;
     }
+    PROF_T(epi0);
     if (SP == 2) {  // l = l_0 + l_1 (fixed order)
       sm.lsum[slot][hc][r] = l;
       named_bar_sync(bar_pair, 64);
@@ -549,6 +558,8 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
       }
       if (hc == 0) args.lse[((size_t)b * args.Hq + h) * N + row] = m + logf(l);
     }
+    PROF_T(epi1);
+    PROF_ADD(8, epi0, epi1);
   }
   tc_fence_before();
   __syncthreads();
@@ -557,9 +568,14 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
     tmem_dealloc(tmem, kTmemCols);
   }
 #ifdef TURBO_PROFILE
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int i = 0; i < 17; ++i)
+      if (prof_acc[i]) atomicAdd(&g_prof[i], (unsigned long long)prof_acc[i]);
   if (threadIdx.x == 0) {
     atomicAdd(&g_prof[20], (unsigned long long)nkv);
     atomicAdd(&g_prof[21], 1ull);
+    atomicAdd(&g_prof[22], (unsigned long long)(clock64() - t_cta0));
   }
 #endif
 }

@@ -129,8 +129,8 @@ __global__ void __launch_bounds__(2 * HD, 256 / HD) quant_prefill_kernel(
 #pragma unroll
   for (int w = 1; w < NW; ++w) a = fmaxf(a, red[kind][w]);
   // s = max|x| / 119, codes = round_half_even(x * (119 / max|x|)) (Alg. 1; R-2, R-3, R-5)
-  const float inv = a > 0.f ? __fdiv_rn(kDiv, a) : 0.f;
-  const float sc = __fdiv_rn(a, kDiv);
+  const float inv = a > 0.f ? div_119_by(a) : 0.f;
+  const float sc = div_by_119(a);
   // stage-1 code of token t, recomputed where needed (2 instructions) instead of held
   auto q1 = [&](int t) -> int {
     return rint_prod((t & 1) ? __high2float(xh[t >> 1]) : __low2float(xh[t >> 1]), inv);
@@ -266,7 +266,7 @@ __global__ void quant_tail_kernel(const __half* __restrict__ k, const __half* __
   if (tid >= 2 * HD) return;
   const int kv = tid / HD, c = tid % HD;
   const float a = a_univ[bh * 2 + kv];
-  const float inv = a > 0.f ? __fdiv_rn(kDiv, a) : 0.f;
+  const float inv = a > 0.f ? div_119_by(a) : 0.f;
   const __half* src = kv == 0 ? k : v;
   int8_t* bslot = buf + (bh * 2 + kv) * (size_t)(kBc * HD);
   for (int t = 0; t < ntail; ++t) {
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(256) quant_append_kernel(
   if (tid < 2 * HD) {
     const int kv = tid / HD, c = tid % HD;
     const float a = a_univ[bh * 2 + kv];
-    const float inv = a > 0.f ? __fdiv_rn(kDiv, a) : 0.f;
+    const float inv = a > 0.f ? div_119_by(a) : 0.f;
     const float x = __half2float((kv == 0 ? k : v)[bh * HD + c]);
     const int code = max(-119, min(119, rint_prod(x, inv)));
     int8_t* bslot = buf + (bh * 2 + kv) * (size_t)(kBc * HD);
@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(256) quant_append_kernel(
   __syncthreads();
 #pragma unroll
   for (int kv = 0; kv < 2; ++kv) pack_record<HD>(tile[kv], kv, bits_dev[h * 2 + kv], rec[kv] + 2 * HD, tid, 256);
-  if (tid < 2) s_parent[(bh * 2 + tid) * max_blocks + n_blocks] = __fdiv_rn(a_univ[bh * 2 + tid], kDiv);
+  if (tid < 2) s_parent[(bh * 2 + tid) * max_blocks + n_blocks] = div_by_119(a_univ[bh * 2 + tid]);
 }
 
 __global__ void append_counters_kernel(int32_t* counters, int B) {

@@ -339,3 +339,15 @@ def test_head_priority_planner_parity(ta, shape):
     n2 = Hkv
     bits = ta.turbo_plan_bits(torch.from_numpy(pr), n2).numpy()
     np.testing.assert_array_equal(bits.reshape(-1), O.plan_bits(ref.reshape(-1), n2))
+
+
+@pytest.mark.parametrize("which,lo,hi", [(0, 0x04000000, 0x7F7FFFFF), (1, 0x03800000, 0x7E800000)])
+def test_fast_division_exhaustive(ta, which, lo, hi):
+    """The fast correctly rounded a/119 and 119/a used for the stage-1 and P
+    scales equal IEEE division for every binary32 in the domain: a/119 for all
+    positive normals with a normal quotient (a >= 2^-119); 119/a for
+    2^-120 <= a <= 2^126 (above 2^126 the reciprocal estimate is subnormal and
+    flushed).  Every scale the path forms is in range: P maxima are <= 1 and
+    FP16 inputs are <= 65504."""
+    bad, first = ta.turbo_selftest_div(which, lo, hi)
+    assert bad == 0, f"{bad} mismatches, first at bits {first:#010x}"
