@@ -49,9 +49,9 @@ struct DecodeArgs {
   turbo_debug_tap_t tap;
 };
 
-TA_DEV uint32_t byte_of(const uint4& v, int i) {
+TA_DEV uint32_t byte_of(const uint4& v, int i) {  // one PRMT (i is a compile-time constant)
   const uint32_t w = i < 4 ? v.x : i < 8 ? v.y : i < 12 ? v.z : v.w;
-  return (w >> (8 * (i & 3))) & 0xFFu;
+  return __byte_perm(w, 0u, 0x4440u | (uint32_t)(i & 3));
 }
 
 // Shared-memory accessors on 32-bit shared addresses.
@@ -304,14 +304,23 @@ TA_DEV void softmax_tile(const DecodeArgs& a, RowState<HD, PACK>& st, int (&sv)[
     const float al_s = sas_eval(__fsub_rn(m_new, m_prev), lut_lane, a.sas.nr_abs);
     const float al = m_prev == -INFINITY ? 0.f : (a.alpha_mode == 1 && m_new == m_prev) ? 1.f : al_s;
     float pt[M::NT], rs = 0.f, pm = 0.f;
+    const f32x2 m2 = pk2(m_new, m_new);
 #pragma unroll
-    for (int t = 0; t < M::NT; ++t) {
-      const float x = __fmul_rn((float)sv[t][e], cqk[e]);
-      float p = sas_eval(__fsub_rn(m_new, x), lut_lane, a.sas.nr_abs);
-      if (!FULL) p = M::tok(t, g, q) < nvalid ? p : 0.f;
-      pt[t] = p;
-      rs += p;
-      pm = fmaxf(pm, p);
+    for (int t = 0; t < M::NT; t += 2) {
+      // x rounded on its own (scalar __fmul_rn: a packed multiply feeding the
+      // subtraction would be contracted into an FFMA2)
+      const f32x2 x2 = pk2(__fmul_rn((float)sv[t][e], cqk[e]), __fmul_rn((float)sv[t + 1][e], cqk[e]));
+      const f32x2 p2 = sas_eval2(sub2(m2, x2), lut_lane, a.sas.nr_abs);
+      float p0 = lo2(p2), p1 = hi2(p2);
+      if (!FULL) {
+        p0 = M::tok(t, g, q) < nvalid ? p0 : 0.f;
+        p1 = M::tok(t + 1, g, q) < nvalid ? p1 : 0.f;
+      }
+      pt[t] = p0;
+      pt[t + 1] = p1;
+      rs += p0;
+      rs += p1;
+      pm = fmaxf(pm, fmaxf(p0, p1));
     }
     rs = grp_sumf<PACK>(rs);
     pm = grp_maxf<PACK>(pm);

@@ -9,8 +9,10 @@ from paper_2412_08585_b200 import binding as ta  # noqa: E402
 from paper_2412_08585_b200 import synth  # noqa: E402
 import bench  # noqa: E402
 
-for name, (B, N, Hq, Hkv, d), splits in (("cfg3", (64, 32768, 40, 10, 128), (4, 6, 8, 12, 16)),
-                                         ("cfg5", (16, 131072, 32, 8, 128), (8, 16, 24, 32, 48))):
+SPL3 = tuple(int(x) for x in os.environ.get("SPL3", "4,6,8,12,16").split(","))
+SPL5 = tuple(int(x) for x in os.environ.get("SPL5", "8,16,24,32,48").split(","))
+for name, (B, N, Hq, Hkv, d), splits in (("cfg3", (64, 32768, 40, 10, 128), SPL3),
+                                         ("cfg5", (16, 131072, 32, 8, 128), SPL5)):
     bits = synth.head_bits_alternating(Hkv)
     p = ta.params(head_dim=d)
     cache = ta.KVCache(B, Hkv, d, max_blocks=N // 64 + 4, bits=bits)
