@@ -187,9 +187,10 @@ def turbo_decode_workspace_bytes(B, Hq, head_dim, n_splits):
     return lib().turbo_decode_workspace_bytes(B, Hq, head_dim, n_splits)
 
 
-def auto_splits(batch, n_kv_heads, n_blocks, target_tasks=4096):
-    """Split count giving ~target_tasks warp tasks (>= 2 waves of the ~1800 resident
-    decode warps on 148 SMs), at least 8 blocks per split."""
+def auto_splits(batch, n_kv_heads, n_blocks, target_tasks=5120):
+    """Split count giving ~target_tasks warp tasks (~3 waves of the ~1800 resident
+    decode warps on 148 SMs), at least 8 blocks per split.  5120 is the best of a
+    B200 sweep on configs[2] (S = 8) and configs[4] (S = 40; tools/sweep_decode.py)."""
     s = -(-target_tasks // max(1, batch * n_kv_heads))
     return max(1, min(s, n_blocks // 8))
 
