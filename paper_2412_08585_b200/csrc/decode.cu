@@ -369,6 +369,16 @@ TA_DEV void pv_block(uint32_t rec, const int8_t* vb, uint32_t pbuf, const int (&
   for (int mt = 0; mt < HD / 16; ++mt) {
     const int c0 = 16 * mt + g, c1 = c0 + 8;
     int c[4] = {0, 0, 0, 0};
+    // the channel pair's code words, loaded once for both units / k-steps
+    uint32_t wv[4] = {0u, 0u, 0u, 0u};
+    if (!BUF) {
+      wv[0] = lds32(codes + c0 * CB + 4 * q);
+      wv[1] = lds32(codes + c1 * CB + 4 * q);
+      if (BV == 4) {
+        wv[2] = lds32(codes + c0 * CB + 4 * (4 + q));
+        wv[3] = lds32(codes + c1 * CB + 4 * (4 + q));
+      }
+    }
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       uint32_t af[4];
@@ -379,35 +389,26 @@ TA_DEV void pv_block(uint32_t rec, const int8_t* vb, uint32_t pbuf, const int (&
         af[3] = *reinterpret_cast<const uint32_t*>(vb + c1 * kBc + 32 * j + 16 + 4 * q);
         const uint32_t b2[2] = {bf[j][0], bf[j][1]};
         imma_s8u8(c, af, b2);
-      } else {
-        if (BV == 4) {
-          // unit j: j = 0 low nibbles (tokens 4q+e | 32+4q+e), j = 1 high nibbles x16
-          // (tokens 16+4q+e | 48+4q+e); word W = 4 j' + q holds both halves of k-step j'.
-          const uint32_t mk = j ? 0xF0F0F0F0u : 0x0F0F0F0Fu;
-          af[0] = lds32(codes + c0 * CB + 4 * q) & mk;
-          af[1] = lds32(codes + c1 * CB + 4 * q) & mk;
-          af[2] = lds32(codes + c0 * CB + 4 * (4 + q)) & mk;
-          af[3] = lds32(codes + c1 * CB + 4 * (4 + q)) & mk;
-        } else {
-          const uint32_t u0 = lds32(codes + c0 * CB + 4 * q);
-          const uint32_t u1 = lds32(codes + c1 * CB + 4 * q);
-          const int sh = 4 * j;
-          af[0] = (u0 >> sh) & 0x03030303u;
-          af[1] = (u1 >> sh) & 0x03030303u;
-          af[2] = (u0 >> (sh + 2)) & 0x03030303u;
-          af[3] = (u1 >> (sh + 2)) & 0x03030303u;
-        }
-        if (BV == 4) {
-          // B rows of unit j: tokens (16 j + 4q..) and (32 + 16 j + 4q..)
-          const uint32_t b2[2] = {j ? bf[0][1] : bf[0][0], j ? bf[1][1] : bf[1][0]};
-          int cu[4] = {0, 0, 0, 0};
-          imma_u8u8(cu, af, b2);
+      } else if (BV == 4) {
+        // unit j: j = 0 low nibbles (tokens 4q+e | 32+4q+e), j = 1 high nibbles x16
+        // (tokens 16+4q+e | 48+4q+e); word W = 4 j' + q holds both halves of k-step j'.
+        const uint32_t mk = j ? 0xF0F0F0F0u : 0x0F0F0F0Fu;
 #pragma unroll
-          for (int i = 0; i < 4; ++i) c[i] += cu[i] >> (4 * j);
-        } else {
-          const uint32_t b2[2] = {bf[j][0], bf[j][1]};
-          imma_u8u8(c, af, b2);
-        }
+        for (int i = 0; i < 4; ++i) af[i] = wv[i] & mk;
+        // B rows of unit j: tokens (16 j + 4q..) and (32 + 16 j + 4q..)
+        const uint32_t b2[2] = {j ? bf[0][1] : bf[0][0], j ? bf[1][1] : bf[1][0]};
+        int cu[4] = {0, 0, 0, 0};
+        imma_u8u8(cu, af, b2);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) c[i] += cu[i] >> (4 * j);
+      } else {
+        const int sh = 4 * j;
+        af[0] = (wv[0] >> sh) & 0x03030303u;
+        af[1] = (wv[1] >> sh) & 0x03030303u;
+        af[2] = (wv[0] >> (sh + 2)) & 0x03030303u;
+        af[3] = (wv[1] >> (sh + 2)) & 0x03030303u;
+        const uint32_t b2[2] = {bf[j][0], bf[j][1]};
+        imma_u8u8(c, af, b2);
       }
     }
 #pragma unroll
