@@ -156,7 +156,7 @@ def run_ours(args, rank, world, device):
     qd, kd, vd = (x[:, 0].contiguous() for x in synth.qkv_torch(4002 + rank, B, 1, Hq, Hkv, d, device=device))
     cache = ta.KVCache(B, Hkv, d, max_blocks=N // 64 + 2, bits=bits, device=device)
     S = args.splits
-    ws = torch.empty(max(ta.turbo_decode_workspace_bytes(B, Hq, d, S), 16), dtype=torch.uint8, device=device)
+    ws = torch.empty(max(ta.turbo_decode_workspace_bytes(B, Hq, Hkv, d, S), 16), dtype=torch.uint8, device=device)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=device)  # > 126 MB L2
     st = torch.cuda.current_stream()
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
@@ -284,10 +284,8 @@ def bench_decode(args, rank, world, device, pk):
     ta.turbo_quantize_kv(p, cache, k, v)  # builds the 32k-token compressed cache
     del k, v
     torch.cuda.empty_cache()
-    S = args.decode_splits
-    if S is None:
-        S = ta.auto_splits(B, Hkv, cache.n_tokens // 64)
-    ws = torch.empty(max(ta.turbo_decode_workspace_bytes(B, Hq, d, S), 16), dtype=torch.uint8, device=device)
+    S = 0 if args.decode_splits is None else args.decode_splits  # 0: balanced schedule
+    ws = torch.empty(max(ta.turbo_decode_workspace_bytes(B, Hq, Hkv, d, S), 16), dtype=torch.uint8, device=device)
     toks = [tuple(x[:, 0].contiguous() for x in synth.qkv_torch(6000 + i, B, 1, Hq, Hkv, d, device=device))
             for i in range(args.warmup + args.steps)]
     st = torch.cuda.current_stream()
@@ -494,8 +492,9 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--splits", type=int, default=4, help="split-KV count of the decode in the step")
-    ap.add_argument("--decode-splits", type=int, default=None, help="default: binding.auto_splits")
+    ap.add_argument("--splits", type=int, default=0, help="split-KV count of the decode in the step (0: balanced)")
+    ap.add_argument("--decode-splits", type=int, default=None,
+                    help="decode split count (default 0: the balanced schedule)")
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--workload", default="step", choices=["step", "prefill_70b", "decode_long"],
                     help="step = the default hot-path step (configs[1] + configs[2] decode)")

@@ -157,18 +157,36 @@ TURBO_API turbo_status_t turbo_attention_prefill(const turbo_params_t* params, i
                                        const void* v1t, const float* k1_scale, const float* v1_scale,
                                        void* o, float* lse, turbo_stream_t stream);
 
-/* Workspace for turbo_attention_decode with n_splits splits (HOST result). */
-TURBO_API size_t turbo_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t head_dim, int32_t n_splits);
+/* Workspace for turbo_attention_decode with n_splits (>= 0) on the current
+ * device (HOST result; 0 = none needed, or invalid arguments).
+ *   n_splits >= 2: S * B * Hq * (d + 1) floats;  n_splits == 0 (balanced):
+ *   (B * Hkv + W) * (Hq / Hkv) * (d + 1) floats, W = turbo_decode_workers(). */
+TURBO_API size_t turbo_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t head_dim,
+                                              int32_t n_splits);
+
+/* Worker warps W of the balanced decode schedule on the current device
+ * (every SM filled to the decode kernel's occupancy; HOST result, 0 if no
+ * device).  Exposed so that callers can reproduce the partition below. */
+TURBO_API int32_t turbo_decode_workers(int32_t Hq, int32_t Hkv, int32_t head_dim);
 
 /* Algorithm 2, TurboAttention decode of one new query per
  * sequence against cache blocks [blk_begin, blk_end) (blk_end = -1: all
- * flushed blocks) and, if with_buffer, the INT8 buffer block last.
- * The block range is cut into n_splits contiguous sub-ranges of
- * ceil(n / n_splits) blocks (the buffer joins the last one); each is one
- * online-softmax pass (same order as Alg. 2) and the partial results are
- * merged by the log-sum-exp combine (R-23).
+ * flushed blocks) and, if with_buffer, the INT8 buffer block last.  Each
+ * sub-range below is one online-softmax pass (same order as Alg. 2); the
+ * partial results are merged by the log-sum-exp combine in ascending order
+ * (R-23).  Sub-ranges:
+ *   n_splits >= 1: the block range of every (b, kv head) is cut into
+ *     n_splits contiguous ranges of ceil(n / n_splits) blocks (the buffer
+ *     joins the last one).
+ *   n_splits == 0 (balanced): the units of every (b, kv head) -- its blocks
+ *     in order, then the buffer block if used (with_buffer and n_buf > 0) --
+ *     are laid end to end in (b, kv head) order; the sequence of all
+ *     `total` units is cut into chunks of C = max(8, ceil(total / W)) units,
+ *     W = turbo_decode_workers(Hq, Hkv, d), and every (b, kv head) range
+ *     is split at the chunk boundaries.  Every warp streams the same number
+ *     of bytes, whatever the lengths of the sequences.
  *   q      FP16 [B][Hq][d]; quantised per (b, head) vector.
- *   workspace  device, >= turbo_decode_workspace_bytes(B, Hq, d, n_splits).
+ *   workspace  device, >= turbo_decode_workspace_bytes(B, Hq, Hkv, d, n_splits).
  *   o      FP16 [B][Hq][d] or NULL;  o_part f32 [B][Hq][d] (normalised) or
  *          NULL -- at least one of them;  lse f32 [B][Hq] (required).
  * Empty range with no buffer tokens: o = 0, lse = -inf. */

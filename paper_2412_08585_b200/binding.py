@@ -20,7 +20,7 @@ TURBO_OK, TURBO_ERR_INVALID_ARG, TURBO_ERR_UNSUPPORTED, TURBO_ERR_CAPACITY, TURB
 _ERR = {1: "TURBO_ERR_INVALID_ARG", 2: "TURBO_ERR_UNSUPPORTED", 3: "TURBO_ERR_CAPACITY", 4: "TURBO_ERR_CUDA"}
 
 EXPORTS = ("turbo_version", "turbo_cache_sizes", "turbo_quantize_kv", "turbo_attention_prefill",
-           "turbo_decode_workspace_bytes", "turbo_attention_decode", "turbo_combine_lse",
+           "turbo_decode_workspace_bytes", "turbo_decode_workers", "turbo_attention_decode", "turbo_combine_lse",
            "turbo_priority_workspace_bytes", "turbo_head_priority", "turbo_plan_bits", "turbo_selftest_div")
 
 
@@ -65,8 +65,11 @@ def lib() -> C.CDLL:
                                         vp, vp, vp]
         L.turbo_attention_prefill.argtypes = [C.POINTER(TurboParams), i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp,
                                               vp, vp]
-        L.turbo_decode_workspace_bytes.argtypes = [i32, i32, i32, i32]
+        L.turbo_decode_workspace_bytes.argtypes = [i32, i32, i32, i32, i32]
         L.turbo_decode_workspace_bytes.restype = sz
+        if hasattr(L, "turbo_decode_workers"):  # (older A/B builds lack it)
+            L.turbo_decode_workers.argtypes = [i32, i32, i32]
+            L.turbo_decode_workers.restype = i32
         L.turbo_attention_decode.argtypes = [C.POINTER(TurboParams), C.POINTER(TurboKVCache), i32, vp, i32, i32, i32,
                                              i32, vp, sz, vp, vp, vp, vp]
         L.turbo_combine_lse.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp, vp]
@@ -183,8 +186,28 @@ def turbo_attention_prefill(p, q, k1, v1t, k1_scale, v1_scale, causal=True, o=No
     return o, lse
 
 
-def turbo_decode_workspace_bytes(B, Hq, head_dim, n_splits):
-    return lib().turbo_decode_workspace_bytes(B, Hq, head_dim, n_splits)
+def turbo_decode_workspace_bytes(B, Hq, Hkv, head_dim, n_splits):
+    return lib().turbo_decode_workspace_bytes(B, Hq, Hkv, head_dim, n_splits)
+
+
+def turbo_decode_workers(Hq, Hkv, head_dim):
+    return lib().turbo_decode_workers(Hq, Hkv, head_dim)
+
+
+def balanced_ranges(unit_counts, Hkv, workers, min_units=8):
+    """The balanced decode schedule's sub-ranges (include/turbo_attention.h):
+    unit_counts[b] = units of each (b, kv head) (blocks + 1 if the buffer block
+    is used).  Returns {(b, kvh): [(u0, u1), ...]} in ascending order."""
+    total = sum(unit_counts) * Hkv
+    C = max(min_units, -(-total // max(1, workers)))
+    out, base = {}, 0
+    for b, U in enumerate(unit_counts):
+        for h in range(Hkv):
+            s0, s1 = base, base + U
+            out[(b, h)] = [(max(s0, w * C) - s0, min(s1, (w + 1) * C) - s0)
+                           for w in range(s0 // C, (s1 - 1) // C + 1)] if U else []
+            base = s1
+    return out
 
 
 def auto_splits(batch, n_kv_heads, n_blocks, target_tasks=5120):
@@ -199,12 +222,11 @@ def turbo_attention_decode(p, cache: KVCache, q, blk_begin=0, blk_end=-1, with_b
                            workspace=None, o=None, o_part=None, lse=None, want_fp16=True, want_f32=False,
                            stream=None):
     """q fp16 [B,Hq,d] -> (o fp16 [B,Hq,d] or None, o_part f32 [B,Hq,d] or None, lse f32 [B,Hq]).
-    n_splits=None picks auto_splits() for the cached length."""
+    n_splits >= 1: equal splits; 0 or None: the balanced schedule."""
     assert q.dtype == torch.float16 and q.is_contiguous()
     B, Hq, d = q.shape
     if n_splits is None:
-        nb = (cache.n_tokens // cache.block_kv) if blk_end < 0 else blk_end
-        n_splits = auto_splits(B, cache.n_kv_heads, max(0, nb - blk_begin))
+        n_splits = 0
     dev = q.device
     if want_fp16 and o is None:
         o = torch.empty((B, Hq, d), dtype=torch.float16, device=dev)
@@ -212,7 +234,7 @@ def turbo_attention_decode(p, cache: KVCache, q, blk_begin=0, blk_end=-1, with_b
         o_part = torch.empty((B, Hq, d), dtype=torch.float32, device=dev)
     if lse is None:
         lse = torch.empty((B, Hq), dtype=torch.float32, device=dev)
-    wsb = turbo_decode_workspace_bytes(B, Hq, d, n_splits)
+    wsb = turbo_decode_workspace_bytes(B, Hq, cache.n_kv_heads, d, n_splits)
     if wsb and workspace is None:
         workspace = torch.empty(wsb, dtype=torch.uint8, device=dev)
     _check("turbo_attention_decode", lib().turbo_attention_decode(

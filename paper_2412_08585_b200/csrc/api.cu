@@ -14,7 +14,8 @@ cudaError_t launch_quant_append(const turbo_kv_cache_t* c, const __half* k, cons
 cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Hq, int Hkv, int causal, const __half* q,
                            const int8_t* k1, const __half* v1t, const float* k1s, const float* v1s, __half* o,
                            float* lse, cudaStream_t st);
-size_t decode_workspace(int B, int Hq, int HD, int S);
+size_t decode_workspace(int B, int Hq, int Hkv, int HD, int S);
+int decode_workers(int Hq, int Hkv, int HD);
 cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, int Hq, const __half* q, int blk_begin,
                           int blk_end, int with_buffer, int S, void* ws, __half* o, float* o_part, float* lse,
                           cudaStream_t st);
@@ -124,9 +125,15 @@ turbo_status_t turbo_attention_prefill(const turbo_params_t* params, int32_t B, 
                                              reinterpret_cast<cudaStream_t>(stream)));
 }
 
-size_t turbo_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t head_dim, int32_t n_splits) {
-  if (B < 1 || Hq < 1 || n_splits < 1) return 0;
-  return ta_host::decode_workspace(B, Hq, head_dim, n_splits);
+size_t turbo_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t head_dim, int32_t n_splits) {
+  if (B < 1 || Hq < 1 || Hkv < 1 || Hq % Hkv != 0 || n_splits < 0) return 0;
+  if (head_dim != 64 && head_dim != 128) return 0;
+  return ta_host::decode_workspace(B, Hq, Hkv, head_dim, n_splits);
+}
+
+int32_t turbo_decode_workers(int32_t Hq, int32_t Hkv, int32_t head_dim) {
+  if (Hq < 1 || Hkv < 1 || Hq % Hkv != 0 || (head_dim != 64 && head_dim != 128)) return 0;
+  return ta_host::decode_workers(Hq, Hkv, head_dim);
 }
 
 turbo_status_t turbo_attention_decode(const turbo_params_t* params, const turbo_kv_cache_t* cache, int32_t Hq,
@@ -139,11 +146,11 @@ turbo_status_t turbo_attention_decode(const turbo_params_t* params, const turbo_
   if (Hq < 1 || !q || !lse || (!o && !o_part)) return TURBO_ERR_INVALID_ARG;
   if (Hq % cache->n_kv_heads != 0) return TURBO_ERR_UNSUPPORTED;
   if (Hq / cache->n_kv_heads > 8) return TURBO_ERR_UNSUPPORTED;
-  if (n_splits < 1 || blk_begin < 0 || (blk_end >= 0 && blk_end < blk_begin)) return TURBO_ERR_INVALID_ARG;
+  if (n_splits < 0 || blk_begin < 0 || (blk_end >= 0 && blk_end < blk_begin)) return TURBO_ERR_INVALID_ARG;
   if (with_buffer != 0 && with_buffer != 1) return TURBO_ERR_INVALID_ARG;
   if (cache->n_tokens < 1) return TURBO_ERR_INVALID_ARG;  // decode on an empty cache
-  if (workspace_bytes < ta_host::decode_workspace(cache->batch, Hq, params->head_dim, n_splits) ||
-      (n_splits > 1 && !workspace))
+  if (workspace_bytes < ta_host::decode_workspace(cache->batch, Hq, cache->n_kv_heads, params->head_dim, n_splits) ||
+      (n_splits != 1 && !workspace))
     return TURBO_ERR_INVALID_ARG;
   return cuda_status(ta_host::launch_decode(params, cache, Hq, reinterpret_cast<const __half*>(q), blk_begin, blk_end,
                                             with_buffer, n_splits, workspace, reinterpret_cast<__half*>(o), o_part,

@@ -15,6 +15,7 @@
 // with q1_c s_c = 128 hi + lo, hi in [-75, 74] (s8), lo in [0, 127] (u8), so the
 // tensor cores see only raw 4-bit / 2-bit codes.
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -23,6 +24,7 @@
 namespace ta {
 
 constexpr int kWarpsPerCta = 4;
+constexpr int kMinUnits = 8;  // balanced schedule: least units (blocks) per warp chunk
 
 template <int HD>
 struct DecodeWarpSmem {
@@ -43,6 +45,9 @@ struct DecodeArgs {
   float* o_parts;   // [S][B][Hq][d]  (or the final f32 output when S == 1)
   float* lse_parts; // [S][B][Hq]
   __half* o16;      // final fp16 output when S == 1 (or NULL)
+  __half* fin_o16;  // balanced schedule: final fp16 output (or NULL)
+  float* fin_o32;   // balanced schedule: final f32 output (or NULL)
+  float* fin_lse;   // balanced schedule: final L
   int B, Hq, Hkv, G, max_blocks, blk_begin, blk_end, with_buffer, n_splits, alpha_mode;
   float scale;
   SasConst sas;
@@ -418,7 +423,8 @@ TA_DEV void pv_block(uint32_t rec, const int8_t* vb, uint32_t pbuf, const int (&
       const int ch = c0 + 8 * hh;
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int v = c[2 * hh + e];
+        // selects, not c[2 * hh + e]: a runtime index would put c[] in local memory
+        const int v = PACK ? (ql ? c[2 + e] : c[e]) : c[2 * h + e];
         if (BUF) {
           acc[ci][e] = v;
         } else {
@@ -429,35 +435,40 @@ TA_DEV void pv_block(uint32_t rec, const int8_t* vb, uint32_t pbuf, const int (&
   }
 }
 
-template <int HD, bool PACK, bool TAP>
-__global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_constant__ DecodeArgs a) {
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  using M = Map<HD, PACK>;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
-  DecodeWarpSmem<HD>& sm = reinterpret_cast<DecodeWarpSmem<HD>*>(smem_raw)[warp];
-  const int task = blockIdx.x * kWarpsPerCta + warp;
-  if (task >= a.B * a.Hkv * a.n_splits) return;
-  const int split = task % a.n_splits, bh = task / a.n_splits, b = bh / a.Hkv, kvh = bh % a.Hkv;
-  const int G = a.G;
+// Units of work of sequence b for one kv head: the blocks of [blk_begin,
+// blk_end) it has flushed, plus the INT8 buffer block when it is used.
+struct SeqUnits {
+  int jb, nblk, nbuf, units;
+};
+TA_DEV SeqUnits seq_units(const DecodeArgs& a, int b) {
   const int nb = a.counters[2 * b], nbuf = a.counters[2 * b + 1];
   const int jb = min(a.blk_begin, nb), je = a.blk_end < 0 ? nb : min(a.blk_end, nb);
-  const int nblk = max(0, je - jb), per = (nblk + a.n_splits - 1) / a.n_splits;
-  const int j0 = min(jb + split * per, je), j1 = min(j0 + per, je);
-  const bool use_buf = a.with_buffer && split == a.n_splits - 1 && nbuf > 0;
+  const int nblk = max(0, je - jb);
+  return SeqUnits{jb, nblk, nbuf, nblk + ((a.with_buffer && nbuf > 0) ? 1 : 0)};
+}
+
+// One online-softmax pass of Alg. 2 for (b, kv head) over the
+// blocks [j0, j1) and, if use_buf, the buffer block last; writes the
+// normalised partial (O, L) of the G query rows to part `part` (rows
+// part*G .. part*G+G-1 of o_parts / lse_parts; the final [B][Hq] layout when
+// part == b*Hkv + kvh).  `it` counts the ring iterations of this warp across
+// segments (stage = it & 1, mbarrier parity = (it >> 1) & 1).
+template <int HD, bool PACK, bool TAP>
+TA_DEV void decode_segment(const DecodeArgs& a, DecodeWarpSmem<HD>& sm, int b, int kvh, int j0, int j1, bool use_buf,
+                           int nbuf, size_t part, bool tap_ok, uint32_t& it, int lane) {
+  using M = Map<HD, PACK>;
+  const int g = lane >> 2, q = lane & 3;
+  const int G = a.G;
   const int bitsK = a.bits[kvh * 2], bitsV = a.bits[kvh * 2 + 1];
   const size_t slotK = ((size_t)b * a.Hkv + kvh) * 2, slotV = slotK + 1;
   constexpr int REC = rec_bytes(HD);
   const uint32_t bytesK = 2 * HD + kBc * HD * bitsK / 8, bytesV = 2 * HD + kBc * HD * bitsV / 8;
   const float lut_lane = sas_lut_lane(a.sas, lane);
-  const int tap_row = TAP && split == 0 && a.tap.batch == b && a.tap.head / G == kvh ? a.tap.head % G : -1;
+  const int tap_row = TAP && tap_ok && a.tap.batch == b && a.tap.head / G == kvh ? a.tap.head % G : -1;
   const uint32_t pbuf = smem_u32(&sm.p[0][0]), q1s = smem_u32(&sm.q1[0][0]);
 
-  if (lane == 0) {
-    mbar_init(&sm.bar[0], 1);
-    mbar_init(&sm.bar[1], 1);
-    fence_barrier_init();
-  }
   __syncwarp();
+  const uint32_t it0 = it;
   auto issue = [&](int j, int stg) {
     if (lane == 0) {
       mbar_expect_tx(&sm.bar[stg], bytesK + bytesV);
@@ -465,8 +476,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
       bulk_load(sm.rec[stg][1], a.block_rec + (slotV * a.max_blocks + j) * REC, bytesV, &sm.bar[stg]);
     }
   };
-  if (j0 < j1) issue(j0, 0);
-  if (j0 + 1 < j1) issue(j0 + 1, 1);
+  if (j0 < j1) issue(j0, it0 & 1);
+  if (j0 + 1 < j1) issue(j0 + 1, (it0 + 1) & 1);
 
   // q stage-1 quantisation per (b, head) vector (Alg. 2): lane quad g
   // quantises row g (rows >= G are zero).
@@ -527,8 +538,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
   };
 
   for (int j = j0; j < j1; ++j) {
-    const int stg = (j - j0) & 1;
-    mbar_wait(&sm.bar[stg], ((j - j0) >> 1) & 1);
+    const uint32_t itj = it0 + (uint32_t)(j - j0);
+    const int stg = itj & 1;
+    mbar_wait(&sm.bar[stg], (itj >> 1) & 1);
     const uint32_t recK = smem_u32(sm.rec[stg][0]), recV = smem_u32(sm.rec[stg][1]);
     int sv[M::NT][2];
     if (bitsK == 4) qk_block<HD, 4, PACK>(recK, qv, q1r, sv, g, q);
@@ -547,6 +559,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
     __syncwarp();
     if (j + 2 < j1) issue(j + 2, stg);
   }
+
+  it = it0 + (uint32_t)max(0, j1 - j0);
 
   if (use_buf) {
     // Buffer block (INT8, universal scale, n_buf valid keys), last.
@@ -574,7 +588,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
     const bool empty = st.l[e] == 0.f;
     const float inv_l = empty ? 0.f : 1.f / st.l[e];
     const size_t orow = (size_t)b * a.Hq + kvh * G + row;
-    const size_t base = ((size_t)split * a.B * a.Hq + orow) * HD;
+    const size_t prow = part * G + row;
+    const size_t base = prow * HD;
 #pragma unroll
     for (int c = 0; c < M::NC; ++c) {
       const float v = st.o[c][e] * inv_l;
@@ -583,8 +598,131 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
       if (a.o16) a.o16[orow * HD + ch] = __float2half_rn(v);
     }
     if (g == 0 && (!PACK || q < 2))
-      a.lse_parts[(size_t)split * a.B * a.Hq + orow] = empty ? -INFINITY : st.m[e] + logf(st.l[e]);
+      a.lse_parts[prow] = empty ? -INFINITY : st.m[e] + logf(st.l[e]);
   }
+}
+
+
+// Two schedules:
+//  * n_splits >= 1: one warp per (b, kv head, split), the split cutting the
+//    block range into n_splits contiguous ranges of ceil(n / n_splits) blocks
+//    (buffer with the last); part = split * B * Hkv + b * Hkv + kvh.
+//  * balanced (n_splits == 0): a persistent grid of W warps; the units of all
+//    (b, kv head) in b-major, kv-head, block order (buffer last) are cut into
+//    W contiguous chunks of C = max(kMinUnits, ceil(total / W)) units; a warp
+//    runs one pass per (b, kv head) piece of its chunk; piece (bh, w) writes
+//    part bh + w (unique: pieces of a later bh belong to no earlier warp).
+template <int HD, bool PACK, bool TAP>
+__global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_constant__ DecodeArgs a) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  DecodeWarpSmem<HD>& sm = reinterpret_cast<DecodeWarpSmem<HD>*>(smem_raw)[warp];
+  if (lane == 0) {
+    mbar_init(&sm.bar[0], 1);
+    mbar_init(&sm.bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  uint32_t it = 0;
+  if (a.n_splits > 0) {
+    const int task = blockIdx.x * kWarpsPerCta + warp;
+    if (task >= a.B * a.Hkv * a.n_splits) return;
+    const int split = task % a.n_splits, bh = task / a.n_splits, b = bh / a.Hkv, kvh = bh % a.Hkv;
+    const SeqUnits su = seq_units(a, b);
+    const int je = su.jb + su.nblk, per = (su.nblk + a.n_splits - 1) / a.n_splits;
+    const int j0 = min(su.jb + split * per, je), j1 = min(j0 + per, je);
+    const bool use_buf = a.with_buffer && split == a.n_splits - 1 && su.nbuf > 0;
+    decode_segment<HD, PACK, TAP>(a, sm, b, kvh, j0, j1, use_buf, su.nbuf, (size_t)split * a.B * a.Hkv + bh,
+                                  split == 0, it, lane);
+    return;
+  }
+  // balanced schedule
+  const int W = gridDim.x * kWarpsPerCta, w = blockIdx.x * kWarpsPerCta + warp;
+  int tot = 0;
+  for (int b0 = 0; b0 < a.B; b0 += 32)
+    if (b0 + lane < a.B) tot += seq_units(a, b0 + lane).units;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  tot *= a.Hkv;
+  const int C = max(kMinUnits, (tot + W - 1) / W);
+  int pos = w * C;
+  const int end = min(pos + C, tot);
+  if (pos >= end) return;
+  // locate the sequence holding unit `pos`: lane-parallel scan over b (a
+  // serial walk would chain B dependent global loads before the first block)
+  int b = 0, base = 0;
+  for (int b0 = 0, carry = 0; b0 < a.B; b0 += 32) {
+    const int u = b0 + lane < a.B ? seq_units(a, b0 + lane).units * a.Hkv : 0;
+    int incl = u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const unsigned hit = __ballot_sync(0xffffffffu, carry + incl > pos);
+    if (hit) {
+      const int l = __ffs(hit) - 1;
+      b = b0 + l;
+      base = carry + __shfl_sync(0xffffffffu, incl - u, l);
+      break;
+    }
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  SeqUnits su = seq_units(a, b);
+  while (pos < end) {
+    const int U = su.units, kvh = (pos - base) / U, u0 = (pos - base) % U;
+    const int seg_end = min(end, base + (kvh + 1) * U), u1 = seg_end - (base + kvh * U);
+    decode_segment<HD, PACK, TAP>(a, sm, b, kvh, su.jb + u0, su.jb + min(u1, su.nblk), u1 > su.nblk, su.nbuf,
+                                  (size_t)b * a.Hkv + kvh + w, true, it, lane);
+    pos = seg_end;
+    while (pos < end && pos >= base + su.units * a.Hkv) {
+      base += su.units * a.Hkv;
+      su = seq_units(a, ++b);
+    }
+  }
+}
+
+// Log-sum-exp merge of the balanced schedule's pieces (R-23): one CTA of
+// 128 threads per output row (b, h); the pieces of (b, kv head) are the
+// parts bh + w for the warps w whose chunks meet its unit range, merged in
+// ascending order with combine_kernel's arithmetic.
+__global__ void combine_balanced_kernel(const __grid_constant__ DecodeArgs a, int W, int d) {
+  const int r = blockIdx.x, b = r / a.Hq, h = r % a.Hq, kvh = h / a.G, row = h % a.G, lane = threadIdx.x & 31;
+  int tot = 0, before = 0;
+  for (int b0 = 0; b0 < a.B; b0 += 32) {
+    const int bb = b0 + lane;
+    const int u = bb < a.B ? seq_units(a, bb).units : 0;
+    tot += u;
+    before += bb < b ? u : 0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    before += __shfl_xor_sync(0xffffffffu, before, o);
+  }
+  const int U = seq_units(a, b).units;
+  const int C = max(kMinUnits, (tot * a.Hkv + W - 1) / W);
+  const int start = before * a.Hkv + kvh * U;
+  const int bh = b * a.Hkv + kvh;
+  const int w0 = U > 0 ? start / C : 0, w1 = U > 0 ? (start + U - 1) / C : -1;
+  float lmax = -INFINITY;
+  for (int w = w0; w <= w1; ++w) lmax = fmaxf(lmax, a.lse_parts[(size_t)(bh + w) * a.G + row]);
+  float wsum = 0.f, inv = 0.f, L = -INFINITY;
+  if (lmax != -INFINITY) {
+    for (int w = w0; w <= w1; ++w) wsum += expf(a.lse_parts[(size_t)(bh + w) * a.G + row] - lmax);
+    inv = 1.f / wsum;
+    L = lmax + logf(wsum);
+  }
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float out = 0.f;
+    if (lmax != -INFINITY)
+      for (int w = w0; w <= w1; ++w)
+        out += expf(a.lse_parts[(size_t)(bh + w) * a.G + row] - lmax) * inv *
+               a.o_parts[((size_t)(bh + w) * a.G + row) * d + c];
+    if (a.fin_o16) a.fin_o16[(size_t)r * d + c] = __float2half_rn(out);
+    if (a.fin_o32) a.fin_o32[(size_t)r * d + c] = out;
+  }
+  if (threadIdx.x == 0) a.fin_lse[r] = L;
 }
 
 // Log-sum-exp combine over parts in ascending order (R-23).  One thread per
@@ -616,9 +754,37 @@ __global__ void combine_kernel(int n_parts, int rows, int d, const float* __rest
 namespace ta_host {
 using namespace ta;
 
-size_t decode_workspace(int B, int Hq, int HD, int S) {
-  if (S <= 1) return 0;
-  return (size_t)S * B * Hq * (HD + 1) * sizeof(float);
+template <int HD, bool PK, bool TP>
+static int decode_ctas_per_sm() {
+  int n = 0;
+  const size_t smem = sizeof(DecodeWarpSmem<HD>) * kWarpsPerCta;
+  cudaFuncSetAttribute(decode_kernel<HD, PK, TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_kernel<HD, PK, TP>, 32 * kWarpsPerCta, smem) !=
+      cudaSuccess)
+    n = 0;
+  return n;
+}
+
+// Worker warps of the balanced schedule on the current device: every SM
+// filled to the decode kernel's occupancy.
+int decode_workers(int Hq, int Hkv, int HD) {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return 0;
+  const bool pack = Hkv > 0 && Hq / Hkv <= 4;
+  const int per_sm = HD == 128 ? (pack ? decode_ctas_per_sm<128, true, false>() : decode_ctas_per_sm<128, false, false>())
+                               : (pack ? decode_ctas_per_sm<64, true, false>() : decode_ctas_per_sm<64, false, false>());
+  const char* ov = getenv("TURBO_DECODE_WORKERS");  // experiments only: override W
+  if (ov && atoi(ov) > 0) return atoi(ov);
+  return sms * per_sm * kWarpsPerCta;
+}
+
+size_t decode_workspace(int B, int Hq, int Hkv, int HD, int S) {
+  if (S == 1) return 0;
+  if (S > 1) return (size_t)S * B * Hq * (HD + 1) * sizeof(float);
+  // balanced: parts bh + w < B * Hkv + W, G rows of d + 1 floats each
+  const int W = decode_workers(Hq, Hkv, HD);
+  return W <= 0 ? 0 : ((size_t)B * Hkv + W) * (Hq / Hkv) * (HD + 1) * sizeof(float);
 }
 
 cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, int Hq, const __half* q, int blk_begin,
@@ -626,6 +792,7 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
                           cudaStream_t st) {
   const int B = c->batch, H = c->n_kv_heads, HD = c->head_dim;
   DecodeArgs a;
+  memset(&a, 0, sizeof(a));
   a.q = q;
   a.block_rec = c->block_rec;
   a.s_parent = c->s_parent;
@@ -647,17 +814,21 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
   fill_sas_const(&a.sas, p->sas_nr);
   const bool has_tap = p->debug_tap != nullptr;
   if (has_tap) a.tap = *reinterpret_cast<const turbo_debug_tap_t*>(p->debug_tap);
-  else memset(&a.tap, 0, sizeof(a.tap));
+  const int W = S == 0 ? decode_workers(Hq, H, HD) : 0;
+  if (S == 0 && W <= 0) return cudaErrorInvalidConfiguration;
   if (S == 1) {
     a.o_parts = o_part;
     a.lse_parts = lse;
     a.o16 = o;
   } else {
+    const size_t parts = S > 1 ? (size_t)S * B * H : (size_t)B * H + W;
     a.o_parts = reinterpret_cast<float*>(ws);
-    a.lse_parts = a.o_parts + (size_t)S * B * Hq * HD;
-    a.o16 = nullptr;
+    a.lse_parts = a.o_parts + parts * a.G * HD;
+    a.fin_o16 = o;
+    a.fin_o32 = o_part;
+    a.fin_lse = lse;
   }
-  const int tasks = B * H * S;
+  const int tasks = S > 0 ? B * H * S : W;
   const dim3 grid((tasks + kWarpsPerCta - 1) / kWarpsPerCta);
   const bool pack = a.G <= 4;
 #define TA_DEC(HDV, PK, TP)                                                                             \
@@ -681,8 +852,12 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
 #undef TA_DEC
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || S == 1) return e;
-  const int rows = B * Hq;
-  combine_kernel<<<(rows * HD + 255) / 256, 256, 0, st>>>(S, rows, HD, a.o_parts, a.lse_parts, o, o_part, lse);
+  if (S == 0) {
+    combine_balanced_kernel<<<B * Hq, 128, 0, st>>>(a, W, HD);
+  } else {
+    const int rows = B * Hq;
+    combine_kernel<<<(rows * HD + 255) / 256, 256, 0, st>>>(S, rows, HD, a.o_parts, a.lse_parts, o, o_part, lse);
+  }
   return cudaGetLastError();
 }
 

@@ -20,7 +20,7 @@ def L():
 
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "turbo_attention.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:TURBO_API\s+)?(?:const char\*|turbo_status_t|size_t)\s+(turbo_\w+)\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:TURBO_API\s+)?(?:const char\*|turbo_status_t|size_t|int32_t)\s+(turbo_\w+)\(", src, re.M)))
 
 
 def test_header_declares_the_boundary():
@@ -65,8 +65,11 @@ def test_host_validation_without_gpu(L):
     bad = b.params(head_dim=128, sas_nr=0)
     assert L.turbo_attention_prefill(C.byref(bad), 1, 64, 2, 2, 1, *[None] * 7, None) == b.TURBO_ERR_UNSUPPORTED
     assert L.turbo_combine_lse(0, 1, 1, None, None, None, None, None, None) == b.TURBO_ERR_INVALID_ARG
-    assert L.turbo_decode_workspace_bytes(2, 8, 128, 1) == 0
-    assert L.turbo_decode_workspace_bytes(2, 8, 128, 4) == 4 * 2 * 8 * 129 * 4
+    assert L.turbo_decode_workspace_bytes(2, 8, 2, 128, 1) == 0
+    assert L.turbo_decode_workspace_bytes(2, 8, 2, 128, 4) == 4 * 2 * 8 * 129 * 4
+    assert L.turbo_decode_workspace_bytes(2, 8, 3, 128, 4) == 0  # Hq % Hkv != 0
+    assert L.turbo_decode_workspace_bytes(2, 8, 2, 128, -1) == 0
+    assert L.turbo_decode_workers(8, 3, 128) == 0
     # quantize_kv / decode with a malformed cache struct
     cache = b.TurboKVCache()
     assert L.turbo_quantize_kv(C.byref(p), C.byref(cache), None, None, 1, 0, None, None, None, None,

@@ -102,10 +102,11 @@ def test_fullsize_prefill_configs3(ta):
         np.testing.assert_allclose(lse[0, h, r0:r1].cpu().numpy(), rl[r0:r1], atol=1e-4, rtol=1e-5)
 
 
-def _decode_fullsize(ta, B, N, Hq, Hkv, d, seed_kv, seed_tok, alpha_mode, samples):
-    """Cache build + one APPEND + split-KV decode with bench.py's auto split
-    count; the oracle rebuilds sampled (b, kv_head) slots and decodes their G
-    query heads over the same split ranges, then combines."""
+def _decode_fullsize(ta, B, N, Hq, Hkv, d, seed_kv, seed_tok, alpha_mode, samples, S):
+    """Cache build + one APPEND + split-KV decode in bench.py's configuration
+    (S = 0: the balanced schedule; S > 1: equal splits); the oracle rebuilds
+    sampled (b, kv_head) slots and decodes their G query heads over the same
+    sub-ranges, then combines."""
     G = Hq // Hkv
     bits = synth.head_bits_alternating(Hkv)
     p = ta.params(head_dim=d, alpha_mode=alpha_mode)
@@ -114,14 +115,17 @@ def _decode_fullsize(ta, B, N, Hq, Hkv, d, seed_kv, seed_tok, alpha_mode, sample
     ta.turbo_quantize_kv(p, cache, k, v)
     qd, kd, vd = (x[:, 0].contiguous() for x in synth.qkv_torch(seed_tok, B, 1, Hq, Hkv, d))
     ta.turbo_quantize_kv(p, cache, kd, vd, mode=1)
-    S = ta.auto_splits(B, Hkv, cache.n_tokens // 64)
     o, _, lse = ta.turbo_attention_decode(p, cache, qd, n_splits=S)
     torch.cuda.synchronize()
-    assert S > 1
     op = O.params(d=d, alpha_mode=alpha_mode)
     nb = N // 64
-    per = -(-nb // S)
-    bounds = [(min(s * per, nb), min(s * per + per, nb)) for s in range(S)]
+    if S > 0:
+        per = -(-nb // S)
+        pieces = {key: [(min(s * per, nb), min(s * per + per, nb), s == S - 1) for s in range(S)] for key in samples}
+    else:  # every sequence: nb blocks + the 1-token buffer block
+        rng = ta.balanced_ranges([nb + 1] * B, Hkv, ta.turbo_decode_workers(Hq, Hkv, d))
+        pieces = {key: [(u0, min(u1, nb), u1 > nb) for u0, u1 in rng[key]] for key in samples}
+        assert max(len(x) for x in pieces.values()) > 1
     for b, kvh in samples:
         ks, vs = O.Slot(op, int(bits[kvh][0]), nb + 4), O.Slot(op, int(bits[kvh][1]), nb + 4)
         ks.prefill(_host(k[b, :, kvh]))
@@ -137,17 +141,25 @@ def _decode_fullsize(ta, B, N, Hq, Hkv, d, seed_kv, seed_tok, alpha_mode, sample
                 np.testing.assert_array_equal(z_int, sl.z_int[j])
         for h in range(kvh * G, kvh * G + G):
             qh = _host(qd[b, h])
-            parts = [O.decode_head(op, qh, ks, vs, a_, e_, s == S - 1) for s, (a_, e_) in enumerate(bounds)]
-            ro, rl = O.combine(np.stack([x for x, _ in parts]), np.array([y for _, y in parts], np.float32))
+            parts = [O.decode_head(op, qh, ks, vs, a_, e_, wb) for a_, e_, wb in pieces[(b, kvh)]]
+            if len(parts) == 1:
+                ro, rl = parts[0]
+            else:
+                ro, rl = O.combine(np.stack([x for x, _ in parts]), np.array([y for _, y in parts], np.float32))
             _close(_host(o[b, h]), ro, f"decode b{b} h{h}")
             assert abs(float(lse[b, h]) - float(rl)) <= 1e-4
 
 
 def test_fullsize_decode_configs2(ta):
     """configs[2] (bench.py's decode object): Phi-3-medium 40/10 heads, B=64, 32k, mixed bits."""
-    _decode_fullsize(ta, 64, 32768, 40, 10, 128, 3003, 6000, 0, ((0, 0), (37, 5), (63, 9)))
+    _decode_fullsize(ta, 64, 32768, 40, 10, 128, 3003, 6000, 0, ((0, 0), (37, 5), (63, 9)), 0)
+
+
+def test_fullsize_decode_configs2_equal_splits(ta):
+    """configs[2] with equal splits (auto_splits), the other schedule."""
+    _decode_fullsize(ta, 64, 32768, 40, 10, 128, 3003, 6000, 0, ((37, 5),), ta.auto_splits(64, 10, 512))
 
 
 def test_fullsize_decode_configs4(ta):
     """configs[4] on one rank (bench.py --workload decode_long): 128k context, B=16, 32/8 heads, alpha_mode 1."""
-    _decode_fullsize(ta, 16, 131072, 32, 8, 128, 9009, 7000, 1, ((0, 0), (15, 7)))
+    _decode_fullsize(ta, 16, 131072, 32, 8, 128, 9009, 7000, 1, ((0, 0), (15, 7)), 0)

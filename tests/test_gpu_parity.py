@@ -146,18 +146,29 @@ DEC_CASES = [  # (B, N_prefill, n_append, Hq, Hkv, d, n_splits, alpha_mode)
     (2, 700, 70, 8, 2, 128, 1, 0),      # GQA, mixed 2/4 bit, buffer + flush
     (2, 700, 5, 8, 2, 128, 3, 1),       # in-GPU split-KV + combine
     (1, 64 * 9, 0, 4, 1, 128, 4, 0),    # G = 4, empty buffer
+    # balanced schedule (n_splits = 0): chunks of >= 8 units cut across (b, kv head) ranges
+    (2, 700, 70, 8, 2, 128, 0, 0),      # pieces incl. a buffer-only piece
+    (3, 64 * 20 + 5, 3, 8, 2, 128, 0, 1),
+    (1, 128, 64, 1, 1, 64, 0, 0),       # d = 64, one piece
+    (1, 64 * 9, 0, 4, 1, 128, 0, 0),    # G = 4, empty buffer
 ]
 
 
 def _oracle_decode(op, q, slots, G, splits_bounds):
-    """Per q head: oracle decode over explicit split ranges + combine."""
+    """Per q head: oracle decode over explicit split ranges + combine.
+    splits_bounds: [(a, e)] (buffer with the last) or, per kv head,
+    {kvh: [(a, e, with_buffer)]}."""
     Hq = q.shape[0]
     outs, lses = np.zeros((Hq, op.d), np.float32), np.zeros(Hq, np.float32)
     for h in range(Hq):
         ks, vs = slots[h // G]
+        if isinstance(splits_bounds, dict):
+            pieces = splits_bounds[h // G]
+        else:
+            pieces = [(a, e, s == len(splits_bounds) - 1) for s, (a, e) in enumerate(splits_bounds)]
         parts, ls = [], []
-        for s, (a, e) in enumerate(splits_bounds):
-            o, l = O.decode_head(op, q[h], ks, vs, a, e, s == len(splits_bounds) - 1)
+        for a, e, wb in pieces:
+            o, l = O.decode_head(op, q[h], ks, vs, a, e, wb)
             parts.append(o)
             ls.append(l)
         if len(parts) == 1:
@@ -165,6 +176,18 @@ def _oracle_decode(op, q, slots, G, splits_bounds):
         else:
             outs[h], lses[h] = O.combine(np.stack(parts), np.array(ls))
     return outs, lses
+
+
+def balanced_bounds(ta, slots_by_b, Hq, Hkv, d):
+    """{b: {kvh: [(a, e, with_buffer)]}} of the balanced schedule, from the
+    documented partition (include/turbo_attention.h) and the oracle's counters."""
+    units = [sl[0][0].n_blocks + (1 if sl[0][0].n_buf > 0 else 0) for sl in slots_by_b]
+    rng = ta.balanced_ranges(units, Hkv, ta.turbo_decode_workers(Hq, Hkv, d))
+    out = {}
+    for b, sl in enumerate(slots_by_b):
+        nb = sl[0][0].n_blocks
+        out[b] = {h: [(u0, min(u1, nb), u1 > nb) for u0, u1 in rng[(b, h)]] for h in range(Hkv)}
+    return out
 
 
 @pytest.mark.parametrize("case", DEC_CASES)
@@ -191,8 +214,12 @@ def test_append_and_decode_parity(ta, case):
     torch.cuda.synchronize()
     o, lse = o.cpu().numpy(), lse.cpu().numpy()
     nb = ref["slots"][0][0][0].n_blocks
-    per = -(-nb // S)
-    bounds = [(min(s * per, nb), min(s * per + per, nb)) for s in range(S)]
+    if S > 0:
+        per = -(-nb // S)
+        bounds = [(min(s * per, nb), min(s * per + per, nb)) for s in range(S)]
+    else:
+        bal = balanced_bounds(ta, ref["slots"], Hq, Hkv, d)
+        assert B * Hkv == 1 or sum(len(v) for x in bal.values() for v in x.values()) > B * Hkv  # really split
     # cache state after the appends is bit-exact
     recs = cache.records().cpu().numpy()
     cnt = cache.counters.view(B, 2).cpu().numpy()
@@ -205,13 +232,14 @@ def test_append_and_decode_parity(ta, case):
                     np.testing.assert_array_equal(codes, sl.codes[j])
                     np.testing.assert_array_equal(s_int, sl.s_int[j])
                     np.testing.assert_array_equal(z_int, sl.z_int[j])
-        ro, rl = _oracle_decode(op, qd[b].astype(np.float32), ref["slots"][b], G, bounds)
+        ro, rl = _oracle_decode(op, qd[b].astype(np.float32), ref["slots"][b], G, bounds if S > 0 else bal[b])
         assert_out_close(o[b], ro, f"decode b{b}")
         np.testing.assert_allclose(lse[b], rl, atol=1e-4, rtol=1e-5)
 
 
 @pytest.mark.parametrize("j_block", [0, 3, -1])
-def test_decode_exact_set_tap(ta, j_block):
+@pytest.mark.parametrize("n_splits", [1, 0])
+def test_decode_exact_set_tap(ta, j_block, n_splits):
     B, N, Hq, Hkv, d = 2, 64 * 5 + 37, 8, 2, 128
     q, k, v = synth.qkv(77, B, N, Hq, Hkv, d)
     bits = synth.head_bits_alternating(Hkv)
@@ -221,7 +249,7 @@ def test_decode_exact_set_tap(ta, j_block):
     cache = ta.KVCache(B, Hkv, d, max_blocks=8, bits=bits)
     ta.turbo_quantize_kv(p, cache, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
     qd, _, _ = synth.decode_token(31, B, Hq, Hkv, d)
-    ta.turbo_attention_decode(p, cache, torch.from_numpy(qd).cuda(), n_splits=1)
+    ta.turbo_attention_decode(p, cache, torch.from_numpy(qd).cuda(), n_splits=n_splits)  # 6 units: one piece
     torch.cuda.synchronize()
     op = O.params(d=d)
     ref = O.build_cache(op, k.astype(np.float32), v.astype(np.float32), bits, 8)

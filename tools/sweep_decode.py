@@ -9,8 +9,8 @@ from paper_2412_08585_b200 import binding as ta  # noqa: E402
 from paper_2412_08585_b200 import synth  # noqa: E402
 import bench  # noqa: E402
 
-SPL3 = tuple(int(x) for x in os.environ.get("SPL3", "4,6,8,12,16").split(","))
-SPL5 = tuple(int(x) for x in os.environ.get("SPL5", "8,16,24,32,48").split(","))
+SPL3 = tuple(int(x) for x in os.environ.get("SPL3", "0,8,12").split(","))
+SPL5 = tuple(int(x) for x in os.environ.get("SPL5", "0,32").split(","))
 for name, (B, N, Hq, Hkv, d), splits in (("cfg3", (64, 32768, 40, 10, 128), SPL3),
                                          ("cfg5", (16, 131072, 32, 8, 128), SPL5)):
     bits = synth.head_bits_alternating(Hkv)
@@ -23,7 +23,7 @@ for name, (B, N, Hq, Hkv, d), splits in (("cfg3", (64, 32768, 40, 10, 128), SPL3
     qd = synth.qkv_torch(7, B, 1, Hq, Hkv, d)[0][:, 0].contiguous()
     byt = bench.decode_bytes(B, Hkv, d, N // 64, 0, bits, Hq)
     for S in splits:
-        ws = torch.empty(max(ta.turbo_decode_workspace_bytes(B, Hq, d, S), 16), dtype=torch.uint8, device="cuda")
+        ws = torch.empty(max(ta.turbo_decode_workspace_bytes(B, Hq, Hkv, d, S), 16), dtype=torch.uint8, device="cuda")
         for _ in range(3):
             ta.turbo_attention_decode(p, cache, qd, n_splits=S, workspace=ws)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
