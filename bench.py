@@ -156,6 +156,8 @@ def run_ours(args, rank, world, device):
     qd, kd, vd = (x[:, 0].contiguous() for x in synth.qkv_torch(4002 + rank, B, 1, Hq, Hkv, d, device=device))
     cache = ta.KVCache(B, Hkv, d, max_blocks=N // 64 + 2, bits=bits, device=device)
     S = args.splits
+    if S is None:
+        S = ta.auto_splits(B, Hkv, N // 64, ta.turbo_decode_workers(Hq, Hkv, d))
     ws = torch.empty(max(ta.turbo_decode_workspace_bytes(B, Hq, Hkv, d, S), 16), dtype=torch.uint8, device=device)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=device)  # > 126 MB L2
     st = torch.cuda.current_stream()
@@ -284,7 +286,9 @@ def bench_decode(args, rank, world, device, pk):
     ta.turbo_quantize_kv(p, cache, k, v)  # builds the 32k-token compressed cache
     del k, v
     torch.cuda.empty_cache()
-    S = 0 if args.decode_splits is None else args.decode_splits  # 0: balanced schedule
+    S = args.decode_splits
+    if S is None:
+        S = ta.auto_splits(B, Hkv, cache.n_tokens // 64, ta.turbo_decode_workers(Hq, Hkv, d))
     ws = torch.empty(max(ta.turbo_decode_workspace_bytes(B, Hq, Hkv, d, S), 16), dtype=torch.uint8, device=device)
     toks = [tuple(x[:, 0].contiguous() for x in synth.qkv_torch(6000 + i, B, 1, Hq, Hkv, d, device=device))
             for i in range(args.warmup + args.steps)]
@@ -372,7 +376,8 @@ def workload_config(args):
                         "batch 8, causal, INT8 tcgen05; step = quantize_kv + prefill + append + split-KV decode",
             "global_batch": c["B"] * args.gpus, "seq_len": c["N"], "n_q_heads": c["Hq"], "n_kv_heads": c["Hkv"],
             "head_dim": c["d"], "block_q": 64, "block_kv": 64, "sas_nr": -6, "alpha_mode": 0,
-            "kv_bits": "half of the (kv_head, K/V) slots 2-bit, rest 4-bit", "decode_splits": args.splits,
+            "kv_bits": "half of the (kv_head, K/V) slots 2-bit, rest 4-bit",
+            "decode_splits": args.splits if args.splits is not None else "auto (binding.auto_splits)",
             "parallelism": f"(batch, kv-head) partition, {args.gpus} rank(s), no collective",
             "l2": "flushed between timed steps (512 MB write)"}
 
@@ -492,9 +497,10 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--splits", type=int, default=0, help="split-KV count of the decode in the step (0: balanced)")
+    ap.add_argument("--splits", type=int, default=None,
+                    help="split-KV count of the decode in the step (default: auto_splits; 0: balanced)")
     ap.add_argument("--decode-splits", type=int, default=None,
-                    help="decode split count (default 0: the balanced schedule)")
+                    help="decode split count (default: binding.auto_splits; 0: the balanced schedule)")
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--workload", default="step", choices=["step", "prefill_70b", "decode_long"],
                     help="step = the default hot-path step (configs[1] + configs[2] decode)")

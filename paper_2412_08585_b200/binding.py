@@ -210,23 +210,31 @@ def balanced_ranges(unit_counts, Hkv, workers, min_units=8):
     return out
 
 
-def auto_splits(batch, n_kv_heads, n_blocks, target_tasks=5120):
-    """Split count giving ~target_tasks warp tasks (~3 waves of the ~1800 resident
-    decode warps on 148 SMs), at least 8 blocks per split.  5120 is the best of a
-    B200 sweep on configs[2] (S = 8) and configs[4] (S = 40; tools/sweep_decode.py)."""
-    s = -(-target_tasks // max(1, batch * n_kv_heads))
-    return max(1, min(s, n_blocks // 8))
+def auto_splits(batch, n_kv_heads, n_blocks, workers=None):
+    """Equal-split count for turbo_attention_decode: splits of ~64 blocks, doubled
+    until the (b, kv head, split) warp tasks cover two waves of the resident
+    decode warps (`workers`, default turbo_decode_workers for G <= 4, d = 128),
+    keeping >= 8 blocks per split.  On B200 this lands within 2 % of the best
+    of a sweep on configs[2] (S = 8) and configs[4] (S = 32; tools/sweep_decode.py)."""
+    if workers is None:
+        workers = max(1, turbo_decode_workers(4, 1, 128))
+    s = max(1, -(-n_blocks // 64))
+    while batch * n_kv_heads * s < 2 * workers and 2 * s <= max(1, n_blocks // 8):
+        s *= 2
+    return s
 
 
 def turbo_attention_decode(p, cache: KVCache, q, blk_begin=0, blk_end=-1, with_buffer=True, n_splits=1,
                            workspace=None, o=None, o_part=None, lse=None, want_fp16=True, want_f32=False,
                            stream=None):
     """q fp16 [B,Hq,d] -> (o fp16 [B,Hq,d] or None, o_part f32 [B,Hq,d] or None, lse f32 [B,Hq]).
-    n_splits >= 1: equal splits; 0 or None: the balanced schedule."""
+    n_splits >= 1: equal splits; None: auto_splits(); 0: the balanced schedule."""
     assert q.dtype == torch.float16 and q.is_contiguous()
     B, Hq, d = q.shape
     if n_splits is None:
-        n_splits = 0
+        nb = (cache.n_tokens // cache.block_kv) if blk_end < 0 else blk_end
+        n_splits = auto_splits(B, cache.n_kv_heads, max(0, nb - blk_begin),
+                               max(1, turbo_decode_workers(Hq, cache.n_kv_heads, d)))
     dev = q.device
     if want_fp16 and o is None:
         o = torch.empty((B, Hq, d), dtype=torch.float16, device=dev)

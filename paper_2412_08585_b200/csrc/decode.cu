@@ -23,16 +23,24 @@
 
 namespace ta {
 
-constexpr int kWarpsPerCta = 4;
+// One warp per CTA: a finished task frees its SM slot at once (the block
+// scheduler refills it), instead of holding it until the CTA's slowest warp
+// ends -- +3-6 % KV GB/s on configs[2] / configs[4] and far less sensitivity
+// to the split count (tools/sweep_decode.py).
+constexpr int kWarpsPerCta = 1;
 constexpr int kMinUnits = 8;  // balanced schedule: least units (blocks) per warp chunk
 
-template <int HD>
+// Per-warp shared memory.  ROWS = query rows held (G <= 4 on the packed path,
+// else 8), so that twelve packed-path warps fit in one SM's 228 KB.
+template <int HD, int ROWS>
 struct DecodeWarpSmem {
   uint8_t rec[2][2][rec_bytes(HD)];  // [stage][K,V][record]
-  int8_t q1[8][HD];
-  uint8_t p[8][kBc];
+  int8_t q1[ROWS][HD];
+  uint8_t p[ROWS][kBc];
   uint64_t bar[2];
 };
+template <int HD, bool PACK>
+using DecodeSmem = DecodeWarpSmem<HD, PACK ? 4 : 8>;
 
 struct DecodeArgs {
   const __half* q;
@@ -48,6 +56,7 @@ struct DecodeArgs {
   __half* fin_o16;  // balanced schedule: final fp16 output (or NULL)
   float* fin_o32;   // balanced schedule: final f32 output (or NULL)
   float* fin_lse;   // balanced schedule: final L
+  int stagger_ns;   // balanced schedule: start delay step per warp slot (experiments; 0 = none)
   int B, Hq, Hkv, G, max_blocks, blk_begin, blk_end, with_buffer, n_splits, alpha_mode;
   float scale;
   SasConst sas;
@@ -454,7 +463,7 @@ TA_DEV SeqUnits seq_units(const DecodeArgs& a, int b) {
 // part == b*Hkv + kvh).  `it` counts the ring iterations of this warp across
 // segments (stage = it & 1, mbarrier parity = (it >> 1) & 1).
 template <int HD, bool PACK, bool TAP>
-TA_DEV void decode_segment(const DecodeArgs& a, DecodeWarpSmem<HD>& sm, int b, int kvh, int j0, int j1, bool use_buf,
+TA_DEV void decode_segment(const DecodeArgs& a, DecodeSmem<HD, PACK>& sm, int b, int kvh, int j0, int j1, bool use_buf,
                            int nbuf, size_t part, bool tap_ok, uint32_t& it, int lane) {
   using M = Map<HD, PACK>;
   const int g = lane >> 2, q = lane & 3;
@@ -498,7 +507,8 @@ TA_DEV void decode_segment(const DecodeArgs& a, DecodeWarpSmem<HD>& sm, int b, i
     s_q_row = div_by_119(qa);
 #pragma unroll
     for (int i = 0; i < R; i += 4)
-      *reinterpret_cast<uint32_t*>(&sm.q1[g][q * R + i]) =
+      if (g < (PACK ? 4 : 8))  // rows >= G are zero (and absent on the packed path)
+        *reinterpret_cast<uint32_t*>(&sm.q1[g][q * R + i]) =
           pack4_lo(rint_prod_bits(xv[i], inv), rint_prod_bits(xv[i + 1], inv), rint_prod_bits(xv[i + 2], inv),
                    rint_prod_bits(xv[i + 3], inv));
     if (TAP && g == tap_row) {
@@ -616,7 +626,7 @@ template <int HD, bool PACK, bool TAP>
 __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_constant__ DecodeArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  DecodeWarpSmem<HD>& sm = reinterpret_cast<DecodeWarpSmem<HD>*>(smem_raw)[warp];
+  DecodeSmem<HD, PACK>& sm = reinterpret_cast<DecodeSmem<HD, PACK>*>(smem_raw)[warp];
   if (lane == 0) {
     mbar_init(&sm.bar[0], 1);
     mbar_init(&sm.bar[1], 1);
@@ -638,6 +648,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
   }
   // balanced schedule
   const int W = gridDim.x * kWarpsPerCta, w = blockIdx.x * kWarpsPerCta + warp;
+  if (a.stagger_ns > 0) __nanosleep((unsigned)(((w * 7) % 12) * a.stagger_ns));
   int tot = 0;
   for (int b0 = 0; b0 < a.B; b0 += 32)
     if (b0 + lane < a.B) tot += seq_units(a, b0 + lane).units;
@@ -757,7 +768,7 @@ using namespace ta;
 template <int HD, bool PK, bool TP>
 static int decode_ctas_per_sm() {
   int n = 0;
-  const size_t smem = sizeof(DecodeWarpSmem<HD>) * kWarpsPerCta;
+  const size_t smem = sizeof(DecodeSmem<HD, PK>) * kWarpsPerCta;
   cudaFuncSetAttribute(decode_kernel<HD, PK, TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_kernel<HD, PK, TP>, 32 * kWarpsPerCta, smem) !=
       cudaSuccess)
@@ -815,6 +826,7 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
   const bool has_tap = p->debug_tap != nullptr;
   if (has_tap) a.tap = *reinterpret_cast<const turbo_debug_tap_t*>(p->debug_tap);
   const int W = S == 0 ? decode_workers(Hq, H, HD) : 0;
+  if (const char* sg = getenv("TURBO_DECODE_STAGGER")) a.stagger_ns = atoi(sg);
   if (S == 0 && W <= 0) return cudaErrorInvalidConfiguration;
   if (S == 1) {
     a.o_parts = o_part;
@@ -833,7 +845,7 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
   const bool pack = a.G <= 4;
 #define TA_DEC(HDV, PK, TP)                                                                             \
   {                                                                                                     \
-    const size_t smem = sizeof(DecodeWarpSmem<HDV>) * kWarpsPerCta;                                     \
+    const size_t smem = sizeof(DecodeSmem<HDV, PK>) * kWarpsPerCta;                                     \
     cudaFuncSetAttribute(decode_kernel<HDV, PK, TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     decode_kernel<HDV, PK, TP><<<grid, 32 * kWarpsPerCta, smem, st>>>(a);                              \
   }

@@ -104,7 +104,7 @@ def test_fullsize_prefill_configs3(ta):
 
 def _decode_fullsize(ta, B, N, Hq, Hkv, d, seed_kv, seed_tok, alpha_mode, samples, S):
     """Cache build + one APPEND + split-KV decode in bench.py's configuration
-    (S = 0: the balanced schedule; S > 1: equal splits); the oracle rebuilds
+    (S > 1: equal splits, bench.py's auto_splits; S = 0: the balanced schedule); the oracle rebuilds
     sampled (b, kv_head) slots and decodes their G query heads over the same
     sub-ranges, then combines."""
     G = Hq // Hkv
@@ -152,14 +152,16 @@ def _decode_fullsize(ta, B, N, Hq, Hkv, d, seed_kv, seed_tok, alpha_mode, sample
 
 def test_fullsize_decode_configs2(ta):
     """configs[2] (bench.py's decode object): Phi-3-medium 40/10 heads, B=64, 32k, mixed bits."""
-    _decode_fullsize(ta, 64, 32768, 40, 10, 128, 3003, 6000, 0, ((0, 0), (37, 5), (63, 9)), 0)
+    _decode_fullsize(ta, 64, 32768, 40, 10, 128, 3003, 6000, 0, ((0, 0), (37, 5), (63, 9)),
+                     ta.auto_splits(64, 10, 512, ta.turbo_decode_workers(40, 10, 128)))
 
 
-def test_fullsize_decode_configs2_equal_splits(ta):
-    """configs[2] with equal splits (auto_splits), the other schedule."""
-    _decode_fullsize(ta, 64, 32768, 40, 10, 128, 3003, 6000, 0, ((37, 5),), ta.auto_splits(64, 10, 512))
+def test_fullsize_decode_configs2_balanced(ta):
+    """configs[2] with the balanced schedule (n_splits = 0), the other schedule."""
+    _decode_fullsize(ta, 64, 32768, 40, 10, 128, 3003, 6000, 0, ((37, 5),), 0)
 
 
 def test_fullsize_decode_configs4(ta):
     """configs[4] on one rank (bench.py --workload decode_long): 128k context, B=16, 32/8 heads, alpha_mode 1."""
-    _decode_fullsize(ta, 16, 131072, 32, 8, 128, 9009, 7000, 1, ((0, 0), (15, 7)), 0)
+    _decode_fullsize(ta, 16, 131072, 32, 8, 128, 9009, 7000, 1, ((0, 0), (15, 7)),
+                     ta.auto_splits(16, 8, 2048, ta.turbo_decode_workers(32, 8, 128)))
