@@ -10,9 +10,9 @@
 // Integer dequantisation (Alg. 2) is folded exactly (Eq. 5, P:275-283,
 // linear because reconstructions never clamp, R-6):
 //   S[t]    = sum_c q1_c (code_tc s_c + z_c)
-//           = 128 * sum_c hi(q1_c s_c) code_tc + sum_c lo(q1_c s_c) code_tc + sum_c q1_c z_c
+//           = 256 * sum_c hi(q1_c s_c) code_tc + sum_c lo(q1_c s_c) code_tc + sum_c q1_c z_c
 //   PV[c]   = sum_t P_t (code_tc s_c + z_c) = s_c * sum_t P_t code_tc + z_c * sum_t P_t
-// with q1_c s_c = 128 hi + lo, hi in [-75, 74] (s8), lo in [0, 127] (u8), so the
+// with q1_c s_c = 256 hi + lo, lo = the signed low byte, hi in [-38, 37] (both s8), so the
 // tensor cores see only raw 4-bit / 2-bit codes.
 #include <climits>
 #include <cstdlib>
@@ -63,6 +63,7 @@ struct DecodeArgs {
   turbo_debug_tap_t tap;
 };
 
+TA_DEV uint32_t word_of(const uint4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
 TA_DEV uint32_t byte_of(const uint4& v, int i) {  // one PRMT (i is a compile-time constant)
   const uint32_t w = i < 4 ? v.x : i < 8 ? v.y : i < 12 ? v.z : v.w;
   return __byte_perm(w, 0u, 0x4440u | (uint32_t)(i & 3));
@@ -90,6 +91,19 @@ TA_DEV int lds_s8(uint32_t a) {
   return v;
 }
 TA_DEV void sts_u8(uint32_t a, uint32_t v) { asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
+// N consecutive 32-bit words from a 4N-byte aligned shared address (one LDS.32/64/128).
+template <int N>
+TA_DEV void lds_words(uint32_t a, uint32_t (&w)[N]) {
+  if (N == 4) {
+    asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(w[0]), "=r"(w[N > 1 ? 1 : 0]), "=r"(w[N > 2 ? 2 : 0]),
+                 "=r"(w[N > 3 ? 3 : 0]) : "r"(a));
+  } else if (N == 2) {
+    asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(w[0]), "=r"(w[N > 1 ? 1 : 0]) : "r"(a));
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w[i]) : "r"(a + 4 * i));
+  }
+}
 
 // Reductions over the lanes that hold the same two query rows: general path
 // (rows 2q, 2q+1): lanes with equal q; packed path (rows 2(q&1), +1): equal q&1.
@@ -171,26 +185,27 @@ TA_DEV void qk_block(uint32_t rec, const int (&qv)[HD / 4], const uint4 (&q1r)[H
   uint4 s4[HD / 64];
 #pragma unroll
   for (int i = 0; i < HD / 64; ++i) s4[i] = lds128(rec + q * R + 16 * i);
-  // B fragments from q1_c * s_c = 128 hi + lo (hi in s8, lo in [0,127]).  Packed
-  // path: column g < 4 holds hi of row g, column g >= 4 holds lo of row g - 4
-  // (one IMMA); general path: separate hi and lo IMMAs.
-  const uint32_t sh = (PACK && g >= 4) ? 0u : 7u;
-  const uint32_t msk = (PACK && g >= 4) ? 0x7F7F7F7Fu : 0xFFFFFFFFu;
+  // B fragments from q1_c * s_c = 256 hi + lo (lo = signed low byte, hi = (q1_c s_c + 128) >> 8,
+  // both s8).  With t = q1_c s_c + 128 from one IDP.4A (s word . q1_c placed in byte c mod 4,
+  // accumulator 128): hi = byte 1 of t, lo = byte 0 of t ^ 0x80 -- byte selects only.  Packed
+  // path: column g < 4 holds hi of row g, column g >= 4 holds lo of row g - 4 (one IMMA);
+  // general path: separate hi and lo IMMAs.
+  const uint32_t psel = (PACK && g >= 4) ? 0x40u : 0x51u;  // PRMT pair select: byte 0 / byte 1
+  const uint32_t pxor = (PACK && g >= 4) ? 0x80808080u : 0u;
   uint32_t bhi[U::N][2], blo[U::N][2];
 #pragma unroll
   for (int u = 0; u < U::N; ++u)
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
-      uint32_t ph[4], pl[4];
+      uint32_t t[4];
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
-        const int loc = U::chan(u, r, m);
-        const int prod = loc < 0 ? 0 : qv[loc] * (int)byte_of(s4[loc >> 4], loc & 15);
-        ph[m] = PACK ? (uint32_t)(prod >> sh) : (uint32_t)(prod >> 7);
-        pl[m] = (uint32_t)prod;
+        const int loc = U::chan(u, r, m);  // zero slot: t = 128 -> hi = lo = 0
+        t[m] = loc < 0 ? 128u : (uint32_t)__dp4a((int)word_of(s4[loc >> 4], (loc & 15) >> 2), qv[loc], 128);
       }
-      bhi[u][r] = pack4_lo(ph[0], ph[1], ph[2], ph[3]) & msk;
-      if (!PACK) blo[u][r] = pack4_lo(pl[0], pl[1], pl[2], pl[3]) & 0x7F7F7F7Fu;
+      bhi[u][r] = __byte_perm(__byte_perm(t[0], t[1], psel), __byte_perm(t[2], t[3], psel), 0x5410) ^ pxor;
+      if (!PACK)
+        blo[u][r] = __byte_perm(__byte_perm(t[0], t[1], 0x40), __byte_perm(t[2], t[3], 0x40), 0x5410) ^ 0x80808080u;
     }
   // z term sum_c q1_c z_c of the lane-quad's row (dp4a, quad reduction).
   int zq = 0;
@@ -213,11 +228,8 @@ TA_DEV void qk_block(uint32_t rec, const int (&qv)[HD / 4], const uint4 (&q1r)[H
   for (int mt = 0; mt < 4; ++mt) {
     uint32_t w0[U::NW], w1[U::NW];
     const uint32_t t0 = codes + (16 * mt + g) * TB + q * U::QB, t1 = t0 + 8 * TB;
-#pragma unroll
-    for (int i = 0; i < U::NW; ++i) {
-      w0[i] = lds32(t0 + 4 * i);
-      w1[i] = lds32(t1 + 4 * i);
-    }
+    lds_words<U::NW>(t0, w0);  // one vector load per token region
+    lds_words<U::NW>(t1, w1);
     int ch[4] = {0, 0, 0, 0}, cl[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int u = 0; u < U::N; ++u) {
@@ -232,7 +244,7 @@ TA_DEV void qk_block(uint32_t rec, const int (&qv)[HD / 4], const uint4 (&q1r)[H
       imma_u8s8(cu, af, bh);
       if (!PACK) {
         const uint32_t bl[2] = {blo[u][0], blo[u][1]};
-        imma_u8u8(cv, af, bl);
+        imma_u8s8(cv, af, bl);
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -249,13 +261,13 @@ TA_DEV void qk_block(uint32_t rec, const int (&qv)[HD / 4], const uint4 (&q1r)[H
         const int snd = ql ? ch[e] : ch[2 + e];
         const int rcv = __shfl_xor_sync(0xffffffffu, snd, 2);
         const int hi = ql ? rcv : own, lo = ql ? own : rcv;
-        sv[mt][e] = 128 * hi + lo + (e ? z1 : z0);
+        sv[mt][e] = 256 * hi + lo + (e ? z1 : z0);
       }
     } else {
-      sv[2 * mt][0] = 128 * ch[0] + cl[0] + z0;
-      sv[2 * mt][1] = 128 * ch[1] + cl[1] + z1;
-      sv[2 * mt + 1][0] = 128 * ch[2] + cl[2] + z0;
-      sv[2 * mt + 1][1] = 128 * ch[3] + cl[3] + z1;
+      sv[2 * mt][0] = 256 * ch[0] + cl[0] + z0;
+      sv[2 * mt][1] = 256 * ch[1] + cl[1] + z1;
+      sv[2 * mt + 1][0] = 256 * ch[2] + cl[2] + z0;
+      sv[2 * mt + 1][1] = 256 * ch[3] + cl[3] + z1;
     }
   }
 }
@@ -526,7 +538,7 @@ TA_DEV void decode_segment(const DecodeArgs& a, DecodeSmem<HD, PACK>& sm, int b,
   for (int i = 0; i < HD / 64; ++i) {
     q1r[i] = lds128(q1s + brow * HD + q * (HD / 4) + 16 * i);
 #pragma unroll
-    for (int e = 0; e < 16; ++e) qv[16 * i + e] = (int)(int8_t)(uint8_t)byte_of(q1r[i], e);
+    for (int e = 0; e < 16; ++e) qv[16 * i + e] = (int)(byte_of(q1r[i], e) << (8 * (e & 3)));  // byte-positioned
   }
   const int rq = PACK ? (q & 1) : q;
   const float sq2[2] = {__shfl_sync(0xffffffffu, s_q_row, 8 * rq), __shfl_sync(0xffffffffu, s_q_row, 8 * rq + 4)};

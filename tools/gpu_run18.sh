@@ -1,0 +1,4 @@
+python __graft_entry__.py build > gpurun_out/build.log 2>&1
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q -k "decode or combine or seq" 2>&1 | tail -2
+export SPL3=8,12 SPL5=32
+bash tools/ab_decode.sh variants/dA.so variants/dB.so variants/dA.so variants/dB.so
