@@ -281,7 +281,7 @@ def run_ours(args, rank, world, device):
                   breakdown_ms={"quantize_kv_prefill": round(statistics.mean(t_quant), 4),
                                 "attention_prefill": round(pre_ms, 4),
                                 "append+decode": round(statistics.mean(t_dec), 4)})
-    del hq, hk, hv, ho, hlse, dq, dk, dv, q, k, v, flush, cache
+    del hq, hk, hv, ho, hlse, dins, outs, q, k, v, flush, cache
     torch.cuda.empty_cache()
     if not args.no_decode:
         result["decode"] = bench_decode(args, rank, world, device, pk)

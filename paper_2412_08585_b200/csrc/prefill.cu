@@ -438,20 +438,20 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
         PROF_T(c1);
         PROF_ADD(3, c0, c1);
 #pragma unroll
-        for (int cc = 0; cc < OW / 16; ++cc) {
-          uint32_t pv[16];
-          TA_TMEM_LD16(tbase + 2 * kBc + hc * OW + cc * 16, pv);
+        for (int cc = 0; cc < OW / 32; ++cc) {  // 32 columns per TMEM round trip
+          uint32_t pv[32];
+          TA_TMEM_LD32(tbase + 2 * kBc + hc * OW + cc * 32, pv);
           tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 16; e += 2) {
+          for (int e = 0; e < 32; e += 2) {
             const f32x2 o2 = fma2(pk2(cpv_p, cpv_p), pk2(__uint_as_float(pv[e]), __uint_as_float(pv[e + 1])),
-                                  pk2(O[cc * 16 + e], O[cc * 16 + e + 1]));
-            O[cc * 16 + e] = lo2(o2);
-            O[cc * 16 + e + 1] = hi2(o2);
+                                  pk2(O[cc * 32 + e], O[cc * 32 + e + 1]));
+            O[cc * 32 + e] = lo2(o2);
+            O[cc * 32 + e + 1] = hi2(o2);
           }
           if (tap_p) {
-            for (int e = 0; e < 16; ++e)
-              args.tap.pv_int[(r & 63) * HD + hc * OW + cc * 16 + e] = (int)__uint_as_float(pv[e]);
+            for (int e = 0; e < 32; ++e)
+              args.tap.pv_int[(r & 63) * HD + hc * OW + cc * 32 + e] = (int)__uint_as_float(pv[e]);
           }
         }
         tc_fence_before();
