@@ -101,24 +101,36 @@ __global__ void __launch_bounds__(2 * HD, 256 / HD) quant_prefill_kernel(
     float* __restrict__ a_univ, int8_t* __restrict__ k1, __half* __restrict__ v1t, float* __restrict__ k1s,
     float* __restrict__ v1s) {
   constexpr int NW = HD / 32;  // warps per kind
-  __shared__ __align__(16) uint8_t tile1[kBc * HD];  // K stage-1 codes [t][c]
-  __shared__ __align__(16) uint8_t tile2[kBc * HD];  // K stage-2 codes [t][c]
+  // The K and V blocks (FP16 [64][HD] each) are staged with coalesced 16-byte loads;
+  // after every thread has taken its column (the barrier of the max reduction) the
+  // space is reused for K's token-major stage-1 / stage-2 code tiles.
+  __shared__ __align__(16) __half xs[2][kBc][HD];
   __shared__ float red[2][NW];
+  uint8_t* tile1 = reinterpret_cast<uint8_t*>(&xs[0][0][0]);            // K stage-1 codes [t][c]
+  uint8_t* tile2 = reinterpret_cast<uint8_t*>(&xs[0][0][0]) + kBc * HD;  // K stage-2 codes [t][c]
   const int j = blockIdx.x, h = blockIdx.y, b = blockIdx.z, tid = threadIdx.x;
   const int kind = tid / HD, c = tid % HD;
   const int Tc = (N + kBc - 1) / kBc;
   const int rows = min(kBc, N - j * kBc);
   const size_t bh = (size_t)b * Hkv + h;
-  const __half* src = (kind ? v : k) + (((size_t)b * N + (size_t)j * kBc) * Hkv + h) * HD + c;
-  const size_t tstride = (size_t)Hkv * HD;
-
+  {
+    constexpr int C8 = HD / 8;  // 16-byte chunks per token row
+#pragma unroll
+    for (int i = tid; i < 2 * kBc * C8; i += 2 * HD) {
+      const int kd = i / (kBc * C8), t = (i / C8) % kBc, c8 = i % C8;
+      uint4 val = make_uint4(0, 0, 0, 0);
+      if (t < rows)
+        val = __ldcs(reinterpret_cast<const uint4*>((kd ? v : k) + (((size_t)b * N + (size_t)j * kBc + t) * Hkv + h) * HD) + c8);
+      *reinterpret_cast<uint4*>(&xs[kd][t][8 * c8]) = val;
+    }
+  }
+  __syncthreads();
   // the channel's 64 tokens as 32 half2
   __half2 xh[kBc / 2];
   __half2 amax2 = __float2half2_rn(0.f);
 #pragma unroll
   for (int t = 0; t < kBc; t += 2) {
-    const __half z = __float2half_rn(0.f);
-    xh[t / 2] = __halves2half2(t < rows ? __ldcs(src + t * tstride) : z, t + 1 < rows ? __ldcs(src + (t + 1) * tstride) : z);
+    xh[t / 2] = __halves2half2(xs[kind][t][c], xs[kind][t + 1][c]);
     amax2 = __hmax2(amax2, __habs2(xh[t / 2]));
   }
   float amax = fmaxf(__low2float(amax2), __high2float(amax2));  // exact: max of fp16 magnitudes
