@@ -276,7 +276,14 @@ def run_ours(args, rank, world, device):
             "peak": round(int8_peak, 1), "unit": "TFLOP/s", "frac": round(achieved / int8_peak, 4),
             "traffic": traffic_per_launch("prefill_kernel"), "peak_source": f"2 x bf16 burst {pk['bf16']} TF/s, {pk['src']}",
             "share_of_step": round(pre_ms / statistics.mean(t_step), 3)}
-    result = dict(value=value, ms_step=ms_step, e2e=e2e, roofline=roof, clocks=clocks,
+    # quantize_kv (a1/a2) as its own HBM-bound kernel: FP16 K, V in; k1 (INT8), v1t (FP16 codes), records,
+    # scales out
+    q_ms = statistics.mean(t_quant)
+    rec_b = B * Hkv * (N // 64) * sum(2 * d + 64 * d * int(bits[h][kd]) // 8 for h in range(Hkv) for kd in range(2)) // Hkv
+    q_bytes = 2 * B * N * Hkv * d * 2 + B * N * Hkv * d + B * N * Hkv * d * 2 + rec_b + 2 * B * Hkv * (N // 64) * 8
+    quant = {"ms": round(q_ms, 4), "bytes": q_bytes, "gbs": round(q_bytes / (q_ms * 1e-3) / 1e9, 1),
+             "frac_hbm": round(q_bytes / (q_ms * 1e-3) / 1e9 / pk["hbm"], 4)}
+    result = dict(value=value, ms_step=ms_step, e2e=e2e, roofline=roof, clocks=clocks, quantize_kv=quant,
                   launches=launches_per_step * args.steps,
                   breakdown_ms={"quantize_kv_prefill": round(statistics.mean(t_quant), 4),
                                 "attention_prefill": round(pre_ms, 4),
@@ -345,6 +352,7 @@ def bench_decode(args, rank, world, device, pk):
             "n_splits": S, "kv_bytes_per_step": byt, "decode_kernel_ms": round(t_dec, 4),
             "step_ms_append_plus_decode": round(t_step, 4), "kv_gbs": round(gbs, 1),
             "tokens_per_s": round(world * B / (t_step * 1e-3), 1),
+            "tokens_per_s_40_layers": round(world * B / (t_step * 1e-3) / 40, 1),  # Phi-3-medium: 40 attention layers
             "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": pk["hbm"], "unit": "GB/s",
                          "traffic": traffic_per_launch("decode_kernel"),
                          "frac": round(gbs / pk["hbm"], 4), "peak_source": pk["src"]}}
@@ -572,7 +580,7 @@ def main():
                 "data": "synthetic (seeded N(0,1) Q/K/V with outlier channels, DESIGN.md §4)",
                 "config": workload_config(args), "roofline": res["roofline"], "cpu_baseline": cpu,
                 "e2e": res["e2e"], "gpu_launches": res["launches"], "clocks": res["clocks"],
-                "breakdown_ms": res["breakdown_ms"], "decode": res.get("decode")}
+                "breakdown_ms": res["breakdown_ms"], "quantize_kv": res["quantize_kv"], "decode": res.get("decode")}
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.barrier()

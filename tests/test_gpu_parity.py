@@ -151,6 +151,10 @@ DEC_CASES = [  # (B, N_prefill, n_append, Hq, Hkv, d, n_splits, alpha_mode)
     (3, 64 * 20 + 5, 3, 8, 2, 128, 0, 1),
     (1, 128, 64, 1, 1, 64, 0, 0),       # d = 64, one piece
     (1, 64 * 9, 0, 4, 1, 128, 0, 0),    # G = 4, empty buffer
+    # G = 8: the general (unpacked) IMMA path, separate hi / lo B fragments
+    (2, 64 * 6 + 17, 3, 16, 2, 128, 2, 0),
+    (1, 64 * 9 + 5, 0, 8, 1, 128, 0, 1),
+    (1, 300, 2, 8, 1, 64, 1, 0),
 ]
 
 
@@ -239,8 +243,9 @@ def test_append_and_decode_parity(ta, case):
 
 @pytest.mark.parametrize("j_block", [0, 3, -1])
 @pytest.mark.parametrize("n_splits", [1, 0])
-def test_decode_exact_set_tap(ta, j_block, n_splits):
-    B, N, Hq, Hkv, d = 2, 64 * 5 + 37, 8, 2, 128
+@pytest.mark.parametrize("Hq", [8, 16])  # G = 4 (packed IMMA path) and G = 8 (general path)
+def test_decode_exact_set_tap(ta, j_block, n_splits, Hq):
+    B, N, Hkv, d = 2, 64 * 5 + 37, 2, 128
     q, k, v = synth.qkv(77, B, N, Hq, Hkv, d)
     bits = synth.head_bits_alternating(Hkv)
     b, h = 1, 5
@@ -249,12 +254,18 @@ def test_decode_exact_set_tap(ta, j_block, n_splits):
     cache = ta.KVCache(B, Hkv, d, max_blocks=8, bits=bits)
     ta.turbo_quantize_kv(p, cache, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
     qd, _, _ = synth.decode_token(31, B, Hq, Hkv, d)
-    ta.turbo_attention_decode(p, cache, torch.from_numpy(qd).cuda(), n_splits=n_splits)  # 6 units: one piece
+    ta.turbo_attention_decode(p, cache, torch.from_numpy(qd).cuda(), n_splits=n_splits)
     torch.cuda.synchronize()
     op = O.params(d=d)
     ref = O.build_cache(op, k.astype(np.float32), v.astype(np.float32), bits, 8)
-    ks, vs = ref["slots"][b][h // (Hq // Hkv)]
-    _, _, rt = O.decode_head(op, qd[b, h].astype(np.float32), ks, vs, tap=j_block)
+    kvh = h // (Hq // Hkv)
+    ks, vs = ref["slots"][b][kvh]
+    a_, e_, wb = 0, ks.n_blocks, True
+    if n_splits == 0:  # the tapped block's piece of the balanced partition (its m, l start there)
+        unit = ks.n_blocks if j_block < 0 else j_block
+        pieces = balanced_bounds(ta, ref["slots"], Hq, Hkv, d)[b][kvh]
+        a_, e_, wb = next(x for x in pieces if x[0] <= unit < (x[1] + (1 if x[2] else 0)))
+    _, _, rt = O.decode_head(op, qd[b, h].astype(np.float32), ks, vs, a_, e_, wb, tap=j_block)
     assert rt["hit"]
     np.testing.assert_array_equal(tap.q1.cpu().numpy()[0], rt["q1"])
     assert tap.s_q.item() == rt["s_q"][0]

@@ -1,0 +1,2 @@
+python __graft_entry__.py build > gpurun_out/build.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -15
