@@ -336,18 +336,22 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
         // x = S s_Q s_K / sqrt(d) (R-18); masked keys -> -inf.
         const float cqk = __fmul_rn(__fmul_rn(s_q, args.k1s[bkv * Tc + j]), args.scale);
         float mt = -INFINITY;
+        // passes 1 and 3 take the whole 64-column row in one TMEM round trip (two x32
+        // loads, one wait): they hold few other values, unlike pass 2
+        constexpr int CW1 = SP == 1 ? 64 : CW;
 #pragma unroll 1
-        for (int ch = 0; ch < SW / CW; ++ch) {
-          uint32_t v[CW];
-          TA_TMEM_LD(CW, tS + ch * CW, v);
+        for (int ch = 0; ch < SW / CW1; ++ch) {
+          uint32_t v[CW1];
+#pragma unroll
+          for (int h2 = 0; h2 < CW1 / CW; ++h2) TA_TMEM_LD(CW, tS + ch * CW1 + h2 * CW, (v + h2 * CW));
           tmem_ld_wait();
           if (tap_j)
-            for (int c = 0; c < CW; ++c)
-              args.tap.s_int[(r & 63) * kBc + hc * SW + ch * CW + c] = ch * CW + c < nv ? (int)v[c] : 0;
+            for (int c = 0; c < CW1; ++c)
+              args.tap.s_int[(r & 63) * kBc + hc * SW + ch * CW1 + c] = ch * CW1 + c < nv ? (int)v[c] : 0;
           const f32x2 cq2 = pk2(cqk, cqk);
           if (full) {
 #pragma unroll
-            for (int c = 0; c < CW; c += 2) {
+            for (int c = 0; c < CW1; c += 2) {
               const f32x2 x2 = mul2(pk2((float)(int)v[c], (float)(int)v[c + 1]), cq2);
               const float x0 = lo2(x2), x1 = hi2(x2);
               mt = fmaxf(mt, fmaxf(x0, x1));
@@ -356,16 +360,17 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
             }
           } else {
 #pragma unroll
-            for (int c = 0; c < CW; c += 2) {
+            for (int c = 0; c < CW1; c += 2) {
               const f32x2 x2 = mul2(pk2((float)(int)v[c], (float)(int)v[c + 1]), cq2);
-              const float x0 = ch * CW + c < nv ? lo2(x2) : -INFINITY;
-              const float x1 = ch * CW + c + 1 < nv ? hi2(x2) : -INFINITY;
+              const float x0 = ch * CW1 + c < nv ? lo2(x2) : -INFINITY;
+              const float x1 = ch * CW1 + c + 1 < nv ? hi2(x2) : -INFINITY;
               mt = fmaxf(mt, fmaxf(x0, x1));
               v[c] = __float_as_uint(x0);
               v[c + 1] = __float_as_uint(x1);
             }
           }
-          TA_TMEM_ST(CW, tS + ch * CW, v);
+#pragma unroll
+          for (int h2 = 0; h2 < CW1 / CW; ++h2) TA_TMEM_ST(CW, tS + ch * CW1 + h2 * CW, (v + h2 * CW));
         }
         if (SP == 2) {  // row max over both halves
           sm.xmax[slot][sb][hc][r] = mt;
@@ -480,13 +485,15 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
         uint8_t* prow = reinterpret_cast<uint8_t*>(sm.p[slot][sb]);
         constexpr float kMagicF16 = 12582912.0f + 25600.0f;  // 1.5*2^23 + 0x6400
         const __half2 c1024 = __half2(__float2half_rn(1024.f), __float2half_rn(1024.f));
+        constexpr int CW3 = SP == 1 ? 64 : CW;
 #pragma unroll 1
-        for (int ch = 0; ch < SW / CW; ++ch) {
-          uint32_t v[CW];
-          TA_TMEM_LD(CW, tS + ch * CW, v);
+        for (int ch = 0; ch < SW / CW3; ++ch) {
+          uint32_t v[CW3];
+#pragma unroll
+          for (int h2 = 0; h2 < CW3 / CW; ++h2) TA_TMEM_LD(CW, tS + ch * CW3 + h2 * CW, (v + h2 * CW));
           tmem_ld_wait();
 #pragma unroll
-          for (int hh = 0; hh < CW / 8; ++hh) {
+          for (int hh = 0; hh < CW3 / 8; ++hh) {
             // y = 1.5*2^23 + 0x6400 + code: its low half-word is the fp16 of 1024 + code
             uint32_t y[8];
             const f32x2 inv2 = pk2(inv_p, inv_p), mf2 = pk2(kMagicF16, kMagicF16);
@@ -503,7 +510,7 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
               const __half2 hv = __hsub2(*reinterpret_cast<const __half2*>(&hb), c1024);  // exact
               w[e] = *reinterpret_cast<const uint32_t*>(&hv);
             }
-            const int chunk = (hc * SW + ch * CW) / 8 + hh;
+            const int chunk = (hc * SW + ch * CW3) / 8 + hh;
             *reinterpret_cast<uint4*>(prow + p_swz(r, chunk)) = make_uint4(w[0], w[1], w[2], w[3]);
             if (tap_j)
               *reinterpret_cast<uint2*>(args.tap.p_codes + (r & 63) * kBc + chunk * 8) =
