@@ -553,7 +553,30 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
       l = sm.lsum[slot][0][r] + sm.lsum[slot][1][r];
     }
     // Epilogue: O_i = diag(l)^-1 O, L_i = m + log l
-    if (row_ok) {
+    if (SP == 1) {
+      // O rows go through shared memory (this warp's 32 rows in the now idle P buffers,
+      // XOR-swizzled 16-byte chunks) so that the global stores are row-contiguous: one
+      // instruction writes two whole 2d-byte rows instead of 32 scattered 16-byte pieces.
+      constexpr int CH = HD / 8;  // 16-byte chunks per row
+      uint8_t* stg = reinterpret_cast<uint8_t*>(sm.p[slot][qd >> 1]) + (qd & 1) * (32 * HD * 2);
+      const float f = row_ok ? A / l : 0.f;
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        __half2 hv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) hv[e] = __floats2half2_rn(O[c * 8 + 2 * e] * f, O[c * 8 + 2 * e + 1] * f);
+        *reinterpret_cast<uint4*>(stg + lane * (HD * 2) + ((c ^ (lane % CH)) << 4)) = *reinterpret_cast<uint4*>(hv);
+      }
+      __syncwarp();
+      constexpr int RPI = 32 / CH;  // rows per store instruction
+#pragma unroll
+      for (int i = 0; i < 32 / RPI; ++i) {
+        const int rr = RPI * i + lane / CH, c = lane % CH, grow = it * kTileM + qd * 32 + rr;
+        const uint4 val = *reinterpret_cast<const uint4*>(stg + rr * (HD * 2) + ((c ^ (rr % CH)) << 4));
+        if (grow < N) reinterpret_cast<uint4*>(args.o + (((size_t)b * N + grow) * args.Hq + h) * HD)[c] = val;
+      }
+      if (row_ok) args.lse[((size_t)b * args.Hq + h) * N + row] = m + logf(l);
+    } else if (row_ok) {
       const float f = A / l;
       __half* orow = args.o + (((size_t)b * N + row) * args.Hq + h) * HD + hc * OW;
 #pragma unroll

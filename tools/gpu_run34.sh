@@ -1,0 +1,2 @@
+for v in pE pR; do TURBO_LIB=variants/$v.so timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "prefill" 2>&1 | tail -1; done
+bash tools/ab.sh tools/time_prefill.py variants/head.so variants/pE.so variants/pR.so
