@@ -198,6 +198,7 @@ TURBO_API turbo_status_t turbo_attention_decode(const turbo_params_t* params, co
 
 /* Log-sum-exp combine of n_parts partial results, in ascending part order
  * (R-23): L = max_s L_s + ln sum_s e^{L_s - max}, O = sum_s e^{L_s - L} O_s.
+ *   d = head_dim (64 or 128, else TURBO_ERR_UNSUPPORTED);
  *   o_parts f32 [n_parts][rows][d], lse_parts f32 [n_parts][rows];
  *   o FP16 [rows][d] (or NULL), o_f32 f32 [rows][d] (or NULL), lse f32 [rows]. */
 TURBO_API turbo_status_t turbo_combine_lse(int32_t n_parts, int32_t rows, int32_t d, const float* o_parts,

@@ -161,6 +161,7 @@ turbo_status_t turbo_combine_lse(int32_t n_parts, int32_t rows, int32_t d, const
                                  const float* lse_parts, void* o, float* o_f32, float* lse, turbo_stream_t stream) {
   if (n_parts < 1 || rows < 1 || d < 1 || !o_parts || !lse_parts || !lse || (!o && !o_f32))
     return TURBO_ERR_INVALID_ARG;
+  if (d != 64 && d != 128) return TURBO_ERR_UNSUPPORTED;
   return cuda_status(ta_host::launch_combine(n_parts, rows, d, o_parts, lse_parts, reinterpret_cast<__half*>(o), o_f32,
                                              lse, reinterpret_cast<cudaStream_t>(stream)));
 }

@@ -750,26 +750,59 @@ __global__ void combine_balanced_kernel(const __grid_constant__ DecodeArgs a, in
 
 // Log-sum-exp combine over parts in ascending order (R-23).  One thread per
 // (row, channel).
-__global__ void combine_kernel(int n_parts, int rows, int d, const float* __restrict__ o_parts,
-                               const float* __restrict__ lse_parts, __half* __restrict__ o16,
-                               float* __restrict__ o32, float* __restrict__ lse) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= rows * d) return;
-  const int r = idx / d, c = idx % d;
-  float lmax = -INFINITY;
-  for (int s = 0; s < n_parts; ++s) lmax = fmaxf(lmax, lse_parts[(size_t)s * rows + r]);
-  float out = 0.f, L = -INFINITY;
-  if (lmax != -INFINITY) {
-    float wsum = 0.f;
-    for (int s = 0; s < n_parts; ++s) wsum += expf(lse_parts[(size_t)s * rows + r] - lmax);
-    const float inv = 1.f / wsum;
-    for (int s = 0; s < n_parts; ++s)
-      out += expf(lse_parts[(size_t)s * rows + r] - lmax) * inv * o_parts[((size_t)s * rows + r) * d + c];
-    L = lmax + logf(wsum);
+// One CTA per row, one thread per channel (coalesced part loads); warp 0
+// computes the part weights once per row into shared memory -- lanes own parts
+// for the max, the sum runs in ascending part order by shuffle -- with the
+// arithmetic of the plain version: wsum += e_s, out += (e_s * inv) * o_s.
+__global__ void __launch_bounds__(128) combine_kernel(int n_parts, int rows, int d, const float* __restrict__ o_parts,
+                                                      const float* __restrict__ lse_parts, __half* __restrict__ o16,
+                                                      float* __restrict__ o32, float* __restrict__ lse) {
+  extern __shared__ float w[];  // [n_parts] weights, then [1] lmax flag
+  const int r = blockIdx.x, c = threadIdx.x, lane = c & 31;
+  if (c < 32) {
+    float lmax = -INFINITY;
+    for (int s = lane; s < n_parts; s += 32) lmax = fmaxf(lmax, lse_parts[(size_t)s * rows + r]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+    float L = -INFINITY;
+    if (lmax != -INFINITY) {
+      float wsum = 0.f;
+      for (int s0 = 0; s0 < n_parts; s0 += 32) {
+        const float e = s0 + lane < n_parts ? expf(lse_parts[(size_t)(s0 + lane) * rows + r] - lmax) : 0.f;
+        const int n = min(32, n_parts - s0);
+        for (int k = 0; k < n; ++k) wsum += __shfl_sync(0xffffffffu, e, k);
+      }
+      const float inv = 1.f / wsum;
+      for (int s = lane; s < n_parts; s += 32) w[s] = expf(lse_parts[(size_t)s * rows + r] - lmax) * inv;
+      L = lmax + logf(wsum);
+    }
+    if (lane == 0) {
+      w[n_parts] = lmax;
+      lse[r] = L;
+    }
+  }
+  __syncthreads();
+  float out = 0.f;
+  if (w[n_parts] != -INFINITY) {
+    const float* op = o_parts + (size_t)r * d + c;
+    const size_t stride = (size_t)rows * d;
+    int s = 0;
+    for (; s + 4 <= n_parts; s += 4) {
+      const float v0 = op[s * stride], v1 = op[(s + 1) * stride], v2 = op[(s + 2) * stride], v3 = op[(s + 3) * stride];
+      out += w[s] * v0;
+      out += w[s + 1] * v1;
+      out += w[s + 2] * v2;
+      out += w[s + 3] * v3;
+    }
+    for (; s < n_parts; ++s) out += w[s] * op[s * stride];
   }
   if (o16) o16[(size_t)r * d + c] = __float2half_rn(out);
   if (o32) o32[(size_t)r * d + c] = out;
-  if (c == 0) lse[r] = L;
+}
+
+static void launch_combine_kernel(int n_parts, int rows, int d, const float* o_parts, const float* lse_parts,
+                                  __half* o16, float* o32, float* lse, cudaStream_t st) {
+  combine_kernel<<<rows, d, (n_parts + 1) * sizeof(float), st>>>(n_parts, rows, d, o_parts, lse_parts, o16, o32, lse);
 }
 
 }  // namespace ta
@@ -880,14 +913,14 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
     combine_balanced_kernel<<<B * Hq, 128, 0, st>>>(a, W, HD);
   } else {
     const int rows = B * Hq;
-    combine_kernel<<<(rows * HD + 255) / 256, 256, 0, st>>>(S, rows, HD, a.o_parts, a.lse_parts, o, o_part, lse);
+    launch_combine_kernel(S, rows, HD, a.o_parts, a.lse_parts, o, o_part, lse, st);
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_combine(int n_parts, int rows, int d, const float* o_parts, const float* lse_parts, __half* o,
                            float* o32, float* lse, cudaStream_t st) {
-  combine_kernel<<<(rows * d + 255) / 256, 256, 0, st>>>(n_parts, rows, d, o_parts, lse_parts, o, o32, lse);
+  launch_combine_kernel(n_parts, rows, d, o_parts, lse_parts, o, o32, lse, st);
   return cudaGetLastError();
 }
 }  // namespace ta_host
