@@ -360,29 +360,46 @@ def bench_decode(args, rank, world, device, pk):
 
 # --------------------------------------------------------------------------- reference (oracle)
 def cpu_sample_oracle(seconds_hint=True):
-    """The CPU oracle (oracle/, plain scalar C) on a bounded sample of the same
-    workload: K/V quantisation + cache build and Alg. 1 for ONE (batch, query
-    head) of configs[1] (N = 4096, d = 128, causal), single thread."""
+    """The CPU oracle (oracle/, plain scalar C, as it stands) on a bounded sample of
+    the same workload: K/V quantisation + cache build and Alg. 1 for one (batch,
+    query head) unit of configs[1] (N = 4096, d = 128, causal) per host core, the
+    units run concurrently on threads (ctypes releases the GIL), plus the
+    single-thread time of one unit."""
     import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
 
     from oracle import oracle as O
     from paper_2412_08585_b200 import synth
 
     N, d = CFG_PREFILL["N"], CFG_PREFILL["d"]
-    q, k, v = synth.qkv(1002, 1, N, 1, 1, d)
-    q, k, v = (x[0, :, 0].astype(np.float32) for x in (q, k, v))
     p = O.params(d=d)
+    ncores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    units = []
+    for u in range(ncores):  # inputs drawn outside the timed region
+        q, k, v = synth.qkv(1002 + u, 1, N, 1, 1, d)
+        units.append(tuple(x[0, :, 0].astype(np.float32) for x in (q, k, v)))
+
+    def one(u):
+        q, k, v = units[u]
+        ks, vs = O.Slot(p, 4, N // 64 + 1), O.Slot(p, 2, N // 64 + 1)
+        ks.prefill(k)
+        vs.prefill(v)
+        O.prefill_head(p, q, k, v, causal=True)
+
+    O.lib()  # build / load once, outside the timing
     t0 = time.perf_counter()
-    ks, vs = O.Slot(p, 4, N // 64 + 1), O.Slot(p, 2, N // 64 + 1)
-    ks.prefill(k)
-    vs.prefill(v)
-    O.prefill_head(p, q, k, v, causal=True)
+    one(0)
+    dt1 = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=ncores) as ex:
+        list(ex.map(one, range(ncores)))
     dt = time.perf_counter() - t0
     ops = prefill_ops(1, N, 1, d)
-    return {"value": ops / dt / 1e12, "unit": "TOPS", "cores": 1, "kind": "oracle",
-            "sample": f"1 of {CFG_PREFILL['B'] * CFG_PREFILL['Hq']} (batch, head) units of configs[1]: quantize + "
-                      f"cache build + Alg. 1, N={N}, d={d}, causal; {dt:.2f} s single-threaded",
-            "seconds": round(dt, 3)}
+    return {"value": ncores * ops / dt / 1e12, "unit": "TOPS", "cores": ncores, "kind": "oracle",
+            "sample": f"{ncores} of {CFG_PREFILL['B'] * CFG_PREFILL['Hq']} (batch, head) units of configs[1] "
+                      f"(quantize + cache build + Alg. 1, N={N}, d={d}, causal), one per host core on "
+                      f"{ncores} threads: {dt:.2f} s; one unit single-threaded {dt1:.2f} s",
+            "value_1core": ops / dt1 / 1e12, "seconds": round(dt, 3)}
 
 
 def run_reference(args, rank, world):
