@@ -15,7 +15,6 @@
 // with q1_c s_c = 256 hi + lo, lo = the signed low byte, hi in [-38, 37] (both s8), so the
 // tensor cores see only raw 4-bit / 2-bit codes.
 #include <climits>
-#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -56,7 +55,6 @@ struct DecodeArgs {
   __half* fin_o16;  // balanced schedule: final fp16 output (or NULL)
   float* fin_o32;   // balanced schedule: final f32 output (or NULL)
   float* fin_lse;   // balanced schedule: final L
-  int stagger_ns;   // balanced schedule: start delay step per warp slot (experiments; 0 = none)
   int B, Hq, Hkv, G, max_blocks, blk_begin, blk_end, with_buffer, n_splits, alpha_mode;
   float scale;
   SasConst sas;
@@ -660,7 +658,6 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
   }
   // balanced schedule
   const int W = gridDim.x * kWarpsPerCta, w = blockIdx.x * kWarpsPerCta + warp;
-  if (a.stagger_ns > 0) __nanosleep((unsigned)(((w * 7) % 12) * a.stagger_ns));
   int tot = 0;
   for (int b0 = 0; b0 < a.B; b0 += 32)
     if (b0 + lane < a.B) tot += seq_units(a, b0 + lane).units;
@@ -830,8 +827,6 @@ int decode_workers(int Hq, int Hkv, int HD) {
   const bool pack = Hkv > 0 && Hq / Hkv <= 4;
   const int per_sm = HD == 128 ? (pack ? decode_ctas_per_sm<128, true, false>() : decode_ctas_per_sm<128, false, false>())
                                : (pack ? decode_ctas_per_sm<64, true, false>() : decode_ctas_per_sm<64, false, false>());
-  const char* ov = getenv("TURBO_DECODE_WORKERS");  // experiments only: override W
-  if (ov && atoi(ov) > 0) return atoi(ov);
   return sms * per_sm * kWarpsPerCta;
 }
 
@@ -871,7 +866,6 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
   const bool has_tap = p->debug_tap != nullptr;
   if (has_tap) a.tap = *reinterpret_cast<const turbo_debug_tap_t*>(p->debug_tap);
   const int W = S == 0 ? decode_workers(Hq, H, HD) : 0;
-  if (const char* sg = getenv("TURBO_DECODE_STAGGER")) a.stagger_ns = atoi(sg);
   if (S == 0 && W <= 0) return cudaErrorInvalidConfiguration;
   if (S == 1) {
     a.o_parts = o_part;
