@@ -95,7 +95,7 @@ TA_DEV uint32_t pack_crumb8(uint2 v) {
 }
 
 template <int HD>
-__global__ void __launch_bounds__(2 * HD, 256 / HD) quant_prefill_kernel(
+__global__ void __launch_bounds__(2 * HD, 3 * 128 / HD) quant_prefill_kernel(
     const __half* __restrict__ k, const __half* __restrict__ v, int N, int Hkv, int max_blocks,
     const int32_t* __restrict__ bits_dev, uint8_t* __restrict__ block_rec, float* __restrict__ s_parent,
     float* __restrict__ a_univ, int8_t* __restrict__ k1, __half* __restrict__ v1t, float* __restrict__ k1s,
