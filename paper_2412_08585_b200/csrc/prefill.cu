@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&sm.kv_full[s], 1);
-      mbar_init(&sm.kv_empty[s], 1);
+      mbar_init(&sm.kv_empty[s], NS);  // one commit per MMA issuer
     }
     for (int t = 0; t < NS; ++t) {
       for (int s = 0; s < 2; ++s) {
@@ -167,8 +167,11 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
           tma_load_3d(sm.v[st], &tm_v, &sm.kv_full[st], 0, 0, (int)(bkv * Tc + j));
         }
       }
-    } else if (warp == 1) {
-      // ---------------------------------------------------------- MMA issuer
+    } else if (warp == 1 || (NS == 2 && warp == 2)) {
+      // ---------------------------------------------------------- MMA issuers
+      // One issuing warp per query tile (warp 1: slot 0, warp 2: slot 1), so a slot
+      // whose softmax runs ahead is not held behind the other slot's P tile.
+      const int t = warp - 1;
       constexpr uint32_t kLayQK = HD == 128 ? kSw128 : kSw64;
       constexpr uint32_t idesc_qk = idesc_i8(kTileM, kBc, true, true);
       // P V runs as kind::f16: codes are small integers (exact in fp16) and every
@@ -184,8 +187,7 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
           PROF_T(m1);
           PROF_ADD(10, m0, m1);
           const uint32_t ka = smem_u32(sm.k[st]);
-#pragma unroll
-          for (int t = 0; t < NS; ++t) {
+          {
             PROF_T(m2);
             if (j >= 2) mbar_wait(&sm.s_free[t][sb], ((j >> 1) - 1) & 1);
             PROF_T(m3);
@@ -205,8 +207,7 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
         if (j >= 1) {
           const int jj = j - 1, pb = jj & 1, st = jj % kStages;
           const uint32_t va = smem_u32(sm.v[st]);
-#pragma unroll
-          for (int t = 0; t < NS; ++t) {
+          {
             PROF_T(m4);
             mbar_wait(&sm.p_full[t][pb], (jj >> 1) & 1);
             PROF_T(m5);
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
                 mma_f16_ss(tmem + t * 256 + 2 * kBc, smem_desc(pa + ks * 32, 1024, kSw128),
                            smem_desc(va + ks * 32, 1024, kSw128), idesc_pv, ks > 0);
               mma_commit(&sm.pv_full[t]);
-              if (t == NS - 1) mma_commit(&sm.kv_empty[st]);
+              mma_commit(&sm.kv_empty[st]);
             }
             __syncwarp();
           }
