@@ -276,13 +276,13 @@ def test_decode_exact_set_tap(ta, j_block, n_splits, Hq):
     np.testing.assert_array_equal(tap.pv_int.cpu().numpy()[0], rt["pv_int"])
 
 
-def test_combine_lse_parity(ta):
-    rng = np.random.default_rng(0)
-    S, rows, d = 5, 37, 128
+@pytest.mark.parametrize("S,rows,d", [(5, 37, 128), (40, 9, 64), (1, 3, 128)])
+def test_combine_lse_parity(ta, S, rows, d):
+    rng = np.random.default_rng(S)
     o_parts = rng.standard_normal((S, rows, d)).astype(np.float32)
     lse_parts = (rng.standard_normal((S, rows)) * 3).astype(np.float32)
-    lse_parts[2, :5] = -np.inf
-    lse_parts[:, 7] = -np.inf
+    lse_parts[min(2, S - 1), :2] = -np.inf
+    lse_parts[:, rows - 2] = -np.inf  # a row with no part at all: O = 0, L = -inf
     o16, _, lse = ta.turbo_combine_lse(torch.from_numpy(o_parts).cuda(), torch.from_numpy(lse_parts).cuda())
     torch.cuda.synchronize()
     for r in range(rows):
@@ -292,6 +292,12 @@ def test_combine_lse_parity(ta):
             assert abs(lse[r].item() - rl) < 1e-5
         else:
             assert lse[r].item() == -np.inf
+
+
+def test_combine_lse_rejects_other_head_dims(ta):
+    o_parts = torch.zeros(2, 3, 96, device="cuda")
+    with pytest.raises(ta.TurboError):
+        ta.turbo_combine_lse(o_parts, torch.zeros(2, 3, device="cuda"))
 
 
 def test_validation_errors(ta):
