@@ -163,17 +163,21 @@ def run_ours(args, rank, world, device):
     st = torch.cuda.current_stream()
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
-    def step(qq, kk, vv, qdd, kdd, vdd, evs=None):
+    def step(qq, kk, vv, qdd, kdd, vdd, evs=None, bufs=None):
+        # bufs: preallocated outputs (the e2e loop double-buffers them; the allocator
+        # would otherwise cudaMalloc -- and synchronise -- while copies are in flight)
         if evs:
             evs[0].record(st)
-        k1, v1t, k1s, v1s = ta.turbo_quantize_kv(p, cache, kk, vv)
+        k1, v1t, k1s, v1s = ta.turbo_quantize_kv(p, cache, kk, vv, out=bufs["kv"] if bufs else None)
         if evs:
             evs[1].record(st)
-        o, lse = ta.turbo_attention_prefill(p, qq, k1, v1t, k1s, v1s, causal=True)
+        o, lse = ta.turbo_attention_prefill(p, qq, k1, v1t, k1s, v1s, causal=True,
+                                            o=bufs["o"] if bufs else None, lse=bufs["lse"] if bufs else None)
         if evs:
             evs[2].record(st)
         ta.turbo_quantize_kv(p, cache, kdd, vdd, mode=1)
-        od, _, lsed = ta.turbo_attention_decode(p, cache, qdd, n_splits=S, workspace=ws)
+        od, _, lsed = ta.turbo_attention_decode(p, cache, qdd, n_splits=S, workspace=ws,
+                                                o=bufs["od"] if bufs else None, lse=bufs["lsed"] if bufs else None)
         if evs:
             evs[3].record(st)
         return o, lse, od, lsed
@@ -219,6 +223,14 @@ def run_ours(args, rank, world, device):
     hlse = torch.empty((B, Hq, N), dtype=torch.float32).pin_memory()
     hod = torch.empty(qd.shape, dtype=torch.float16).pin_memory()
     dins = [[torch.empty_like(x) for x in (q, k, v, qd, kd, vd)] for _ in range(2)]
+    tcb = N // 64
+    douts = [{"kv": (torch.empty((B, Hkv, N, d), dtype=torch.int8, device=device),
+                     torch.empty((B, Hkv, tcb, d, 64), dtype=torch.float16, device=device),
+                     torch.empty((B, Hkv, tcb), dtype=torch.float32, device=device),
+                     torch.empty((B, Hkv, tcb), dtype=torch.float32, device=device)),
+              "o": torch.empty_like(q), "lse": torch.empty((B, Hq, N), dtype=torch.float32, device=device),
+              "od": torch.empty_like(qd), "lsed": torch.empty((B, Hq), dtype=torch.float32, device=device)}
+             for _ in range(2)]
     s_in, s_out = torch.cuda.Stream(device), torch.cuda.Stream(device)
     e2e_steps = max(4, min(args.steps, 32))  # amortises the pipeline fill and drain
     e0, e1 = ev(), ev()
@@ -242,7 +254,7 @@ def run_ours(args, rank, world, device):
         st.wait_event(in_ready[i])
         if i >= 2:
             st.wait_event(out_done[i - 2])  # the outputs of step i-2 have left the device
-        outs[i] = step(*buf)
+        outs[i] = step(*buf, bufs=douts[i % 2])
         in_free[i] = torch.cuda.Event()
         in_free[i].record(st)
         with torch.cuda.stream(s_out):
@@ -253,8 +265,6 @@ def run_ours(args, rank, world, device):
             hod.copy_(od, non_blocking=True)
             out_done[i] = torch.cuda.Event()
             out_done[i].record(s_out)
-        for t_ in outs[i]:
-            t_.record_stream(s_out)
     st.wait_stream(s_out)
     e1.record(st)
     torch.cuda.synchronize()
@@ -330,7 +340,7 @@ def run_ours(args, rank, world, device):
                   breakdown_ms={"quantize_kv_prefill": round(statistics.mean(t_quant), 4),
                                 "attention_prefill": round(pre_ms, 4),
                                 "append+decode": round(statistics.mean(t_dec), 4)})
-    del hq, hk, hv, ho, hlse, dins, outs, q, k, v, flush, cache
+    del hq, hk, hv, ho, hlse, dins, douts, outs, q, k, v, flush, cache
     torch.cuda.empty_cache()
     if not args.no_decode:
         result["decode"] = bench_decode(args, rank, world, device, pk)

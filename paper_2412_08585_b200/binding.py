@@ -150,18 +150,23 @@ class KVCache:
                                                           self.counters))
 
 
-def turbo_quantize_kv(p, cache: KVCache, k, v, mode=0, stream=None):
-    """mode 0 (PREFILL): k, v fp16 [B,N,Hkv,d] -> returns (k1, v1t, k1_scale, v1_scale);
-    mode 1 (APPEND): k, v fp16 [B,Hkv,d] -> returns None."""
+def turbo_quantize_kv(p, cache: KVCache, k, v, mode=0, stream=None, out=None):
+    """mode 0 (PREFILL): k, v fp16 [B,N,Hkv,d] -> returns (k1, v1t, k1_scale, v1_scale)
+    (written into `out` when given); mode 1 (APPEND): k, v fp16 [B,Hkv,d] -> returns None."""
     assert k.dtype == torch.float16 and v.dtype == torch.float16 and k.is_contiguous() and v.is_contiguous()
     if mode == 0:
         B, N, H, d = k.shape
         tc = -(-N // p.block_kv)
         dev = k.device
-        k1 = torch.empty((B, H, N, d), dtype=torch.int8, device=dev)
-        v1t = torch.empty((B, H, tc, d, p.block_kv), dtype=torch.float16, device=dev)
-        k1s = torch.empty((B, H, tc), dtype=torch.float32, device=dev)
-        v1s = torch.empty((B, H, tc), dtype=torch.float32, device=dev)
+        if out is not None:
+            k1, v1t, k1s, v1s = out
+            assert k1.shape == (B, H, N, d) and v1t.shape == (B, H, tc, d, p.block_kv)
+            assert k1s.shape == (B, H, tc) and v1s.shape == (B, H, tc)
+        else:
+            k1 = torch.empty((B, H, N, d), dtype=torch.int8, device=dev)
+            v1t = torch.empty((B, H, tc, d, p.block_kv), dtype=torch.float16, device=dev)
+            k1s = torch.empty((B, H, tc), dtype=torch.float32, device=dev)
+            v1s = torch.empty((B, H, tc), dtype=torch.float32, device=dev)
         _check("turbo_quantize_kv", lib().turbo_quantize_kv(C.byref(p), C.byref(cache.c), _ptr(k), _ptr(v), N, 0,
                                                             _ptr(k1), _ptr(v1t), _ptr(k1s), _ptr(v1s),
                                                             _stream(stream)))
@@ -211,17 +216,26 @@ def balanced_ranges(unit_counts, Hkv, workers, min_units=8):
 
 
 def auto_splits(batch, n_kv_heads, n_blocks, workers=None):
-    """Equal-split count for turbo_attention_decode: splits of ~64 blocks, doubled
-    until the (b, kv head, split) warp tasks cover two waves of the resident
-    decode warps (`workers`, default turbo_decode_workers for G <= 4, d = 128),
-    keeping >= 8 blocks per split.  On B200 this lands within 2 % of the best
-    of a sweep on configs[2] (S = 8) and configs[4] (S = 32; tools/sweep_decode.py)."""
+    """Equal-split count for turbo_attention_decode.  Among the counts that keep >= 8
+    blocks per split and whose last split is not short (>= 3/4 of the others, so no
+    (b, kv head) ends with a straggler), pick the one whose task count
+    batch * n_kv_heads * S is closest to 4.5 waves of the resident decode warps
+    (`workers`, default turbo_decode_workers for G <= 4, d = 128).  On B200 this is
+    the best of a sweep on configs[2] (S = 12) and within 0.1 % on configs[4] (S = 64;
+    tools/sweep_decode.py)."""
     if workers is None:
         workers = max(1, turbo_decode_workers(4, 1, 128))
-    s = max(1, -(-n_blocks // 64))
-    while batch * n_kv_heads * s < 2 * workers and 2 * s <= max(1, n_blocks // 8):
-        s *= 2
-    return s
+    bh = max(1, batch * n_kv_heads)
+    best, best_err = 1, None
+    for s in range(1, max(1, n_blocks // 8) + 1):
+        per = -(-n_blocks // s)
+        last = n_blocks - per * (s - 1)
+        if s > 1 and (last <= 0 or 4 * last < 3 * per):
+            continue
+        err = abs(bh * s / workers - 4.5)
+        if best_err is None or err < best_err - 1e-9:
+            best, best_err = s, err
+    return best
 
 
 def turbo_attention_decode(p, cache: KVCache, q, blk_begin=0, blk_end=-1, with_buffer=True, n_splits=1,

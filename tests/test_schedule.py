@@ -48,3 +48,21 @@ def test_balanced_partition_random():
         B, Hkv, W = r.randint(1, 9), r.randint(1, 6), r.randint(1, 300)
         units = [r.choice([0, 1, r.randint(1, 40), r.randint(1, 400)]) for _ in range(B)]
         _check(units, Hkv, W, r.choice([1, 8]))
+
+
+def test_auto_splits_rule():
+    """Equal-split heuristic: >= 8 blocks per split (or no split), no short last split,
+    task count nearest 4.5 waves of the resident warps among the admissible counts."""
+    from paper_2412_08585_b200.binding import auto_splits
+
+    assert auto_splits(64, 10, 512, 1776) == 12   # configs[2]
+    assert auto_splits(16, 8, 2048, 1776) == 64   # configs[4]
+    assert auto_splits(8, 8, 64, 1776) == 8       # bench step decode (capped at 8 blocks per split)
+    assert auto_splits(1, 1, 7, 1776) == 1
+    r = random.Random(3)
+    for _ in range(200):
+        B, H, nb, W = r.randint(1, 64), r.randint(1, 16), r.randint(0, 4096), r.randint(100, 4000)
+        s = auto_splits(B, H, nb, W)
+        assert s == 1 or nb // s >= 8
+        per = -(-nb // s)
+        assert s == 1 or 4 * (nb - per * (s - 1)) >= 3 * per
