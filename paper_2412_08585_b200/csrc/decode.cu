@@ -1,9 +1,9 @@
 // decode.cu -- Algorithm 2 (TurboAttention decode) on sm_100a,
 // plus the split-KV log-sum-exp combine (R-23).
 //
-// One WARP = one (batch, kv head, split) task; it owns the G = Hq/Hkv query
-// rows of that KV head (GQA, R-22) and walks its contiguous block range in
-// Alg. 2 order.  Block records (s_int | z_int | packed codes) stream through a
+// One WARP (= one CTA) = one (batch, kv head, split) task, or one chunk of the
+// balanced schedule; it owns the G = Hq/Hkv query rows of that KV head (GQA,
+// R-22) and walks its contiguous block range in Alg. 2 order.  Block records (s_int | z_int | packed codes) stream through a
 // per-warp 2-stage smem ring with cp.async.bulk (TMA 1-D) + mbarrier; codes are
 // unpacked in registers straight into mma.sync m16n8k32 IMMA fragments.
 //

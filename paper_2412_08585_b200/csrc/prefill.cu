@@ -1,17 +1,21 @@
 // prefill.cu -- Algorithm 1 (TurboAttention prefill) on sm_100a.
 //
-// One CTA = one (batch, query head, 128-row query tile); the tile holds two
-// B_r = 64 quantisation blocks (or one B_r = 128 block).  Warp roles:
-//   warp 0      TMA producer: K_j [64 x d] and V_j^T [d x 64] INT8 tiles into a
-//               3-stage smem ring (cp.async.bulk.tensor, 128B/64B swizzle).
-//   warp 1      TMEM owner + single-thread tcgen05.mma issuer (kind::i8):
-//               S_j = Q^q1 K_j^q1^T -> TMEM (int32, double-buffered) and
-//               PV_j = Q(P~_j) V_j^q1 -> TMEM (int32).
-//   warps 4-7   softmax/correction warpgroup, thread = query row = TMEM lane:
-//               Q stage-1 quantisation, integer row max, SAS (LUT x POLY) in
-//               registers, P tile scale + INT8 codes -> smem (A operand of the
-//               PV MMA), and O = alpha O + s_P s_V PV_int in FP32 registers
-//               one tile behind (overlapping the next MMA).
+// One CTA = one (batch, pair of GQA query heads sharing a KV head, 128-row
+// query tile); each tile holds two B_r = 64 quantisation blocks (or one
+// B_r = 128 block).  One CTA per SM (all 512 TMEM columns).  Warp roles:
+//   warp 0      TMA producer: K_j [64 x d] INT8 and V_j^T [d x 64] FP16-code
+//               tiles into a 3-stage smem ring shared by both query tiles
+//               (cp.async.bulk.tensor, 128B/64B swizzle).
+//   warps 1, 2  one single-thread tcgen05.mma issuer per query tile (warp 1
+//               also owns TMEM): S_j = Q^q1 K_j^q1^T (kind::i8 -> int32 TMEM,
+//               double-buffered) and PV_j = Q(P~_j) V_j^q1 (kind::f16 on the
+//               exact integer codes -> fp32 TMEM, exact).
+//   warps 4-11  one softmax warpgroup per query tile, thread = query row =
+//               TMEM lane: Q stage-1 quantisation, x and the row max (pass 1),
+//               SAS (LUT x POLY) + row sum + P max (pass 2), P tile scale and
+//               codes -> smem, the A operand of the PV MMA (pass 3), and
+//               O += (s_P s_V / A) PV_int in FP32 registers one tile behind;
+//               the epilogue writes O through smem (row-contiguous stores).
 #include <algorithm>
 #include <climits>
 #include <cstring>
