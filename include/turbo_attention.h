@@ -157,6 +157,23 @@ TURBO_API turbo_status_t turbo_attention_prefill(const turbo_params_t* params, i
                                        const void* v1t, const float* k1_scale, const float* v1_scale,
                                        void* o, float* lse, turbo_stream_t stream);
 
+/* Chunked prefill (NEXT-3, reading R-28): Algorithm 1 for Nq new queries at
+ * absolute positions [Nk - Nq, Nk) against Nk keys, e.g. a compressed-cache
+ * prefix of Nk - Nq tokens (its stage-1 reconstruction from
+ * turbo_dequantize_cache) followed by the chunk's own keys (turbo_quantize_kv
+ * mode 2).  turbo_attention_prefill is the case Nq = Nk.
+ *   q       FP16 [B][Nq][Hq][d];  k1 int8 [B][Hkv][Nk][d];
+ *   v1t     FP16 codes [B][Hkv][T_k][d][B_c], T_k = ceil(Nk / B_c);
+ *   k1_scale, v1_scale  f32 [B][Hkv][T_k];
+ *   causal  1 = key <= Nk - Nq + query row, 0 = all Nk keys;
+ *   o       FP16 [B][Nq][Hq][d];  lse f32 [B][Hq][Nq].
+ * Errors: TURBO_ERR_INVALID_ARG if Nq < 1 or Nk < Nq. */
+TURBO_API turbo_status_t turbo_attention_prefill_chunk(const turbo_params_t* params, int32_t B, int32_t Nq,
+                                                       int32_t Nk, int32_t Hq, int32_t Hkv, int32_t causal,
+                                                       const void* q, const int8_t* k1, const void* v1t,
+                                                       const float* k1_scale, const float* v1_scale, void* o,
+                                                       float* lse, turbo_stream_t stream);
+
 /* Workspace for turbo_attention_decode with n_splits (>= 0) on the current
  * device (HOST result; 0 = none needed, or invalid arguments).
  *   n_splits >= 2: S * B * Hq * (d + 1) floats;  n_splits == 0 (balanced):

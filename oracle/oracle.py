@@ -97,6 +97,10 @@ def _declare(L):
     L.tq_cache_prefill_slot.restype = i32
     L.tq_cache_append_slot.argtypes = [C.POINTER(Params), vp, C.POINTER(_Slot)]
     L.tq_cache_append_slot.restype = i32
+    L.tq_cache_prefill_append_slot.argtypes = [C.POINTER(Params), i32, vp, C.POINTER(_Slot), vp, vp]
+    L.tq_cache_prefill_append_slot.restype = i32
+    L.tq_prefill_chunk_head.argtypes = [C.POINTER(Params), i32, i32, i32, vp, vp, vp, vp, vp, vp, vp]
+    L.tq_prefill_chunk_head.restype = i32
     L.tq_prefill_head.argtypes = [C.POINTER(Params), i32, i32, vp, vp, vp, vp, vp, vp]
     L.tq_prefill_head.restype = i32
     L.tq_prefill_head_blocks.argtypes = [C.POINTER(Params), i32, i32, vp, vp, vp, i32, i32, vp, vp, vp]
@@ -212,6 +216,26 @@ class Slot:
             raise ValueError(f"tq_cache_prefill_slot -> {rc}")
         return x1, sc
 
+    def prefill_append(self, x: np.ndarray):
+        """A further prefill chunk (R-28; needs n_buf == 0): returns the chunk's
+        stage-1 operands (x1 [n][d] int8, x1_scale [ceil(n / B_c)] f32)."""
+        x = _f32(x)
+        n = x.shape[0]
+        tc = -(-n // self.p.block_kv)
+        x1 = np.zeros((n, self.p.d), np.int8)
+        sc = np.zeros(tc, np.float32)
+        rc = lib().tq_cache_prefill_append_slot(C.byref(self.p), n, _p(x), C.byref(self.c), _p(x1), _p(sc))
+        if rc != 0:
+            raise ValueError(f"tq_cache_prefill_append_slot -> {rc}")
+        return x1, sc
+
+    def stage1_prefix(self, n_blocks: int):
+        """Stage-1 reconstruction of blocks [0, n_blocks): int8 [n_blocks B_c][d] codes
+        code s^int + z^int (Alg. 2) with the blocks' parent scales."""
+        x1 = np.concatenate([self.dequant_block(j) for j in range(n_blocks)], 0) if n_blocks else \
+            np.zeros((0, self.p.d), np.int32)
+        return x1.astype(np.int8), self.s_parent[:n_blocks].copy()
+
     def append(self, x: np.ndarray):
         x = _f32(x)
         rc = lib().tq_cache_append_slot(C.byref(self.p), _p(x), C.byref(self.c))
@@ -256,6 +280,23 @@ def prefill_head(p: Params, q, k, v, causal=True, tap=None, blocks=None):
     if tap is not None:
         arrs["hit"] = bool(t.hit)
         return o, lse, arrs
+    return o, lse
+
+
+def prefill_chunk_head(p: Params, q, k1, sk, v1, sv, causal=True):
+    """Chunked prefill (R-28): Alg. 1 for the nq rows of q at positions nk - nq ..
+    nk - 1 against nk keys given as stage-1 operands k1, v1 (int8 [nk][d]) with
+    block scales sk, sv.  Returns (O [nq][d] f32, L [nq] f32)."""
+    q = _f32(q)
+    k1, v1 = np.ascontiguousarray(k1, np.int8), np.ascontiguousarray(v1, np.int8)
+    sk, sv = _f32(sk), _f32(sv)
+    nq, nk = q.shape[0], k1.shape[0]
+    o = np.zeros((nq, p.d), np.float32)
+    lse = np.zeros(nq, np.float32)
+    rc = lib().tq_prefill_chunk_head(C.byref(p), nq, nk, int(causal), _p(q), _p(k1), _p(sk), _p(v1), _p(sv),
+                                     _p(o), _p(lse))
+    if rc != 0:
+        raise ValueError(f"tq_prefill_chunk_head -> {rc}")
     return o, lse
 
 

@@ -171,6 +171,37 @@ int32_t tq_cache_prefill_slot(const tq_params* p, int32_t n, const float* x, tq_
   return 0;
 }
 
+/* PREFILL of a further chunk (R-28): the slot must hold whole blocks only
+ * (n_buf = 0).  The universal scale becomes the max-abs over every prefill
+ * chunk so far (R-9); the chunk's blocks are stage-1 quantised (the chunked
+ * prefill's operands) and its full blocks appended after the existing ones;
+ * its tail goes to the INT8 buffer with the updated universal scale. */
+int32_t tq_cache_prefill_append_slot(const tq_params* p, int32_t n, const float* x, tq_slot* s,
+                                     int8_t* x1, float* x1_scale) {
+  int32_t d = p->d, bc = p->block_kv;
+  if (n < 1 || s->n_buf != 0) return -1;
+  int32_t tc = (n + bc - 1) / bc, nfull = n / bc;
+  if (s->n_blocks + nfull > s->max_blocks) return -3;
+  int8_t* blk = (int8_t*)malloc((size_t)bc * d);
+  float a_univ = s->a_univ;
+  for (int64_t i = 0; i < (int64_t)n * d; ++i) a_univ = fmaxf(a_univ, fabsf(x[i]));
+  s->a_univ = a_univ;
+  for (int32_t j = 0; j < tc; ++j) {
+    int32_t rows = (j + 1) * bc <= n ? bc : n - j * bc;
+    float sc;
+    tq_quant_sym8(x + (int64_t)j * bc * d, (int64_t)rows * d, blk, &sc);
+    if (x1) memcpy(x1 + (int64_t)j * bc * d, blk, (size_t)rows * d);
+    if (x1_scale) x1_scale[j] = sc;
+    if (rows == bc) flush_block(p, s, blk, sc);
+  }
+  s->n_buf = n - nfull * bc;
+  for (int32_t t = 0; t < s->n_buf; ++t)
+    for (int32_t c = 0; c < d; ++c)
+      s->buf[(int64_t)t * d + c] = quant_univ(x[((int64_t)nfull * bc + t) * d + c], a_univ);
+  free(blk);
+  return 0;
+}
+
 /* APPEND one decode token (append, then attend).  When the buffer
  * reaches n_b = B_c tokens it is progressively quantised with the universal
  * scale as its parent scale. */
@@ -249,13 +280,22 @@ int32_t tq_prefill_head(const tq_params* p, int32_t n, int32_t causal, const flo
 /* Alg. 1's outer loop restricted to query blocks i in [i_begin, i_end): every
  * iteration of that loop is independent, so this computes exactly
  * the same rows as the full call; rows of other blocks are left untouched. */
+/* Alg. 1 for nq query rows at absolute positions q0 .. q0+nq-1
+ * against nk keys given as stage-1 operands k1, v1 (int8 [nk][d]) with block
+ * scales sk, sv [ceil(nk / B_c)]; k, v (raw [nk][d]) are read only in exact
+ * mode (quant = 0).  The prefill (q0 = 0, nq = nk) and the chunked prefill
+ * (R-28) both run this loop. */
+static int32_t prefill_core(const tq_params* p, int32_t nq, int32_t nk, int32_t q0, int32_t causal,
+                            const float* q, const float* k, const float* v, const int8_t* k1,
+                            const int8_t* v1, const float* sk, const float* sv, int32_t i_begin,
+                            int32_t i_end, float* o, float* lse, tq_prefill_tap* tap);
+
 int32_t tq_prefill_head_blocks(const tq_params* p, int32_t n, int32_t causal, const float* q,
                                const float* k, const float* v, int32_t i_begin, int32_t i_end,
                                float* o, float* lse, tq_prefill_tap* tap) {
-  const int32_t d = p->d, br = p->block_q, bc = p->block_kv;
+  const int32_t d = p->d, bc = p->block_kv;
   if (n < 1 || i_begin < 0) return -1;
-  const int32_t tr = (n + br - 1) / br, tc = (n + bc - 1) / bc;
-  if (i_end > tr) i_end = tr;
+  const int32_t tc = (n + bc - 1) / bc;
 
   /* Stage-1 K_j, V_j; done once per block instead of once per
    * (i, j) -- identical values (R-21). */
@@ -268,6 +308,26 @@ int32_t tq_prefill_head_blocks(const tq_params* p, int32_t n, int32_t causal, co
     tq_quant_sym8(k + (int64_t)j * bc * d, (int64_t)rows * d, k1 + (int64_t)j * bc * d, &sk[j]);
     tq_quant_sym8(v + (int64_t)j * bc * d, (int64_t)rows * d, v1 + (int64_t)j * bc * d, &sv[j]);
   }
+  const int32_t rc = prefill_core(p, n, n, 0, causal, q, k, v, k1, v1, sk, sv, i_begin, i_end, o, lse, tap);
+  free(k1); free(v1); free(sk); free(sv);
+  return rc;
+}
+
+int32_t tq_prefill_chunk_head(const tq_params* p, int32_t nq, int32_t nk, int32_t causal, const float* q,
+                              const int8_t* k1, const float* sk, const int8_t* v1, const float* sv,
+                              float* o, float* lse) {
+  if (nq < 1 || nk < nq || !p->quant) return -1;
+  return prefill_core(p, nq, nk, nk - nq, causal, q, NULL, NULL, k1, v1, sk, sv, 0, INT32_MAX, o, lse, NULL);
+}
+
+static int32_t prefill_core(const tq_params* p, int32_t nq, int32_t nk, int32_t q0, int32_t causal,
+                            const float* q, const float* k, const float* v, const int8_t* k1,
+                            const int8_t* v1, const float* sk, const float* sv, int32_t i_begin,
+                            int32_t i_end, float* o, float* lse, tq_prefill_tap* tap) {
+  const int32_t d = p->d, br = p->block_q, bc = p->block_kv;
+  const int32_t n = nq;  /* query rows */
+  const int32_t tr = (n + br - 1) / br, tc = (nk + bc - 1) / bc;
+  if (i_end > tr) i_end = tr;
 
   int8_t* q1 = (int8_t*)malloc((size_t)br * d);
   float* x = (float*)malloc(sizeof(float) * br * bc);
@@ -290,9 +350,9 @@ int32_t tq_prefill_head_blocks(const tq_params* p, int32_t n, int32_t causal, co
       l[r] = 0.0;
       for (int32_t c = 0; c < d; ++c) O[(int64_t)r * d + c] = 0.0;
     }
-    const int32_t jmax = causal ? (r0 + nr - 1) / bc : tc - 1; /* R-20 */
+    const int32_t jmax = causal ? (q0 + r0 + nr - 1) / bc : tc - 1; /* R-20 */
     for (int32_t j = 0; j <= jmax; ++j) {         /* for 1 <= j <= T_c */
-      const int32_t c0 = j * bc, nc = (c0 + bc <= n) ? bc : n - c0;
+      const int32_t c0 = j * bc, nc = (c0 + bc <= nk) ? bc : nk - c0;
       const int32_t tapped = tap && tap->i_block == i && tap->j_block == j;
       /* S = s_Q s_K Q^q1 K^q1^T, scaled by 1/sqrt(d) (R-18). */
       const float cqk = (sq * sk[j]) * p->softmax_scale;
@@ -300,7 +360,7 @@ int32_t tq_prefill_head_blocks(const tq_params* p, int32_t n, int32_t causal, co
         for (int32_t c = 0; c < nc; ++c) {
           float* xe = &x[(int64_t)r * bc + c];
           sint[(int64_t)r * bc + c] = 0;
-          if (causal && c0 + c > r0 + r) { *xe = -INFINITY; continue; }
+          if (causal && c0 + c > q0 + r0 + r) { *xe = -INFINITY; continue; }
           if (p->quant) {
             int32_t acc = 0;
             for (int32_t e = 0; e < d; ++e)
@@ -375,7 +435,7 @@ int32_t tq_prefill_head_blocks(const tq_params* p, int32_t n, int32_t causal, co
       lse[r0 + r] = (float)((double)m[r] + log(l[r]));
     }
   }
-  free(k1); free(v1); free(sk); free(sv); free(q1); free(x); free(sint); free(pt); free(pc);
+  free(q1); free(x); free(sint); free(pt); free(pc);
   free(pv); free(O); free(l); free(alpha); free(m); free(active);
   return 0;
 }

@@ -101,6 +101,14 @@ int32_t tq_prefill_head(const tq_params* p, int32_t n, int32_t causal, const flo
 int32_t tq_prefill_head_blocks(const tq_params* p, int32_t n, int32_t causal, const float* q,
                                const float* k, const float* v, int32_t i_begin, int32_t i_end,
                                float* o, float* lse, tq_prefill_tap* tap);
+/* Chunked prefill (R-28): Alg. 1 for nq queries at positions nk-nq .. nk-1
+ * against nk keys given as stage-1 operands (k1, v1 int8 [nk][d], block
+ * scales sk, sv); quantisation mode only. */
+int32_t tq_prefill_chunk_head(const tq_params* p, int32_t nq, int32_t nk, int32_t causal, const float* q,
+                              const int8_t* k1, const float* sk, const int8_t* v1, const float* sv,
+                              float* o, float* lse);
+int32_t tq_cache_prefill_append_slot(const tq_params* p, int32_t n_tokens, const float* x, tq_slot* s,
+                                     int8_t* x1, float* x1_scale);
 int32_t tq_decode_head(const tq_params* p, const float* q, const tq_slot* ks, const tq_slot* vs,
                        const float* k_raw, const float* v_raw, int32_t n_raw,
                        int32_t blk_begin, int32_t blk_end, int32_t with_buffer,

@@ -20,6 +20,7 @@ TURBO_OK, TURBO_ERR_INVALID_ARG, TURBO_ERR_UNSUPPORTED, TURBO_ERR_CAPACITY, TURB
 _ERR = {1: "TURBO_ERR_INVALID_ARG", 2: "TURBO_ERR_UNSUPPORTED", 3: "TURBO_ERR_CAPACITY", 4: "TURBO_ERR_CUDA"}
 
 EXPORTS = ("turbo_version", "turbo_cache_sizes", "turbo_quantize_kv", "turbo_attention_prefill",
+           "turbo_attention_prefill_chunk", "turbo_dequantize_cache",
            "turbo_decode_workspace_bytes", "turbo_decode_workers", "turbo_attention_decode", "turbo_combine_lse",
            "turbo_priority_workspace_bytes", "turbo_head_priority", "turbo_plan_bits", "turbo_selftest_div")
 
@@ -65,6 +66,11 @@ def lib() -> C.CDLL:
                                         vp, vp, vp]
         L.turbo_attention_prefill.argtypes = [C.POINTER(TurboParams), i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp,
                                               vp, vp]
+        if hasattr(L, "turbo_attention_prefill_chunk"):  # (older A/B builds lack it)
+            L.turbo_attention_prefill_chunk.argtypes = [C.POINTER(TurboParams), i32, i32, i32, i32, i32, i32, vp, vp,
+                                                        vp, vp, vp, vp, vp, vp]
+            L.turbo_dequantize_cache.argtypes = [C.POINTER(TurboParams), C.POINTER(TurboKVCache), i32, i32, vp, vp,
+                                                 vp, vp, i32, vp]
         L.turbo_decode_workspace_bytes.argtypes = [i32, i32, i32, i32, i32]
         L.turbo_decode_workspace_bytes.restype = sz
         if hasattr(L, "turbo_decode_workers"):  # (older A/B builds lack it)
@@ -188,6 +194,22 @@ def turbo_attention_prefill(p, q, k1, v1t, k1_scale, v1_scale, causal=True, o=No
     _check("turbo_attention_prefill", lib().turbo_attention_prefill(
         C.byref(p), B, N, Hq, Hkv, int(causal), _ptr(q), _ptr(k1), _ptr(v1t), _ptr(k1_scale), _ptr(v1_scale),
         _ptr(o), _ptr(lse), _stream(stream)))
+    return o, lse
+
+
+def turbo_attention_prefill_chunk(p, q, k1, v1t, k1_scale, v1_scale, causal=True, o=None, lse=None, stream=None):
+    """Chunked prefill: q fp16 [B,Nq,Hq,d] at positions [Nk-Nq, Nk) against k1 [B,Hkv,Nk,d]
+    -> (o fp16 [B,Nq,Hq,d], lse f32 [B,Hq,Nq])."""
+    assert q.dtype == torch.float16 and q.is_contiguous()
+    B, Nq, Hq, d = q.shape
+    Hkv, Nk = k1.shape[1], k1.shape[2]
+    if o is None:
+        o = torch.empty_like(q)
+    if lse is None:
+        lse = torch.empty((B, Hq, Nq), dtype=torch.float32, device=q.device)
+    _check("turbo_attention_prefill_chunk", lib().turbo_attention_prefill_chunk(
+        C.byref(p), B, Nq, Nk, Hq, Hkv, int(causal), _ptr(q), _ptr(k1), _ptr(v1t), _ptr(k1_scale),
+        _ptr(v1_scale), _ptr(o), _ptr(lse), _stream(stream)))
     return o, lse
 
 

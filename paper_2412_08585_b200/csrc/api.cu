@@ -11,7 +11,7 @@ namespace ta_host {
 cudaError_t launch_quant_prefill(const turbo_kv_cache_t* c, const __half* k, const __half* v, int N, int8_t* k1,
                                  __half* v1t, float* k1s, float* v1s, cudaStream_t st);
 cudaError_t launch_quant_append(const turbo_kv_cache_t* c, const __half* k, const __half* v, cudaStream_t st);
-cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Hq, int Hkv, int causal, const __half* q,
+cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Nk, int Hq, int Hkv, int causal, const __half* q,
                            const int8_t* k1, const __half* v1t, const float* k1s, const float* v1s, __half* o,
                            float* lse, cudaStream_t st);
 size_t decode_workspace(int B, int Hq, int Hkv, int HD, int S);
@@ -111,18 +111,26 @@ turbo_status_t turbo_quantize_kv(const turbo_params_t* params, turbo_kv_cache_t*
   return TURBO_ERR_INVALID_ARG;
 }
 
+turbo_status_t turbo_attention_prefill_chunk(const turbo_params_t* params, int32_t B, int32_t Nq, int32_t Nk,
+                                             int32_t Hq, int32_t Hkv, int32_t causal, const void* q, const int8_t* k1,
+                                             const void* v1t, const float* k1_scale, const float* v1_scale, void* o,
+                                             float* lse, turbo_stream_t stream) {
+  turbo_status_t s = check_params(params);
+  if (s != TURBO_OK) return s;
+  if (B < 1 || Nq < 1 || Nk < Nq || Hq < 1 || Hkv < 1 || (causal != 0 && causal != 1)) return TURBO_ERR_INVALID_ARG;
+  if (Hq % Hkv != 0) return TURBO_ERR_UNSUPPORTED;
+  if (!q || !k1 || !v1t || !k1_scale || !v1_scale || !o || !lse) return TURBO_ERR_INVALID_ARG;
+  return cuda_status(ta_host::launch_prefill(params, B, Nq, Nk, Hq, Hkv, causal, reinterpret_cast<const __half*>(q),
+                                             k1, reinterpret_cast<const __half*>(v1t), k1_scale, v1_scale,
+                                             reinterpret_cast<__half*>(o), lse, reinterpret_cast<cudaStream_t>(stream)));
+}
+
 turbo_status_t turbo_attention_prefill(const turbo_params_t* params, int32_t B, int32_t N, int32_t Hq, int32_t Hkv,
                                        int32_t causal, const void* q, const int8_t* k1, const void* v1t,
                                        const float* k1_scale, const float* v1_scale, void* o, float* lse,
                                        turbo_stream_t stream) {
-  turbo_status_t s = check_params(params);
-  if (s != TURBO_OK) return s;
-  if (B < 1 || N < 1 || Hq < 1 || Hkv < 1 || (causal != 0 && causal != 1)) return TURBO_ERR_INVALID_ARG;
-  if (Hq % Hkv != 0) return TURBO_ERR_UNSUPPORTED;
-  if (!q || !k1 || !v1t || !k1_scale || !v1_scale || !o || !lse) return TURBO_ERR_INVALID_ARG;
-  return cuda_status(ta_host::launch_prefill(params, B, N, Hq, Hkv, causal, reinterpret_cast<const __half*>(q), k1,
-                                             reinterpret_cast<const __half*>(v1t), k1_scale, v1_scale, reinterpret_cast<__half*>(o), lse,
-                                             reinterpret_cast<cudaStream_t>(stream)));
+  return turbo_attention_prefill_chunk(params, B, N, N, Hq, Hkv, causal, q, k1, v1t, k1_scale, v1_scale, o, lse,
+                                       stream);
 }
 
 size_t turbo_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t head_dim, int32_t n_splits) {

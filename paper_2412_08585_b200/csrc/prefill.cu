@@ -67,6 +67,7 @@ struct PrefillArgs {
   const float* k1s;
   const float* v1s;
   int B, N, Hq, Hkv, causal, block_q, alpha_mode, n_qtiles, unit_group;
+  int Nk, q0;  // keys per sequence; absolute position of query row 0 (chunked prefill: Nk - N)
   float scale;
   SasConst sas;
   int has_tap;
@@ -124,9 +125,9 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
   const int it = args.n_qtiles - 1 - rem / UGg;
   const int u = grp_i * UG + rem % UGg, b = u / (args.Hkv * GS), kvh = (u / GS) % args.Hkv, hg = u % GS;
   const int h0 = kvh * G + hg * NS;
-  const int N = args.N, Tc = (N + kBc - 1) / kBc;
+  const int N = args.N, Tc = (args.Nk + kBc - 1) / kBc;  // N query rows, Tc key tiles
   const int last_row = min(it * kTileM + kTileM - 1, N - 1);
-  const int nkv = args.causal ? min(Tc, last_row / kBc + 1) : Tc;
+  const int nkv = args.causal ? min(Tc, (args.q0 + last_row) / kBc + 1) : Tc;
   const size_t bkv = (size_t)b * args.Hkv + kvh;
 
   if (threadIdx.x == 0) {
@@ -320,7 +321,7 @@ __global__ void __launch_bounds__(128 * (1 + NS * SP), 1)
     float m = -INFINITY, l = 0.f, A = 1.f;
     float cpv_p = 0.f;
     bool tap_p = false;
-    const int kmax = row_ok ? (args.causal ? row : N - 1) : -1;  // last visible key of this row
+    const int kmax = row_ok ? (args.causal ? args.q0 + row : args.Nk - 1) : -1;  // last visible key of this row
 
     for (int j = 0; j <= nkv; ++j) {
       float cpv = 0.f, alpha_j = 0.f, sp_j = 0.f;
@@ -656,13 +657,13 @@ extern "C" TURBO_API void turbo_debug_prof(unsigned long long* out, int reset) {
 }
 #endif
 
-cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Hq, int Hkv, int causal, const __half* q,
+cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Nk, int Hq, int Hkv, int causal, const __half* q,
                            const int8_t* k1, const __half* v1t, const float* k1s, const float* v1s, __half* o,
                            float* lse, cudaStream_t st) {
-  const int HD = p->head_dim, Tc = (N + kBc - 1) / kBc;
+  const int HD = p->head_dim, Tc = (Nk + kBc - 1) / kBc;
   CUtensorMap tmk, tmv;
   const CUtensorMapSwizzle swk = HD == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
-  if (!make_map_3d(&tmk, k1, HD, N, (uint64_t)B * Hkv, HD, (uint64_t)N * HD, HD, kBc, swk))
+  if (!make_map_3d(&tmk, k1, HD, Nk, (uint64_t)B * Hkv, HD, (uint64_t)Nk * HD, HD, kBc, swk))
     return cudaErrorInvalidValue;
   if (!make_map_3d(&tmv, v1t, kBc, HD, (uint64_t)B * Hkv * Tc, kBc * 2, (uint64_t)HD * kBc * 2, kBc, HD,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16))
@@ -675,6 +676,8 @@ cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Hq, int Hk
   a.v1s = v1s;
   a.B = B;
   a.N = N;
+  a.Nk = Nk;
+  a.q0 = Nk - N;
   a.Hq = Hq;
   a.Hkv = Hkv;
   a.causal = causal;
