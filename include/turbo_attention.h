@@ -138,7 +138,17 @@ TURBO_API turbo_status_t turbo_cache_sizes(int32_t batch, int32_t n_kv_heads, in
  *     n_tokens must be 1).  Quantised with the universal scale and clamped to
  *     +-119 into the buffer; a full buffer (n_b = B_c tokens) is flushed to a
  *     stage-2 block with parent scale a_univ/119.  The *_out pointers must be
- *     NULL.  Updates cache->n_tokens (host) and the device counters. */
+ *     NULL.  Updates cache->n_tokens (host) and the device counters.
+ *   mode 2 = PREFILL_CHUNK (R-28, NEXT-3): k, v FP16 [B][n_tokens][Hkv][d], a
+ *     further prefill chunk after the P = cache->n_tokens cached tokens, which
+ *     must be a whole number of blocks (else TURBO_ERR_INVALID_ARG).  The
+ *     universal scales become the running max over all chunks; the chunk's
+ *     full blocks are appended at block P / B_c, its tail goes to the buffer.
+ *     The stage-1 outputs cover Nk = P + n_tokens tokens (k1_out
+ *     [B][Hkv][Nk][d], v1t_out [B][Hkv][ceil(Nk/B_c)][d][B_c], scales
+ *     [B][Hkv][ceil(Nk/B_c)]); the chunk's are written at token P / block
+ *     P / B_c (the prefix part comes from turbo_dequantize_cache).  Updates
+ *     cache->n_tokens to Nk. */
 TURBO_API turbo_status_t turbo_quantize_kv(const turbo_params_t* params, turbo_kv_cache_t* cache, const void* k,
                                  const void* v, int32_t n_tokens, int32_t mode, int8_t* k1_out,
                                  void* v1t_out, float* k1_scale_out, float* v1_scale_out,
@@ -156,6 +166,18 @@ TURBO_API turbo_status_t turbo_attention_prefill(const turbo_params_t* params, i
                                        int32_t Hkv, int32_t causal, const void* q, const int8_t* k1,
                                        const void* v1t, const float* k1_scale, const float* v1_scale,
                                        void* o, float* lse, turbo_stream_t stream);
+
+/* Stage-1 reconstruction of flushed cache blocks [blk_begin, blk_end)
+ * (blk_end = -1: all; blocks past a sequence's count are skipped), the
+ * prefix operands of a chunked prefill (R-28): k1_out [B][Hkv][Nk][d] rows
+ * [64 j, 64 j + 64) and v1t_out [B][Hkv][ceil(Nk/B_c)][d][B_c] block j get
+ * code s_int + z_int (Alg. 2), the scales the blocks' parent
+ * scales.  Nk = token capacity of k1_out (>= B_c x the last block).  The
+ * cache is not modified. */
+TURBO_API turbo_status_t turbo_dequantize_cache(const turbo_params_t* params, const turbo_kv_cache_t* cache,
+                                                int32_t blk_begin, int32_t blk_end, int8_t* k1_out, void* v1t_out,
+                                                float* k1_scale_out, float* v1_scale_out, int32_t Nk,
+                                                turbo_stream_t stream);
 
 /* Chunked prefill (NEXT-3, reading R-28): Algorithm 1 for Nq new queries at
  * absolute positions [Nk - Nq, Nk) against Nk keys, e.g. a compressed-cache

@@ -158,22 +158,25 @@ class KVCache:
 
 def turbo_quantize_kv(p, cache: KVCache, k, v, mode=0, stream=None, out=None):
     """mode 0 (PREFILL): k, v fp16 [B,N,Hkv,d] -> returns (k1, v1t, k1_scale, v1_scale)
-    (written into `out` when given); mode 1 (APPEND): k, v fp16 [B,Hkv,d] -> returns None."""
+    (written into `out` when given); mode 2 (PREFILL_CHUNK): the same for a further chunk,
+    outputs over Nk = cached + N tokens (the chunk at token `cached`; pass `out` holding the
+    turbo_dequantize_cache prefix); mode 1 (APPEND): k, v fp16 [B,Hkv,d] -> returns None."""
     assert k.dtype == torch.float16 and v.dtype == torch.float16 and k.is_contiguous() and v.is_contiguous()
-    if mode == 0:
+    if mode in (0, 2):
         B, N, H, d = k.shape
-        tc = -(-N // p.block_kv)
+        Nk = N if mode == 0 else cache.n_tokens + N
+        tc = -(-Nk // p.block_kv)
         dev = k.device
         if out is not None:
             k1, v1t, k1s, v1s = out
-            assert k1.shape == (B, H, N, d) and v1t.shape == (B, H, tc, d, p.block_kv)
+            assert k1.shape == (B, H, Nk, d) and v1t.shape == (B, H, tc, d, p.block_kv)
             assert k1s.shape == (B, H, tc) and v1s.shape == (B, H, tc)
         else:
-            k1 = torch.empty((B, H, N, d), dtype=torch.int8, device=dev)
+            k1 = torch.empty((B, H, Nk, d), dtype=torch.int8, device=dev)
             v1t = torch.empty((B, H, tc, d, p.block_kv), dtype=torch.float16, device=dev)
             k1s = torch.empty((B, H, tc), dtype=torch.float32, device=dev)
             v1s = torch.empty((B, H, tc), dtype=torch.float32, device=dev)
-        _check("turbo_quantize_kv", lib().turbo_quantize_kv(C.byref(p), C.byref(cache.c), _ptr(k), _ptr(v), N, 0,
+        _check("turbo_quantize_kv", lib().turbo_quantize_kv(C.byref(p), C.byref(cache.c), _ptr(k), _ptr(v), N, mode,
                                                             _ptr(k1), _ptr(v1t), _ptr(k1s), _ptr(v1s),
                                                             _stream(stream)))
         return k1, v1t, k1s, v1s
@@ -195,6 +198,24 @@ def turbo_attention_prefill(p, q, k1, v1t, k1_scale, v1_scale, causal=True, o=No
         C.byref(p), B, N, Hq, Hkv, int(causal), _ptr(q), _ptr(k1), _ptr(v1t), _ptr(k1_scale), _ptr(v1_scale),
         _ptr(o), _ptr(lse), _stream(stream)))
     return o, lse
+
+
+def turbo_dequantize_cache(p, cache: KVCache, Nk, blk_begin=0, blk_end=-1, out=None, stream=None):
+    """Stage-1 reconstruction of cache blocks [blk_begin, blk_end) into prefill operands over
+    Nk tokens -> (k1 int8 [B,Hkv,Nk,d], v1t fp16 [B,Hkv,Tk,d,B_c], k1_scale, v1_scale [B,Hkv,Tk])."""
+    B, H, d = cache.batch, cache.n_kv_heads, cache.head_dim
+    tk = -(-Nk // p.block_kv)
+    if out is None:
+        dev = cache.counters.device
+        out = (torch.zeros((B, H, Nk, d), dtype=torch.int8, device=dev),
+               torch.zeros((B, H, tk, d, p.block_kv), dtype=torch.float16, device=dev),
+               torch.zeros((B, H, tk), dtype=torch.float32, device=dev),
+               torch.zeros((B, H, tk), dtype=torch.float32, device=dev))
+    k1, v1t, k1s, v1s = out
+    _check("turbo_dequantize_cache", lib().turbo_dequantize_cache(
+        C.byref(p), C.byref(cache.c), blk_begin, blk_end, _ptr(k1), _ptr(v1t), _ptr(k1s), _ptr(v1s), Nk,
+        _stream(stream)))
+    return out
 
 
 def turbo_attention_prefill_chunk(p, q, k1, v1t, k1_scale, v1_scale, causal=True, o=None, lse=None, stream=None):

@@ -1,6 +1,8 @@
 // api.cu -- extern "C" entry points of libturboattn.so (include/turbo_attention.h):
 // host-side validation, then the kernel launchers.  No allocation, no
 // synchronisation, no mutable global state.
+#include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstring>
 
@@ -9,6 +11,8 @@
 
 namespace ta_host {
 cudaError_t launch_quant_prefill(const turbo_kv_cache_t* c, const __half* k, const __half* v, int N, int8_t* k1,
+                                 __half* v1t, float* k1s, float* v1s, cudaStream_t st, int j0, int Nk);
+cudaError_t launch_dequant_cache(const turbo_kv_cache_t* c, int blk_begin, int blk_end, int Nk, int8_t* k1,
                                  __half* v1t, float* k1s, float* v1s, cudaStream_t st);
 cudaError_t launch_quant_append(const turbo_kv_cache_t* c, const __half* k, const __half* v, cudaStream_t st);
 cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Nk, int Hq, int Hkv, int causal, const __half* q,
@@ -95,8 +99,20 @@ turbo_status_t turbo_quantize_kv(const turbo_params_t* params, turbo_kv_cache_t*
     s = cuda_status(ta_host::launch_quant_prefill(cache, reinterpret_cast<const __half*>(k),
                                                   reinterpret_cast<const __half*>(v), n_tokens, k1_out,
                                                   reinterpret_cast<__half*>(v1t_out),
-                                                  k1_scale_out, v1_scale_out, st));
+                                                  k1_scale_out, v1_scale_out, st, 0, n_tokens));
     if (s == TURBO_OK) cache->n_tokens = n_tokens;
+    return s;
+  }
+  if (mode == 2) {  // a further prefill chunk (R-28): the cache must hold whole blocks
+    if (n_tokens < 1 || !k1_out || !v1t_out || !k1_scale_out || !v1_scale_out) return TURBO_ERR_INVALID_ARG;
+    if (cache->n_tokens < 1 || cache->n_tokens % params->block_kv != 0) return TURBO_ERR_INVALID_ARG;
+    const int64_t nk = cache->n_tokens + n_tokens;
+    if (nk / params->block_kv > cache->max_blocks || nk > INT32_MAX) return TURBO_ERR_CAPACITY;
+    s = cuda_status(ta_host::launch_quant_prefill(cache, reinterpret_cast<const __half*>(k),
+                                                  reinterpret_cast<const __half*>(v), n_tokens, k1_out,
+                                                  reinterpret_cast<__half*>(v1t_out), k1_scale_out, v1_scale_out,
+                                                  st, (int)(cache->n_tokens / params->block_kv), (int)nk));
+    if (s == TURBO_OK) cache->n_tokens = nk;
     return s;
   }
   if (mode == 1) {
@@ -109,6 +125,22 @@ turbo_status_t turbo_quantize_kv(const turbo_params_t* params, turbo_kv_cache_t*
     return s;
   }
   return TURBO_ERR_INVALID_ARG;
+}
+
+turbo_status_t turbo_dequantize_cache(const turbo_params_t* params, const turbo_kv_cache_t* cache,
+                                      int32_t blk_begin, int32_t blk_end, int8_t* k1_out, void* v1t_out,
+                                      float* k1_scale_out, float* v1_scale_out, int32_t Nk, turbo_stream_t stream) {
+  turbo_status_t s = check_params(params);
+  if (s != TURBO_OK) return s;
+  if ((s = check_cache(params, cache)) != TURBO_OK) return s;
+  if (!k1_out || !v1t_out || !k1_scale_out || !v1_scale_out || blk_begin < 0) return TURBO_ERR_INVALID_ARG;
+  const int64_t flushed = cache->n_tokens / params->block_kv;
+  const int64_t last = blk_end < 0 ? flushed : std::min<int64_t>(blk_end, flushed);
+  if (blk_end >= 0 && blk_end < blk_begin) return TURBO_ERR_INVALID_ARG;
+  if (Nk < 1 || last * params->block_kv > Nk) return TURBO_ERR_INVALID_ARG;
+  return cuda_status(ta_host::launch_dequant_cache(cache, blk_begin, blk_end, Nk, k1_out,
+                                                   reinterpret_cast<__half*>(v1t_out), k1_scale_out, v1_scale_out,
+                                                   reinterpret_cast<cudaStream_t>(stream)));
 }
 
 turbo_status_t turbo_attention_prefill_chunk(const turbo_params_t* params, int32_t B, int32_t Nq, int32_t Nk,

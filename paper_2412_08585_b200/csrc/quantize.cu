@@ -2,6 +2,7 @@
 // Sec. 3.3): stage-1 symmetric INT8 per B_c block, stage-2
 // channelwise asymmetric INT4/INT2 (integer only) into packed block records,
 // the universal-scale INT8 decode buffer and its flush.
+#include <algorithm>
 #include "common.cuh"
 #include "layout.cuh"
 
@@ -96,7 +97,7 @@ TA_DEV uint32_t pack_crumb8(uint2 v) {
 
 template <int HD>
 __global__ void __launch_bounds__(2 * HD, 3 * 128 / HD) quant_prefill_kernel(
-    const __half* __restrict__ k, const __half* __restrict__ v, int N, int Hkv, int max_blocks,
+    const __half* __restrict__ k, const __half* __restrict__ v, int N, int Hkv, int max_blocks, int j0, int Nk,
     const int32_t* __restrict__ bits_dev, uint8_t* __restrict__ block_rec, float* __restrict__ s_parent,
     float* __restrict__ a_univ, int8_t* __restrict__ k1, __half* __restrict__ v1t, float* __restrict__ k1s,
     float* __restrict__ v1s) {
@@ -110,7 +111,8 @@ __global__ void __launch_bounds__(2 * HD, 3 * 128 / HD) quant_prefill_kernel(
   uint8_t* tile2 = reinterpret_cast<uint8_t*>(&xs[0][0][0]) + kBc * HD;  // K stage-2 codes [t][c]
   const int j = blockIdx.x, h = blockIdx.y, b = blockIdx.z, tid = threadIdx.x;
   const int kind = tid / HD, c = tid % HD;
-  const int Tc = (N + kBc - 1) / kBc;
+  // chunk block j is cache block j0 + j; the stage-1 outputs cover Nk tokens (Tc blocks)
+  const int Tc = (Nk + kBc - 1) / kBc;
   const int rows = min(kBc, N - j * kBc);
   const size_t bh = (size_t)b * Hkv + h;
   {
@@ -148,10 +150,10 @@ __global__ void __launch_bounds__(2 * HD, 3 * 128 / HD) quant_prefill_kernel(
     return rint_prod((t & 1) ? __high2float(xh[t >> 1]) : __low2float(xh[t >> 1]), inv);
   };
   if (c == 0) {
-    (kind ? v1s : k1s)[bh * Tc + j] = sc;
+    (kind ? v1s : k1s)[bh * Tc + j0 + j] = sc;
     // universal max-abs per (b, h, K/V) (R-9): non-negative floats order as ints
     atomicMax(reinterpret_cast<int*>(a_univ + bh * 2 + kind), __float_as_int(a));
-    if (rows == kBc) s_parent[(bh * 2 + kind) * max_blocks + j] = sc;
+    if (rows == kBc) s_parent[(bh * 2 + kind) * max_blocks + j0 + j] = sc;
   }
   if (kind == 0) {
 #pragma unroll
@@ -159,7 +161,7 @@ __global__ void __launch_bounds__(2 * HD, 3 * 128 / HD) quant_prefill_kernel(
   } else {
     // v1t: the block transposed, [d][B_c], codes as fp16 (exact) -- the B operand
     // of the prefill's kind::f16 P V MMA; tokens past N are 0.
-    uint4* dst = reinterpret_cast<uint4*>(v1t + ((bh * Tc + j) * HD + c) * kBc);
+    uint4* dst = reinterpret_cast<uint4*>(v1t + ((bh * Tc + j0 + j) * HD + c) * kBc);
 #pragma unroll
     for (int t8 = 0; t8 < kBc / 8; ++t8) {
       uint32_t u[4];
@@ -173,7 +175,7 @@ __global__ void __launch_bounds__(2 * HD, 3 * 128 / HD) quant_prefill_kernel(
   }
   const int bits = bits_dev[h * 2 + kind];
   constexpr int REC = rec_bytes(HD);
-  uint8_t* rec = block_rec + ((bh * 2 + kind) * (size_t)max_blocks + j) * REC;
+  uint8_t* rec = block_rec + ((bh * 2 + kind) * (size_t)max_blocks + j0 + j) * REC;
   if (rows == kBc) {
     // Stage 2 of this channel (integer only, R-6): z = min, s = max(1, ceil((max-min)/(2^b-1))),
     // code = floor((2 (v - z) + s) / (2 s)) = fl((2(v-z)+s) * fl(1/(2s)) + 2^-10) truncated
@@ -232,13 +234,13 @@ __global__ void __launch_bounds__(2 * HD, 3 * 128 / HD) quant_prefill_kernel(
   for (int i = tid; i < CH16; i += 2 * HD) {
     const int t = i / (HD / 16), c16 = i % (HD / 16);
     if (t < rows)
-      *reinterpret_cast<uint4*>(k1 + (bh * N + (size_t)j * kBc + t) * HD + c16 * 16) =
+      *reinterpret_cast<uint4*>(k1 + (bh * Nk + (size_t)(j0 + j) * kBc + t) * HD + c16 * 16) =
           *reinterpret_cast<const uint4*>(tile1 + t * HD + c16 * 16);
   }
   if (rows < kBc) return;  // partial tail block: goes to the buffer (tail kernel)
   // K record codes: token-major, natural channel order, LSB-first; one uint4 = 4 words per thread
   const int kbits = bits_dev[h * 2];
-  uint8_t* krec = block_rec + ((bh * 2) * (size_t)max_blocks + j) * REC + 2 * HD;
+  uint8_t* krec = block_rec + ((bh * 2) * (size_t)max_blocks + j0 + j) * REC + 2 * HD;
   if (kbits == 4) {
     for (int i = tid; i < kBc * HD / 32; i += 2 * HD) {  // 32 channels (16 B of codes) per item
       const int t = i / (HD / 32), c32 = i % (HD / 32);
@@ -267,12 +269,12 @@ __global__ void __launch_bounds__(2 * HD, 3 * 128 / HD) quant_prefill_kernel(
 template <int HD>
 __global__ void quant_tail_kernel(const __half* __restrict__ k, const __half* __restrict__ v, int N, int Hkv,
                                   const float* __restrict__ a_univ, int8_t* __restrict__ buf,
-                                  int32_t* __restrict__ counters) {
+                                  int32_t* __restrict__ counters, int j0) {
   const int h = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
   const int nfull = N / kBc, ntail = N - nfull * kBc;
   const size_t bh = (size_t)b * Hkv + h;
   if (h == 0 && tid == 0) {
-    counters[b * 2 + 0] = nfull;
+    counters[b * 2 + 0] = j0 + nfull;
     counters[b * 2 + 1] = ntail;
   }
   if (tid >= 2 * HD) return;
@@ -346,6 +348,51 @@ __global__ void append_counters_kernel(int32_t* counters, int B) {
   counters[b * 2 + 1] = nbuf;
 }
 
+// ---------------------------------------------------------------------------
+// Stage-1 reconstruction of cache blocks (chunked prefill, R-28): block j of
+// (b, kv head) -> k1 rows [64 j, 64 j + 64) and v1t block j of the prefill
+// operand layout, values code s_int + z_int (Alg. 2; exact in int8,
+// R-6), scales = the blocks' parent scales.  One CTA per (block, kv head,
+// batch), thread = (K/V, channel).
+template <int HD>
+__global__ void __launch_bounds__(2 * HD) dequant_cache_kernel(
+    int Hkv, int max_blocks, int blk_begin, int blk_end, int Nk, const int32_t* __restrict__ bits_dev,
+    const uint8_t* __restrict__ block_rec, const float* __restrict__ s_parent, const int32_t* __restrict__ counters,
+    int8_t* __restrict__ k1, __half* __restrict__ v1t, float* __restrict__ k1s, float* __restrict__ v1s) {
+  const int j = blk_begin + blockIdx.x, h = blockIdx.y, b = blockIdx.z, tid = threadIdx.x;
+  const int nb = counters[b * 2];
+  if (j >= nb || (blk_end >= 0 && j >= blk_end)) return;
+  const int kind = tid / HD, c = tid % HD, Tk = (Nk + kBc - 1) / kBc;
+  const size_t bh = (size_t)b * Hkv + h;
+  const int bits = bits_dev[h * 2 + kind];
+  constexpr int REC = rec_bytes(HD);
+  const uint8_t* rec = block_rec + ((bh * 2 + kind) * (size_t)max_blocks + j) * REC;
+  const int sc = rec[c], zc = (int)(int8_t)rec[HD + c];
+  const uint8_t* codes = rec + 2 * HD;
+  const uint32_t mask = (1u << bits) - 1u;
+  if (tid % HD == 0) (kind ? v1s : k1s)[bh * Tk + j] = s_parent[(bh * 2 + kind) * max_blocks + j];
+  if (kind == 0) {
+    // K: token-major, channel c in byte c bits / 8 at bit (c bits) % 8 (layout.cuh)
+    const int TB = HD * bits / 8, byte = c * bits / 8, sh = (c * bits) % 8;
+#pragma unroll 4
+    for (int t = 0; t < kBc; ++t)
+      k1[(bh * Nk + (size_t)j * kBc + t) * HD + c] = (int8_t)((int)((codes[t * TB + byte] >> sh) & mask) * sc + zc);
+  } else {
+    // V: channel-major words in the IMMA token order (layout.cuh v_token_of)
+    const int CB = kBc * bits / 8;
+    __half row[kBc];
+    for (int wi = 0; wi < CB / 4; ++wi)
+      for (int i = 0; i < 32 / bits; ++i) {
+        int e, sh;
+        const int t = v_token_of(bits, wi, i, &e, &sh);
+        row[t] = __int2half_rn((int)((codes[c * CB + 4 * wi + e] >> sh) & mask) * sc + zc);
+      }
+    uint4* dst = reinterpret_cast<uint4*>(v1t + ((bh * Tk + j) * HD + c) * kBc);
+#pragma unroll
+    for (int t8 = 0; t8 < kBc / 8; ++t8) dst[t8] = reinterpret_cast<const uint4*>(row)[t8];
+  }
+}
+
 }  // namespace ta
 
 // ---------------------------------------------------------------------------
@@ -354,23 +401,43 @@ namespace ta_host {
 using namespace ta;
 
 cudaError_t launch_quant_prefill(const turbo_kv_cache_t* c, const __half* k, const __half* v, int N, int8_t* k1,
-                                 __half* v1t, float* k1s, float* v1s, cudaStream_t st) {
+                                 __half* v1t, float* k1s, float* v1s, cudaStream_t st, int j0, int Nk) {
+  // j0 = 0, Nk = N: PREFILL (resets the universal scales and the buffer); j0 > 0: a
+  // further prefill chunk appended at cache block j0 (R-28), stage-1 outputs over Nk tokens.
   const int B = c->batch, H = c->n_kv_heads, HD = c->head_dim;
   const int Tc = (N + kBc - 1) / kBc;
-  cudaError_t e = cudaMemsetAsync(c->a_univ, 0, sizeof(float) * B * H * 2, st);
-  if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(c->buf, 0, (size_t)B * H * 2 * kBc * HD, st);
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
+  if (j0 == 0) {
+    e = cudaMemsetAsync(c->a_univ, 0, sizeof(float) * B * H * 2, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(c->buf, 0, (size_t)B * H * 2 * kBc * HD, st);
+    if (e != cudaSuccess) return e;
+  }
   dim3 grid(Tc, H, B);
   if (HD == 128) {
-    quant_prefill_kernel<128><<<grid, 256, 0, st>>>(k, v, N, H, c->max_blocks, c->bits_dev, c->block_rec,
+    quant_prefill_kernel<128><<<grid, 256, 0, st>>>(k, v, N, H, c->max_blocks, j0, Nk, c->bits_dev, c->block_rec,
                                                     c->s_parent, c->a_univ, k1, v1t, k1s, v1s);
-    quant_tail_kernel<128><<<dim3(H, B), 256, 0, st>>>(k, v, N, H, c->a_univ, c->buf, c->counters);
+    quant_tail_kernel<128><<<dim3(H, B), 256, 0, st>>>(k, v, N, H, c->a_univ, c->buf, c->counters, j0);
   } else {
-    quant_prefill_kernel<64><<<grid, 128, 0, st>>>(k, v, N, H, c->max_blocks, c->bits_dev, c->block_rec,
+    quant_prefill_kernel<64><<<grid, 128, 0, st>>>(k, v, N, H, c->max_blocks, j0, Nk, c->bits_dev, c->block_rec,
                                                    c->s_parent, c->a_univ, k1, v1t, k1s, v1s);
-    quant_tail_kernel<64><<<dim3(H, B), 256, 0, st>>>(k, v, N, H, c->a_univ, c->buf, c->counters);
+    quant_tail_kernel<64><<<dim3(H, B), 256, 0, st>>>(k, v, N, H, c->a_univ, c->buf, c->counters, j0);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dequant_cache(const turbo_kv_cache_t* c, int blk_begin, int blk_end, int Nk, int8_t* k1,
+                                 __half* v1t, float* k1s, float* v1s, cudaStream_t st) {
+  const int B = c->batch, H = c->n_kv_heads, HD = c->head_dim;
+  const int last = blk_end >= 0 ? std::min(blk_end, c->max_blocks) : c->max_blocks;
+  if (last <= blk_begin) return cudaSuccess;
+  dim3 grid(last - blk_begin, H, B);
+  if (HD == 128)
+    dequant_cache_kernel<128><<<grid, 256, 0, st>>>(H, c->max_blocks, blk_begin, blk_end, Nk, c->bits_dev,
+                                                    c->block_rec, c->s_parent, c->counters, k1, v1t, k1s, v1s);
+  else
+    dequant_cache_kernel<64><<<grid, 128, 0, st>>>(H, c->max_blocks, blk_begin, blk_end, Nk, c->bits_dev,
+                                                   c->block_rec, c->s_parent, c->counters, k1, v1t, k1s, v1s);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,89 @@
+"""Chunked prefill (NEXT-3, reading R-28) on the GPU against the oracle, through the
+C-ABI: a prefix prefill, the stage-1 reconstruction of its cached blocks
+(turbo_dequantize_cache), a further chunk (turbo_quantize_kv mode 2) and
+turbo_attention_prefill_chunk.  Bit-exact: the stage-1 operands of prefix and
+chunk, every cache record, the universal scales, the buffer and the counters;
+tolerance set: O and L."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2412_08585_b200 import synth
+from tests import cache_layout
+from tests.test_gpu_parity import assert_out_close, ta  # noqa: F401  (fixture)
+
+pytestmark = pytest.mark.gpu
+
+CASES = [  # (B, P, Nq, Hq, Hkv, d, causal)
+    (2, 128, 64, 8, 2, 128, True),
+    (1, 256, 100, 4, 1, 128, True),    # ragged chunk: its tail goes to the buffer
+    (2, 64, 1, 8, 2, 128, True),       # one-token chunk
+    (1, 192, 130, 2, 2, 64, True),     # d = 64
+    (1, 128, 70, 4, 2, 128, False),    # non-causal: every query sees all P + Nq keys
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_chunked_prefill_parity(ta, case):  # noqa: F811
+    B, P, Nq, Hq, Hkv, d, causal = case
+    G, Nk = Hq // Hkv, P + Nq
+    q, k, v = synth.qkv(4100 + Nk, B, Nk, Hq, Hkv, d)
+    bits = synth.head_bits_alternating(Hkv)
+    p = ta.params(head_dim=d)
+    maxb = Nk // 64 + 2
+    cache = ta.KVCache(B, Hkv, d, max_blocks=maxb, bits=bits)
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()  # noqa: E731
+    ta.turbo_quantize_kv(p, cache, dev(k[:, :P]), dev(v[:, :P]))
+    ops = ta.turbo_dequantize_cache(p, cache, Nk)
+    ta.turbo_quantize_kv(p, cache, dev(k[:, P:]), dev(v[:, P:]), mode=2, out=ops)
+    o, lse = ta.turbo_attention_prefill_chunk(p, dev(q[:, P:]), *ops, causal=causal)
+    torch.cuda.synchronize()
+    assert cache.n_tokens == Nk
+    k1, v1t, k1s, v1s = (x.cpu().numpy() for x in ops)
+    o, lse = o.cpu().numpy(), lse.cpu().numpy()
+    recs = cache.records().cpu().numpy()
+    cnt = cache.counters.view(B, 2).cpu().numpy()
+    a_univ = cache.a_univ.view(B, Hkv, 2).cpu().numpy()
+    op = O.params(d=d)
+    for b in range(B):
+        for h in range(Hkv):
+            ops_ref = []
+            for kind, x in ((0, k), (1, v)):
+                sl = O.Slot(op, int(bits[h][kind]), maxb)
+                sl.prefill(x[b, :P, h].astype(np.float32))
+                xp, sp = sl.stage1_prefix(P // 64)
+                xc, sc = sl.prefill_append(x[b, P:, h].astype(np.float32))
+                ops_ref.append((np.concatenate([xp, xc]), np.concatenate([sp, sc])))
+                # cache state after both chunks
+                assert tuple(cnt[b]) == (sl.n_blocks, sl.n_buf)
+                assert a_univ[b, h, kind] == sl.a_univ
+                for j in range(sl.n_blocks):
+                    codes, s_int, z_int = cache_layout.unpack_record(recs[b, h, kind, j], d, int(bits[h][kind]), kind)
+                    np.testing.assert_array_equal(codes, sl.codes[j])
+                    np.testing.assert_array_equal(s_int, sl.s_int[j])
+                    np.testing.assert_array_equal(z_int, sl.z_int[j])
+            (K1, SK), (V1, SV) = ops_ref
+            # stage-1 operands: prefix reconstruction + chunk, bit-exact
+            np.testing.assert_array_equal(k1[b, h], K1)
+            np.testing.assert_array_equal(k1s[b, h], SK)
+            np.testing.assert_array_equal(v1s[b, h], SV)
+            vt = v1t[b, h].astype(np.float32)  # [Tk][d][64] codes
+            for j in range(-(-Nk // 64)):
+                rows = min(64, Nk - 64 * j)
+                np.testing.assert_array_equal(vt[j][:, :rows].T, V1[64 * j:64 * j + rows])
+            for hq in range(h * G, h * G + G):
+                ro, rl = O.prefill_chunk_head(op, q[b, P:, hq].astype(np.float32), K1, SK, V1, SV, causal=causal)
+                assert_out_close(o[b, :, hq], ro, f"chunk b{b} h{hq}")
+                np.testing.assert_allclose(lse[b, hq], rl, atol=1e-4, rtol=1e-5)
+
+
+def test_chunk_needs_whole_cached_blocks(ta):  # noqa: F811
+    B, N, Hkv, d = 1, 100, 1, 128
+    _, k, v = synth.qkv(3, B, N + 64, Hkv, Hkv, d)
+    p = ta.params(head_dim=d)
+    cache = ta.KVCache(B, Hkv, d, max_blocks=8, bits=[[4, 4]])
+    ta.turbo_quantize_kv(p, cache, torch.from_numpy(k[:, :N].copy()).cuda(), torch.from_numpy(v[:, :N].copy()).cuda())
+    with pytest.raises(ta.TurboError):
+        ta.turbo_quantize_kv(p, cache, torch.from_numpy(k[:, N:].copy()).cuda(),
+                             torch.from_numpy(v[:, N:].copy()).cuda(), mode=2)
