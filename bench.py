@@ -536,6 +536,49 @@ def run_prefill_70b(args, rank, world, device):
                        "per_rank_heads": [hq, hkv]}}
 
 
+def run_prefill_chunk(args, rank, world, device):
+    """NEXT-3 chunked prefill (R-28) on the configs[1] shape: a 1024-token chunk after a
+    3072-token compressed prefix (B = 8, 32/8 heads, d = 128, causal); per step:
+    turbo_dequantize_cache (prefix operands) + turbo_quantize_kv mode 2 (chunk) +
+    turbo_attention_prefill_chunk.  Ops = 4 d x unmasked (query, key) pairs of the chunk."""
+    import torch
+
+    from paper_2412_08585_b200 import binding as ta
+    from paper_2412_08585_b200 import synth
+
+    c = CFG_PREFILL
+    B, Hq, Hkv, d = c["B"], c["Hq"], c["Hkv"], c["d"]
+    P, Nq = 3072, 1024
+    Nk = P + Nq
+    p = ta.params(head_dim=d)
+    q, k, v = synth.qkv_torch(6006 + rank, B, Nk, Hq, Hkv, d, device=device)
+    qc, kp, vp, kc, vc = (x.contiguous() for x in (q[:, P:], k[:, :P], v[:, :P], k[:, P:], v[:, P:]))
+    cache = ta.KVCache(B, Hkv, d, max_blocks=Nk // 64 + 1, bits=synth.head_bits_alternating(Hkv), device=device)
+    ops_buf = ta.turbo_dequantize_cache(p, cache, Nk)
+    o = torch.empty_like(qc)
+    lse = torch.empty((B, Hq, Nq), dtype=torch.float32, device=device)
+    st = torch.cuda.current_stream()
+    tot = 0.0
+    for i in range(args.warmup + args.steps):
+        ta.turbo_quantize_kv(p, cache, kp, vp)  # the prefix (untimed: restores the cache to P tokens)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        ta.turbo_dequantize_cache(p, cache, Nk, out=ops_buf)
+        ta.turbo_quantize_kv(p, cache, kc, vc, mode=2, out=ops_buf)
+        ta.turbo_attention_prefill_chunk(p, qc, *ops_buf, causal=True, o=o, lse=lse)
+        e1.record(st)
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            tot += e0.elapsed_time(e1)
+    ms = _max_over_ranks(tot, world, device) / args.steps
+    ops = 4.0 * d * B * Hq * sum(P + r + 1 for r in range(Nq)) * world
+    return {"value": ops / (ms * 1e-3) / 1e12, "unit": "TOPS", "ms_step": ms, "scaling": "weak",
+            "config": {"workload": "NEXT-3 chunked prefill (R-28): 1024-token chunk after a 3072-token compressed "
+                                   "prefix, configs[1] shape (B=8, 32/8 heads, d=128), causal; step = "
+                                   "dequantize_cache + quantize_kv(chunk) + prefill_chunk",
+                       "parallelism": f"{world} rank(s), each its own batch, no collective"}}
+
+
 def run_decode_long(args, rank, world, device):
     """configs[4]: 128k-context decode, batch 16 (Llama-3-8B attention shape,
     32/8 heads, mixed INT4/INT2), cache sequence-sharded over the ranks; per
@@ -606,7 +649,7 @@ def main():
     ap.add_argument("--decode-splits", type=int, default=None,
                     help="decode split count (default: binding.auto_splits; 0: the balanced schedule)")
     ap.add_argument("--no-decode", action="store_true")
-    ap.add_argument("--workload", default="step", choices=["step", "prefill_70b", "decode_long"],
+    ap.add_argument("--workload", default="step", choices=["step", "prefill_70b", "decode_long", "prefill_chunk"],
                     help="step = the default hot-path step (configs[1] + configs[2] decode)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -626,7 +669,8 @@ def main():
 
     build.build()
     if args.workload != "step":
-        fn = run_prefill_70b if args.workload == "prefill_70b" else run_decode_long
+        fn = {"prefill_70b": run_prefill_70b, "decode_long": run_decode_long,
+              "prefill_chunk": run_prefill_chunk}[args.workload]
         res = fn(args, rank, world, local)
         if rank == 0:
             line = {"metric": BASE_METRIC, "value": round(res["value"], 2), "unit": res["unit"], "n_gpus": world,
