@@ -7,7 +7,8 @@ never imports it; inputs come from ``paper_2412_08585_b200.synth`` (seeded
 generators that hold none of the method's arithmetic) or from the tests.
 
 Every function mirrors one routine of the paper (citations in turbo_oracle.c):
-Alg. 1 prefill, Alg. 2 decode, SAS
+Alg. 1 prefill and its chunked form (reading R-28), Alg. 2 decode
+(PAPER.md:945-997), SAS
 (PAPER.md:455-493, 1006-1032), FlashQ stage 1/2 and the
 enhanced KV buffer.
 """

@@ -9,7 +9,7 @@
  * Precision: the paper fixes the stage-1 codes to INT8 with divisor 119
  * (Alg. 1), stage-2 to INT4/INT2 integers, and runs the
  * score/softmax arithmetic in a GPU float format.  Readings
- * R-1..R-26 pin the float arithmetic to binary32; the running
+ * R-1..R-28 pin the float arithmetic to binary32; the running
  * output O and row sum l are kept in double here (they are in the tolerance
  * set, not the exact set).
  */
