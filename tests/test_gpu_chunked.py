@@ -87,3 +87,56 @@ def test_chunk_needs_whole_cached_blocks(ta):  # noqa: F811
     with pytest.raises(ta.TurboError):
         ta.turbo_quantize_kv(p, cache, torch.from_numpy(k[:, N:].copy()).cuda(),
                              torch.from_numpy(v[:, N:].copy()).cuda(), mode=2)
+
+
+def test_two_chunks_after_a_prefix(ta):  # noqa: F811
+    """prefix 128 -> chunk 64 -> chunk 100: block offsets and the running universal scale
+    across several chunks; the second chunk's attention and the final cache vs the oracle."""
+    B, P, N1, N2, Hq, Hkv, d = 1, 128, 64, 100, 4, 2, 128
+    G, Nk = Hq // Hkv, P + N1 + N2
+    q, k, v = synth.qkv(4321, B, Nk, Hq, Hkv, d)
+    k[:, P + 10] *= 3.0  # the second and third segments carry the largest magnitudes (universal scale grows)
+    v[:, P + N1 + 5] *= 2.0
+    bits = synth.head_bits_alternating(Hkv)
+    p = ta.params(head_dim=d)
+    maxb = Nk // 64 + 2
+    cache = ta.KVCache(B, Hkv, d, max_blocks=maxb, bits=bits)
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()  # noqa: E731
+    ta.turbo_quantize_kv(p, cache, dev(k[:, :P]), dev(v[:, :P]))
+    ops1 = ta.turbo_dequantize_cache(p, cache, P + N1)
+    ta.turbo_quantize_kv(p, cache, dev(k[:, P:P + N1]), dev(v[:, P:P + N1]), mode=2, out=ops1)
+    ops2 = ta.turbo_dequantize_cache(p, cache, Nk)
+    ta.turbo_quantize_kv(p, cache, dev(k[:, P + N1:]), dev(v[:, P + N1:]), mode=2, out=ops2)
+    o, lse = ta.turbo_attention_prefill_chunk(p, dev(q[:, P + N1:]), *ops2)
+    torch.cuda.synchronize()
+    o, lse = o.cpu().numpy(), lse.cpu().numpy()
+    recs = cache.records().cpu().numpy()
+    cnt = cache.counters.view(B, 2).cpu().numpy()
+    a_univ = cache.a_univ.view(B, Hkv, 2).cpu().numpy()
+    buf = cache.buf.view(B, Hkv, 2, 64 * d).cpu().numpy()
+    op = O.params(d=d)
+    for h in range(Hkv):
+        ops_ref = []
+        for kind, x in ((0, k), (1, v)):
+            sl = O.Slot(op, int(bits[h][kind]), maxb)
+            sl.prefill(x[0, :P, h].astype(np.float32))
+            sl.prefill_append(x[0, P:P + N1, h].astype(np.float32))
+            xp, sp = sl.stage1_prefix((P + N1) // 64)
+            xc, sc = sl.prefill_append(x[0, P + N1:, h].astype(np.float32))
+            ops_ref.append((np.concatenate([xp, xc]), np.concatenate([sp, sc])))
+            assert tuple(cnt[0]) == (sl.n_blocks, sl.n_buf)
+            assert a_univ[0, h, kind] == sl.a_univ
+            for j in range(sl.n_blocks):
+                codes, s_int, z_int = cache_layout.unpack_record(recs[0, h, kind, j], d, int(bits[h][kind]), kind)
+                np.testing.assert_array_equal(codes, sl.codes[j])
+                np.testing.assert_array_equal(s_int, sl.s_int[j])
+            # buffer: K token-major, V channel-major (DESIGN.md §6)
+            bref = sl.buf[:sl.n_buf]
+            bgpu = buf[0, h, kind].reshape(64, d)[:sl.n_buf] if kind == 0 else buf[0, h, kind].reshape(d, 64)[:, :sl.n_buf].T
+            np.testing.assert_array_equal(bgpu, bref)
+        (K1, SK), (V1, SV) = ops_ref
+        np.testing.assert_array_equal(ops2[0][0, h].cpu().numpy(), K1)
+        for hq in range(h * G, h * G + G):
+            ro, rl = O.prefill_chunk_head(op, q[0, P + N1:, hq].astype(np.float32), K1, SK, V1, SV)
+            assert_out_close(o[0, :, hq], ro, f"chunk 2 h{hq}")
+            np.testing.assert_allclose(lse[0, hq], rl, atol=1e-4, rtol=1e-5)
