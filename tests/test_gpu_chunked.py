@@ -21,6 +21,7 @@ CASES = [  # (B, P, Nq, Hq, Hkv, d, causal)
     (2, 64, 1, 8, 2, 128, True),       # one-token chunk
     (1, 192, 130, 2, 2, 64, True),     # d = 64
     (1, 128, 70, 4, 2, 128, False),    # non-causal: every query sees all P + Nq keys
+    (1, 128, 300, 2, 2, 128, True),    # MHA: query-tile pairs with a prefix offset
 ]
 
 

@@ -45,6 +45,8 @@ CASES = [  # (B, N, Hq, Hkv, d, causal, block_q, alpha_mode)
     (2, 200, 8, 2, 128, True, 64, 0),     # GQA, ragged tail, several tiles
     (1, 333, 4, 4, 128, False, 64, 1),    # non-causal, ragged, alpha mode 1
     (1, 256, 2, 1, 64, True, 128, 0),     # B_r = 128
+    (2, 700, 3, 3, 128, True, 64, 0),     # MHA (G = 1): adjacent query-tile pairs, ragged last pair
+    (1, 520, 6, 2, 128, True, 64, 1),     # odd G = 3: tile pairs of one head
 ]
 
 
@@ -58,10 +60,11 @@ def test_quantize_kv_prefill_bit_exact(ta, case):
     q, k, v = synth.qkv(500 + N, B, N, Hq, Hkv, d)
     bits = synth.head_bits_alternating(Hkv)
     p = ta.params(head_dim=d, block_q=bq, alpha_mode=am)
-    cache = ta.KVCache(B, Hkv, d, max_blocks=8, bits=bits)
+    mb = N // 64 + 2
+    cache = ta.KVCache(B, Hkv, d, max_blocks=mb, bits=bits)
     k1, v1t, k1s, v1s = ta.turbo_quantize_kv(p, cache, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
     torch.cuda.synchronize()
-    ref = O.build_cache(_oracle_params(d, bq, am), k.astype(np.float32), v.astype(np.float32), bits, 8)
+    ref = O.build_cache(_oracle_params(d, bq, am), k.astype(np.float32), v.astype(np.float32), bits, mb)
     np.testing.assert_array_equal(k1.cpu().numpy(), ref["k1"])
     np.testing.assert_array_equal(k1s.cpu().numpy(), ref["k1s"])
     np.testing.assert_array_equal(v1s.cpu().numpy(), ref["v1s"])
@@ -72,7 +75,7 @@ def test_quantize_kv_prefill_bit_exact(ta, case):
     np.testing.assert_array_equal(v1[:, :, :N], ref["v1"])
     assert not v1[:, :, N:].any()
     recs = cache.records().cpu().numpy()
-    spar = cache.s_parent[: B * Hkv * 2 * 8].view(B, Hkv, 2, 8).cpu().numpy()
+    spar = cache.s_parent[: B * Hkv * 2 * mb].view(B, Hkv, 2, mb).cpu().numpy()
     buf = cache.buf.view(B, Hkv, 2, 64 * d).cpu().numpy()
     a_univ = cache.a_univ.view(B, Hkv, 2).cpu().numpy()
     cnt = cache.counters.view(B, 2).cpu().numpy()
@@ -97,7 +100,7 @@ def test_prefill_parity(ta, case):
     q, k, v = synth.qkv(700 + N, B, N, Hq, Hkv, d)
     bits = synth.head_bits_alternating(Hkv)
     p = ta.params(head_dim=d, block_q=bq, alpha_mode=am)
-    cache = ta.KVCache(B, Hkv, d, max_blocks=8, bits=bits)
+    cache = ta.KVCache(B, Hkv, d, max_blocks=N // 64 + 2, bits=bits)
     qt, kt, vt = (torch.from_numpy(x).cuda() for x in (q, k, v))
     k1, v1t, k1s, v1s = ta.turbo_quantize_kv(p, cache, kt, vt)
     o, lse = ta.turbo_attention_prefill(p, qt, k1, v1t, k1s, v1s, causal=causal)
@@ -125,7 +128,7 @@ def test_prefill_exact_set_tap(ta, case):
     for (b, h, i, j) in sorted({(B - 1, Hq - 1, T - 1, T - 1), (0, 0, 1, 0), (0, Hq // 2, T - 1, 0)}):
         tap = ta.DebugTap(b, h, i, j, d)
         p = ta.params(head_dim=d, block_q=bq, alpha_mode=am, debug_tap=tap)
-        cache = ta.KVCache(B, Hkv, d, max_blocks=8, bits=bits)
+        cache = ta.KVCache(B, Hkv, d, max_blocks=N // 64 + 2, bits=bits)
         k1, v1t, k1s, v1s = ta.turbo_quantize_kv(p, cache, kt, vt)
         ta.turbo_attention_prefill(p, qt, k1, v1t, k1s, v1s, causal=causal)
         torch.cuda.synchronize()

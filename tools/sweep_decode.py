@@ -11,8 +11,12 @@ import bench  # noqa: E402
 
 SPL3 = tuple(int(x) for x in os.environ.get("SPL3", "0,8,12").split(","))
 SPL5 = tuple(int(x) for x in os.environ.get("SPL5", "0,32").split(","))
-for name, (B, N, Hq, Hkv, d), splits in (("cfg3", (64, 32768, 40, 10, 128), SPL3),
-                                         ("cfg5", (16, 131072, 32, 8, 128), SPL5)):
+SHAPES = [("cfg3", (64, 32768, 40, 10, 128), SPL3), ("cfg5", (16, 131072, 32, 8, 128), SPL5)]
+if os.environ.get("DEC_SHAPES"):  # "B,N,Hq,Hkv,d;..." with split list SPLX (e.g. the G = 8 shapes)
+    SPLX = tuple(int(x) for x in os.environ.get("SPLX", "0").split(","))
+    SHAPES = [("G%d" % (int(t.split(",")[2]) // int(t.split(",")[3])), tuple(int(x) for x in t.split(",")), SPLX)
+              for t in os.environ["DEC_SHAPES"].split(";")]
+for name, (B, N, Hq, Hkv, d), splits in SHAPES:
     bits = synth.head_bits_alternating(Hkv)
     p = ta.params(head_dim=d)
     cache = ta.KVCache(B, Hkv, d, max_blocks=N // 64 + 4, bits=bits)
@@ -33,6 +37,6 @@ for name, (B, N, Hq, Hkv, d), splits in (("cfg3", (64, 32768, 40, 10, 128), SPL3
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 20
-        print(f"{name} S={S:3d} {ms * 1e3:8.1f} us  {byt / ms / 1e6:8.1f} GB/s", flush=True)
+        print(f"{name} B={B} N={N} S={S:3d} {ms * 1e3:8.1f} us  {byt / ms / 1e6:8.1f} GB/s", flush=True)
     del cache
     torch.cuda.empty_cache()

@@ -10,6 +10,8 @@ from paper_2412_08585_b200 import binding as ta  # noqa: E402
 from paper_2412_08585_b200 import synth  # noqa: E402
 
 B, N, Hq, Hkv, d = (1, 32768, 64, 8, 128) if os.environ.get("TP_CFG") == "70b" else (8, 4096, 32, 8, 128)
+if os.environ.get("TP_SHAPE"):  # "B,N,Hq,Hkv,d" (e.g. MHA: 8,4096,32,32,128)
+    B, N, Hq, Hkv, d = (int(x) for x in os.environ["TP_SHAPE"].split(","))
 p = ta.params(head_dim=d)
 q, k, v = synth.qkv_torch(1002, B, N, Hq, Hkv, d)
 cache = ta.KVCache(B, Hkv, d, max_blocks=N // 64 + 2, bits=synth.head_bits_alternating(Hkv))
@@ -26,5 +28,5 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / ITERS
 ops = 4.0 * d * N * (N + 1) / 2 * B * Hq
-print(f"{os.environ.get('TURBO_LIB', 'in-tree')}: {ms * 1e3:8.1f} us  {ops / ms / 1e9:7.1f} TOPS  "
+print(f"{os.environ.get('TURBO_LIB', 'in-tree')} {B},{N},{Hq},{Hkv},{d}: {ms * 1e3:8.1f} us  {ops / ms / 1e9:7.1f} TOPS  "
       f"checksum {o.float().abs().sum().item():.6e}")
