@@ -440,15 +440,13 @@ TA_DEV void pv_block(uint32_t rec, const int8_t* vb, uint32_t pbuf, const int (&
       const int hh = PACK ? (ql ? 1 : 0) : h;  // which channel of the pair (c0 / c1)
       const int ci = PACK ? mt : 2 * mt + h;
       const int ch = c0 + 8 * hh;
+      // the channel's s_int / z_int, loaded once for both rows
+      const int s_c = BUF ? 0 : (int)lds_u8(rec + ch), z_c = BUF ? 0 : lds_s8(rec + HD + ch);
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         // selects, not c[2 * hh + e]: a runtime index would put c[] in local memory
         const int v = PACK ? (ql ? c[2 + e] : c[e]) : c[2 * h + e];
-        if (BUF) {
-          acc[ci][e] = v;
-        } else {
-          acc[ci][e] = (int)lds_u8(rec + ch) * v + lds_s8(rec + HD + ch) * sum_p[e];
-        }
+        acc[ci][e] = BUF ? v : s_c * v + z_c * sum_p[e];
       }
     }
   }
