@@ -212,9 +212,9 @@ TURBO_API int32_t turbo_decode_workers(int32_t Hq, int32_t Hkv, int32_t head_dim
  * sequence against cache blocks [blk_begin, blk_end) (blk_end = -1: all
  * flushed blocks) and, if with_buffer, the INT8 buffer block last.  Each
  * sub-range below is one online-softmax pass (same order as Alg. 2); the
- * partial results are merged by the log-sum-exp combine in ascending order
- * (R-23).  Sub-ranges:
- *   n_splits >= 1: the block range of every (b, kv head) is cut into
+ * partial results are merged by the log-sum-exp combine (R-23; fixed
+ * summation order, see turbo_combine_lse).  Sub-ranges:
+ *   n_splits in [1, 12000]: the block range of every (b, kv head) is cut into
  *     n_splits contiguous ranges of ceil(n / n_splits) blocks (the buffer
  *     joins the last one).
  *   n_splits == 0 (balanced): the units of every (b, kv head) -- its blocks
@@ -235,8 +235,11 @@ TURBO_API turbo_status_t turbo_attention_decode(const turbo_params_t* params, co
                                       size_t workspace_bytes, void* o, float* o_part, float* lse,
                                       turbo_stream_t stream);
 
-/* Log-sum-exp combine of n_parts partial results, in ascending part order
- * (R-23): L = max_s L_s + ln sum_s e^{L_s - max}, O = sum_s e^{L_s - L} O_s.
+/* Log-sum-exp combine of n_parts partial results (R-23):
+ * L = max_s L_s + ln sum_s e^{L_s - max}, O = sum_s e^{L_s - L} O_s.
+ * Deterministic fixed summation order: the weight sum lane-strided then by
+ * butterfly; O over W <= 8 contiguous part ranges (about 4 parts per range),
+ * each ascending, the ranges added in order.  n_parts <= 12000.
  *   d = head_dim (64 or 128, else TURBO_ERR_UNSUPPORTED);
  *   o_parts f32 [n_parts][rows][d], lse_parts f32 [n_parts][rows];
  *   o FP16 [rows][d] (or NULL), o_f32 f32 [rows][d] (or NULL), lse f32 [rows]. */

@@ -700,11 +700,100 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
   }
 }
 
-// Log-sum-exp merge of the balanced schedule's pieces (R-23): one CTA of
-// 128 threads per output row (b, h); the pieces of (b, kv head) are the
-// parts bh + w for the warps w whose chunks meet its unit range, merged in
-// ascending order with combine_kernel's arithmetic.
-__global__ void combine_balanced_kernel(const __grid_constant__ DecodeArgs a, int W, int d) {
+// Log-sum-exp merge of n partial (O_s, L_s) of one output row (R-23):
+// L = max + log sum_s e^{L_s - max},  O = sum_s (e^{L_s - max} / wsum) O_s.
+// Part s sits at lse[s * lse_stride], o[s * o_stride + c].  W = blockDim / 32
+// <= kCombWarps warps (comb_warps: about 4 parts per warp): warp 0 computes the
+// weights into shared memory (lane-strided sums, fixed butterfly order); warp k
+// then sums the contiguous part range [k n / W, (k+1) n / W) in ascending order for all d channels (d / 32
+// consecutive channels per lane, one vector load per part, 8 parts in flight),
+// and the W partial rows are added in warp order -- deterministic, and with
+// many parts in flight per row instead of one serial chain (B = 1 decode runs
+// 32 rows of 128-512 parts).
+constexpr int kCombWarps = 8;
+static inline int comb_warps(int n) { return n >= 4 * kCombWarps ? kCombWarps : (n + 3) / 4 < 1 ? 1 : (n + 3) / 4; }
+template <int VEC>
+TA_DEV void combine_row(int n, const float* __restrict__ lse, size_t lse_stride, const float* __restrict__ o,
+                        size_t o_stride, int d, float* w, float (*part)[128], __half* o16, float* o32, float* L_out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (warp == 0) {
+    float lmax = -INFINITY;
+    for (int s = lane; s < n; s += 32) lmax = fmaxf(lmax, lse[s * lse_stride]);
+#pragma unroll
+    for (int x = 16; x > 0; x >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, x));
+    float wsum = 0.f;
+    if (lmax != -INFINITY)
+      for (int s = lane; s < n; s += 32) {
+        const float e = expf(lse[s * lse_stride] - lmax);
+        w[s] = e;
+        wsum += e;
+      }
+#pragma unroll
+    for (int x = 16; x > 0; x >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, x);
+    const float inv = lmax != -INFINITY ? 1.f / wsum : 0.f;
+    __syncwarp();
+    for (int s = lane; s < n; s += 32) w[s] = lmax != -INFINITY ? w[s] * inv : 0.f;
+    if (lane == 0) {
+      w[n] = lmax;
+      if (L_out) *L_out = lmax != -INFINITY ? lmax + logf(wsum) : -INFINITY;
+    }
+  }
+  __syncthreads();
+  const bool live = w[n] != -INFINITY;
+  const int c0 = lane * VEC;
+  float acc[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) acc[v] = 0.f;
+  if (live && c0 < d) {
+    const int s0 = (int)((long long)warp * n / nw), s1 = (int)((long long)(warp + 1) * n / nw);
+    int s = s0;
+    for (; s + 8 <= s1; s += 8) {
+      float x[8][VEC];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float* src = o + (size_t)(s + k) * o_stride + c0;
+        if (VEC == 4) {
+          const float4 t = *reinterpret_cast<const float4*>(src);
+          x[k][0] = t.x; x[k][VEC > 1 ? 1 : 0] = t.y; x[k][VEC > 2 ? 2 : 0] = t.z; x[k][VEC > 3 ? 3 : 0] = t.w;
+        } else if (VEC == 2) {
+          const float2 t = *reinterpret_cast<const float2*>(src);
+          x[k][0] = t.x; x[k][VEC > 1 ? 1 : 0] = t.y;
+        } else {
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) x[k][v] = src[v];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[v] += w[s + k] * x[k][v];
+    }
+    for (; s < s1; ++s)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) acc[v] += w[s] * o[(size_t)s * o_stride + c0 + v];
+  }
+  if (c0 < d)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) part[warp][c0 + v] = acc[v];
+  __syncthreads();
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float out = 0.f;
+#pragma unroll
+    for (int k = 0; k < kCombWarps; ++k)
+      if (k < nw) out += part[k][c];
+    if (o16) o16[c] = __float2half_rn(out);
+    if (o32) o32[c] = out;
+  }
+}
+
+// Balanced schedule (R-23): one CTA per output row (b, h); the pieces of
+// (b, kv head) are the parts bh + w for the warps w whose chunks meet its unit
+// range.
+template <int VEC>
+__global__ void __launch_bounds__(32 * kCombWarps) combine_balanced_kernel(const __grid_constant__ DecodeArgs a, int W,
+                                                                             int d) {
+  extern __shared__ float w[];  // [n + 1]
+  __shared__ float part[kCombWarps][128];
   const int r = blockIdx.x, b = r / a.Hq, h = r % a.Hq, kvh = h / a.G, row = h % a.G, lane = threadIdx.x & 31;
   int tot = 0, before = 0;
   for (int b0 = 0; b0 < a.B; b0 += 32) {
@@ -722,82 +811,35 @@ __global__ void combine_balanced_kernel(const __grid_constant__ DecodeArgs a, in
   const int C = max(kMinUnits, (tot * a.Hkv + W - 1) / W);
   const int start = before * a.Hkv + kvh * U;
   const int bh = b * a.Hkv + kvh;
-  const int w0 = U > 0 ? start / C : 0, w1 = U > 0 ? (start + U - 1) / C : -1;
-  float lmax = -INFINITY;
-  for (int w = w0; w <= w1; ++w) lmax = fmaxf(lmax, a.lse_parts[(size_t)(bh + w) * a.G + row]);
-  float wsum = 0.f, inv = 0.f, L = -INFINITY;
-  if (lmax != -INFINITY) {
-    for (int w = w0; w <= w1; ++w) wsum += expf(a.lse_parts[(size_t)(bh + w) * a.G + row] - lmax);
-    inv = 1.f / wsum;
-    L = lmax + logf(wsum);
-  }
-  for (int c = threadIdx.x; c < d; c += blockDim.x) {
-    float out = 0.f;
-    if (lmax != -INFINITY)
-      for (int w = w0; w <= w1; ++w)
-        out += expf(a.lse_parts[(size_t)(bh + w) * a.G + row] - lmax) * inv *
-               a.o_parts[((size_t)(bh + w) * a.G + row) * d + c];
-    if (a.fin_o16) a.fin_o16[(size_t)r * d + c] = __float2half_rn(out);
-    if (a.fin_o32) a.fin_o32[(size_t)r * d + c] = out;
-  }
-  if (threadIdx.x == 0) a.fin_lse[r] = L;
+  const int w0 = U > 0 ? start / C : 0, n = U > 0 ? (start + U - 1) / C - w0 + 1 : 0;
+  const size_t p0 = (size_t)(bh + w0) * a.G + row;
+  combine_row<VEC>(n, a.lse_parts + p0, a.G, a.o_parts + p0 * d, (size_t)a.G * d, d, w, part,
+                   a.fin_o16 ? a.fin_o16 + (size_t)r * d : nullptr, a.fin_o32 ? a.fin_o32 + (size_t)r * d : nullptr,
+                   threadIdx.x == 0 ? a.fin_lse + r : nullptr);
 }
 
-// Log-sum-exp combine over parts in ascending order (R-23).  One thread per
-// (row, channel).
-// One CTA per row, one thread per channel (coalesced part loads); warp 0
-// computes the part weights once per row into shared memory -- lanes own parts
-// for the max, the sum runs in ascending part order by shuffle -- with the
-// arithmetic of the plain version: wsum += e_s, out += (e_s * inv) * o_s.
-__global__ void __launch_bounds__(128) combine_kernel(int n_parts, int rows, int d, const float* __restrict__ o_parts,
-                                                      const float* __restrict__ lse_parts, __half* __restrict__ o16,
-                                                      float* __restrict__ o32, float* __restrict__ lse) {
-  extern __shared__ float w[];  // [n_parts] weights, then [1] lmax flag
-  const int r = blockIdx.x, c = threadIdx.x, lane = c & 31;
-  if (c < 32) {
-    float lmax = -INFINITY;
-    for (int s = lane; s < n_parts; s += 32) lmax = fmaxf(lmax, lse_parts[(size_t)s * rows + r]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
-    float L = -INFINITY;
-    if (lmax != -INFINITY) {
-      float wsum = 0.f;
-      for (int s0 = 0; s0 < n_parts; s0 += 32) {
-        const float e = s0 + lane < n_parts ? expf(lse_parts[(size_t)(s0 + lane) * rows + r] - lmax) : 0.f;
-        const int n = min(32, n_parts - s0);
-        for (int k = 0; k < n; ++k) wsum += __shfl_sync(0xffffffffu, e, k);
-      }
-      const float inv = 1.f / wsum;
-      for (int s = lane; s < n_parts; s += 32) w[s] = expf(lse_parts[(size_t)s * rows + r] - lmax) * inv;
-      L = lmax + logf(wsum);
-    }
-    if (lane == 0) {
-      w[n_parts] = lmax;
-      lse[r] = L;
-    }
-  }
-  __syncthreads();
-  float out = 0.f;
-  if (w[n_parts] != -INFINITY) {
-    const float* op = o_parts + (size_t)r * d + c;
-    const size_t stride = (size_t)rows * d;
-    int s = 0;
-    for (; s + 4 <= n_parts; s += 4) {
-      const float v0 = op[s * stride], v1 = op[(s + 1) * stride], v2 = op[(s + 2) * stride], v3 = op[(s + 3) * stride];
-      out += w[s] * v0;
-      out += w[s + 1] * v1;
-      out += w[s + 2] * v2;
-      out += w[s + 3] * v3;
-    }
-    for (; s < n_parts; ++s) out += w[s] * op[s * stride];
-  }
-  if (o16) o16[(size_t)r * d + c] = __float2half_rn(out);
-  if (o32) o32[(size_t)r * d + c] = out;
+// Equal splits / turbo_combine_lse: one CTA per row r, parts s at
+// lse_parts[s rows + r], o_parts[(s rows + r) d + c].
+template <int VEC>
+__global__ void __launch_bounds__(32 * kCombWarps) combine_kernel(int n_parts, int rows, int d,
+                                                                    const float* __restrict__ o_parts,
+                                                                    const float* __restrict__ lse_parts,
+                                                                    __half* __restrict__ o16, float* __restrict__ o32,
+                                                                    float* __restrict__ lse) {
+  extern __shared__ float w[];  // [n_parts + 1]
+  __shared__ float part[kCombWarps][128];
+  const int r = blockIdx.x;
+  combine_row<VEC>(n_parts, lse_parts + r, rows, o_parts + (size_t)r * d, (size_t)rows * d, d, w, part,
+                   o16 ? o16 + (size_t)r * d : nullptr, o32 ? o32 + (size_t)r * d : nullptr,
+                   threadIdx.x == 0 ? lse + r : nullptr);
 }
 
 static void launch_combine_kernel(int n_parts, int rows, int d, const float* o_parts, const float* lse_parts,
                                   __half* o16, float* o32, float* lse, cudaStream_t st) {
-  combine_kernel<<<rows, d, (n_parts + 1) * sizeof(float), st>>>(n_parts, rows, d, o_parts, lse_parts, o16, o32, lse);
+  const size_t smem = (n_parts + 1) * sizeof(float);
+  const int thr = 32 * comb_warps(n_parts);
+  if (d == 128) combine_kernel<4><<<rows, thr, smem, st>>>(n_parts, rows, d, o_parts, lse_parts, o16, o32, lse);
+  else combine_kernel<2><<<rows, thr, smem, st>>>(n_parts, rows, d, o_parts, lse_parts, o16, o32, lse);
 }
 
 }  // namespace ta
@@ -902,7 +944,11 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || S == 1) return e;
   if (S == 0) {
-    combine_balanced_kernel<<<B * Hq, 128, 0, st>>>(a, W, HD);
+    const size_t smem = (size_t)(W + 2) * sizeof(float);  // a row's pieces: at most W
+    // pieces per row ~ W / (B Hkv) + 1
+    const int thr = 32 * comb_warps(W / (B * H) + 1);
+    if (HD == 128) combine_balanced_kernel<4><<<B * Hq, thr, smem, st>>>(a, W, HD);
+    else combine_balanced_kernel<2><<<B * Hq, thr, smem, st>>>(a, W, HD);
   } else {
     const int rows = B * Hq;
     launch_combine_kernel(S, rows, HD, a.o_parts, a.lse_parts, o, o_part, lse, st);
