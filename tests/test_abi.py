@@ -65,6 +65,7 @@ def test_host_validation_without_gpu(L):
     bad = b.params(head_dim=128, sas_nr=0)
     assert L.turbo_attention_prefill(C.byref(bad), 1, 64, 2, 2, 1, *[None] * 7, None) == b.TURBO_ERR_UNSUPPORTED
     assert L.turbo_combine_lse(0, 1, 1, None, None, None, None, None, None) == b.TURBO_ERR_INVALID_ARG
+    assert L.turbo_combine_lse(12001, 1, 128, 1, 1, 1, None, 1, None) == b.TURBO_ERR_INVALID_ARG
     # chunked prefill: Nk < Nq, and null operands
     dummy = C.c_void_p(16)
     assert L.turbo_attention_prefill_chunk(C.byref(p), 1, 128, 64, 2, 2, 1, *[dummy] * 7,
@@ -75,6 +76,7 @@ def test_host_validation_without_gpu(L):
     assert L.turbo_decode_workspace_bytes(2, 8, 2, 128, 4) == 4 * 2 * 8 * 129 * 4
     assert L.turbo_decode_workspace_bytes(2, 8, 3, 128, 4) == 0  # Hq % Hkv != 0
     assert L.turbo_decode_workspace_bytes(2, 8, 2, 128, -1) == 0
+    assert L.turbo_decode_workspace_bytes(2, 8, 2, 128, 12001) == 0  # n_splits bound (combine weights in smem)
     assert L.turbo_decode_workers(8, 3, 128) == 0
     # quantize_kv / decode with a malformed cache struct
     cache = b.TurboKVCache()
