@@ -279,7 +279,8 @@ def test_decode_exact_set_tap(ta, j_block, n_splits, Hq):
     np.testing.assert_array_equal(tap.pv_int.cpu().numpy()[0], rt["pv_int"])
 
 
-@pytest.mark.parametrize("S,rows,d", [(5, 37, 128), (40, 9, 64), (1, 3, 128)])
+# part counts covering 1-8 warps per row, the 8-parts-in-flight loop and its remainder (S = 300, 101)
+@pytest.mark.parametrize("S,rows,d", [(5, 37, 128), (40, 9, 64), (1, 3, 128), (300, 7, 128), (101, 5, 64)])
 def test_combine_lse_parity(ta, S, rows, d):
     rng = np.random.default_rng(S)
     o_parts = rng.standard_normal((S, rows, d)).astype(np.float32)
