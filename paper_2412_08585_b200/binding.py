@@ -285,9 +285,13 @@ def turbo_attention_decode(p, cache: KVCache, q, blk_begin=0, blk_end=-1, with_b
                            workspace=None, o=None, o_part=None, lse=None, want_fp16=True, want_f32=False,
                            stream=None):
     """q fp16 [B,Hq,d] -> (o fp16 [B,Hq,d] or None, o_part f32 [B,Hq,d] or None, lse f32 [B,Hq]).
-    n_splits >= 1: equal splits; None: auto_splits(); 0: the balanced schedule."""
+    n_splits >= 1: equal splits; 0: the balanced schedule; None: auto_splits() for G <= 4,
+    the balanced schedule for G > 4 (the general-path decode is issue-bound: measured 5-10 %
+    faster than auto_splits' count on B200 for 8 x 32k, 16 x 32k and 64 x 8k at 64 / 8 heads)."""
     assert q.dtype == torch.float16 and q.is_contiguous()
     B, Hq, d = q.shape
+    if n_splits is None and Hq // cache.n_kv_heads > 4:
+        n_splits = 0
     if n_splits is None:
         nb = (cache.n_tokens // cache.block_kv) if blk_end < 0 else blk_end
         n_splits = auto_splits(B, cache.n_kv_heads, max(0, nb - blk_begin),
