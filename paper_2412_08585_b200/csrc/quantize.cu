@@ -96,34 +96,36 @@ TA_DEV uint32_t pack_crumb8(uint2 v) {
 }
 
 template <int HD>
-__global__ void __launch_bounds__(2 * HD, 3 * 128 / HD) quant_prefill_kernel(
+__global__ void __launch_bounds__(HD, 6 * 128 / HD) quant_prefill_kernel(
     const __half* __restrict__ k, const __half* __restrict__ v, int N, int Hkv, int max_blocks, int j0, int Nk,
     const int32_t* __restrict__ bits_dev, uint8_t* __restrict__ block_rec, float* __restrict__ s_parent,
     float* __restrict__ a_univ, int8_t* __restrict__ k1, __half* __restrict__ v1t, float* __restrict__ k1s,
     float* __restrict__ v1s) {
-  constexpr int NW = HD / 32;  // warps per kind
-  // The K and V blocks (FP16 [64][HD] each) are staged with coalesced 16-byte loads;
-  // after every thread has taken its column (the barrier of the max reduction) the
-  // space is reused for K's token-major stage-1 / stage-2 code tiles.
-  __shared__ __align__(16) __half xs[2][kBc][HD];
-  __shared__ float red[2][NW];
-  uint8_t* tile1 = reinterpret_cast<uint8_t*>(&xs[0][0][0]);            // K stage-1 codes [t][c]
-  uint8_t* tile2 = reinterpret_cast<uint8_t*>(&xs[0][0][0]) + kBc * HD;  // K stage-2 codes [t][c]
-  const int j = blockIdx.x, h = blockIdx.y, b = blockIdx.z, tid = threadIdx.x;
-  const int kind = tid / HD, c = tid % HD;
+  constexpr int NW = HD / 32;  // warps
+  // One CTA per (block, kv head, batch, K or V): 6 small CTAs per SM keep more loads in
+  // flight than 3 CTAs doing K and V together.  The block (FP16 [64][HD]) is staged with
+  // coalesced 16-byte loads; after every thread has taken its column (the barrier of the
+  // max reduction) the space is reused for K's token-major stage-1 / stage-2 code tiles.
+  __shared__ __align__(16) __half xs[kBc][HD];
+  __shared__ float red[NW];
+  uint8_t* tile1 = reinterpret_cast<uint8_t*>(&xs[0][0]);            // K stage-1 codes [t][c]
+  uint8_t* tile2 = reinterpret_cast<uint8_t*>(&xs[0][0]) + kBc * HD;  // K stage-2 codes [t][c]
+  const int j = blockIdx.x, h = blockIdx.y, b = blockIdx.z >> 1, kind = blockIdx.z & 1, tid = threadIdx.x;
+  const int c = tid;
   // chunk block j is cache block j0 + j; the stage-1 outputs cover Nk tokens (Tc blocks)
   const int Tc = (Nk + kBc - 1) / kBc;
   const int rows = min(kBc, N - j * kBc);
   const size_t bh = (size_t)b * Hkv + h;
   {
     constexpr int C8 = HD / 8;  // 16-byte chunks per token row
+    const __half* src = kind ? v : k;
 #pragma unroll
-    for (int i = tid; i < 2 * kBc * C8; i += 2 * HD) {
-      const int kd = i / (kBc * C8), t = (i / C8) % kBc, c8 = i % C8;
+    for (int i = tid; i < kBc * C8; i += HD) {
+      const int t = i / C8, c8 = i % C8;
       uint4 val = make_uint4(0, 0, 0, 0);
       if (t < rows)
-        val = __ldcs(reinterpret_cast<const uint4*>((kd ? v : k) + (((size_t)b * N + (size_t)j * kBc + t) * Hkv + h) * HD) + c8);
-      *reinterpret_cast<uint4*>(&xs[kd][t][8 * c8]) = val;
+        val = __ldcs(reinterpret_cast<const uint4*>(src + (((size_t)b * N + (size_t)j * kBc + t) * Hkv + h) * HD) + c8);
+      *reinterpret_cast<uint4*>(&xs[t][8 * c8]) = val;
     }
   }
   __syncthreads();
@@ -132,16 +134,16 @@ __global__ void __launch_bounds__(2 * HD, 3 * 128 / HD) quant_prefill_kernel(
   __half2 amax2 = __float2half2_rn(0.f);
 #pragma unroll
   for (int t = 0; t < kBc; t += 2) {
-    xh[t / 2] = __halves2half2(xs[kind][t][c], xs[kind][t + 1][c]);
+    xh[t / 2] = __halves2half2(xs[t][c], xs[t + 1][c]);
     amax2 = __hmax2(amax2, __habs2(xh[t / 2]));
   }
   float amax = fmaxf(__low2float(amax2), __high2float(amax2));  // exact: max of fp16 magnitudes
   amax = warp_max(amax);
-  if ((tid & 31) == 0) red[kind][c >> 5] = amax;
+  if ((tid & 31) == 0) red[c >> 5] = amax;
   __syncthreads();
-  float a = red[kind][0];
+  float a = red[0];
 #pragma unroll
-  for (int w = 1; w < NW; ++w) a = fmaxf(a, red[kind][w]);
+  for (int w = 1; w < NW; ++w) a = fmaxf(a, red[w]);
   // s = max|x| / 119, codes = round_half_even(x * (119 / max|x|)) (Alg. 1; R-2, R-3, R-5)
   const float inv = a > 0.f ? div_119_by(a) : 0.f;
   const float sc = div_by_119(a);
@@ -228,10 +230,11 @@ __global__ void __launch_bounds__(2 * HD, 3 * 128 / HD) quant_prefill_kernel(
       *reinterpret_cast<uint4*>(rec + 2 * HD + c * (kBc / 4)) = make_uint4(w[0], w[1], w[2], w[3]);
     }
   }
+  if (kind == 1) return;  // V: done (its record words were written per channel)
   __syncthreads();
   // k1 rows (token-major, natural channel order) from tile1
   constexpr int CH16 = kBc * HD / 16;
-  for (int i = tid; i < CH16; i += 2 * HD) {
+  for (int i = tid; i < CH16; i += HD) {
     const int t = i / (HD / 16), c16 = i % (HD / 16);
     if (t < rows)
       *reinterpret_cast<uint4*>(k1 + (bh * Nk + (size_t)(j0 + j) * kBc + t) * HD + c16 * 16) =
@@ -242,7 +245,7 @@ __global__ void __launch_bounds__(2 * HD, 3 * 128 / HD) quant_prefill_kernel(
   const int kbits = bits_dev[h * 2];
   uint8_t* krec = block_rec + ((bh * 2) * (size_t)max_blocks + j0 + j) * REC + 2 * HD;
   if (kbits == 4) {
-    for (int i = tid; i < kBc * HD / 32; i += 2 * HD) {  // 32 channels (16 B of codes) per item
+    for (int i = tid; i < kBc * HD / 32; i += HD) {  // 32 channels (16 B of codes) per item
       const int t = i / (HD / 32), c32 = i % (HD / 32);
       const uint4 lo = *reinterpret_cast<const uint4*>(tile2 + t * HD + c32 * 32);
       const uint4 hi = *reinterpret_cast<const uint4*>(tile2 + t * HD + c32 * 32 + 16);
@@ -251,7 +254,7 @@ __global__ void __launch_bounds__(2 * HD, 3 * 128 / HD) quant_prefill_kernel(
                      pack_nib8(make_uint2(hi.x, hi.y)), pack_nib8(make_uint2(hi.z, hi.w)));
     }
   } else {
-    for (int i = tid; i < kBc * HD / 64; i += 2 * HD) {  // 64 channels (16 B of codes) per item
+    for (int i = tid; i < kBc * HD / 64; i += HD) {  // 64 channels (16 B of codes) per item
       const int t = i / (HD / 64), c64 = i % (HD / 64);
       uint32_t w[4];
 #pragma unroll
@@ -413,13 +416,13 @@ cudaError_t launch_quant_prefill(const turbo_kv_cache_t* c, const __half* k, con
     e = cudaMemsetAsync(c->buf, 0, (size_t)B * H * 2 * kBc * HD, st);
     if (e != cudaSuccess) return e;
   }
-  dim3 grid(Tc, H, B);
+  dim3 grid(Tc, H, 2 * B);  // z = 2 b + (K, V)
   if (HD == 128) {
-    quant_prefill_kernel<128><<<grid, 256, 0, st>>>(k, v, N, H, c->max_blocks, j0, Nk, c->bits_dev, c->block_rec,
+    quant_prefill_kernel<128><<<grid, 128, 0, st>>>(k, v, N, H, c->max_blocks, j0, Nk, c->bits_dev, c->block_rec,
                                                     c->s_parent, c->a_univ, k1, v1t, k1s, v1s);
     quant_tail_kernel<128><<<dim3(H, B), 256, 0, st>>>(k, v, N, H, c->a_univ, c->buf, c->counters, j0);
   } else {
-    quant_prefill_kernel<64><<<grid, 128, 0, st>>>(k, v, N, H, c->max_blocks, j0, Nk, c->bits_dev, c->block_rec,
+    quant_prefill_kernel<64><<<grid, 64, 0, st>>>(k, v, N, H, c->max_blocks, j0, Nk, c->bits_dev, c->block_rec,
                                                    c->s_parent, c->a_univ, k1, v1t, k1s, v1s);
     quant_tail_kernel<64><<<dim3(H, B), 256, 0, st>>>(k, v, N, H, c->a_univ, c->buf, c->counters, j0);
   }
