@@ -158,6 +158,11 @@ DEC_CASES = [  # (B, N_prefill, n_append, Hq, Hkv, d, n_splits, alpha_mode)
     (2, 64 * 6 + 17, 3, 16, 2, 128, 2, 0),
     (1, 64 * 9 + 5, 0, 8, 1, 128, 0, 1),
     (1, 300, 2, 8, 1, 64, 1, 0),
+    # odd / small groups on the packed path (rows >= G absent): G = 3 split, G = 2 balanced at d = 64
+    (1, 64 * 5 + 9, 5, 6, 2, 128, 2, 0),
+    (2, 64 * 20 + 5, 3, 4, 2, 64, 0, 0),
+    # G = 6 (general path) through n_splits=None, which selects the balanced schedule for G > 4
+    (1, 64 * 7 + 3, 2, 6, 1, 128, None, 0),
 ]
 
 
@@ -221,6 +226,9 @@ def test_append_and_decode_parity(ta, case):
     torch.cuda.synchronize()
     o, lse = o.cpu().numpy(), lse.cpu().numpy()
     nb = ref["slots"][0][0][0].n_blocks
+    if S is None:  # the binding's default: balanced for G > 4
+        assert G > 4
+        S = 0
     if S > 0:
         per = -(-nb // S)
         bounds = [(min(s * per, nb), min(s * per + per, nb)) for s in range(S)]
