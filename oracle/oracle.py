@@ -29,7 +29,12 @@ CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11", "-fPIC", "-s
 
 
 def build(force: bool = False) -> str:
-    """Compile the oracle with gcc (scalar, no fast-math, no FMA contraction)."""
+    """Compile the oracle with gcc (scalar, no fast-math, no FMA contraction).
+
+    ``TURBO_ORACLE_LIB`` names a prebuilt library instead (used only by
+    tests/test_oracle_mutations.py to load deliberately broken oracles)."""
+    if os.environ.get("TURBO_ORACLE_LIB"):
+        return os.environ["TURBO_ORACLE_LIB"]
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
         os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "turbo_oracle.h"))
     ):
