@@ -59,6 +59,9 @@ typedef struct {
   int32_t alpha_mode;    /* 0: alpha = SAS(m_prev - m_new) literally (Alg. 1, R-15);
                             1: alpha = 1 when the running max is unchanged */
   float softmax_scale;   /* 1/sqrt(d_H) (Eq. 1; R-18) */
+  int32_t p_scale_rows;  /* prefill P-scale granularity: 0 = per B_r x B_c tile (Alg. 1, default);
+                            1 = per query row x B_c block, as Alg. 2 does -- NEXT-2 variant,
+                            oracle flag p_row.  The decode is always per row. */
   void* debug_tap;       /* NULL, or a turbo_debug_tap_t* (see below) */
 } turbo_params_t;
 

@@ -340,6 +340,7 @@ static int32_t prefill_core(const tq_params* p, int32_t nq, int32_t nk, int32_t 
   double* alpha = (double*)malloc(sizeof(double) * br);
   float* m = (float*)malloc(sizeof(float) * br);
   uint8_t* active = (uint8_t*)malloc((size_t)br);
+  float* sp_row = (float*)malloc(sizeof(float) * br);
 
   for (int32_t i = i_begin; i < i_end; ++i) {    /* for 1 <= i <= T_r */
     const int32_t r0 = i * br, nr = (r0 + br <= n) ? br : n - r0;
@@ -384,7 +385,14 @@ static int32_t prefill_core(const tq_params* p, int32_t nq, int32_t nk, int32_t 
       if (p->quant) {
         for (int32_t r = 0; r < nr; ++r)        /* compact the tile to width nc */
           for (int32_t c = 0; c < nc; ++c) pt[(int64_t)r * nc + c] = pt[(int64_t)r * bc + c];
-        sp = quant_p((int64_t)nr * nc, pt, active, nc, pc);
+        if (p->p_row) {                         /* per row x B_c block (P:976-977 granularity) */
+          for (int32_t r = 0; r < nr; ++r)
+            sp_row[r] = quant_p(nc, pt + (int64_t)r * nc, active + r, nc, pc + (int64_t)r * nc);
+          sp = sp_row[0];
+        } else {                                /* per B_r x B_c tile */
+          sp = quant_p((int64_t)nr * nc, pt, active, nc, pc);
+          for (int32_t r = 0; r < nr; ++r) sp_row[r] = sp;
+        }
         for (int32_t r = 0; r < nr; ++r)
           for (int32_t e = 0; e < d; ++e) {
             int32_t acc = 0;
@@ -392,9 +400,9 @@ static int32_t prefill_core(const tq_params* p, int32_t nq, int32_t nk, int32_t 
               acc += (int32_t)pc[(int64_t)r * nc + c] * (int32_t)v1[(int64_t)(c0 + c) * d + e];
             pv[(int64_t)r * d + e] = acc;
           }
-        const float cpv = sp * sv[j];
         for (int32_t r = 0; r < nr; ++r) {
           if (!active[r]) continue;
+          const float cpv = sp_row[r] * sv[j];
           for (int32_t e = 0; e < d; ++e) {
             double* oe = &O[(int64_t)r * d + e];
             *oe = alpha[r] * (*oe) + (double)(cpv * (float)pv[(int64_t)r * d + e]);
@@ -436,7 +444,7 @@ static int32_t prefill_core(const tq_params* p, int32_t nq, int32_t nk, int32_t 
     }
   }
   free(q1); free(x); free(sint); free(pt); free(pc);
-  free(pv); free(O); free(l); free(alpha); free(m); free(active);
+  free(pv); free(O); free(l); free(alpha); free(m); free(active); free(sp_row);
   return 0;
 }
 

@@ -31,6 +31,8 @@ typedef struct {
   float softmax_scale;   /* 1/sqrt(d_H) (Eq. 1; R-18) */
   int32_t quant;         /* 1: FlashQ quantization as in Alg. 1/2; 0: exact-mode switch (pin P5) */
   int32_t sas;           /* 1: SAS exponent; 0: exact exp (pin P5) */
+  int32_t p_row;         /* prefill P scale: 0 per B_r x B_c tile (Alg. 1); 1 per row x B_c block,
+                            the granularity Alg. 2 uses -- NEXT-2 variant */
 } tq_params;
 
 /* One cache "slot" = one (batch, kv_head, K-or-V) stream.  Logical layout

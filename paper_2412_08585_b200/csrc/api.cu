@@ -49,6 +49,7 @@ turbo_status_t check_params(const turbo_params_t* p) {
   if (p->sas_nr < -30 || p->sas_nr > -1) return TURBO_ERR_UNSUPPORTED;
   if (p->alpha_mode != 0 && p->alpha_mode != 1) return TURBO_ERR_INVALID_ARG;
   if (!(p->softmax_scale > 0.0f) || !std::isfinite(p->softmax_scale)) return TURBO_ERR_INVALID_ARG;
+  if (p->p_scale_rows != 0 && p->p_scale_rows != 1) return TURBO_ERR_INVALID_ARG;
   return TURBO_OK;
 }
 

@@ -184,3 +184,33 @@ def test_rounding_ties_half_even_and_half_up(oracle):
     assert c2.tolist() == [0, 1, 3, 3]
     c4, s4, z4 = oracle.quant_asym(np.array([-30, -29, 0], np.int8), 4)  # s = ceil(30/15) = 2
     assert (s4, z4) == (2, -30) and c4.tolist() == [0, 1, 15]
+
+
+@pytest.mark.parametrize("alpha_mode", [0, 1])
+def test_prefill_row_p_scale_equals_decode(oracle, alpha_mode):
+    """NEXT-2 variant p_row (P scale per row x B_c block, the granularity of Alg. 2,
+    P:976-977): with every query row of the B_r block holding the block's max |q| (so
+    the block's s_Q and codes are each row's own) and a lossless cache, non-causal Alg. 1
+    with p_row = 1 gives every row exactly the decode of that row; with the paper's
+    per-tile scale it does not."""
+    d, n, nq = 128, 4 * BC + 9, 64
+    rng = np.random.default_rng(11 + alpha_mode)
+    k = lossless_stream(rng, n, d, 4)
+    v = lossless_stream(rng, n, d, 2)
+    q = (rng.standard_normal((nq, d)) * 0.5).clip(-1.9, 1.9)
+    for r in range(nq):
+        q[r, (5 * r) % d] = 2.0 if r % 2 else -2.0  # the same max |q| in every row
+    q = q.astype(np.float16).astype(np.float32)
+    rows_equal = {}
+    for p_row in (1, 0):
+        p = oracle.params(d=d, alpha_mode=alpha_mode, p_row=p_row)
+        ks, vs, k1, sk, v1, sv = _cache(oracle, p, k, v, 4, 2)
+        o, l = oracle.prefill_chunk_head(p, q, k1, sk, v1, sv, causal=False)
+        rows_equal[p_row] = 0
+        for r in range(nq):
+            od, ld = oracle.decode_head(p, q[r], ks, vs)
+            if p_row:
+                np.testing.assert_array_equal(o[r], od)
+                assert l[r] == ld
+            rows_equal[p_row] += int(np.array_equal(o[r], od))
+    assert rows_equal[0] < nq // 2

@@ -12,7 +12,8 @@ from paper_2412_08585_b200 import synth  # noqa: E402
 B, N, Hq, Hkv, d = (1, 32768, 64, 8, 128) if os.environ.get("TP_CFG") == "70b" else (8, 4096, 32, 8, 128)
 if os.environ.get("TP_SHAPE"):  # "B,N,Hq,Hkv,d" (e.g. MHA: 8,4096,32,32,128)
     B, N, Hq, Hkv, d = (int(x) for x in os.environ["TP_SHAPE"].split(","))
-p = ta.params(head_dim=d)
+p = ta.params(head_dim=d, p_scale_rows=int(os.environ.get("TP_PROW", "0")),
+              alpha_mode=int(os.environ.get("TP_ALPHA", "0")), block_q=int(os.environ.get("TP_BQ", "64")))
 q, k, v = synth.qkv_torch(1002, B, N, Hq, Hkv, d)
 cache = ta.KVCache(B, Hkv, d, max_blocks=N // 64 + 2, bits=synth.head_bits_alternating(Hkv))
 k1, v1t, k1s, v1s = ta.turbo_quantize_kv(p, cache, k, v)
