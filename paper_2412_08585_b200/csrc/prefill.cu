@@ -19,7 +19,7 @@
 //
 // Scaled output accumulator (tolerance set, R-16): O_true = O^ / R per row, with
 // R_j = R_{j-1} / alpha_j, so tile j's alpha never touches O^ (P:921 rescale folded
-// into R).  F = s_P s_V R is kept in [2^-8, 2^5] by exact power-of-two rescales of
+// into R).  F = s_P s_V R is kept in [2^-14, 60] by exact power-of-two rescales of
 // the row of O^ (rare); alpha = 0 restarts the row.  P' = Pc F with F = F_hi + F_lo,
 // F_hi = F rounded to 4 significant bits, so Pc F_hi (<= 11 bits) is exact in fp16
 // and only Pc F_lo is rounded: P' carries a relative error <= 2^-15 (the running O
@@ -71,6 +71,14 @@ TA_DEV uint32_t q1_swz(int r, int chunk) {
   return r * 64 + ((chunk ^ ((r >> 1) & 3)) << 4);
 }
 
+// Window of F = s_P s_V R outside which the row of O^ is rescaled by a power of two.
+// Upper: fp16(-1024 F_hi) must be finite (F_hi <= 63.97) for the P' hi/lo split.
+// Lower: F_hi must be a normal fp16 (>= 2^-14) so that P c F_hi stays exact; below
+// 2^-9 the lo part is subnormal, an absolute error <= 2^-25 per P' element against
+// a row whose largest tile has F >= 1 (the first visible tile sets F in [1, 2)).
+constexpr float kFmax = 60.f;
+constexpr float kFmin = 0.00006103515625f;  // 2^-14
+
 // F = 2^e m, m in [1, 2): 2^-e (exact power of two; F normal and positive)
 TA_DEV float inv_pow2_of(float F) { return __uint_as_float((uint32_t)(254 - (__float_as_uint(F) >> 23)) << 23); }
 
@@ -114,7 +122,7 @@ __global__ void __launch_bounds__(384, 1)
     for (int t = 0; t < 2; ++t) {
       for (int s = 0; s < 2; ++s) {
         mbar_init(&sm.s_full[t][s], 1);
-        mbar_init(&sm.p_full[t][s], 128);
+        mbar_init(&sm.p_full[t][s], 4);  // one arrival per softmax warp
       }
       mbar_init(&sm.pv_done[t], 1);
     }
@@ -221,7 +229,7 @@ __global__ void __launch_bounds__(384, 1)
           qa = fmaxf(qa, fmaxf(fabsf(f.x), fabsf(f.y)));
         }
       }
-      qa = warp_max(qa);
+      qa = warp_max_nonneg(qa);
       if (lane == 0) sm.red_a[slot][qd] = qa;
       named_bar_sync(bar_slot, 128);
       const float a_q = args.block_q == 64 ? fmaxf(sm.red_a[slot][2 * half], sm.red_a[slot][2 * half + 1])
@@ -272,16 +280,20 @@ __global__ void __launch_bounds__(384, 1)
       // x = S s_Q s_K / sqrt(d) (R-18); masked keys -> -inf
       const float cqk = __fmul_rn(__fmul_rn(s_q, args.k1s[bkv * Tc + j]), args.scale);
       const float s_v = args.v1s[bkv * Tc + j];
-      float mt = -INFINITY;
+      float mt = -INFINITY, mt1 = -INFINITY;
       {
         const f32x2 cq2 = pk2(cqk, cqk);
         if (full) {
 #pragma unroll
-          for (int c = 0; c < kBc; c += 2) {
+          for (int c = 0; c < kBc; c += 4) {  // two independent max chains
             const f32x2 x2 = mul2(pk2((float)(int)v[c], (float)(int)v[c + 1]), cq2);
+            const f32x2 y2 = mul2(pk2((float)(int)v[c + 2], (float)(int)v[c + 3]), cq2);
             mt = fmaxf(mt, fmaxf(lo2(x2), hi2(x2)));
+            mt1 = fmaxf(mt1, fmaxf(lo2(y2), hi2(y2)));
             v[c] = __float_as_uint(lo2(x2));
             v[c + 1] = __float_as_uint(hi2(x2));
+            v[c + 2] = __float_as_uint(lo2(y2));
+            v[c + 3] = __float_as_uint(hi2(y2));
           }
         } else {
 #pragma unroll
@@ -294,6 +306,7 @@ __global__ void __launch_bounds__(384, 1)
             v[c + 1] = __float_as_uint(x1);
           }
         }
+        mt = fmaxf(mt, mt1);
       }
       // m_new, alpha = SAS(m_prev - m_new) (R-15)
       const float m_new = fmaxf(m, mt);
@@ -303,8 +316,9 @@ __global__ void __launch_bounds__(384, 1)
       const float m_use = active ? m_new : 0.f;  // inactive row: every x = -inf -> P~ = 0
       // P~ = SAS(x - m_new) in registers; two elements per FADD2 / FFMA2 / FMUL2,
       // bit-identical to the scalar sas_eval.
-      float pmax = 0.f;
-      f32x2 rsum2 = pk2(0.f, 0.f);
+      float pmax = 0.f, pmax1 = 0.f;
+      f32x2 rsum2;
+      f32x2 rs[4] = {pk2(0.f, 0.f), pk2(0.f, 0.f), pk2(0.f, 0.f), pk2(0.f, 0.f)};  // 4 row-sum chains
       {
         const f32x2 m2 = pk2(m_use, m_use), mg2 = pk2(kMagic, kMagic);
         const f32x2 c3 = pk2(-0.1025f, -0.1025f), c2 = pk2(0.4626f, 0.4626f), c1 = pk2(-0.9922f, -0.9922f),
@@ -320,11 +334,14 @@ __global__ void __launch_bounds__(384, 1)
           const f32x2 lp = mul2(pk2(l0, l1), p2);
           const float pt0 = lo2(d2) > nr_abs ? 0.f : lo2(lp);
           const float pt1 = hi2(d2) > nr_abs ? 0.f : hi2(lp);
-          rsum2 = add2(rsum2, pk2(pt0, pt1));
-          pmax = fmaxf(pmax, fmaxf(pt0, pt1));
+          rs[(c >> 1) & 3] = add2(rs[(c >> 1) & 3], pk2(pt0, pt1));
+          if (c & 2) pmax1 = fmaxf(pmax1, fmaxf(pt0, pt1));  // two independent max chains
+          else pmax = fmaxf(pmax, fmaxf(pt0, pt1));
           v[c] = __float_as_uint(pt0);
           v[c + 1] = __float_as_uint(pt1);
         }
+        rsum2 = add2(add2(rs[0], rs[1]), add2(rs[2], rs[3]));
+        pmax = fmaxf(pmax, pmax1);
       }
       const float m_prev = m;
       if (active) {
@@ -334,7 +351,7 @@ __global__ void __launch_bounds__(384, 1)
       // P scale: max P~ over the B_r x B_c tile (or, PROW, over the row)
       float a_p = pmax;
       if (!PROW) {
-        const float wmax = warp_max(pmax);
+        const float wmax = warp_max_nonneg(pmax);
         if (lane == 0) sm.red_p[slot][sb][qd] = wmax;
         named_bar_sync(bar_grp, grp_threads);
         a_p = args.block_q == 64 ? fmaxf(sm.red_p[slot][sb][2 * half], sm.red_p[slot][sb][2 * half + 1])
@@ -356,7 +373,7 @@ __global__ void __launch_bounds__(384, 1)
         const float sps = __fmul_rn(s_p, s_v);
         if (R == 0.f && sps > 0.f) R = inv_pow2_of(sps);  // first contribution: F in [1, 2)
         F = __fmul_rn(sps, R);
-        if (F > 32.f || (F > 0.f && F < 0.00390625f)) {
+        if (F > kFmax || (F > 0.f && F < kFmin)) {
           const float f = inv_pow2_of(F);
           R *= f;
           F *= f;
@@ -423,7 +440,8 @@ __global__ void __launch_bounds__(384, 1)
       }
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&sm.p_full[slot][sb]);
+      __syncwarp();  // every lane's P' stores precede the warp's single arrival
+      if (lane == 0) mbar_arrive(&sm.p_full[slot][sb]);
       if (TAP && tap_row && j == tap_j) {
         args.tap.m_new[r & 63] = m;
         if ((r & 63) == 0) args.tap.s_p[0] = s_p;

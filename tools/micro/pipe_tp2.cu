@@ -60,6 +60,22 @@ __global__ void __launch_bounds__(1024, 1) kern(int iters, float seed, unsigned 
         asm volatile("fma.rn.f16x2 %0, %0, %1, %2;" : "+r"(u[k]) : "r"(h2c), "r"(h2d));
       }
       if (OP == 12) asm volatile("max.f32 %0, %0, %1, %2;" : "+f"(a[k]) : "f"(a[(k + 1) & 7]), "f"(seed));
+      if (OP == 14) p[k] = fma2(p[k], pk2(1.0001f, 1.0001f), pk2(1e-7f, 1e-7f));  // FFMA2 imm b, c
+      if (OP == 15) p[k] = fma2(p[k], p[(k + 1) & 7], p[(k + 2) & 7]);           // FFMA2 3-reg
+      if (OP == 16) p[k] = add2(p[k], pk2(1e-7f, 1e-7f));                       // FADD2 imm
+      if (OP == 17) p[k] = add2(p[k], p[(k + 1) & 7]);                          // FADD2 reg pair
+      if (OP == 18) p[k] = mul2(p[k], pk2(seed, seed));                          // FMUL2 scalar-reg broadcast
+      if (OP == 19) a[k] = fmaf(a[k], 1.0001f, 1e-7f);                           // FFMA imm
+      if (OP == 20) a[k] = fmaf(a[k], a[(k + 1) & 7], a[(k + 2) & 7]);           // FFMA 3-reg
+      if (OP == 21) p[k] = fma2(p[k], pk2(seed, seed), pk2(1e-7f, 1e-7f));       // FFMA2 scalar b, imm c
+      if (OP == 22) asm volatile("cvt.rn.f32.s32 %0, %1;" : "=f"(a[k]) : "r"(u[k]));  // I2F alone (no dep)
+      if (OP == 23) {                                                          // FADD2 imm + I2F
+        p[k] = add2(p[k], pk2(1e-7f, 1e-7f));
+        asm volatile("cvt.rn.f32.s32 %0, %1;" : "=f"(a[k]) : "r"(u[k] ^ k));
+      }
+      if (OP == 24) {  // REDUX max
+        u[k] = __reduce_max_sync(0xffffffffu, u[k] + k);
+      }
       if (OP == 13) {
         asm volatile("{\n\t.reg .pred q;\n\tsetp.gt.f32 q, %1, 0f3F000000;\n\tselp.f32 %0, %1, %2, q;\n\t}"
                      : "=f"(a[k])
@@ -112,6 +128,17 @@ int main() {
     run<11>("FFMA2+HFMA2", w, 2);
     run<12>("FMNMX3", w, 1);
     run<13>("FSETP+SEL+FFMA2", w, 3);
+    run<14>("FFMA2 imm", w, 1);
+    run<15>("FFMA2 3reg", w, 1);
+    run<16>("FADD2 imm", w, 1);
+    run<17>("FADD2 reg", w, 1);
+    run<18>("FMUL2 bcast", w, 1);
+    run<19>("FFMA imm", w, 1);
+    run<20>("FFMA 3reg", w, 1);
+    run<21>("FFMA2 bc+imm", w, 1);
+    run<22>("I2F", w, 1);
+    run<23>("FADD2imm+I2F", w, 2);
+    run<24>("REDUX.MAX", w, 1);
   }
   return 0;
 }
