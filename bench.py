@@ -150,14 +150,23 @@ def run_ours(args, rank, world, device):
     bind_host_to_gpu(device)
     c = CFG_PREFILL
     B, N, Hq, Hkv, d = c["B"], c["N"], c["Hq"], c["Hkv"], c["d"]
-    bits = synth.head_bits_alternating(Hkv)
     p = ta.params(head_dim=d, block_q=64, alpha_mode=0)
     q, k, v = synth.qkv_torch(1002 + 7919 * rank, B, N, Hq, Hkv, d, device=device)
+    # NEXT-1 (Sec. 3.2): the headwise 2/4-bit plan of this layer from the on-device
+    # head-priority planner over the prefill K/V (a per-layer calibration, outside the timed step);
+    # half of the 2 Hkv (kv head, K/V) slots at 2 bits
+    e_pl0, e_pl1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_pl0.record()
+    prio = ta.turbo_head_priority(k, v)
+    e_pl1.record()
+    bits = ta.turbo_plan_bits(prio, Hkv).numpy()
+    planner = {"priority_kernel_ms": round(e_pl0.elapsed_time(e_pl1), 4), "n_2bit_slots": Hkv,
+               "bits_kv": bits.tolist()}
     qd, kd, vd = (x[:, 0].contiguous() for x in synth.qkv_torch(4002 + rank, B, 1, Hq, Hkv, d, device=device))
     cache = ta.KVCache(B, Hkv, d, max_blocks=N // 64 + 2, bits=bits, device=device)
     S = args.splits
-    if S is None:
-        S = ta.auto_splits(B, Hkv, N // 64, ta.turbo_decode_workers(Hq, Hkv, d))
+    if S is None:  # the binding's deterministic default (device-independent partition)
+        S = ta.auto_splits(B, Hkv, N // 64, ta.reference_workers(Hq, Hkv, d))
     ws = torch.empty(max(ta.turbo_decode_workspace_bytes(B, Hq, Hkv, d, S), 16), dtype=torch.uint8, device=device)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=device)  # > 126 MB L2
     st = torch.cuda.current_stream()
@@ -335,7 +344,39 @@ def run_ours(args, rank, world, device):
     q_bytes = 2 * B * N * Hkv * d * 2 + B * N * Hkv * d + B * N * Hkv * d * 2 + rec_b + 2 * B * Hkv * (N // 64) * 8
     quant = {"ms": round(q_ms, 4), "bytes": q_bytes, "gbs": round(q_bytes / (q_ms * 1e-3) / 1e9, 1),
              "frac_hbm": round(q_bytes / (q_ms * 1e-3) / 1e9 / pk["hbm"], 4)}
+    # ---- deviation from exact attention (Eq. 2), reported separately (north_star):
+    # sampled (b, q head) units and query rows of configs[1], both alpha modes (after the timed region)
+    deviation = None
+    if rank == 0 and not args.no_deviation:
+        o0 = step(q, k, v, qd, kd, vd)[0]
+        p1 = ta.params(head_dim=d, block_q=64, alpha_mode=1)
+        k1_, v1t_, k1s_, v1s_ = ta.turbo_quantize_kv(p1, cache, k, v)
+        o1, _ = ta.turbo_attention_prefill(p1, q, k1_, v1t_, k1s_, v1s_, causal=True)
+        units = [(0, 0), (1, 5), (3, 13), (5, 22), (7, 31)]
+        rows = sorted(set(range(7, N, 29)) | {N - 1})
+        deviation = {"prefill_configs1": dict(
+            units=f"(b, q head) {units}, {len(rows)} query rows each (every 29th + the last)",
+            **deviation_prefill(p, q, k, v, {0: o0, 1: o1}, units, rows))}
+        # NEXT-2 variant: prefill P scale per row x B_c block (Alg. 2's granularity) instead of
+        # per B_r x B_c tile (Alg. 1): kernel speed and deviation on the same units
+        pr = ta.params(head_dim=d, block_q=64, alpha_mode=0, p_scale_rows=1)
+        k1_, v1t_, k1s_, v1s_ = ta.turbo_quantize_kv(pr, cache, k, v)
+        orow, lrow = ta.turbo_attention_prefill(pr, q, k1_, v1t_, k1s_, v1s_, causal=True)
+        g0, g1 = ev(), ev()
+        g0.record(st)
+        for _ in range(10):
+            ta.turbo_attention_prefill(pr, q, k1_, v1t_, k1s_, v1s_, causal=True, o=orow, lse=lrow)
+        g1.record(st)
+        torch.cuda.synchronize()
+        row_ms = g0.elapsed_time(g1) / 10
+        variants = {"prefill_p_scale_per_row": {
+            "kernel_ms": round(row_ms, 4), "tops": round(ops / (row_ms * 1e-3) / 1e12, 1),
+            "deviation_alpha_mode_0": deviation_prefill(pr, q, k, v, {0: orow}, units, rows)["alpha_mode_0"]}}
+        deviation["variants"] = variants
+        del o0, o1, orow, lrow, k1_, v1t_, k1s_, v1s_
     result = dict(value=value, ms_step=ms_step, e2e=e2e, roofline=roof, clocks=clocks, quantize_kv=quant,
+                  deviation=deviation,
+                  planner=planner,
                   launches=launches_per_step * args.steps,
                   breakdown_ms={"quantize_kv_prefill": round(statistics.mean(t_quant), 4),
                                 "attention_prefill": round(pre_ms, 4),
@@ -370,11 +411,15 @@ def bench_decode(args, rank, world, device, pk):
     cache = ta.KVCache(B, Hkv, d, max_blocks=N // 64 + 4, bits=bits, device=device)
     _, k, v = synth.qkv_torch(3003 + rank, B, N, Hkv, Hkv, d, device=device)
     ta.turbo_quantize_kv(p, cache, k, v)  # builds the 32k-token compressed cache
+    dev_units = [(0, 0), (13, 7), (40, 22), (63, 39)]  # (b, q head) sampled for the deviation report
+    G = Hq // Hkv
+    host_kv = {(b, h // G): (k[b, :, h // G].float().cpu().numpy(), v[b, :, h // G].float().cpu().numpy())
+               for b, h in dev_units}
     del k, v
     torch.cuda.empty_cache()
     S = args.decode_splits
-    if S is None:
-        S = ta.auto_splits(B, Hkv, cache.n_tokens // 64, ta.turbo_decode_workers(Hq, Hkv, d))
+    if S is None:  # the binding's deterministic default (device-independent partition)
+        S = ta.resolve_splits(None, B, Hq, cache)
     ws = torch.empty(max(ta.turbo_decode_workspace_bytes(B, Hq, Hkv, d, S), 16), dtype=torch.uint8, device=device)
     toks = [tuple(x[:, 0].contiguous() for x in synth.qkv_torch(6000 + i, B, 1, Hq, Hkv, d, device=device))
             for i in range(args.warmup + args.steps)]
@@ -394,13 +439,43 @@ def bench_decode(args, rank, world, device, pk):
         ta.turbo_attention_decode(p, cache, qd, n_splits=S, workspace=ws)
         evs[i][2].record(st)
     torch.cuda.synchronize()
+    deviation = None
+    if rank == 0 and not args.no_deviation:
+        import numpy as np
+
+        qd = synth.qkv_torch(6999, B, 1, Hq, Hkv, d, device=device)[0][:, 0].contiguous()
+        outs = {}
+        for mode in (0, 1):
+            pm = ta.params(head_dim=d, alpha_mode=mode)
+            outs[(mode, S)] = ta.turbo_attention_decode(pm, cache, qd, n_splits=S)[0].float().cpu().numpy()
+            outs[(mode, 1)] = ta.turbo_attention_decode(pm, cache, qd, n_splits=1)[0].float().cpu().numpy()
+        qh = qd.float().cpu().numpy()
+        refs, vr = [], []
+        for b, h in dev_units:
+            kk, vv = host_kv[(b, h // G)]
+            ka = np.concatenate([kk] + [toks[i][1][b, h // G].float().cpu().numpy()[None] for i in range(len(toks))])
+            va = np.concatenate([vv] + [toks[i][2][b, h // G].float().cpu().numpy()[None] for i in range(len(toks))])
+            refs.append(exact_attention(qh[b, h][None], ka, va, 1.0 / math.sqrt(d))[0])
+            vr.append(va)
+        v_rms = float(np.sqrt(np.mean(np.concatenate(vr) ** 2)))
+        ref = np.stack(refs)
+        pick = lambda o: np.stack([o[b, h] for b, h in dev_units])  # noqa: E731
+        deviation = {"units": f"(b, q head) {dev_units}, one query after {cache.n_tokens} tokens; "
+                              f"(K, V) bits {[tuple(int(x) for x in bits[h // G]) for _, h in dev_units]}",
+                     "default_splits": S}
+        for mode in (0, 1):
+            deviation[f"alpha_mode_{mode}"] = {
+                "unsplit_vs_exact": dev_stats(pick(outs[(mode, 1)]), ref, v_rms),
+                "split_vs_exact": dev_stats(pick(outs[(mode, S)]), ref, v_rms),
+                "split_vs_unsplit_rel_l2": dev_stats(outs[(mode, S)], outs[(mode, 1)], 1.0)["rel_l2"]}
     t_dec = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
     t_step = statistics.mean(e[0].elapsed_time(e[2]) for e in evs)
     ntok = cache.n_tokens
     nblk, nbuf = ntok // 64, ntok % 64
     byt = decode_bytes(B, Hkv, d, nblk, nbuf, bits, Hq)
     gbs = byt / (t_dec * 1e-3) / 1e9
-    return {"config": "Phi-3-medium attention (40 Q / 10 KV heads, d=128), batch 64, 32k context, mixed INT4/INT2",
+    return {"deviation": deviation,
+            "config": "Phi-3-medium attention (40 Q / 10 KV heads, d=128), batch 64, 32k context, mixed INT4/INT2",
             "n_splits": S, "kv_bytes_per_step": byt, "decode_kernel_ms": round(t_dec, 4),
             "step_ms_append_plus_decode": round(t_step, 4), "kv_gbs": round(gbs, 1),
             "tokens_per_s": round(world * B / (t_step * 1e-3), 1),
@@ -408,6 +483,88 @@ def bench_decode(args, rank, world, device, pk):
             "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": pk["hbm"], "unit": "GB/s",
                          "traffic": traffic_per_launch("decode_kernel"),
                          "frac": round(gbs / pk["hbm"], 4), "peak_source": pk["src"]}}
+
+
+# --------------------------------------------------------------------------- deviation from exact attention
+def exact_attention(q, k, v, scale, q_pos=None):
+    """Eq. 2 in FP64: softmax(q k^T scale) v for query rows q [n, d] at absolute
+    positions q_pos (causal: keys 0..q_pos; None: all keys visible).  The plain definition, no
+    quantisation, no SAS -- the reference the method's deviation is reported against."""
+    import numpy as np
+
+    q, k, v = (np.asarray(x, np.float64) for x in (q, k, v))
+    s = (q @ k.T) * scale
+    if q_pos is not None:
+        s = np.where(np.arange(k.shape[0])[None, :] <= np.asarray(q_pos)[:, None], s, -np.inf)
+    s -= s.max(axis=1, keepdims=True)
+    w = np.exp(s)
+    return (w / w.sum(axis=1, keepdims=True)) @ v
+
+
+def dev_stats(o, ref, v_rms):
+    import numpy as np
+
+    o, ref = np.asarray(o, np.float64), np.asarray(ref, np.float64)
+    return {"rel_l2": float(np.linalg.norm(o - ref) / np.linalg.norm(ref)),
+            "max_abs": float(np.abs(o - ref).max()), "max_abs_over_rms_v": float(np.abs(o - ref).max() / v_rms),
+            "rms_err_over_rms_v": float(np.sqrt(np.mean((o - ref) ** 2)) / v_rms)}
+
+
+def deviation_prefill(p_mode, q, k, v, o_by_mode, units, rows):
+    """configs[1] prefill: the GPU output of sampled (b, q head) units and query rows against Eq. 2,
+    per alpha mode (R-15)."""
+    import numpy as np
+
+    G = q.shape[2] // k.shape[2]
+    d = q.shape[3]
+    out = {}
+    for mode, o in o_by_mode.items():
+        os_, rs, vr = [], [], []
+        for b, h in units:
+            qh = q[b, :, h].float().cpu().numpy()
+            kh, vh = k[b, :, h // G].float().cpu().numpy(), v[b, :, h // G].float().cpu().numpy()
+            ref = exact_attention(qh[rows], kh, vh, 1.0 / math.sqrt(d), rows)
+            os_.append(o[b, rows, h].float().cpu().numpy())
+            rs.append(ref)
+            vr.append(vh)
+        out[f"alpha_mode_{mode}"] = dev_stats(np.concatenate(os_), np.concatenate(rs),
+                                              float(np.sqrt(np.mean(np.concatenate(vr) ** 2))))
+    return out
+
+
+def trend_v_probe(device):
+    """PAPER.md:921 rescale read literally (alpha_mode 0, R-15) multiplies the history by
+    SAS(0) = 0.9996 per tile: a positional bias that only a value trend exposes.  One 32k-token
+    sequence, V = position / N + 0.1 N(0, 1) (fp16), one query head group, K and V at 4 bits (so
+    that the 2-bit reconstruction error does not hide the alpha-chain bias); decode against Eq. 2,
+    unsplit and with the default split count, both alpha modes."""
+    import numpy as np
+    import torch
+
+    from paper_2412_08585_b200 import binding as ta
+    from paper_2412_08585_b200 import synth
+
+    N, d, Hq, Hkv = 32768 + 17, 128, 4, 1
+    qx, kx, _ = synth.qkv_torch(777, 1, N, Hq, Hkv, d, device=device)
+    gen = torch.Generator(device=device)
+    gen.manual_seed(778)
+    vx = (torch.arange(N, device=device, dtype=torch.float32)[None, :, None, None] / N
+          + 0.1 * torch.randn((1, N, Hkv, d), generator=gen, device=device)).half()
+    cache = ta.KVCache(1, Hkv, d, max_blocks=N // 64 + 2, bits=[[4, 4]], device=device)
+    ta.turbo_quantize_kv(ta.params(head_dim=d), cache, kx.contiguous(), vx.contiguous())
+    qd = qx[:, -1].contiguous()
+    kh, vh = kx[0, :, 0].float().cpu().numpy(), vx[0, :, 0].float().cpu().numpy()
+    ref = exact_attention(qd[0].float().cpu().numpy(), kh, vh, 1.0 / math.sqrt(d))
+    S = ta.resolve_splits(None, 1, Hq, cache)
+    res = {"config": f"B=1, N={N}, 4/1 heads, d=128, 4-bit K and V, V = t/N + 0.1 N(0,1), split count {S}"}
+    for mode in (0, 1):
+        p = ta.params(head_dim=d, alpha_mode=mode)
+        o1 = ta.turbo_attention_decode(p, cache, qd, n_splits=1)[0][0].float().cpu().numpy()
+        oS = ta.turbo_attention_decode(p, cache, qd, n_splits=S)[0][0].float().cpu().numpy()
+        res[f"alpha_mode_{mode}"] = {"unsplit_vs_exact": dev_stats(o1, ref, float(np.sqrt(np.mean(vh ** 2))))["rel_l2"],
+                                     "split_vs_exact": dev_stats(oS, ref, float(np.sqrt(np.mean(vh ** 2))))["rel_l2"],
+                                     "split_vs_unsplit": dev_stats(oS, o1, 1.0)["rel_l2"]}
+    return res
 
 
 # --------------------------------------------------------------------------- reference (oracle)
@@ -447,7 +604,13 @@ def cpu_sample_oracle(seconds_hint=True):
         list(ex.map(one, range(ncores)))
     dt = time.perf_counter() - t0
     ops = prefill_ops(1, N, 1, d)
-    return {"value": ncores * ops / dt / 1e12, "unit": "TOPS", "cores": ncores, "kind": "oracle",
+    cpu_model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            cpu_model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), None)
+    except OSError:
+        pass
+    return {"value": ncores * ops / dt / 1e12, "unit": "TOPS", "cores": ncores, "kind": "oracle", "cpu_model": cpu_model,
             "sample": f"{ncores} of {CFG_PREFILL['B'] * CFG_PREFILL['Hq']} (batch, head) units of configs[1] "
                       f"(quantize + cache build + Alg. 1, N={N}, d={d}, causal), one per host core on "
                       f"{ncores} threads: {dt:.2f} s; one unit single-threaded {dt1:.2f} s",
@@ -518,18 +681,30 @@ def run_prefill_70b(args, rank, world, device):
     q, k, v = synth.qkv_torch(5005 + rank, B, N, hq, hkv, d, device=device)
     cache = ta.KVCache(B, hkv, d, max_blocks=N // 64 + 1, bits=synth.head_bits_alternating(hkv), device=device)
     st = torch.cuda.current_stream()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    clk = Clocks(device) if rank == 0 else None
     for i in range(args.warmup + args.steps):
-        if i >= args.warmup:
-            evs[i - args.warmup][0].record(st)
+        e = evs[i - args.warmup] if i >= args.warmup else None
+        if e:
+            e[0].record(st)
         k1_, v1t, k1s, v1s = ta.turbo_quantize_kv(p, cache, k, v)
+        if e:
+            e[1].record(st)
         ta.turbo_attention_prefill(p, q, k1_, v1t, k1s, v1s, causal=True)
-        if i >= args.warmup:
-            evs[i - args.warmup][1].record(st)
+        if e:
+            e[2].record(st)
     torch.cuda.synchronize()
-    ms = _max_over_ranks(sum(a.elapsed_time(b) for a, b in evs), world, device) / args.steps
+    clocks = clk.stop() if clk else None
+    ms = _max_over_ranks(sum(e[0].elapsed_time(e[2]) for e in evs), world, device) / args.steps
     ops = prefill_ops(B, N, c["Hq"], d)
-    return {"value": ops / (ms * 1e-3) / 1e12, "unit": "TOPS", "ms_step": ms, "scaling": "strong",
+    pk = peaks()
+    pre_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+    ach = prefill_ops(B, N, hq, d) / (pre_ms * 1e-3) / 1e12  # this rank's heads / its kernel time
+    return {"value": ops / (ms * 1e-3) / 1e12, "unit": "TOPS", "ms_step": ms, "scaling": "strong", "clocks": clocks,
+            "roofline": {"bound": "tensor", "kernel": "prefill_kernel<128> (rank 0)", "achieved": round(ach, 1),
+                         "peak": round(2.0 * pk["bf16"], 1), "unit": "TFLOP/s",
+                         "frac": round(ach / (2.0 * pk["bf16"]), 4), "traffic": None,
+                         "peak_source": f"2 x bf16 burst {pk['bf16']} TF/s, {pk['src']}"},
             "config": {"workload": "configs[3]: Llama-3-70B attention shape (64 Q / 8 KV heads, d=128), prefill 32k, "
                                    "batch 1, causal; step = quantize_kv + prefill",
                        "parallelism": f"KV heads partitioned over {world} rank(s), no collective",
@@ -596,7 +771,10 @@ def run_decode_long(args, rank, world, device):
     p = ta.params(head_dim=d, alpha_mode=1)
     cache = ta.KVCache(B, Hkv, d, max_blocks=n_loc // 64 + 4, bits=bits, device=device)
     _, k, v = synth.qkv_torch(9009 + rank, B, n_loc, Hkv, Hkv, d, device=device)
-    ta.turbo_quantize_kv(p, cache, k, v)
+    if world > 1:  # global universal scale: one all-reduce(MAX) at cache construction (parallel.py)
+        parallel.prefill_seq_sharded(p, cache, k, v, torch.distributed.group.WORLD)
+    else:
+        ta.turbo_quantize_kv(p, cache, k, v)
     del k, v
     torch.cuda.empty_cache()
     last = rank == world - 1
@@ -619,23 +797,59 @@ def run_decode_long(args, rank, world, device):
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
+    clk = Clocks(device) if rank == 0 else None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
     for i in range(args.steps):
         step(args.warmup + i)
     e1.record(st)
     torch.cuda.synchronize()
+    clocks = clk.stop() if clk else None
     ms = _max_over_ranks(e0.elapsed_time(e1), world, device) / args.steps
     nblk = cache.n_tokens // 64
     byt = decode_bytes(B, Hkv, d, nblk, cache.n_tokens % 64, bits, Hq)
     total = _max_over_ranks(float(byt), world, device) * world  # shards are equal up to one block
+    # roofline of the local decode (kernel + in-GPU split combine), timed alone on this rank
+    qd0 = toks[-1][0]
+    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    d0.record(st)
+    for _ in range(args.steps):
+        ta.turbo_attention_decode(p, cache, qd0, with_buffer=last, n_splits=args.decode_splits,
+                                  want_fp16=world == 1, want_f32=world > 1)
+    d1.record(st)
+    torch.cuda.synchronize()
+    dec_ms = d0.elapsed_time(d1) / args.steps
+    pk = peaks()
+    roof = {"bound": "hbm", "kernel": "decode_kernel + combine (rank 0)", "achieved": round(byt / (dec_ms * 1e-3) / 1e9, 1),
+            "peak": pk["hbm"], "unit": "GB/s", "frac": round(byt / (dec_ms * 1e-3) / 1e9 / pk["hbm"], 4),
+            "traffic": None, "peak_source": pk["src"]}
     return {"value": total / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms_step": ms, "scaling": "strong",
+            "clocks": clocks, "roofline": roof,
             "tokens_per_s": B / (ms * 1e-3),
             "config": {"workload": "configs[4]: decode 128k context, batch 16, Llama-3-8B attention shape "
                                    "(32 Q / 8 KV heads, d=128), mixed INT4/INT2; step = append + split-KV decode "
                                    "+ all-gather + LSE combine",
                        "parallelism": f"sequence-sharded cache over {world} rank(s), NCCL all-gather of (O, L)",
                        "decode_splits_per_rank": args.decode_splits}}
+
+
+def relaunch_under_torchrun(n):
+    """`python bench.py --gpus N` without torchrun: check that N GPUs are visible, then re-execute
+    this command as N ranks on this node (torch.distributed.run, 127.0.0.1 rendezvous)."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < n:
+        sys.exit(f"bench.py: --gpus {n} needs {n} visible GPUs, found {have}")
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -649,11 +863,14 @@ def main():
     ap.add_argument("--decode-splits", type=int, default=None,
                     help="decode split count (default: binding.auto_splits; 0: the balanced schedule)")
     ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--no-deviation", action="store_true", help="skip the deviation-from-exact report")
     ap.add_argument("--workload", default="step", choices=["step", "prefill_70b", "decode_long", "prefill_chunk"],
                     help="step = the default hot-path step (configs[1] + configs[2] decode)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        relaunch_under_torchrun(args.gpus)  # one rank per GPU (does not return)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -661,6 +878,12 @@ def main():
         run_reference(args, rank, world)
         return
     import torch
+
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU "
+                 f"(torchrun --nproc-per-node {args.gpus}, or plain `python bench.py --gpus {args.gpus}`)")
+    if torch.cuda.device_count() < world or local >= torch.cuda.device_count():
+        sys.exit(f"bench.py: {world} rank(s) requested but only {torch.cuda.device_count()} GPU(s) visible")
 
     if world > 1:
         torch.cuda.set_device(local)
@@ -679,6 +902,9 @@ def main():
                     "data": "synthetic", "config": res["config"]}
             if "tokens_per_s" in res:
                 line["tokens_per_s"] = round(res["tokens_per_s"], 1)
+            for key in ("clocks", "roofline"):
+                if key in res:
+                    line[key] = res[key]
             print(json.dumps(line), flush=True)
         if world > 1:
             torch.distributed.barrier()
@@ -693,7 +919,17 @@ def main():
                 "data": "synthetic (seeded N(0,1) Q/K/V with outlier channels, DESIGN.md §4)",
                 "config": workload_config(args), "roofline": res["roofline"], "cpu_baseline": cpu,
                 "e2e": res["e2e"], "gpu_launches": res["launches"], "clocks": res["clocks"],
-                "breakdown_ms": res["breakdown_ms"], "quantize_kv": res["quantize_kv"], "decode": res.get("decode")}
+                "breakdown_ms": res["breakdown_ms"], "quantize_kv": res["quantize_kv"], "decode": res.get("decode"),
+                "planner": res["planner"], "deviation": None}
+        dev = {}
+        if res.get("deviation"):
+            dev.update(res["deviation"])
+        if line["decode"] and line["decode"].get("deviation"):
+            dev["decode_configs2"] = line["decode"].pop("deviation")
+        if dev and not args.no_deviation:
+            dev["trend_v_probe"] = trend_v_probe(local)
+            dev["reference"] = "Eq. 2 (PAPER.md:229-233) in FP64 on the same fp16 inputs"
+        line["deviation"] = dev or None
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.barrier()

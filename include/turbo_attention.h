@@ -199,10 +199,11 @@ TURBO_API turbo_status_t turbo_attention_prefill_chunk(const turbo_params_t* par
                                                        const float* k1_scale, const float* v1_scale, void* o,
                                                        float* lse, turbo_stream_t stream);
 
-/* Workspace for turbo_attention_decode with n_splits (>= 0) on the current
- * device (HOST result; 0 = none needed, or invalid arguments).
- *   n_splits >= 2: S * B * Hq * (d + 1) floats;  n_splits == 0 (balanced):
- *   (B * Hkv + W) * (Hq / Hkv) * (d + 1) floats, W = turbo_decode_workers(). */
+/* Workspace for turbo_attention_decode with n_splits on the current device
+ * (HOST result; 0 = none needed, or invalid arguments).
+ *   n_splits >= 2: S * B * Hq * (d + 1) floats;  n_splits <= 0 (balanced):
+ *   (B * Hkv + W) * (Hq / Hkv) * (d + 1) floats, W = -n_splits, or
+ *   turbo_decode_workers() for n_splits == 0. */
 TURBO_API size_t turbo_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t head_dim,
                                               int32_t n_splits);
 
@@ -220,13 +221,23 @@ TURBO_API int32_t turbo_decode_workers(int32_t Hq, int32_t Hkv, int32_t head_dim
  *   n_splits in [1, 12000]: the block range of every (b, kv head) is cut into
  *     n_splits contiguous ranges of ceil(n / n_splits) blocks (the buffer
  *     joins the last one).
- *   n_splits == 0 (balanced): the units of every (b, kv head) -- its blocks
- *     in order, then the buffer block if used (with_buffer and n_buf > 0) --
- *     are laid end to end in (b, kv head) order; the sequence of all
- *     `total` units is cut into chunks of C = max(8, ceil(total / W)) units,
- *     W = turbo_decode_workers(Hq, Hkv, d), and every (b, kv head) range
- *     is split at the chunk boundaries.  Every warp streams the same number
- *     of bytes, whatever the lengths of the sequences.
+ *   n_splits in [-12000, 0] (balanced): the units of every (b, kv head) --
+ *     its blocks in order, then the buffer block if used (with_buffer and
+ *     n_buf > 0) -- are laid end to end in (b, kv head) order; the sequence
+ *     of all `total` units is cut into chunks of C = max(8, ceil(total / W))
+ *     units, W = -n_splits workers, or W = turbo_decode_workers(Hq, Hkv, d)
+ *     (the current device's resident decode warps) for n_splits == 0, and
+ *     every (b, kv head) range is split at the chunk boundaries.  Every warp
+ *     streams the same number of bytes, whatever the lengths of the sequences.
+ * SPLIT DEPENDENCE: the result is a deterministic function of the inputs and
+ * of the sub-range partition, but it DEPENDS on the partition: each pass has
+ * its own running max, alpha chain and per-row P scales, so a
+ * split decode is not bit-identical to the unsplit Alg. 2 (n_splits = 1); the
+ * size of the difference is reported by bench.py (`deviation.decode_split`,
+ * both alpha modes).  Every n_splits != 0 gives a device-independent
+ * partition; n_splits == 0 follows the device's SM count and occupancy, so its
+ * numbers can differ between GPUs (the Python binding's default therefore
+ * passes an explicit worker count, never 0).
  *   q      FP16 [B][Hq][d]; quantised per (b, head) vector.
  *   workspace  device, >= turbo_decode_workspace_bytes(B, Hq, Hkv, d, n_splits).
  *   o      FP16 [B][Hq][d] or NULL;  o_part f32 [B][Hq][d] (normalised) or

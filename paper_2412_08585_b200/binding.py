@@ -170,6 +170,10 @@ def turbo_quantize_kv(p, cache: KVCache, k, v, mode=0, stream=None, out=None):
         Nk = N if mode == 0 else cache.n_tokens + N
         tc = -(-Nk // p.block_kv)
         dev = k.device
+        if mode == 2 and out is None:
+            # the chunk kernel writes only the chunk's rows; the prefix rows must come from
+            # turbo_dequantize_cache (fresh buffers would hand garbage prefix keys on)
+            raise ValueError("turbo_quantize_kv mode 2 needs `out` holding the turbo_dequantize_cache prefix")
         if out is not None:
             k1, v1t, k1s, v1s = out
             assert k1.shape == (B, H, Nk, d) and v1t.shape == (B, H, tc, d, p.block_kv)
@@ -261,6 +265,19 @@ def balanced_ranges(unit_counts, Hkv, workers, min_units=8):
     return out
 
 
+B200_SMS = 148
+
+
+def reference_workers(Hq, Hkv, head_dim):
+    """Resident decode warps of ONE B200 (148 SMs x the decode kernel's warps per SM: 12 for the
+    packed G <= 4 path and for d = 64, 8 for the general d = 128 path at 239 registers).  The default
+    decode schedule uses this fixed count on every device, so that its split partition -- and hence
+    its numbers (turbo_attention.h, SPLIT DEPENDENCE) -- never depend on the GPU it runs on; on a
+    B200 it equals turbo_decode_workers() (tests/test_gpu_parity.py checks it)."""
+    per_sm = 12 if (Hq // Hkv <= 4 or head_dim == 64) else 8
+    return B200_SMS * per_sm
+
+
 def auto_splits(batch, n_kv_heads, n_blocks, workers=None):
     """Equal-split count for turbo_attention_decode.  Among the counts that keep >= 8
     blocks per split and whose last split is not short (>= 3/4 of the others, so no
@@ -270,7 +287,7 @@ def auto_splits(batch, n_kv_heads, n_blocks, workers=None):
     the best of a sweep on configs[2] (S = 12) and within 0.1 % on configs[4] (S = 64;
     tools/sweep_decode.py)."""
     if workers is None:
-        workers = max(1, turbo_decode_workers(4, 1, 128))
+        workers = reference_workers(4, 1, 128)
     bh = max(1, batch * n_kv_heads)
     best, best_err = 1, None
     for s in range(1, max(1, n_blocks // 8) + 1):
@@ -284,21 +301,31 @@ def auto_splits(batch, n_kv_heads, n_blocks, workers=None):
     return best
 
 
+def resolve_splits(n_splits, B, Hq, cache, blk_begin=0, blk_end=-1):
+    """The n_splits value turbo_attention_decode passes to the library for a binding-level
+    n_splits (None: the deterministic default)."""
+    if n_splits is not None:
+        return n_splits
+    Hkv, d = cache.n_kv_heads, cache.head_dim
+    if Hq // Hkv > 4:
+        return -reference_workers(Hq, Hkv, d)
+    nb = (cache.n_tokens // cache.block_kv) if blk_end < 0 else blk_end
+    return auto_splits(B, Hkv, max(0, nb - blk_begin), reference_workers(Hq, Hkv, d))
+
+
 def turbo_attention_decode(p, cache: KVCache, q, blk_begin=0, blk_end=-1, with_buffer=True, n_splits=1,
                            workspace=None, o=None, o_part=None, lse=None, want_fp16=True, want_f32=False,
                            stream=None):
     """q fp16 [B,Hq,d] -> (o fp16 [B,Hq,d] or None, o_part f32 [B,Hq,d] or None, lse f32 [B,Hq]).
-    n_splits >= 1: equal splits; 0: the balanced schedule; None: auto_splits() for G <= 4,
-    the balanced schedule for G > 4 (the general-path decode is issue-bound: measured 5-10 %
-    faster than auto_splits' count on B200 for 8 x 32k, 16 x 32k and 64 x 8k at 64 / 8 heads)."""
+    n_splits >= 1: equal splits; 0: the balanced schedule over this device's workers; -W: the
+    balanced schedule over W workers; None (deterministic default, device-independent):
+    auto_splits() with reference_workers() for G <= 4, the balanced schedule over
+    reference_workers() for G > 4 (the general-path decode is issue-bound: measured 5-10 % faster
+    than auto_splits' count on B200 for 8 x 32k, 16 x 32k and 64 x 8k at 64 / 8 heads).  The result
+    depends on the partition (turbo_attention.h, SPLIT DEPENDENCE); n_splits = 1 is unsplit Alg. 2."""
     assert q.dtype == torch.float16 and q.is_contiguous()
     B, Hq, d = q.shape
-    if n_splits is None and Hq // cache.n_kv_heads > 4:
-        n_splits = 0
-    if n_splits is None:
-        nb = (cache.n_tokens // cache.block_kv) if blk_end < 0 else blk_end
-        n_splits = auto_splits(B, cache.n_kv_heads, max(0, nb - blk_begin),
-                               max(1, turbo_decode_workers(Hq, cache.n_kv_heads, d)))
+    n_splits = resolve_splits(n_splits, B, Hq, cache, blk_begin, blk_end)
     dev = q.device
     if want_fp16 and o is None:
         o = torch.empty((B, Hq, d), dtype=torch.float16, device=dev)

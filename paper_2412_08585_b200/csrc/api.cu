@@ -167,7 +167,7 @@ turbo_status_t turbo_attention_prefill(const turbo_params_t* params, int32_t B, 
 }
 
 size_t turbo_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t head_dim, int32_t n_splits) {
-  if (B < 1 || Hq < 1 || Hkv < 1 || Hq % Hkv != 0 || n_splits < 0 || n_splits > 12000) return 0;
+  if (B < 1 || Hq < 1 || Hkv < 1 || Hq % Hkv != 0 || n_splits < -12000 || n_splits > 12000) return 0;
   if (head_dim != 64 && head_dim != 128) return 0;
   return ta_host::decode_workspace(B, Hq, Hkv, head_dim, n_splits);
 }
@@ -187,7 +187,8 @@ turbo_status_t turbo_attention_decode(const turbo_params_t* params, const turbo_
   if (Hq < 1 || !q || !lse || (!o && !o_part)) return TURBO_ERR_INVALID_ARG;
   if (Hq % cache->n_kv_heads != 0) return TURBO_ERR_UNSUPPORTED;
   if (Hq / cache->n_kv_heads > 8) return TURBO_ERR_UNSUPPORTED;
-  if (n_splits < 0 || n_splits > 12000 || blk_begin < 0 || (blk_end >= 0 && blk_end < blk_begin)) return TURBO_ERR_INVALID_ARG;
+  if (n_splits < -12000 || n_splits > 12000 || blk_begin < 0 || (blk_end >= 0 && blk_end < blk_begin))
+    return TURBO_ERR_INVALID_ARG;
   if (with_buffer != 0 && with_buffer != 1) return TURBO_ERR_INVALID_ARG;
   if (cache->n_tokens < 1) return TURBO_ERR_INVALID_ARG;  // decode on an empty cache
   if (workspace_bytes < ta_host::decode_workspace(cache->batch, Hq, cache->n_kv_heads, params->head_dim, n_splits) ||

@@ -836,10 +836,17 @@ __global__ void __launch_bounds__(32 * kCombWarps) combine_kernel(int n_parts, i
 
 static void launch_combine_kernel(int n_parts, int rows, int d, const float* o_parts, const float* lse_parts,
                                   __half* o16, float* o32, float* lse, cudaStream_t st) {
+  // (n_parts + 1) weights: up to 48 KB at the 12000-part bound, over the default 48 KB
+  // dynamic limit once the 4 KB of static shared memory are added -- raise it explicitly.
   const size_t smem = (n_parts + 1) * sizeof(float);
   const int thr = 32 * comb_warps(n_parts);
-  if (d == 128) combine_kernel<4><<<rows, thr, smem, st>>>(n_parts, rows, d, o_parts, lse_parts, o16, o32, lse);
-  else combine_kernel<2><<<rows, thr, smem, st>>>(n_parts, rows, d, o_parts, lse_parts, o16, o32, lse);
+  if (d == 128) {
+    cudaFuncSetAttribute(combine_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    combine_kernel<4><<<rows, thr, smem, st>>>(n_parts, rows, d, o_parts, lse_parts, o16, o32, lse);
+  } else {
+    cudaFuncSetAttribute(combine_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    combine_kernel<2><<<rows, thr, smem, st>>>(n_parts, rows, d, o_parts, lse_parts, o16, o32, lse);
+  }
 }
 
 }  // namespace ta
@@ -873,8 +880,8 @@ int decode_workers(int Hq, int Hkv, int HD) {
 size_t decode_workspace(int B, int Hq, int Hkv, int HD, int S) {
   if (S == 1) return 0;
   if (S > 1) return (size_t)S * B * Hq * (HD + 1) * sizeof(float);
-  // balanced: parts bh + w < B * Hkv + W, G rows of d + 1 floats each
-  const int W = decode_workers(Hq, Hkv, HD);
+  // balanced: parts bh + w < B * Hkv + W, G rows of d + 1 floats each (S < 0: W = -S workers)
+  const int W = S < 0 ? -S : decode_workers(Hq, Hkv, HD);
   return W <= 0 ? 0 : ((size_t)B * Hkv + W) * (Hq / Hkv) * (HD + 1) * sizeof(float);
 }
 
@@ -905,8 +912,8 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
   fill_sas_const(&a.sas, p->sas_nr);
   const bool has_tap = p->debug_tap != nullptr;
   if (has_tap) a.tap = *reinterpret_cast<const turbo_debug_tap_t*>(p->debug_tap);
-  const int W = S == 0 ? decode_workers(Hq, H, HD) : 0;
-  if (S == 0 && W <= 0) return cudaErrorInvalidConfiguration;
+  const int W = S == 0 ? decode_workers(Hq, H, HD) : S < 0 ? -S : 0;  // balanced: device or explicit workers
+  if (S <= 0 && W <= 0) return cudaErrorInvalidConfiguration;
   if (S == 1) {
     a.o_parts = o_part;
     a.lse_parts = lse;
@@ -943,12 +950,17 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
 #undef TA_DEC
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || S == 1) return e;
-  if (S == 0) {
+  if (S <= 0) {
     const size_t smem = (size_t)(W + 2) * sizeof(float);  // a row's pieces: at most W
     // pieces per row ~ W / (B Hkv) + 1
     const int thr = 32 * comb_warps(W / (B * H) + 1);
-    if (HD == 128) combine_balanced_kernel<4><<<B * Hq, thr, smem, st>>>(a, W, HD);
-    else combine_balanced_kernel<2><<<B * Hq, thr, smem, st>>>(a, W, HD);
+    if (HD == 128) {
+      cudaFuncSetAttribute(combine_balanced_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      combine_balanced_kernel<4><<<B * Hq, thr, smem, st>>>(a, W, HD);
+    } else {
+      cudaFuncSetAttribute(combine_balanced_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      combine_balanced_kernel<2><<<B * Hq, thr, smem, st>>>(a, W, HD);
+    }
   } else {
     const int rows = B * Hq;
     launch_combine_kernel(S, rows, HD, a.o_parts, a.lse_parts, o, o_part, lse, st);

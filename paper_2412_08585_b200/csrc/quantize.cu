@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(2 * HD) dequant_cache_kernel(
   } else {
     // V: channel-major words in the IMMA token order (layout.cuh v_token_of)
     const int CB = kBc * bits / 8;
-    __half row[kBc];
+    __align__(16) __half row[kBc];  // read back as uint4 below
     for (int wi = 0; wi < CB / 4; ++wi)
       for (int i = 0; i < 32 / bits; ++i) {
         int e, sh;

@@ -75,7 +75,10 @@ def test_host_validation_without_gpu(L):
     assert L.turbo_decode_workspace_bytes(2, 8, 2, 128, 1) == 0
     assert L.turbo_decode_workspace_bytes(2, 8, 2, 128, 4) == 4 * 2 * 8 * 129 * 4
     assert L.turbo_decode_workspace_bytes(2, 8, 3, 128, 4) == 0  # Hq % Hkv != 0
-    assert L.turbo_decode_workspace_bytes(2, 8, 2, 128, -1) == 0
+    # balanced schedule over an explicit worker count W = -n_splits: (B Hkv + W) G (d + 1) floats
+    assert L.turbo_decode_workspace_bytes(2, 8, 2, 128, -1) == (2 * 2 + 1) * 4 * 129 * 4
+    assert L.turbo_decode_workspace_bytes(2, 8, 2, 128, -1776) == (2 * 2 + 1776) * 4 * 129 * 4
+    assert L.turbo_decode_workspace_bytes(2, 8, 2, 128, -12001) == 0
     assert L.turbo_decode_workspace_bytes(2, 8, 2, 128, 12001) == 0  # n_splits bound (combine weights in smem)
     assert L.turbo_decode_workers(8, 3, 128) == 0
     # quantize_kv / decode with a malformed cache struct
@@ -105,6 +108,23 @@ def test_sass_uses_tcgen05_and_tma():
     assert "LDTM" in sass
     assert "UTMALDG" in sass
     assert "UBLKCP" in sass
+
+
+def test_default_decode_schedule_is_device_independent():
+    """binding.resolve_splits (the n_splits=None default) depends only on the problem shape, never on
+    the device: equal splits by auto_splits over the B200 reference worker count for G <= 4, the
+    balanced schedule over that count (n_splits = -W) for G > 4 (include/turbo_attention.h)."""
+    from paper_2412_08585_b200 import binding as b
+
+    class FakeCache:
+        n_kv_heads, head_dim, block_kv, n_tokens = 10, 128, 64, 32768
+
+    assert b.reference_workers(40, 10, 128) == 148 * 12
+    assert b.reference_workers(64, 8, 128) == 148 * 8
+    assert b.resolve_splits(None, 64, 40, FakeCache) == b.auto_splits(64, 10, 512, 148 * 12) == 12
+    FakeCache.n_kv_heads = 8
+    assert b.resolve_splits(None, 8, 64, FakeCache) == -148 * 8
+    assert b.resolve_splits(3, 8, 64, FakeCache) == 3
 
 
 def test_plan_bits_host_only(L):

@@ -85,7 +85,15 @@ def test_chunk_needs_whole_cached_blocks(ta):  # noqa: F811
     p = ta.params(head_dim=d)
     cache = ta.KVCache(B, Hkv, d, max_blocks=8, bits=[[4, 4]])
     ta.turbo_quantize_kv(p, cache, torch.from_numpy(k[:, :N].copy()).cuda(), torch.from_numpy(v[:, :N].copy()).cuda())
+    nk, tc = N + 64, -(-(N + 64) // 64)
+    out = (torch.empty((B, Hkv, nk, d), dtype=torch.int8, device="cuda"),
+           torch.empty((B, Hkv, tc, d, 64), dtype=torch.float16, device="cuda"),
+           torch.empty((B, Hkv, tc), dtype=torch.float32, device="cuda"),
+           torch.empty((B, Hkv, tc), dtype=torch.float32, device="cuda"))
     with pytest.raises(ta.TurboError):
+        ta.turbo_quantize_kv(p, cache, torch.from_numpy(k[:, N:].copy()).cuda(),
+                             torch.from_numpy(v[:, N:].copy()).cuda(), mode=2, out=out)
+    with pytest.raises(ValueError):  # the binding requires the prefix operands for mode 2
         ta.turbo_quantize_kv(p, cache, torch.from_numpy(k[:, N:].copy()).cuda(),
                              torch.from_numpy(v[:, N:].copy()).cuda(), mode=2)
 

@@ -161,8 +161,12 @@ DEC_CASES = [  # (B, N_prefill, n_append, Hq, Hkv, d, n_splits, alpha_mode)
     # odd / small groups on the packed path (rows >= G absent): G = 3 split, G = 2 balanced at d = 64
     (1, 64 * 5 + 9, 5, 6, 2, 128, 2, 0),
     (2, 64 * 20 + 5, 3, 4, 2, 64, 0, 0),
-    # G = 6 (general path) through n_splits=None, which selects the balanced schedule for G > 4
+    # G = 6 (general path) through n_splits=None, which selects the balanced schedule over the
+    # fixed reference worker count (device-independent) for G > 4
     (1, 64 * 7 + 3, 2, 6, 1, 128, None, 0),
+    # balanced schedule over an explicit worker count (n_splits = -W), a G <= 4 default (None)
+    (3, 64 * 20 + 5, 3, 8, 2, 128, -7, 1),
+    (2, 64 * 40 + 9, 4, 8, 2, 128, None, 0),
 ]
 
 
@@ -190,11 +194,11 @@ def _oracle_decode(op, q, slots, G, splits_bounds):
     return outs, lses
 
 
-def balanced_bounds(ta, slots_by_b, Hq, Hkv, d):
+def balanced_bounds(ta, slots_by_b, Hq, Hkv, d, workers=None):
     """{b: {kvh: [(a, e, with_buffer)]}} of the balanced schedule, from the
     documented partition (include/turbo_attention.h) and the oracle's counters."""
     units = [sl[0][0].n_blocks + (1 if sl[0][0].n_buf > 0 else 0) for sl in slots_by_b]
-    rng = ta.balanced_ranges(units, Hkv, ta.turbo_decode_workers(Hq, Hkv, d))
+    rng = ta.balanced_ranges(units, Hkv, workers or ta.turbo_decode_workers(Hq, Hkv, d))
     out = {}
     for b, sl in enumerate(slots_by_b):
         nb = sl[0][0].n_blocks
@@ -226,14 +230,14 @@ def test_append_and_decode_parity(ta, case):
     torch.cuda.synchronize()
     o, lse = o.cpu().numpy(), lse.cpu().numpy()
     nb = ref["slots"][0][0][0].n_blocks
-    if S is None:  # the binding's default: balanced for G > 4
-        assert G > 4
-        S = 0
+    if S is None:  # the binding's default, recomputed from its documented rule
+        S = ta.reference_workers(Hq, Hkv, d)
+        S = -S if G > 4 else ta.auto_splits(B, Hkv, nb, S)
     if S > 0:
         per = -(-nb // S)
         bounds = [(min(s * per, nb), min(s * per + per, nb)) for s in range(S)]
     else:
-        bal = balanced_bounds(ta, ref["slots"], Hq, Hkv, d)
+        bal = balanced_bounds(ta, ref["slots"], Hq, Hkv, d, -S if S < 0 else None)
         assert B * Hkv == 1 or sum(len(v) for x in bal.values() for v in x.values()) > B * Hkv  # really split
     # cache state after the appends is bit-exact
     recs = cache.records().cpu().numpy()
@@ -408,3 +412,65 @@ def test_fast_division_exhaustive(ta, which, lo, hi):
     FP16 inputs are <= 65504."""
     bad, first = ta.turbo_selftest_div(which, lo, hi)
     assert bad == 0, f"{bad} mismatches, first at bits {first:#010x}"
+
+
+@pytest.mark.parametrize("Hq,Hkv,d", [(8, 2, 128), (16, 2, 128), (8, 2, 64), (16, 2, 64)])
+def test_reference_workers_match_b200(ta, Hq, Hkv, d):
+    """The deterministic default schedule assumes the B200's resident decode warps; on a B200 the
+    device's own count must equal it (so the default keeps the measured-fastest schedule)."""
+    if torch.cuda.get_device_properties(0).multi_processor_count != ta.B200_SMS:
+        pytest.skip("not a 148-SM B200")
+    assert ta.turbo_decode_workers(Hq, Hkv, d) == ta.reference_workers(Hq, Hkv, d)
+
+
+def test_combine_at_the_part_bound(ta):
+    """turbo_combine_lse at n_parts = 12000 (the documented maximum): the weights need > 48 KB of
+    shared memory with the static part, which the launch raises explicitly."""
+    S, rows, d = 12000, 2, 64
+    rng = np.random.default_rng(7)
+    parts = rng.standard_normal((S, rows, d)).astype(np.float32)
+    lses = rng.standard_normal((S, rows)).astype(np.float32)
+    o, _, lse = ta.turbo_combine_lse(torch.from_numpy(parts).cuda(), torch.from_numpy(lses).cuda())
+    torch.cuda.synchronize()
+    for r in range(rows):
+        ro, rl = O.combine(parts[:, r], lses[:, r])
+        np.testing.assert_allclose(o[r].float().cpu().numpy(), ro, atol=2e-3, rtol=0)
+        assert abs(lse[r].item() - rl) < 1e-4
+
+
+def test_seq_sharded_prefill_global_universal_scale(ta):
+    """Sequence-sharded cache construction (parallel.prefill_seq_sharded, emulated ranks on one GPU):
+    every rank quantises its whole blocks, the per-rank a_univ are reduced by MAX (the all-reduce),
+    then the last rank quantises the tail with the global scale (turbo_quantize_kv mode 2).  The
+    blocks, the universal scales and the buffer equal the single-device cache bit for bit (R-9)."""
+    from paper_2412_08585_b200 import parallel
+
+    B, N, Hkv, d, W = 2, 64 * 11 + 37, 2, 128, 3
+    _, k, v = synth.qkv(4250, B, N, Hkv, Hkv, d)
+    k[1, 40, 1] *= 6.0   # the largest |K| of (b=1, kv head 1) on rank 0: the tail must use it
+    v[0, N - 5, 0] *= 3.0  # the largest |V| of (b=0, kv head 0) in the tail itself
+    bits = synth.head_bits_alternating(Hkv)
+    p = ta.params(head_dim=d)
+    kt, vt = torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda()
+    whole = ta.KVCache(B, Hkv, d, max_blocks=16, bits=bits)
+    ta.turbo_quantize_kv(p, whole, kt, vt)
+    caches, amax = [], []
+    for r in range(W):
+        t0, t1 = parallel.seq_shard_tokens(N, W, r)
+        c = ta.KVCache(B, Hkv, d, max_blocks=16, bits=bits)
+        amax.append(parallel.prefill_shard_blocks(p, c, kt[:, t0:t1], vt[:, t0:t1]))
+        caches.append((c, t0, t1))
+    a_glob = torch.stack(amax).amax(0)
+    for c, t0, t1 in caches:
+        parallel.prefill_shard_tail(p, c, kt[:, t0:t1], vt[:, t0:t1], a_glob)
+    torch.cuda.synchronize()
+    nau = B * Hkv * 2
+    last = caches[-1][0]
+    np.testing.assert_array_equal(last.a_univ[:nau].cpu().numpy(), whole.a_univ[:nau].cpu().numpy())
+    np.testing.assert_array_equal(last.buf.cpu().numpy(), whole.buf.cpu().numpy())
+    np.testing.assert_array_equal(last.counters.view(B, 2)[:, 1].cpu().numpy(),
+                                  whole.counters.view(B, 2)[:, 1].cpu().numpy())
+    rw = whole.records().cpu().numpy()
+    for c, t0, t1 in caches:
+        nb = (t1 - t0) // 64
+        np.testing.assert_array_equal(c.records().cpu().numpy()[:, :, :, :nb], rw[:, :, :, t0 // 64:t0 // 64 + nb])
