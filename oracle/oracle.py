@@ -61,6 +61,7 @@ class Params(C.Structure):
         ("d", C.c_int32), ("block_q", C.c_int32), ("block_kv", C.c_int32), ("sas_nr", C.c_int32),
         ("alpha_mode", C.c_int32), ("softmax_scale", C.c_float), ("quant", C.c_int32), ("sas", C.c_int32),
         ("p_row", C.c_int32),
+        ("scale_fp16", C.c_int32),
     ]
 
 
@@ -120,12 +121,13 @@ def _declare(L):
     L.tq_head_priority.argtypes = [i32, i32, vp, vp]
 
 
-def params(d=128, block_q=64, block_kv=64, sas_nr=-6, alpha_mode=0, softmax_scale=None, quant=1, sas=1, p_row=0):
+def params(d=128, block_q=64, block_kv=64, sas_nr=-6, alpha_mode=0, softmax_scale=None, quant=1, sas=1, p_row=0,
+           scale_fp16=0):
     """Paper defaults: B_r = B_c = n_b = 64, n_r = -6; p_row=1 is the
     per-row prefill P scale (NEXT-2 variant)."""
     if softmax_scale is None:
         softmax_scale = float(np.float32(1.0) / np.sqrt(np.float32(d)))
-    return Params(d, block_q, block_kv, sas_nr, alpha_mode, softmax_scale, quant, sas, p_row)
+    return Params(d, block_q, block_kv, sas_nr, alpha_mode, softmax_scale, quant, sas, p_row, scale_fp16)
 
 
 def _f32(x):

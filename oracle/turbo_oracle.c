@@ -67,6 +67,25 @@ void tq_sas_softmax_rows(int32_t rows, int32_t cols, const float* x, int32_t nr,
   }
 }
 
+/* IEEE binary16 rounding (nearest, ties to even) of a float, returned as a float: the
+ * first-stage scales of the scale_fp16 variant ("FP16" scales; R-29).  Written out
+ * from the format's definition: 11 significant bits, quantum 2^(e-11) for |s| in
+ * [2^(e-1), 2^e), never finer than the subnormal quantum 2^-24, overflow past 65504. */
+static float round_fp16(float s) {
+  double a = fabs((double)s);
+  if (a == 0.0 || !isfinite(a)) return s;
+  int e;
+  frexp(a, &e);
+  int q = e - 11;
+  if (q < -24) q = -24;
+  double r = ldexp(rint(ldexp(a, -q)), q);  /* rint: round half to even (default mode) */
+  if (r > 65504.0) r = INFINITY;
+  return (float)(s < 0.0f ? -r : r);
+}
+
+/* A first-stage scale as used and stored: FP32, or its FP16 rounding (scale_fp16). */
+static float st1(const tq_params* p, float s) { return p->scale_fp16 ? round_fp16(s) : s; }
+
 /* ------------------------------------------------------------------------ */
 /* FlashQ stage 1: symmetric INT8 per block (Eq. 9; Alg. 1) */
 /* ------------------------------------------------------------------------ */
@@ -159,6 +178,7 @@ int32_t tq_cache_prefill_slot(const tq_params* p, int32_t n, const float* x, tq_
     int32_t rows = (j + 1) * bc <= n ? bc : n - j * bc;
     float sc;
     tq_quant_sym8(x + (int64_t)j * bc * d, (int64_t)rows * d, blk, &sc);
+    sc = st1(p, sc);
     if (x1) memcpy(x1 + (int64_t)j * bc * d, blk, (size_t)rows * d);
     if (x1_scale) x1_scale[j] = sc;
     if (rows == bc) flush_block(p, s, blk, sc);
@@ -190,6 +210,7 @@ int32_t tq_cache_prefill_append_slot(const tq_params* p, int32_t n, const float*
     int32_t rows = (j + 1) * bc <= n ? bc : n - j * bc;
     float sc;
     tq_quant_sym8(x + (int64_t)j * bc * d, (int64_t)rows * d, blk, &sc);
+    sc = st1(p, sc);
     if (x1) memcpy(x1 + (int64_t)j * bc * d, blk, (size_t)rows * d);
     if (x1_scale) x1_scale[j] = sc;
     if (rows == bc) flush_block(p, s, blk, sc);
@@ -211,7 +232,7 @@ int32_t tq_cache_append_slot(const tq_params* p, const float* x, tq_slot* s) {
   for (int32_t c = 0; c < d; ++c) s->buf[(int64_t)s->n_buf * d + c] = quant_univ(x[c], s->a_univ);
   s->n_buf += 1;
   if (s->n_buf == bc) {
-    flush_block(p, s, s->buf, s->a_univ / TQ_DIV);
+    flush_block(p, s, s->buf, st1(p, s->a_univ / TQ_DIV));
     s->n_buf = 0;
   }
   return 0;
@@ -307,6 +328,8 @@ int32_t tq_prefill_head_blocks(const tq_params* p, int32_t n, int32_t causal, co
     int32_t rows = (j + 1) * bc <= n ? bc : n - j * bc;
     tq_quant_sym8(k + (int64_t)j * bc * d, (int64_t)rows * d, k1 + (int64_t)j * bc * d, &sk[j]);
     tq_quant_sym8(v + (int64_t)j * bc * d, (int64_t)rows * d, v1 + (int64_t)j * bc * d, &sv[j]);
+    sk[j] = st1(p, sk[j]);
+    sv[j] = st1(p, sv[j]);
   }
   const int32_t rc = prefill_core(p, n, n, 0, causal, q, k, v, k1, v1, sk, sv, i_begin, i_end, o, lse, tap);
   free(k1); free(v1); free(sk); free(sv);
@@ -346,6 +369,7 @@ static int32_t prefill_core(const tq_params* p, int32_t nq, int32_t nk, int32_t 
     const int32_t r0 = i * br, nr = (r0 + br <= n) ? br : n - r0;
     float sq = 0.0f;
     if (p->quant) tq_quant_sym8(q + (int64_t)r0 * d, (int64_t)nr * d, q1, &sq); /* P:907 */
+    sq = st1(p, sq);
     for (int32_t r = 0; r < nr; ++r) {            /* init O, l, m (P:903) */
       m[r] = -INFINITY;
       l[r] = 0.0;
@@ -475,6 +499,7 @@ int32_t tq_decode_head(const tq_params* p, const float* q, const tq_slot* ks, co
   float sq = 0.0f, m = -INFINITY;
   double l = 0.0;
   if (p->quant) tq_quant_sym8(q, d, q1, &sq);            /* s_Q, Q^q1 */
+  sq = st1(p, sq);
   const int32_t n_tiles = (blk_end - blk_begin) + ((with_buffer && ks->n_buf > 0) ? 1 : 0);
   for (int32_t t = 0; t < n_tiles; ++t) {
     const int32_t is_buf = blk_begin + t >= blk_end;
@@ -495,8 +520,8 @@ int32_t tq_decode_head(const tq_params* p, const float* q, const tq_slot* ks, co
             vh[ie] = (int8_t)tq_dequant_q2(vs->codes[cb], vs->s_int[sb], vs->z_int[sb]);
           }
         }
-      s_k = is_buf ? ks->a_univ / TQ_DIV : ks->s_parent[j];
-      s_v = is_buf ? vs->a_univ / TQ_DIV : vs->s_parent[j];
+      s_k = is_buf ? st1(p, ks->a_univ / TQ_DIV) : ks->s_parent[j];
+      s_v = is_buf ? st1(p, vs->a_univ / TQ_DIV) : vs->s_parent[j];
     } else {
       s_k = s_v = 0.0f;
     }

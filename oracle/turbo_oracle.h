@@ -33,6 +33,9 @@ typedef struct {
   int32_t sas;           /* 1: SAS exponent; 0: exact exp (pin P5) */
   int32_t p_row;         /* prefill P scale: 0 per B_r x B_c tile (Alg. 1); 1 per row x B_c block,
                             the granularity Alg. 2 uses -- NEXT-2 variant */
+  int32_t scale_fp16;    /* first-stage scales stored in FP16 (Eq. 8 text): every stage-1 scale
+                            s = max|x|/119 (Q, K, V blocks, decode q, parent scales, s_univ) is rounded to
+                            binary16 (nearest even) before use; codes unchanged (R-29) -- NEXT-2 variant */
 } tq_params;
 
 /* One cache "slot" = one (batch, kv_head, K-or-V) stream.  Logical layout

@@ -18,11 +18,11 @@ PINS = ["tests/test_oracle_decode_pins.py", "tests/test_oracle_pins.py", "tests/
 # (name, original text, mutated text) -- each original must occur in the source
 MUTATIONS = [
     ("V parent scale from the K slot (P:970)",
-     "s_v = is_buf ? vs->a_univ / TQ_DIV : vs->s_parent[j];",
-     "s_v = is_buf ? vs->a_univ / TQ_DIV : ks->s_parent[j];"),
+     "s_v = is_buf ? st1(p, vs->a_univ / TQ_DIV) : vs->s_parent[j];",
+     "s_v = is_buf ? st1(p, vs->a_univ / TQ_DIV) : ks->s_parent[j];"),
     ("buffer K scale not a_univ/119 (P:451-453)",
-     "s_k = is_buf ? ks->a_univ / TQ_DIV : ks->s_parent[j];",
-     "s_k = is_buf ? ks->a_univ / 127.0f : ks->s_parent[j];"),
+     "s_k = is_buf ? st1(p, ks->a_univ / TQ_DIV) : ks->s_parent[j];",
+     "s_k = is_buf ? st1(p, ks->a_univ / 127.0f) : ks->s_parent[j];"),
     ("buffer V codes read from the K slot",
      "vh[ie] = vs->buf[ie];",
      "vh[ie] = ks->buf[ie];"),
@@ -46,6 +46,12 @@ MUTATIONS = [
     ("prefill P scale per row instead of per B_r x B_c tile (P:918)",
      "sp = quant_p((int64_t)nr * nc, pt, active, nc, pc);",
      "for (int32_t r = 0; r < nr; ++r) sp = quant_p(nc, pt + (int64_t)r * nc, active + r, nc, pc + (int64_t)r * nc);"),
+    ("FP16 scale variant: flushed-buffer parent scale left in FP32 (R-29)",
+     "flush_block(p, s, s->buf, st1(p, s->a_univ / TQ_DIV));",
+     "flush_block(p, s, s->buf, s->a_univ / TQ_DIV);"),
+    ("FP16 scale variant: binary16 ties rounded away from zero (R-29)",
+     "double r = ldexp(rint(ldexp(a, -q)), q);",
+     "double r = ldexp(round(ldexp(a, -q)), q);"),
     ("universal scale from the last block only (R-9)",
      "float a_univ = 0.0f;\n  for (int64_t i = 0; i < (int64_t)n * d; ++i) a_univ = fmaxf(a_univ, fabsf(x[i]));",
      "float a_univ = 0.0f;\n  for (int64_t i = (int64_t)(n - 1) / bc * bc * d; i < (int64_t)n * d; ++i)"

@@ -415,3 +415,75 @@ def test_prefill_query_block_subset(oracle):
         np.testing.assert_array_equal(part[128:], full[128:])
         np.testing.assert_array_equal(lp[128:], lf[128:])
         assert not part[:128].any() and not lp[:128].any()
+
+
+def test_scale_fp16_variant_rounds_every_first_stage_scale(oracle):
+    """NEXT-2 variant scale_fp16 (P:297 FP16 first-stage scales, R-29): each stored block scale is
+    the binary16 round-to-nearest-even of the FP32 scale max|x|/119 -- checked against numpy's own
+    float16 conversion over blocks whose scales span normal and subnormal binary16 (amax 2^-20 ...
+    2^10) -- the codes are unchanged, the parent scales and the buffer scale a_univ/119 follow."""
+    rng = np.random.default_rng(5)
+    d = 64
+    for e in range(-20, 11, 3):
+        x = (rng.standard_normal((64 * 3 + 17, d)) * 2.0 ** e).astype(np.float16).astype(np.float32)
+        p32, p16 = oracle.params(d=d), oracle.params(d=d, scale_fp16=1)
+        s32, s16 = oracle.Slot(p32, 4, 8), oracle.Slot(p16, 4, 8)
+        x1a, sca = s32.prefill(x)
+        x1b, scb = s16.prefill(x)
+        np.testing.assert_array_equal(x1a, x1b)  # codes unchanged
+        np.testing.assert_array_equal(scb, sca.astype(np.float16).astype(np.float32))
+        np.testing.assert_array_equal(s16.s_parent[:3], scb[:3])
+        assert np.abs(scb - sca).max() <= np.abs(sca).max() * 2.0 ** -11 + 2.0 ** -25
+        # a flushed buffer block takes fp16(a_univ / 119) as its parent scale (P:451-453)
+        for t in range(64 - 17):
+            s16.append(x[t])
+        assert s16.n_blocks == 4 and s16.n_buf == 0
+        parent = np.float32(s16.a_univ) / np.float32(119.0)
+        assert s16.s_parent[3] == np.float32(np.float16(parent))
+
+
+def test_scale_fp16_variant_attention_changes_little(oracle):
+    """The FP16 scales move the prefill and the decode outputs by far less than the method's own
+    distance from exact attention (the variant is a storage-format choice, not a different
+    method), and they do move them (the flag is live)."""
+    d, n = 128, 200
+    q, k, v = synth.qkv(6, 1, n, 1, 1, d)
+    q, k, v = (x[0, :, 0].astype(np.float32) for x in (q, k, v))
+    o32, _ = oracle.prefill_head(oracle.params(d=d), q, k, v)
+    o16, _ = oracle.prefill_head(oracle.params(d=d, scale_fp16=1), q, k, v)
+    ex, _ = oracle.reference_attention(q, k, v, causal=True)
+    assert 0 < rel_l2(o16, o32) < 0.1 * rel_l2(o32, ex)
+    res = {}
+    for f in (0, 1):
+        p = oracle.params(d=d, scale_fp16=f)
+        ks, vs = oracle.Slot(p, 4, 8), oracle.Slot(p, 2, 8)
+        ks.prefill(k)
+        vs.prefill(v)
+        res[f] = oracle.decode_head(p, q[-1], ks, vs)[0]
+    assert 0 < rel_l2(res[1], res[0]) < 1e-2
+
+
+def test_scale_fp16_variant_ties_to_even(oracle):
+    """R-29's binary16 rounding on exact ties: block maxima chosen so that fl(max/119) lies exactly
+    halfway between two binary16 values; the stored scale must be the even one (numpy float16)."""
+    d, hits = 64, 0
+    p16 = oracle.params(d=d, scale_fp16=1)
+    for k, q in ((1024, -12), (1536, -10), (2046, -8), (1110, -14), (1300, -20), (1998, -6)):
+        # k even (11 bits): k + 1/2 is halfway between two binary16 values; ties-to-even keeps k,
+        # rounding half away from zero would give k + 1
+        s_tie = np.float32(np.ldexp(k + 0.5, q))
+        a = np.float32(s_tie * np.float32(119.0))
+        for _ in range(64):  # nudge a until fl(a / 119) is exactly the tie
+            if np.float32(a / np.float32(119.0)) == s_tie:
+                break
+            a = np.nextafter(a, np.float32(np.inf) if np.float32(a / np.float32(119.0)) < s_tie else np.float32(0))
+        if np.float32(a / np.float32(119.0)) != s_tie:
+            continue
+        x = np.zeros((64, d), np.float32)
+        x[3, 5] = a
+        x[10, 7] = -a / 3
+        sl = oracle.Slot(p16, 4, 2)
+        _, sc = sl.prefill(x)
+        assert sc[0] == np.float32(np.float16(s_tie)) == np.float32(np.ldexp(k, q)), (k, q)
+        hits += 1
+    assert hits >= 4
