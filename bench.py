@@ -372,6 +372,20 @@ def run_ours(args, rank, world, device):
         variants = {"prefill_p_scale_per_row": {
             "kernel_ms": round(row_ms, 4), "tops": round(ops / (row_ms * 1e-3) / 1e12, 1),
             "deviation_alpha_mode_0": deviation_prefill(pr, q, k, v, {0: orow}, units, rows)["alpha_mode_0"]}}
+        # NEXT-2 variant: first-stage scales stored in FP16 (R-29)
+        pf = ta.params(head_dim=d, block_q=64, alpha_mode=0, scale_fp16=1)
+        k1_, v1t_, k1s_, v1s_ = ta.turbo_quantize_kv(pf, cache, k, v)
+        of, lf = ta.turbo_attention_prefill(pf, q, k1_, v1t_, k1s_, v1s_, causal=True)
+        g0.record(st)
+        for _ in range(10):
+            ta.turbo_attention_prefill(pf, q, k1_, v1t_, k1s_, v1s_, causal=True, o=of, lse=lf)
+        g1.record(st)
+        torch.cuda.synchronize()
+        f_ms = g0.elapsed_time(g1) / 10
+        variants["first_stage_scales_fp16"] = {
+            "kernel_ms": round(f_ms, 4), "tops": round(ops / (f_ms * 1e-3) / 1e12, 1),
+            "deviation_alpha_mode_0": deviation_prefill(pf, q, k, v, {0: of}, units, rows)["alpha_mode_0"]}
+        del of, lf
         deviation["variants"] = variants
         del o0, o1, orow, lrow, k1_, v1t_, k1s_, v1s_
     result = dict(value=value, ms_step=ms_step, e2e=e2e, roofline=roof, clocks=clocks, quantize_kv=quant,

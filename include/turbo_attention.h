@@ -62,6 +62,11 @@ typedef struct {
   int32_t p_scale_rows;  /* prefill P-scale granularity: 0 = per B_r x B_c tile (Alg. 1, default);
                             1 = per query row x B_c block, as Alg. 2 does -- NEXT-2 variant,
                             oracle flag p_row.  The decode is always per row. */
+  int32_t scale_fp16;    /* 0 (default): first-stage scales in FP32 (R-4); 1: every stage-1 scale -- Q, K, V
+                            blocks, decode q, parent scales, s_univ -- rounded to binary16 (nearest even)
+                            before it is stored or used, as the paper stores them; codes unchanged
+                            (R-29) -- NEXT-2 variant, oracle flag scale_fp16.  Must match the value the
+                            cache was built with. */
   void* debug_tap;       /* NULL, or a turbo_debug_tap_t* (see below) */
 } turbo_params_t;
 

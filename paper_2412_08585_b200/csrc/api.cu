@@ -11,10 +11,12 @@
 
 namespace ta_host {
 cudaError_t launch_quant_prefill(const turbo_kv_cache_t* c, const __half* k, const __half* v, int N, int8_t* k1,
-                                 __half* v1t, float* k1s, float* v1s, cudaStream_t st, int j0, int Nk);
+                                 __half* v1t, float* k1s, float* v1s, cudaStream_t st, int j0, int Nk,
+                                 int scale_fp16);
 cudaError_t launch_dequant_cache(const turbo_kv_cache_t* c, int blk_begin, int blk_end, int Nk, int8_t* k1,
                                  __half* v1t, float* k1s, float* v1s, cudaStream_t st);
-cudaError_t launch_quant_append(const turbo_kv_cache_t* c, const __half* k, const __half* v, cudaStream_t st);
+cudaError_t launch_quant_append(const turbo_kv_cache_t* c, const __half* k, const __half* v, cudaStream_t st,
+                                int scale_fp16);
 cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Nk, int Hq, int Hkv, int causal, const __half* q,
                            const int8_t* k1, const __half* v1t, const float* k1s, const float* v1s, __half* o,
                            float* lse, cudaStream_t st);
@@ -50,6 +52,7 @@ turbo_status_t check_params(const turbo_params_t* p) {
   if (p->alpha_mode != 0 && p->alpha_mode != 1) return TURBO_ERR_INVALID_ARG;
   if (!(p->softmax_scale > 0.0f) || !std::isfinite(p->softmax_scale)) return TURBO_ERR_INVALID_ARG;
   if (p->p_scale_rows != 0 && p->p_scale_rows != 1) return TURBO_ERR_INVALID_ARG;
+  if (p->scale_fp16 != 0 && p->scale_fp16 != 1) return TURBO_ERR_INVALID_ARG;
   return TURBO_OK;
 }
 
@@ -100,7 +103,8 @@ turbo_status_t turbo_quantize_kv(const turbo_params_t* params, turbo_kv_cache_t*
     s = cuda_status(ta_host::launch_quant_prefill(cache, reinterpret_cast<const __half*>(k),
                                                   reinterpret_cast<const __half*>(v), n_tokens, k1_out,
                                                   reinterpret_cast<__half*>(v1t_out),
-                                                  k1_scale_out, v1_scale_out, st, 0, n_tokens));
+                                                  k1_scale_out, v1_scale_out, st, 0, n_tokens,
+                                                  params->scale_fp16));
     if (s == TURBO_OK) cache->n_tokens = n_tokens;
     return s;
   }
@@ -112,7 +116,8 @@ turbo_status_t turbo_quantize_kv(const turbo_params_t* params, turbo_kv_cache_t*
     s = cuda_status(ta_host::launch_quant_prefill(cache, reinterpret_cast<const __half*>(k),
                                                   reinterpret_cast<const __half*>(v), n_tokens, k1_out,
                                                   reinterpret_cast<__half*>(v1t_out), k1_scale_out, v1_scale_out,
-                                                  st, (int)(cache->n_tokens / params->block_kv), (int)nk));
+                                                  st, (int)(cache->n_tokens / params->block_kv), (int)nk,
+                                                  params->scale_fp16));
     if (s == TURBO_OK) cache->n_tokens = nk;
     return s;
   }
@@ -121,7 +126,7 @@ turbo_status_t turbo_quantize_kv(const turbo_params_t* params, turbo_kv_cache_t*
     if (cache->n_tokens < 1) return TURBO_ERR_INVALID_ARG;  // universal scale comes from a prefill
     if ((cache->n_tokens + 1) / params->block_kv > cache->max_blocks) return TURBO_ERR_CAPACITY;
     s = cuda_status(ta_host::launch_quant_append(cache, reinterpret_cast<const __half*>(k),
-                                                 reinterpret_cast<const __half*>(v), st));
+                                                 reinterpret_cast<const __half*>(v), st, params->scale_fp16));
     if (s == TURBO_OK) cache->n_tokens += 1;
     return s;
   }

@@ -55,7 +55,7 @@ struct DecodeArgs {
   __half* fin_o16;  // balanced schedule: final fp16 output (or NULL)
   float* fin_o32;   // balanced schedule: final f32 output (or NULL)
   float* fin_lse;   // balanced schedule: final L
-  int B, Hq, Hkv, G, max_blocks, blk_begin, blk_end, with_buffer, n_splits, alpha_mode;
+  int B, Hq, Hkv, G, max_blocks, blk_begin, blk_end, with_buffer, n_splits, alpha_mode, scale_fp16;
   float scale;
   SasConst sas;
   turbo_debug_tap_t tap;
@@ -512,7 +512,7 @@ TA_DEV void decode_segment(const DecodeArgs& a, DecodeSmem<HD, PACK>& sm, int b,
     qa = fmaxf(qa, __shfl_xor_sync(0xffffffffu, qa, 1));
     qa = fmaxf(qa, __shfl_xor_sync(0xffffffffu, qa, 2));
     const float inv = qa > 0.f ? div_119_by(qa) : 0.f;
-    s_q_row = div_by_119(qa);
+    s_q_row = st1_scale(div_by_119(qa), a.scale_fp16);  // (FP16 variant: R-29)
 #pragma unroll
     for (int i = 0; i < R; i += 4)
       if (g < (PACK ? 4 : 8))  // rows >= G are zero (and absent on the packed path)
@@ -584,7 +584,8 @@ TA_DEV void decode_segment(const DecodeArgs& a, DecodeSmem<HD, PACK>& sm, int b,
     // Buffer block (INT8, universal scale, n_buf valid keys), last.
     const int8_t* kb = a.buf + slotK * (size_t)(kBc * HD);
     const int8_t* vb = a.buf + slotV * (size_t)(kBc * HD);
-    const float sK = div_by_119(a.a_univ[slotK]), sV = div_by_119(a.a_univ[slotV]);
+    const float sK = st1_scale(div_by_119(a.a_univ[slotK]), a.scale_fp16),
+                sV = st1_scale(div_by_119(a.a_univ[slotV]), a.scale_fp16);
     int sv[M::NT][2];
     qk_buffer<HD, PACK>(kb, q1s, sv, g, q);
     const float cqk[2] = {__fmul_rn(__fmul_rn(sq2[0], sK), a.scale), __fmul_rn(__fmul_rn(sq2[1], sK), a.scale)};
@@ -908,6 +909,7 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
   a.with_buffer = with_buffer;
   a.n_splits = S;
   a.alpha_mode = p->alpha_mode;
+  a.scale_fp16 = p->scale_fp16;
   a.scale = p->softmax_scale;
   fill_sas_const(&a.sas, p->sas_nr);
   const bool has_tap = p->debug_tap != nullptr;

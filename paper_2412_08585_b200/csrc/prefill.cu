@@ -55,7 +55,7 @@ struct PrefillArgs {
   float* lse;
   const float* k1s;
   const float* v1s;
-  int B, N, Hq, Hkv, causal, block_q, alpha_mode, n_qtiles, unit_group;
+  int B, N, Hq, Hkv, causal, block_q, alpha_mode, n_qtiles, unit_group, scale_fp16;
   int Nk, q0;  // keys per sequence; absolute position of query row 0 (chunked prefill: Nk - N)
   float scale;
   SasConst sas;
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(384, 1)
                                            : fmaxf(fmaxf(sm.red_a[slot][0], sm.red_a[slot][1]),
                                                    fmaxf(sm.red_a[slot][2], sm.red_a[slot][3]));
       const float inv_q = a_q > 0.f ? div_119_by(a_q) : 0.f;
-      s_q = div_by_119(a_q);
+      s_q = st1_scale(div_by_119(a_q), args.scale_fp16);  // (FP16 variant: R-29)
 #pragma unroll
       for (int c = 0; c < HD / 16; ++c) {
         uint32_t w[4];
@@ -557,6 +557,7 @@ cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Nk, int Hq
   a.causal = causal;
   a.block_q = p->block_q;
   a.alpha_mode = p->alpha_mode;
+  a.scale_fp16 = p->scale_fp16;
   const int G = Hq / Hkv;
   const bool pair = (G % 2) == 0;  // slots = two heads of a GQA group, else two adjacent query tiles
   a.n_qtiles = (N + kTileM - 1) / kTileM;

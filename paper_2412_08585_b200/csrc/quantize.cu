@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(HD, 6 * 128 / HD) quant_prefill_kernel(
     const __half* __restrict__ k, const __half* __restrict__ v, int N, int Hkv, int max_blocks, int j0, int Nk,
     const int32_t* __restrict__ bits_dev, uint8_t* __restrict__ block_rec, float* __restrict__ s_parent,
     float* __restrict__ a_univ, int8_t* __restrict__ k1, __half* __restrict__ v1t, float* __restrict__ k1s,
-    float* __restrict__ v1s) {
+    float* __restrict__ v1s, int scale_fp16) {
   constexpr int NW = HD / 32;  // warps
   // One CTA per (block, kv head, batch, K or V): 6 small CTAs per SM keep more loads in
   // flight than 3 CTAs doing K and V together.  The block (FP16 [64][HD]) is staged with
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(HD, 6 * 128 / HD) quant_prefill_kernel(
   for (int w = 1; w < NW; ++w) a = fmaxf(a, red[w]);
   // s = max|x| / 119, codes = round_half_even(x * (119 / max|x|)) (Alg. 1; R-2, R-3, R-5)
   const float inv = a > 0.f ? div_119_by(a) : 0.f;
-  const float sc = div_by_119(a);
+  const float sc = st1_scale(div_by_119(a), scale_fp16);  // (FP16 variant: R-29; codes unchanged)
   // stage-1 code of token t, recomputed where needed (2 instructions) instead of held
   auto q1 = [&](int t) -> int {
     return rint_prod((t & 1) ? __high2float(xh[t >> 1]) : __low2float(xh[t >> 1]), inv);
@@ -299,7 +299,8 @@ template <int HD>
 __global__ void __launch_bounds__(256) quant_append_kernel(
     const __half* __restrict__ k, const __half* __restrict__ v, int Hkv, int max_blocks,
     const int32_t* __restrict__ bits_dev, const float* __restrict__ a_univ, int8_t* __restrict__ buf,
-    uint8_t* __restrict__ block_rec, float* __restrict__ s_parent, const int32_t* __restrict__ counters) {
+    uint8_t* __restrict__ block_rec, float* __restrict__ s_parent, const int32_t* __restrict__ counters,
+    int scale_fp16) {
   __shared__ __align__(16) int8_t tile[2][kBc * HD];
   const int h = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
   const int n_blocks = counters[b * 2 + 0], n_buf = counters[b * 2 + 1];
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(256) quant_append_kernel(
   __syncthreads();
 #pragma unroll
   for (int kv = 0; kv < 2; ++kv) pack_record<HD>(tile[kv], kv, bits_dev[h * 2 + kv], rec[kv] + 2 * HD, tid, 256);
-  if (tid < 2) s_parent[(bh * 2 + tid) * max_blocks + n_blocks] = div_by_119(a_univ[bh * 2 + tid]);
+  if (tid < 2) s_parent[(bh * 2 + tid) * max_blocks + n_blocks] = st1_scale(div_by_119(a_univ[bh * 2 + tid]), scale_fp16);
 }
 
 __global__ void append_counters_kernel(int32_t* counters, int B) {
@@ -404,7 +405,8 @@ namespace ta_host {
 using namespace ta;
 
 cudaError_t launch_quant_prefill(const turbo_kv_cache_t* c, const __half* k, const __half* v, int N, int8_t* k1,
-                                 __half* v1t, float* k1s, float* v1s, cudaStream_t st, int j0, int Nk) {
+                                 __half* v1t, float* k1s, float* v1s, cudaStream_t st, int j0, int Nk,
+                                 int scale_fp16) {
   // j0 = 0, Nk = N: PREFILL (resets the universal scales and the buffer); j0 > 0: a
   // further prefill chunk appended at cache block j0 (R-28), stage-1 outputs over Nk tokens.
   const int B = c->batch, H = c->n_kv_heads, HD = c->head_dim;
@@ -419,11 +421,11 @@ cudaError_t launch_quant_prefill(const turbo_kv_cache_t* c, const __half* k, con
   dim3 grid(Tc, H, 2 * B);  // z = 2 b + (K, V)
   if (HD == 128) {
     quant_prefill_kernel<128><<<grid, 128, 0, st>>>(k, v, N, H, c->max_blocks, j0, Nk, c->bits_dev, c->block_rec,
-                                                    c->s_parent, c->a_univ, k1, v1t, k1s, v1s);
+                                                    c->s_parent, c->a_univ, k1, v1t, k1s, v1s, scale_fp16);
     quant_tail_kernel<128><<<dim3(H, B), 256, 0, st>>>(k, v, N, H, c->a_univ, c->buf, c->counters, j0);
   } else {
     quant_prefill_kernel<64><<<grid, 64, 0, st>>>(k, v, N, H, c->max_blocks, j0, Nk, c->bits_dev, c->block_rec,
-                                                   c->s_parent, c->a_univ, k1, v1t, k1s, v1s);
+                                                   c->s_parent, c->a_univ, k1, v1t, k1s, v1s, scale_fp16);
     quant_tail_kernel<64><<<dim3(H, B), 256, 0, st>>>(k, v, N, H, c->a_univ, c->buf, c->counters, j0);
   }
   return cudaGetLastError();
@@ -444,14 +446,15 @@ cudaError_t launch_dequant_cache(const turbo_kv_cache_t* c, int blk_begin, int b
   return cudaGetLastError();
 }
 
-cudaError_t launch_quant_append(const turbo_kv_cache_t* c, const __half* k, const __half* v, cudaStream_t st) {
+cudaError_t launch_quant_append(const turbo_kv_cache_t* c, const __half* k, const __half* v, cudaStream_t st,
+                                int scale_fp16) {
   const int B = c->batch, H = c->n_kv_heads, HD = c->head_dim;
   if (HD == 128)
     quant_append_kernel<128><<<dim3(H, B), 256, 0, st>>>(k, v, H, c->max_blocks, c->bits_dev, c->a_univ, c->buf,
-                                                         c->block_rec, c->s_parent, c->counters);
+                                                         c->block_rec, c->s_parent, c->counters, scale_fp16);
   else
     quant_append_kernel<64><<<dim3(H, B), 256, 0, st>>>(k, v, H, c->max_blocks, c->bits_dev, c->a_univ, c->buf,
-                                                        c->block_rec, c->s_parent, c->counters);
+                                                        c->block_rec, c->s_parent, c->counters, scale_fp16);
   append_counters_kernel<<<(B + 127) / 128, 128, 0, st>>>(c->counters, B);
   return cudaGetLastError();
 }

@@ -220,3 +220,43 @@ def test_prefill_row_p_scale_tap(ta):
     np.testing.assert_array_equal(tap.p_codes.cpu().numpy()[:rows], rt["p_codes"][:rows])
     np.testing.assert_array_equal(tap.pv_int.cpu().numpy()[:rows], rt["pv_int"][:rows])
     assert tap.s_p.item() == rt["s_p"][0]
+
+
+@pytest.mark.parametrize("d,bq", [(128, 64), (64, 128)])
+def test_scale_fp16_variant_prefill(ta, d, bq):
+    """NEXT-2 variant scale_fp16 (R-29): stage-1 K/V scales and parent scales bit-exact
+    binary16 values, codes identical to the FP32 build, prefill output within tolerance of the
+    oracle with the same flag; Q's scale too (through the output)."""
+    B, N, Hq, Hkv = 2, 64 * 5 + 29, 4, 2
+    q, k, v = synth.qkv(5300 + d, B, N, Hq, Hkv, d)
+    k[:, :, 1] *= 1e-3  # small scales: binary16 near its subnormal range
+    bits = synth.head_bits_alternating(Hkv)
+    p = ta.params(head_dim=d, block_q=bq, scale_fp16=1)
+    cache, k1, o, lse = _prefill(ta, p, q, k, v, bits)
+    op = O.params(d=d, block_q=bq, scale_fp16=1)
+    ref = O.build_cache(op, k.astype(np.float32), v.astype(np.float32), bits, N // 64 + 2)
+    np.testing.assert_array_equal(k1.cpu().numpy(), ref["k1"])
+    sp = cache.s_parent.view(B, Hkv, 2, -1).cpu().numpy()
+    for b in range(B):
+        for h in range(Hkv):
+            for kind, sl in enumerate(ref["slots"][b][h]):
+                np.testing.assert_array_equal(sp[b, h, kind, :sl.n_blocks], sl.s_parent[:sl.n_blocks])
+                assert (sp[b, h, kind, :sl.n_blocks] == sp[b, h, kind, :sl.n_blocks].astype(np.float16)).all()
+    _check_prefill_heads(op, q, k, v, o, lse, [(b, h) for b in range(B) for h in range(Hq)])
+
+
+def test_scale_fp16_variant_decode_with_flush(ta):
+    """scale_fp16 through appends that flush the buffer (parent fp16(a_univ / 119)) and the buffer
+    block's scales, equal splits and the default schedule."""
+    B, N, Hq, Hkv, d = 2, 64 * 4 + 50, 8, 2, 128
+    q, k, v = synth.qkv(5400, B, N, Hq, Hkv, d)
+    bits = synth.head_bits_alternating(Hkv)
+    p, op = ta.params(head_dim=d, scale_fp16=1), O.params(d=d, scale_fp16=1)
+    apps = [synth.decode_token(5500 + t, B, Hq, Hkv, d)[1:] for t in range(20)]
+    cache, ref = _decode_setup(ta, p, op, q, k, v, bits, apps)
+    sp = cache.s_parent.view(B, Hkv, 2, -1).cpu().numpy()
+    sl = ref["slots"][1][1][1]
+    np.testing.assert_array_equal(sp[1, 1, 1, :sl.n_blocks], sl.s_parent[:sl.n_blocks])
+    qd, _, _ = synth.decode_token(5600, B, Hq, Hkv, d)
+    _check_decode(ta, p, op, cache, ref, qd, Hq // Hkv, S=1)
+    _check_decode(ta, p, op, cache, ref, qd, Hq // Hkv, S=3)
