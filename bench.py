@@ -402,13 +402,13 @@ def run_ours(args, rank, world, device):
     return result
 
 
-def decode_bytes(B, Hkv, d, nblk, nbuf, bits, Hq):
+def decode_bytes(B, Hkv, d, nblk, nbuf, bits, Hq, bc=64):
     """Algorithmic HBM bytes of one decode step: block records (s_int, z_int,
-    packed codes), parent scales, buffer rows, q in, o/lse out."""
+    packed codes), parent scales, buffer rows, q in, o/lse out (nblk blocks of bc tokens)."""
     per_bh = 0
     for h in range(Hkv):
         for kind in range(2):
-            per_bh += nblk * (2 * d + 64 * d * int(bits[h][kind]) // 8 + 4) + nbuf * d + 4
+            per_bh += nblk * (2 * d + bc * d * int(bits[h][kind]) // 8 + 4) + nbuf * d + 4
     return B * per_bh + B * Hq * d * 2 * 2 + B * Hq * 4
 
 

@@ -13,7 +13,7 @@
  *     on `stream` (0 = legacy default stream) and completes asynchronously.
  *   * Arguments are validated on the host before any launch.  Errors:
  *       TURBO_ERR_INVALID_ARG  null pointer, non-positive size, bad enum value;
- *       TURBO_ERR_UNSUPPORTED  head_dim not in {64,128}, block_kv != 64,
+ *       TURBO_ERR_UNSUPPORTED  head_dim not in {64,128}, block_kv not in {64,128},
  *                              block_q not in {64,128}, Hq % Hkv != 0,
  *                              Hq/Hkv > 8 (decode), sas_nr not in [-30,-1];
  *       TURBO_ERR_CAPACITY     an append/prefill would exceed cache->max_blocks;
@@ -54,7 +54,9 @@ typedef void* turbo_stream_t; /* a cudaStream_t */
 typedef struct {
   int32_t head_dim;      /* d_H in {64, 128} (Eq. 1) */
   int32_t block_q;       /* B_r in {64, 128}: Q stage-1 block rows and P-scale tile rows (Alg. 1) */
-  int32_t block_kv;      /* B_c = n_b = 64: K/V stage-1 block, Q2 group length, buffer size */
+  int32_t block_kv;      /* B_c = n_b in {64 (default), 128 (the block-size ablation, Table 3
+                            P:758-779)}: K/V stage-1 block, Q2 group length, buffer size, prefill key
+                            tile; must equal the cache's block_kv */
   int32_t sas_nr;        /* n_r in [-30, -1]; SAS(x) = 0 for x - m < n_r */
   int32_t alpha_mode;    /* 0: alpha = SAS(m_prev - m_new) literally (Alg. 1, R-15);
                             1: alpha = 1 when the running max is unchanged */
@@ -77,8 +79,9 @@ typedef struct {
  *   block_rec  uint8  [B][Hkv][2][max_blocks][rec_bytes]   one record per flushed
  *              Q2 block: s_int u8[d] | z_int i8[d] | packed codes (see
  *              DESIGN.md §6 "cache layout": K token-major, V channel-major with
- *              a fixed token permutation; 2-bit records use the first half of
- *              the code area).  rec_bytes = 2 d + B_c d / 2.
+ *              a fixed token permutation per 64-token sub-block -- B_c = 128
+ *              blocks hold two sub-blocks back to back; 2-bit records use the
+ *              first half of the code area).  rec_bytes = 2 d + B_c d / 2.
  *   s_parent   f32    [B][Hkv][2][max_blocks]   first-stage scale of the block
  *   buf        int8   [B][Hkv][2][B_c * d]      INT8 decode buffer (universal
  *              scale): K token-major [t][c], V channel-major [c][t]
@@ -112,9 +115,9 @@ typedef struct {
   int32_t batch, head, i_block, j_block;
   int8_t* q1;        /* [64][d] prefill, [d] decode */
   float* s_q;        /* [1] */
-  int32_t* s_int;    /* [64][64] prefill, [64] decode */
+  int32_t* s_int;    /* [64][B_c] prefill, [B_c] decode */
   float* m_new;      /* [64] / [1] */
-  uint8_t* p_codes;  /* [64][64] / [64] */
+  uint8_t* p_codes;  /* [64][B_c] / [B_c] */
   float* s_p;        /* [1] */
   int32_t* pv_int;   /* [64][d] / [d] */
 } turbo_debug_tap_t;

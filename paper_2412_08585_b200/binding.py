@@ -357,14 +357,14 @@ def turbo_combine_lse(o_parts, lse_parts, o=None, o_f32=None, want_fp16=True, st
 class DebugTap:
     """Device buffers of a turbo_debug_tap_t (exact-set intermediates of one tile)."""
 
-    def __init__(self, batch, head, i_block, j_block, head_dim, decode=False, device="cuda"):
+    def __init__(self, batch, head, i_block, j_block, head_dim, decode=False, device="cuda", block_kv=64):
         rows = 1 if decode else 64
         z = lambda *s, dt: torch.zeros(s, dtype=dt, device=device)  # noqa: E731
         self.q1 = z(rows, head_dim, dt=torch.int8)
         self.s_q = z(1, dt=torch.float32)
-        self.s_int = z(rows, 64, dt=torch.int32)
+        self.s_int = z(rows, block_kv, dt=torch.int32)
         self.m_new = z(rows, dt=torch.float32)
-        self.p_codes = z(rows, 64, dt=torch.uint8)
+        self.p_codes = z(rows, block_kv, dt=torch.uint8)
         self.s_p = z(1, dt=torch.float32)
         self.pv_int = z(rows, head_dim, dt=torch.int32)
         self.c = TurboDebugTap(batch, head, i_block, j_block, *[t.data_ptr() for t in (

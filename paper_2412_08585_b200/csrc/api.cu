@@ -46,7 +46,7 @@ namespace {
 turbo_status_t check_params(const turbo_params_t* p) {
   if (!p) return TURBO_ERR_INVALID_ARG;
   if (p->head_dim != 64 && p->head_dim != 128) return TURBO_ERR_UNSUPPORTED;
-  if (p->block_kv != 64) return TURBO_ERR_UNSUPPORTED;
+  if (p->block_kv != 64 && p->block_kv != 128) return TURBO_ERR_UNSUPPORTED;
   if (p->block_q != 64 && p->block_q != 128) return TURBO_ERR_UNSUPPORTED;
   if (p->sas_nr < -30 || p->sas_nr > -1) return TURBO_ERR_UNSUPPORTED;
   if (p->alpha_mode != 0 && p->alpha_mode != 1) return TURBO_ERR_INVALID_ARG;
@@ -79,9 +79,9 @@ turbo_status_t turbo_cache_sizes(int32_t batch, int32_t n_kv_heads, int32_t head
                                  size_t* buf_bytes, size_t* a_univ_bytes, size_t* counters_bytes) {
   if (batch < 1 || n_kv_heads < 1 || max_blocks < 0) return TURBO_ERR_INVALID_ARG;
   if (head_dim != 64 && head_dim != 128) return TURBO_ERR_UNSUPPORTED;
-  if (block_kv != 64) return TURBO_ERR_UNSUPPORTED;
+  if (block_kv != 64 && block_kv != 128) return TURBO_ERR_UNSUPPORTED;
   const size_t slots = (size_t)batch * n_kv_heads * 2;
-  if (block_rec_bytes) *block_rec_bytes = slots * max_blocks * ta::rec_bytes(head_dim);
+  if (block_rec_bytes) *block_rec_bytes = slots * max_blocks * ta::rec_bytes(head_dim, block_kv);
   if (s_parent_bytes) *s_parent_bytes = slots * max_blocks * sizeof(float);
   if (buf_bytes) *buf_bytes = slots * block_kv * head_dim;
   if (a_univ_bytes) *a_univ_bytes = slots * sizeof(float);

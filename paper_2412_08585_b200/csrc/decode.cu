@@ -31,15 +31,15 @@ constexpr int kMinUnits = 8;  // balanced schedule: least units (blocks) per war
 
 // Per-warp shared memory.  ROWS = query rows held (G <= 4 on the packed path,
 // else 8), so that twelve packed-path warps fit in one SM's 228 KB.
-template <int HD, int ROWS>
+template <int HD, int ROWS, int BC>
 struct DecodeWarpSmem {
-  uint8_t rec[2][2][rec_bytes(HD)];  // [stage][K,V][record]
+  uint8_t rec[2][2][rec_bytes(HD, BC)];  // [stage][K,V][record]
   int8_t q1[ROWS][HD];
-  uint8_t p[ROWS][kBc];
+  uint8_t p[ROWS][BC];
   uint64_t bar[2];
 };
-template <int HD, bool PACK>
-using DecodeSmem = DecodeWarpSmem<HD, PACK ? 4 : 8>;
+template <int HD, bool PACK, int BC>
+using DecodeSmem = DecodeWarpSmem<HD, PACK ? 4 : 8, BC>;
 
 struct DecodeArgs {
   const __half* q;
@@ -175,9 +175,9 @@ struct Map {
 };
 
 // QK^T on a stage-2 block (Alg. 2, folded): S_int per thread value.
-template <int HD, int BK, bool PACK>
-TA_DEV void qk_block(uint32_t rec, const int (&qv)[HD / 4], const uint4 (&q1r)[HD / 64], int (&sv)[Map<HD, PACK>::NT][2],
-                     int g, int q) {
+template <int HD, int BK, bool PACK, int BC>
+TA_DEV void qk_block(uint32_t rec, const int (&qv)[HD / 4], const uint4 (&q1r)[HD / 64],
+                     int (&sv)[Map<HD, PACK>::NT * BC / 64][2], int g, int q) {
   using U = KUnits<HD, BK>;
   constexpr int R = HD / 4;
   uint4 s4[HD / 64];
@@ -223,7 +223,7 @@ TA_DEV void qk_block(uint32_t rec, const int (&qv)[HD / 4], const uint4 (&q1r)[H
   constexpr int TB = HD * BK / 8;
   const uint32_t codes = rec + 2 * HD;
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt) {
+  for (int mt = 0; mt < BC / 16; ++mt) {
     uint32_t w0[U::NW], w1[U::NW];
     const uint32_t t0 = codes + (16 * mt + g) * TB + q * U::QB, t1 = t0 + 8 * TB;
     lds_words<U::NW>(t0, w0);  // one vector load per token region
@@ -271,11 +271,11 @@ TA_DEV void qk_block(uint32_t rec, const int (&qv)[HD / 4], const uint4 (&q1r)[H
 }
 
 // QK^T on the INT8 buffer block (token-major K, natural channels; s8 x s8).
-template <int HD, bool PACK>
-TA_DEV void qk_buffer(const int8_t* kb, uint32_t q1s, int (&sv)[Map<HD, PACK>::NT][2], int g, int q) {
+template <int HD, bool PACK, int BC>
+TA_DEV void qk_buffer(const int8_t* kb, uint32_t q1s, int (&sv)[Map<HD, PACK>::NT * BC / 64][2], int g, int q) {
   const int rn = PACK ? (g & 3) : g;
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt) {
+  for (int mt = 0; mt < BC / 16; ++mt) {
     int c[4] = {0, 0, 0, 0};
     const int t0 = 16 * mt + g, t1 = t0 + 8;
 #pragma unroll
@@ -309,17 +309,18 @@ struct RowState {
 
 // One tile of Alg. 2 on the thread's score values: running max,
 // alpha, SAS, row sum, per-row P scale and codes (to smem rows).
-template <int HD, bool PACK, bool TAP, bool FULL>
-TA_DEV void softmax_tile(const DecodeArgs& a, RowState<HD, PACK>& st, int (&sv)[Map<HD, PACK>::NT][2], int nvalid,
+template <int HD, bool PACK, bool TAP, bool FULL, int BC>
+TA_DEV void softmax_tile(const DecodeArgs& a, RowState<HD, PACK>& st, int (&sv)[Map<HD, PACK>::NT * BC / 64][2], int nvalid,
                          const float (&cqk)[2], uint32_t pbuf, float lut_lane, float (&alpha)[2], float (&s_p)[2],
                          int (&sum_p)[2], bool tap, int tap_row, int g, int q) {
   using M = Map<HD, PACK>;
+  constexpr int NT = M::NT * BC / 64;  // score values per thread and row
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
     const int row = M::row(q, e);
     int smax = INT_MIN;
 #pragma unroll
-    for (int t = 0; t < M::NT; ++t)
+    for (int t = 0; t < NT; ++t)
       if (FULL || M::tok(t, g, q) < nvalid) smax = max(smax, sv[t][e]);
     smax = grp_maxi<PACK>(smax);
     const float m_prev = st.m[e];
@@ -327,10 +328,10 @@ TA_DEV void softmax_tile(const DecodeArgs& a, RowState<HD, PACK>& st, int (&sv)[
     // alpha = SAS(m_prev - m_new) (R-15); every lane evaluates (shuffle LUT)
     const float al_s = sas_eval(__fsub_rn(m_new, m_prev), lut_lane, a.sas.nr_abs);
     const float al = m_prev == -INFINITY ? 0.f : (a.alpha_mode == 1 && m_new == m_prev) ? 1.f : al_s;
-    float pt[M::NT], rs = 0.f, pm = 0.f;
+    float pt[NT], rs = 0.f, pm = 0.f;
     const f32x2 m2 = pk2(m_new, m_new);
 #pragma unroll
-    for (int t = 0; t < M::NT; t += 2) {
+    for (int t = 0; t < NT; t += 2) {
       // x rounded on its own (scalar __fmul_rn: a packed multiply feeding the
       // subtraction would be contracted into an FFMA2)
       const f32x2 x2 = pk2(__fmul_rn((float)sv[t][e], cqk[e]), __fmul_rn((float)sv[t + 1][e], cqk[e]));
@@ -356,10 +357,10 @@ TA_DEV void softmax_tile(const DecodeArgs& a, RowState<HD, PACK>& st, int (&sv)[
     s_p[e] = div_by_119(pm);
     int sp = 0;
 #pragma unroll
-    for (int t = 0; t < M::NT; ++t) {
+    for (int t = 0; t < NT; ++t) {
       const int c = rint_prod(pt[t], inv_p);
       sp += c;
-      sts_u8(pbuf + row * kBc + M::tok(t, g, q), (uint32_t)c);
+      sts_u8(pbuf + row * BC + M::tok(t, g, q), (uint32_t)c);
       if (TAP && tap && row == tap_row) {
         a.tap.p_codes[M::tok(t, g, q)] = (uint8_t)c;
         a.tap.s_int[M::tok(t, g, q)] = M::tok(t, g, q) < nvalid ? sv[t][e] : 0;
@@ -376,63 +377,73 @@ TA_DEV void softmax_tile(const DecodeArgs& a, RowState<HD, PACK>& st, int (&sv)[
 
 // P V on a stage-2 block: raw V codes x P codes, then the exact per-channel
 // fixup s_c * acc + z_c * sum(P) (Eq. 5 fold).  Buffer block: INT8 V, no fixup.
-template <int HD, int BV, bool PACK, bool BUF>
+// B_c = 128: the two 64-token sub-blocks (layout.cuh) accumulate into the same
+// IMMA sums before the fixup.
+template <int HD, int BV, bool PACK, bool BUF, int BC>
 TA_DEV void pv_block(uint32_t rec, const int8_t* vb, uint32_t pbuf, const int (&sum_p)[2],
                      int (&acc)[Map<HD, PACK>::NC][2], int g, int q) {
   const int rn = PACK ? (g & 3) : g;
-  uint32_t bf[2][2];
+  constexpr int NU = BC / kSub;     // 64-token sub-blocks
+  constexpr int CB = kSub * BV / 8;  // bytes per channel of V codes per sub-block
+  uint32_t bf[NU][2][2];
 #pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    bf[j][0] = lds32(pbuf + rn * kBc + 32 * j + 4 * q);
-    bf[j][1] = lds32(pbuf + rn * kBc + 32 * j + 16 + 4 * q);
-  }
-  constexpr int CB = kBc * BV / 8;  // bytes per channel of V codes
+  for (int u = 0; u < NU; ++u)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      bf[u][j][0] = lds32(pbuf + rn * BC + kSub * u + 32 * j + 4 * q);
+      bf[u][j][1] = lds32(pbuf + rn * BC + kSub * u + 32 * j + 16 + 4 * q);
+    }
   const uint32_t codes = rec + 2 * HD;
   const bool ql = q >= 2;
 #pragma unroll
   for (int mt = 0; mt < HD / 16; ++mt) {
     const int c0 = 16 * mt + g, c1 = c0 + 8;
     int c[4] = {0, 0, 0, 0};
-    // the channel pair's code words, loaded once for both units / k-steps
-    uint32_t wv[4] = {0u, 0u, 0u, 0u};
-    if (!BUF) {
-      wv[0] = lds32(codes + c0 * CB + 4 * q);
-      wv[1] = lds32(codes + c1 * CB + 4 * q);
-      if (BV == 4) {
-        wv[2] = lds32(codes + c0 * CB + 4 * (4 + q));
-        wv[3] = lds32(codes + c1 * CB + 4 * (4 + q));
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+      // the channel pair's code words, loaded once for both units / k-steps
+      uint32_t wv[4] = {0u, 0u, 0u, 0u};
+      const uint32_t cu0 = codes + u * HD * CB;
+      if (!BUF) {
+        wv[0] = lds32(cu0 + c0 * CB + 4 * q);
+        wv[1] = lds32(cu0 + c1 * CB + 4 * q);
+        if (BV == 4) {
+          wv[2] = lds32(cu0 + c0 * CB + 4 * (4 + q));
+          wv[3] = lds32(cu0 + c1 * CB + 4 * (4 + q));
+        }
       }
-    }
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      uint32_t af[4];
-      if (BUF) {
-        af[0] = *reinterpret_cast<const uint32_t*>(vb + c0 * kBc + 32 * j + 4 * q);
-        af[1] = *reinterpret_cast<const uint32_t*>(vb + c1 * kBc + 32 * j + 4 * q);
-        af[2] = *reinterpret_cast<const uint32_t*>(vb + c0 * kBc + 32 * j + 16 + 4 * q);
-        af[3] = *reinterpret_cast<const uint32_t*>(vb + c1 * kBc + 32 * j + 16 + 4 * q);
-        const uint32_t b2[2] = {bf[j][0], bf[j][1]};
-        imma_s8u8(c, af, b2);
-      } else if (BV == 4) {
-        // unit j: j = 0 low nibbles (tokens 4q+e | 32+4q+e), j = 1 high nibbles x16
-        // (tokens 16+4q+e | 48+4q+e); word W = 4 j' + q holds both halves of k-step j'.
-        const uint32_t mk = j ? 0xF0F0F0F0u : 0x0F0F0F0Fu;
+      for (int j = 0; j < 2; ++j) {
+        uint32_t af[4];
+        if (BUF) {
+          const int8_t* vu = vb + kSub * u;
+          af[0] = *reinterpret_cast<const uint32_t*>(vu + c0 * BC + 32 * j + 4 * q);
+          af[1] = *reinterpret_cast<const uint32_t*>(vu + c1 * BC + 32 * j + 4 * q);
+          af[2] = *reinterpret_cast<const uint32_t*>(vu + c0 * BC + 32 * j + 16 + 4 * q);
+          af[3] = *reinterpret_cast<const uint32_t*>(vu + c1 * BC + 32 * j + 16 + 4 * q);
+          const uint32_t b2[2] = {bf[u][j][0], bf[u][j][1]};
+          imma_s8u8(c, af, b2);
+        } else if (BV == 4) {
+          // unit j: j = 0 low nibbles (tokens 4q+e | 32+4q+e), j = 1 high nibbles x16
+          // (tokens 16+4q+e | 48+4q+e); word W = 4 j' + q holds both halves of k-step j'.
+          const uint32_t mk = j ? 0xF0F0F0F0u : 0x0F0F0F0Fu;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) af[i] = wv[i] & mk;
-        // B rows of unit j: tokens (16 j + 4q..) and (32 + 16 j + 4q..)
-        const uint32_t b2[2] = {j ? bf[0][1] : bf[0][0], j ? bf[1][1] : bf[1][0]};
-        int cu[4] = {0, 0, 0, 0};
-        imma_u8u8(cu, af, b2);
+          for (int i = 0; i < 4; ++i) af[i] = wv[i] & mk;
+          // B rows of unit j: tokens (16 j + 4q..) and (32 + 16 j + 4q..)
+          const uint32_t b2[2] = {j ? bf[u][0][1] : bf[u][0][0], j ? bf[u][1][1] : bf[u][1][0]};
+          int cu[4] = {0, 0, 0, 0};
+          imma_u8u8(cu, af, b2);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) c[i] += cu[i] >> (4 * j);
-      } else {
-        const int sh = 4 * j;
-        af[0] = (wv[0] >> sh) & 0x03030303u;
-        af[1] = (wv[1] >> sh) & 0x03030303u;
-        af[2] = (wv[0] >> (sh + 2)) & 0x03030303u;
-        af[3] = (wv[1] >> (sh + 2)) & 0x03030303u;
-        const uint32_t b2[2] = {bf[j][0], bf[j][1]};
-        imma_u8u8(c, af, b2);
+          for (int i = 0; i < 4; ++i) c[i] += cu[i] >> (4 * j);
+        } else {
+          const int sh = 4 * j;
+          af[0] = (wv[0] >> sh) & 0x03030303u;
+          af[1] = (wv[1] >> sh) & 0x03030303u;
+          af[2] = (wv[0] >> (sh + 2)) & 0x03030303u;
+          af[3] = (wv[1] >> (sh + 2)) & 0x03030303u;
+          const uint32_t b2[2] = {bf[u][j][0], bf[u][j][1]};
+          imma_u8u8(c, af, b2);
+        }
       }
     }
 #pragma unroll
@@ -470,16 +481,17 @@ TA_DEV SeqUnits seq_units(const DecodeArgs& a, int b) {
 // part*G .. part*G+G-1 of o_parts / lse_parts; the final [B][Hq] layout when
 // part == b*Hkv + kvh).  `it` counts the ring iterations of this warp across
 // segments (stage = it & 1, mbarrier parity = (it >> 1) & 1).
-template <int HD, bool PACK, bool TAP>
-TA_DEV void decode_segment(const DecodeArgs& a, DecodeSmem<HD, PACK>& sm, int b, int kvh, int j0, int j1, bool use_buf,
+template <int HD, bool PACK, bool TAP, int BC>
+TA_DEV void decode_segment(const DecodeArgs& a, DecodeSmem<HD, PACK, BC>& sm, int b, int kvh, int j0, int j1, bool use_buf,
                            int nbuf, size_t part, bool tap_ok, uint32_t& it, int lane) {
   using M = Map<HD, PACK>;
   const int g = lane >> 2, q = lane & 3;
   const int G = a.G;
   const int bitsK = a.bits[kvh * 2], bitsV = a.bits[kvh * 2 + 1];
   const size_t slotK = ((size_t)b * a.Hkv + kvh) * 2, slotV = slotK + 1;
-  constexpr int REC = rec_bytes(HD);
-  const uint32_t bytesK = 2 * HD + kBc * HD * bitsK / 8, bytesV = 2 * HD + kBc * HD * bitsV / 8;
+  constexpr int REC = rec_bytes(HD, BC);
+  constexpr int NT = M::NT * BC / 64;
+  const uint32_t bytesK = 2 * HD + BC * HD * bitsK / 8, bytesV = 2 * HD + BC * HD * bitsV / 8;
   const float lut_lane = sas_lut_lane(a.sas, lane);
   const int tap_row = TAP && tap_ok && a.tap.batch == b && a.tap.head / G == kvh ? a.tap.head % G : -1;
   const uint32_t pbuf = smem_u32(&sm.p[0][0]), q1s = smem_u32(&sm.q1[0][0]);
@@ -560,18 +572,18 @@ TA_DEV void decode_segment(const DecodeArgs& a, DecodeSmem<HD, PACK>& sm, int b,
     const int stg = itj & 1;
     mbar_wait(&sm.bar[stg], (itj >> 1) & 1);
     const uint32_t recK = smem_u32(sm.rec[stg][0]), recV = smem_u32(sm.rec[stg][1]);
-    int sv[M::NT][2];
-    if (bitsK == 4) qk_block<HD, 4, PACK>(recK, qv, q1r, sv, g, q);
-    else qk_block<HD, 2, PACK>(recK, qv, q1r, sv, g, q);
+    int sv[NT][2];
+    if (bitsK == 4) qk_block<HD, 4, PACK, BC>(recK, qv, q1r, sv, g, q);
+    else qk_block<HD, 2, PACK, BC>(recK, qv, q1r, sv, g, q);
     const float sK = a.s_parent[slotK * a.max_blocks + j], sV = a.s_parent[slotV * a.max_blocks + j];
     const float cqk[2] = {__fmul_rn(__fmul_rn(sq2[0], sK), a.scale), __fmul_rn(__fmul_rn(sq2[1], sK), a.scale)};
     const bool tap = TAP && tap_row >= 0 && a.tap.j_block == j;
     float alpha[2], s_p[2];
     int sum_p[2];
-    softmax_tile<HD, PACK, TAP, true>(a, st, sv, kBc, cqk, pbuf, lut_lane, alpha, s_p, sum_p, tap, tap_row, g, q);
+    softmax_tile<HD, PACK, TAP, true, BC>(a, st, sv, BC, cqk, pbuf, lut_lane, alpha, s_p, sum_p, tap, tap_row, g, q);
     int acc[M::NC][2];
-    if (bitsV == 4) pv_block<HD, 4, PACK, false>(recV, nullptr, pbuf, sum_p, acc, g, q);
-    else pv_block<HD, 2, PACK, false>(recV, nullptr, pbuf, sum_p, acc, g, q);
+    if (bitsV == 4) pv_block<HD, 4, PACK, false, BC>(recV, nullptr, pbuf, sum_p, acc, g, q);
+    else pv_block<HD, 2, PACK, false, BC>(recV, nullptr, pbuf, sum_p, acc, g, q);
     const float cpv[2] = {__fmul_rn(s_p[0], sV), __fmul_rn(s_p[1], sV)};
     update(acc, alpha, cpv, tap);
     __syncwarp();
@@ -582,19 +594,19 @@ TA_DEV void decode_segment(const DecodeArgs& a, DecodeSmem<HD, PACK>& sm, int b,
 
   if (use_buf) {
     // Buffer block (INT8, universal scale, n_buf valid keys), last.
-    const int8_t* kb = a.buf + slotK * (size_t)(kBc * HD);
-    const int8_t* vb = a.buf + slotV * (size_t)(kBc * HD);
+    const int8_t* kb = a.buf + slotK * (size_t)(BC * HD);
+    const int8_t* vb = a.buf + slotV * (size_t)(BC * HD);
     const float sK = st1_scale(div_by_119(a.a_univ[slotK]), a.scale_fp16),
                 sV = st1_scale(div_by_119(a.a_univ[slotV]), a.scale_fp16);
-    int sv[M::NT][2];
-    qk_buffer<HD, PACK>(kb, q1s, sv, g, q);
+    int sv[NT][2];
+    qk_buffer<HD, PACK, BC>(kb, q1s, sv, g, q);
     const float cqk[2] = {__fmul_rn(__fmul_rn(sq2[0], sK), a.scale), __fmul_rn(__fmul_rn(sq2[1], sK), a.scale)};
     const bool tap = TAP && tap_row >= 0 && a.tap.j_block == -1;
     float alpha[2], s_p[2];
     int sum_p[2];
-    softmax_tile<HD, PACK, TAP, false>(a, st, sv, nbuf, cqk, pbuf, lut_lane, alpha, s_p, sum_p, tap, tap_row, g, q);
+    softmax_tile<HD, PACK, TAP, false, BC>(a, st, sv, nbuf, cqk, pbuf, lut_lane, alpha, s_p, sum_p, tap, tap_row, g, q);
     int acc[M::NC][2];
-    pv_block<HD, 4, PACK, true>(0, vb, pbuf, sum_p, acc, g, q);
+    pv_block<HD, 4, PACK, true, BC>(0, vb, pbuf, sum_p, acc, g, q);
     const float cpv[2] = {__fmul_rn(s_p[0], sV), __fmul_rn(s_p[1], sV)};
     update(acc, alpha, cpv, tap);
   }
@@ -631,11 +643,11 @@ TA_DEV void decode_segment(const DecodeArgs& a, DecodeSmem<HD, PACK>& sm, int b,
 //    W contiguous chunks of C = max(kMinUnits, ceil(total / W)) units; a warp
 //    runs one pass per (b, kv head) piece of its chunk; piece (bh, w) writes
 //    part bh + w (unique: pieces of a later bh belong to no earlier warp).
-template <int HD, bool PACK, bool TAP>
+template <int HD, bool PACK, bool TAP, int BC>
 __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_constant__ DecodeArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  DecodeSmem<HD, PACK>& sm = reinterpret_cast<DecodeSmem<HD, PACK>*>(smem_raw)[warp];
+  DecodeSmem<HD, PACK, BC>& sm = reinterpret_cast<DecodeSmem<HD, PACK, BC>*>(smem_raw)[warp];
   if (lane == 0) {
     mbar_init(&sm.bar[0], 1);
     mbar_init(&sm.bar[1], 1);
@@ -651,7 +663,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
     const int je = su.jb + su.nblk, per = (su.nblk + a.n_splits - 1) / a.n_splits;
     const int j0 = min(su.jb + split * per, je), j1 = min(j0 + per, je);
     const bool use_buf = a.with_buffer && split == a.n_splits - 1 && su.nbuf > 0;
-    decode_segment<HD, PACK, TAP>(a, sm, b, kvh, j0, j1, use_buf, su.nbuf, (size_t)split * a.B * a.Hkv + bh,
+    decode_segment<HD, PACK, TAP, BC>(a, sm, b, kvh, j0, j1, use_buf, su.nbuf, (size_t)split * a.B * a.Hkv + bh,
                                   split == 0, it, lane);
     return;
   }
@@ -691,7 +703,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
   while (pos < end) {
     const int U = su.units, kvh = (pos - base) / U, u0 = (pos - base) % U;
     const int seg_end = min(end, base + (kvh + 1) * U), u1 = seg_end - (base + kvh * U);
-    decode_segment<HD, PACK, TAP>(a, sm, b, kvh, su.jb + u0, su.jb + min(u1, su.nblk), u1 > su.nblk, su.nbuf,
+    decode_segment<HD, PACK, TAP, BC>(a, sm, b, kvh, su.jb + u0, su.jb + min(u1, su.nblk), u1 > su.nblk, su.nbuf,
                                   (size_t)b * a.Hkv + kvh + w, true, it, lane);
     pos = seg_end;
     while (pos < end && pos >= base + su.units * a.Hkv) {
@@ -858,16 +870,17 @@ using namespace ta;
 template <int HD, bool PK, bool TP>
 static int decode_ctas_per_sm() {
   int n = 0;
-  const size_t smem = sizeof(DecodeSmem<HD, PK>) * kWarpsPerCta;
-  cudaFuncSetAttribute(decode_kernel<HD, PK, TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_kernel<HD, PK, TP>, 32 * kWarpsPerCta, smem) !=
+  const size_t smem = sizeof(DecodeSmem<HD, PK, 64>) * kWarpsPerCta;
+  cudaFuncSetAttribute(decode_kernel<HD, PK, TP, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_kernel<HD, PK, TP, 64>, 32 * kWarpsPerCta, smem) !=
       cudaSuccess)
     n = 0;
   return n;
 }
 
 // Worker warps of the balanced schedule on the current device: every SM
-// filled to the decode kernel's occupancy.
+// filled to the decode kernel's occupancy (of the B_c = 64 kernel; with B_c = 128
+// the same count is a plain partition of the units).
 int decode_workers(int Hq, int Hkv, int HD) {
   int dev = 0, sms = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
@@ -931,12 +944,14 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
   const int tasks = S > 0 ? B * H * S : W;
   const dim3 grid((tasks + kWarpsPerCta - 1) / kWarpsPerCta);
   const bool pack = a.G <= 4;
-#define TA_DEC(HDV, PK, TP)                                                                             \
-  {                                                                                                     \
-    const size_t smem = sizeof(DecodeSmem<HDV, PK>) * kWarpsPerCta;                                     \
-    cudaFuncSetAttribute(decode_kernel<HDV, PK, TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    decode_kernel<HDV, PK, TP><<<grid, 32 * kWarpsPerCta, smem, st>>>(a);                              \
+#define TA_DEC_B(HDV, PK, TP, BCV)                                                                        \
+  {                                                                                                         \
+    const size_t smem = sizeof(DecodeSmem<HDV, PK, BCV>) * kWarpsPerCta;                                    \
+    cudaFuncSetAttribute(decode_kernel<HDV, PK, TP, BCV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    decode_kernel<HDV, PK, TP, BCV><<<grid, 32 * kWarpsPerCta, smem, st>>>(a);                             \
   }
+#define TA_DEC(HDV, PK, TP) \
+  if (c->block_kv == 64) TA_DEC_B(HDV, PK, TP, 64) else TA_DEC_B(HDV, PK, TP, 128)
 #define TA_DEC2(HDV)                                                  \
   if (pack) {                                                         \
     if (has_tap) TA_DEC(HDV, true, true) else TA_DEC(HDV, true, false)  \
@@ -950,6 +965,7 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
   }
 #undef TA_DEC2
 #undef TA_DEC
+#undef TA_DEC_B
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || S == 1) return e;
   if (S <= 0) {

@@ -32,16 +32,19 @@
 
 namespace ta {
 
-constexpr int kStages = 3;
 constexpr int kTileM = 128;
-constexpr int kSlotCols = 256;  // per slot: S_0 [0,64) S_1 [64,128) O [128, 128 + d)
+constexpr int kSlotCols = 256;  // per slot: S [0,128) (B_c = 64: S_0 [0,64) S_1 [64,128)) O [128, 128 + d)
+// K/V ring depth: 3 stages of 24 KB (B_c = 64), 2 stages of 48 KB (B_c = 128; 227 KB of smem)
+template <int BC>
+constexpr int stages_of() { return BC == 64 ? 3 : 2; }
 
-template <int HD>
+template <int HD, int BC>
 struct PrefillSmem {
+  static constexpr int kStages = stages_of<BC>();
   int8_t q1[2][kTileM * HD];   // Q^q1, K-major, swizzled rows of HD bytes
-  int8_t k[kStages][kBc * HD];  // K_j^q1 [64][HD]
-  __half v[kStages][HD * kBc];  // V_j^q1 codes as fp16, transposed [HD][64] (128-B rows, SW128)
-  __half stg[2][kTileM * HD];   // epilogue staging of O rows (per slot)
+  int8_t k[kStages][BC * HD];  // K_j^q1 [B_c][HD]
+  __half v[kStages][HD * BC];  // V_j^q1 codes as fp16, transposed, B_c / 64 tiles [HD][64] (128-B rows, SW128)
+  __half stg[2][kTileM * HD];  // epilogue staging of O rows (per slot)
   uint64_t kv_full[kStages], kv_empty[kStages];
   uint64_t s_full[2][2], p_full[2][2], pv_done[2], q_ready;
   uint32_t tmem_base;
@@ -82,12 +85,13 @@ constexpr float kFmin = 0.00006103515625f;  // 2^-14
 // F = 2^e m, m in [1, 2): 2^-e (exact power of two; F normal and positive)
 TA_DEV float inv_pow2_of(float F) { return __uint_as_float((uint32_t)(254 - (__float_as_uint(F) >> 23)) << 23); }
 
-template <int HD, bool TAP, bool TP, bool PROW>
+template <int HD, bool TAP, bool TP, bool PROW, int BC>
 __global__ void __launch_bounds__(384, 1)
     prefill_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                    const __grid_constant__ PrefillArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  using Smem = PrefillSmem<HD>;
+  using Smem = PrefillSmem<HD, BC>;
+  constexpr int kStages = Smem::kStages;
   // 1024-B aligned (128B-swizzle atoms); pointer arithmetic keeps the shared address space.
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -103,13 +107,13 @@ __global__ void __launch_bounds__(384, 1)
   const int it = args.n_qtiles - 1 - rem / UGg;
   const int u = grp_i * UG + rem % UGg, b = u / (args.Hkv * GS), kvh = (u / GS) % args.Hkv, hg = u % GS;
   const int h0 = kvh * G + hg * (TP ? 1 : 2);
-  const int N = args.N, Tc = (args.Nk + kBc - 1) / kBc;  // N query rows, Tc key tiles
+  const int N = args.N, Tc = (args.Nk + BC - 1) / BC;  // N query rows, Tc key tiles (B_c keys each)
   auto tile_of = [&](int s) { return TP ? 2 * it + s : it; };
   auto nkv_of = [&](int s) {
     const int ti = tile_of(s);
     if (ti * kTileM >= N) return 0;
     const int last_row = min(ti * kTileM + kTileM - 1, N - 1);
-    return args.causal ? min(Tc, (args.q0 + last_row) / kBc + 1) : Tc;
+    return args.causal ? min(Tc, (args.q0 + last_row) / BC + 1) : Tc;
   };
   const int nkv = max(nkv_of(0), nkv_of(1));  // key tiles the CTA streams (both slots walk all of them)
   const size_t bkv = (size_t)b * args.Hkv + kvh;
@@ -145,9 +149,11 @@ __global__ void __launch_bounds__(384, 1)
         for (int j = 0; j < nkv; ++j) {
           const int st = j % kStages, n = j / kStages;
           if (n > 0) mbar_wait(&sm.kv_empty[st], (n - 1) & 1);
-          mbar_expect_tx(&sm.kv_full[st], 3 * kBc * HD);  // K int8 + V fp16
-          tma_load_3d(sm.k[st], &tm_k, &sm.kv_full[st], 0, j * kBc, (int)bkv);
-          tma_load_3d(sm.v[st], &tm_v, &sm.kv_full[st], 0, 0, (int)(bkv * Tc + j));
+          mbar_expect_tx(&sm.kv_full[st], 3 * BC * HD);  // K int8 + V fp16
+          tma_load_3d(sm.k[st], &tm_k, &sm.kv_full[st], 0, j * BC, (int)bkv);
+#pragma unroll
+          for (int u = 0; u < BC / 64; ++u)  // V^T: one [HD][64] box per 64 keys
+            tma_load_3d(sm.v[st] + u * HD * 64, &tm_v, &sm.kv_full[st], 64 * u, 0, (int)(bkv * Tc + j));
         }
       }
     } else if (warp == 1 || warp == 2) {
@@ -157,38 +163,44 @@ __global__ void __launch_bounds__(384, 1)
       // thread executes in order.
       const int t = warp - 1;
       constexpr uint32_t kLayQK = HD == 128 ? kSw128 : kSw64;
-      constexpr uint32_t idesc_qk = idesc_i8(kTileM, kBc, true, true);
+      constexpr uint32_t idesc_qk = idesc_i8(kTileM, BC, true, true);
       constexpr uint32_t idesc_pv = idesc_f16(kTileM, HD);
       const uint32_t tslot = tmem + t * kSlotCols;
       mbar_wait(&sm.q_ready, 0);
       tc_fence_after();
-      for (int j = 0; j <= nkv; ++j) {
+      // B_c = 64: S double-buffered (S_{j+1} issued before PV_j).  B_c = 128: S_j takes all
+      // 128 columns, so S_{j+1} follows PV_j (lag 0).
+      constexpr int kLag = BC == 64 ? 1 : 0;
+      for (int j = 0; j < nkv + kLag; ++j) {
         if (j < nkv) {
-          const int st = j % kStages, sb = j & 1;
+          const int st = j % kStages, sb = BC == 64 ? (j & 1) : 0;
           mbar_wait(&sm.kv_full[st], (j / kStages) & 1);
           tc_fence_after();
           if (elect_one()) {
             const uint32_t q1a = smem_u32(sm.q1[t]), ka = smem_u32(sm.k[st]);
 #pragma unroll
             for (int ks = 0; ks < HD / 32; ++ks)
-              mma_i8_ss(tslot + sb * kBc, smem_desc(q1a + ks * 32, 8 * HD, kLayQK),
+              mma_i8_ss(tslot + sb * 64, smem_desc(q1a + ks * 32, 8 * HD, kLayQK),
                         smem_desc(ka + ks * 32, 8 * HD, kLayQK), idesc_qk, ks > 0);
             mma_commit(&sm.s_full[t][sb]);
           }
           __syncwarp();
         }
-        if (j >= 1) {
-          const int jj = j - 1, pb = jj & 1, st = jj % kStages;
-          mbar_wait(&sm.p_full[t][pb], (jj >> 1) & 1);
+        if (j >= kLag) {
+          const int jj = j - kLag, pb = BC == 64 ? (jj & 1) : 0, st = jj % kStages;
+          mbar_wait(&sm.p_full[t][pb], BC == 64 ? ((jj >> 1) & 1) : (jj & 1));
           tc_fence_after();
           if (elect_one()) {
             const uint32_t va = smem_u32(sm.v[st]);
 #pragma unroll
-            for (int part = 0; part < 2; ++part)  // P'_hi, then P'_lo (32 columns each)
+            for (int u = 0; u < BC / 64; ++u)  // 64-key sub-tiles: P' in columns [64u, 64u + 64)
 #pragma unroll
-              for (int ks = 0; ks < kBc / 16; ++ks)
-                mma_f16_ts(tslot + 2 * kBc, tslot + pb * kBc + part * 32 + ks * 8,
-                           smem_desc(va + ks * 32, 1024, kSw128), idesc_pv, (jj | part | ks) != 0);
+              for (int part = 0; part < 2; ++part)  // P'_hi, then P'_lo (32 columns each)
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks)
+                  mma_f16_ts(tslot + 128, tslot + (pb + u) * 64 + part * 32 + ks * 8,
+                             smem_desc(va + u * HD * 128 + ks * 32, 1024, kSw128), idesc_pv,
+                             (jj | u | part | ks) != 0);
             mma_commit(&sm.pv_done[t]);
             mma_commit(&sm.kv_empty[st]);
           }
@@ -264,19 +276,19 @@ __global__ void __launch_bounds__(384, 1)
     const int tap_j = TAP ? args.tap.j_block : -2;
 
     for (int j = 0; j < nkv; ++j) {
-      const int sb = j & 1;
-      const uint32_t tS = tbase + sb * kBc;
-      mbar_wait_spin(&sm.s_full[slot][sb], (j >> 1) & 1);
+      const int sb = BC == 64 ? (j & 1) : 0, rb = j & 1;  // S buffer; P-max exchange parity
+      const uint32_t tS = tbase + sb * 64;
+      mbar_wait_spin(&sm.s_full[slot][sb], BC == 64 ? ((j >> 1) & 1) : (j & 1));
       tc_fence_after();
-      const int nvalid = max(0, min(kBc, kmax - j * kBc + 1));  // visible keys of the tile
+      const int nvalid = max(0, min(BC, kmax - j * BC + 1));  // visible keys of the tile
       const bool active = nvalid > 0;
-      const bool full = __all_sync(0xffffffffu, nvalid == kBc);
-      uint32_t v[kBc];
-      TA_TMEM_LD32(tS, v);
-      TA_TMEM_LD32(tS + 32, (v + 32));
+      const bool full = __all_sync(0xffffffffu, nvalid == BC);
+      uint32_t v[BC];
+#pragma unroll
+      for (int c = 0; c < BC; c += 32) TA_TMEM_LD32(tS + c, (v + c));
       tmem_ld_wait();
       if (TAP && tap_row && j == tap_j)
-        for (int c = 0; c < kBc; ++c) args.tap.s_int[(r & 63) * kBc + c] = c < nvalid ? (int)v[c] : 0;
+        for (int c = 0; c < BC; ++c) args.tap.s_int[(r & 63) * BC + c] = c < nvalid ? (int)v[c] : 0;
       // x = S s_Q s_K / sqrt(d) (R-18); masked keys -> -inf
       const float cqk = __fmul_rn(__fmul_rn(s_q, args.k1s[bkv * Tc + j]), args.scale);
       const float s_v = args.v1s[bkv * Tc + j];
@@ -285,7 +297,7 @@ __global__ void __launch_bounds__(384, 1)
         const f32x2 cq2 = pk2(cqk, cqk);
         if (full) {
 #pragma unroll
-          for (int c = 0; c < kBc; c += 4) {  // two independent max chains
+          for (int c = 0; c < BC; c += 4) {  // two independent max chains
             const f32x2 x2 = mul2(pk2((float)(int)v[c], (float)(int)v[c + 1]), cq2);
             const f32x2 y2 = mul2(pk2((float)(int)v[c + 2], (float)(int)v[c + 3]), cq2);
             mt = fmaxf(mt, fmaxf(lo2(x2), hi2(x2)));
@@ -297,7 +309,7 @@ __global__ void __launch_bounds__(384, 1)
           }
         } else {
 #pragma unroll
-          for (int c = 0; c < kBc; c += 2) {
+          for (int c = 0; c < BC; c += 2) {
             const f32x2 x2 = mul2(pk2((float)(int)v[c], (float)(int)v[c + 1]), cq2);
             const float x0 = c < nvalid ? lo2(x2) : -INFINITY;
             const float x1 = c + 1 < nvalid ? hi2(x2) : -INFINITY;
@@ -324,7 +336,7 @@ __global__ void __launch_bounds__(384, 1)
         const f32x2 c3 = pk2(-0.1025f, -0.1025f), c2 = pk2(0.4626f, 0.4626f), c1 = pk2(-0.9922f, -0.9922f),
                     c0 = pk2(0.9996f, 0.9996f);
 #pragma unroll
-        for (int c = 0; c < kBc; c += 2) {
+        for (int c = 0; c < BC; c += 2) {
           const f32x2 d2 = sub2(m2, pk2(__uint_as_float(v[c]), __uint_as_float(v[c + 1])));
           const f32x2 t2 = add2_rd(d2, mg2);         // kMagic + floor(d)
           const f32x2 f2 = sub2(d2, sub2(t2, mg2));  // d - floor(d), exact
@@ -352,11 +364,11 @@ __global__ void __launch_bounds__(384, 1)
       float a_p = pmax;
       if (!PROW) {
         const float wmax = warp_max_nonneg(pmax);
-        if (lane == 0) sm.red_p[slot][sb][qd] = wmax;
+        if (lane == 0) sm.red_p[slot][rb][qd] = wmax;
         named_bar_sync(bar_grp, grp_threads);
-        a_p = args.block_q == 64 ? fmaxf(sm.red_p[slot][sb][2 * half], sm.red_p[slot][sb][2 * half + 1])
-                                 : fmaxf(fmaxf(sm.red_p[slot][sb][0], sm.red_p[slot][sb][1]),
-                                         fmaxf(sm.red_p[slot][sb][2], sm.red_p[slot][sb][3]));
+        a_p = args.block_q == 64 ? fmaxf(sm.red_p[slot][rb][2 * half], sm.red_p[slot][rb][2 * half + 1])
+                                 : fmaxf(fmaxf(sm.red_p[slot][rb][0], sm.red_p[slot][rb][1]),
+                                         fmaxf(sm.red_p[slot][rb][2], sm.red_p[slot][rb][3]));
       }
       const float inv_p = a_p > 0.f ? div_119_by(a_p) : 0.f;
       const float s_p = div_by_119(a_p);
@@ -392,7 +404,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll 1
           for (int cc = 0; cc < HD / 32; ++cc) {
             uint32_t o[32];
-            TA_TMEM_LD32(tbase + 2 * kBc + cc * 32, o);
+            TA_TMEM_LD32(tbase + 128 + cc * 32, o);
             tmem_ld_wait();
             for (int e = 0; e < 32; ++e) args.tap.pv_int[(r & 63) * HD + cc * 32 + e] = (int)__uint_as_float(o[e]);
           }
@@ -402,11 +414,11 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll 1
         for (int cc = 0; cc < HD / 32; ++cc) {
           uint32_t o[32];
-          TA_TMEM_LD32(tbase + 2 * kBc + cc * 32, o);
+          TA_TMEM_LD32(tbase + 128 + cc * 32, o);
           tmem_ld_wait();
 #pragma unroll
           for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * fix);
-          TA_TMEM_ST32(tbase + 2 * kBc + cc * 32, o);
+          TA_TMEM_ST32(tbase + 128 + cc * 32, o);
         }
         tmem_st_wait();
       }
@@ -420,23 +432,27 @@ __global__ void __launch_bounds__(384, 1)
                        nfl2 = (uint32_t)__half_as_ushort(nfl) * 0x10001u;
         constexpr float kMagicF16 = 12582912.0f + 25600.0f;  // 1.5*2^23 + 0x6400: low half = fp16(1024 + code)
         const f32x2 inv2 = pk2(inv_p, inv_p), mf2 = pk2(kMagicF16, kMagicF16);
-        uint32_t y[kBc / 2];
 #pragma unroll
-        for (int e = 0; e < kBc / 2; ++e) {
-          const f32x2 y2 = fma2(pk2(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1])), inv2, mf2);
-          if (TAP && tap_row && j == tap_j) {
-            args.tap.p_codes[(r & 63) * kBc + 2 * e] = (uint8_t)__float_as_uint(lo2(y2));
-            args.tap.p_codes[(r & 63) * kBc + 2 * e + 1] = (uint8_t)__float_as_uint(hi2(y2));
+        for (int u = 0; u < BC / 64; ++u) {  // per 64 keys: P'_hi in columns [64u, 64u + 32), P'_lo after it
+          uint32_t y[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const int c = 64 * u + 2 * e;
+            const f32x2 y2 = fma2(pk2(__uint_as_float(v[c]), __uint_as_float(v[c + 1])), inv2, mf2);
+            if (TAP && tap_row && j == tap_j) {
+              args.tap.p_codes[(r & 63) * BC + c] = (uint8_t)__float_as_uint(lo2(y2));
+              args.tap.p_codes[(r & 63) * BC + c + 1] = (uint8_t)__float_as_uint(hi2(y2));
+            }
+            y[e] = __byte_perm(__float_as_uint(lo2(y2)), __float_as_uint(hi2(y2)), 0x5410);
           }
-          y[e] = __byte_perm(__float_as_uint(lo2(y2)), __float_as_uint(hi2(y2)), 0x5410);
+          uint32_t ph[32], pl[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) ph[e] = hfma2_u32(y[e], fh2, nfh2);  // Pc F_hi, exact
+          TA_TMEM_ST32(tS + 64 * u, ph);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) pl[e] = hfma2_u32(y[e], fl2, nfl2);  // Pc F_lo, one rounding
+          TA_TMEM_ST32(tS + 64 * u + 32, pl);
         }
-        uint32_t ph[kBc / 2], pl[kBc / 2];
-#pragma unroll
-        for (int e = 0; e < kBc / 2; ++e) ph[e] = hfma2_u32(y[e], fh2, nfh2);  // Pc F_hi, exact
-        TA_TMEM_ST32(tS, ph);
-#pragma unroll
-        for (int e = 0; e < kBc / 2; ++e) pl[e] = hfma2_u32(y[e], fl2, nfl2);  // Pc F_lo, one rounding
-        TA_TMEM_ST32(tS + 32, pl);
       }
       tmem_st_wait();
       tc_fence_before();
@@ -454,7 +470,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll 1
       for (int cc = 0; cc < HD / 32; ++cc) {
         uint32_t o[32];
-        TA_TMEM_LD32(tbase + 2 * kBc + cc * 32, o);
+        TA_TMEM_LD32(tbase + 128 + cc * 32, o);
         tmem_ld_wait();
         for (int e = 0; e < 32; ++e) args.tap.pv_int[(r & 63) * HD + cc * 32 + e] = (int)__uint_as_float(o[e]);
       }
@@ -468,7 +484,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
       for (int cc = 0; cc < HD / 32; ++cc) {
         uint32_t o[32];
-        TA_TMEM_LD32(tbase + 2 * kBc + cc * 32, o);
+        TA_TMEM_LD32(tbase + 128 + cc * 32, o);
         tmem_ld_wait();
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -534,12 +550,13 @@ static bool make_map_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t 
 cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Nk, int Hq, int Hkv, int causal, const __half* q,
                            const int8_t* k1, const __half* v1t, const float* k1s, const float* v1s, __half* o,
                            float* lse, cudaStream_t st) {
-  const int HD = p->head_dim, Tc = (Nk + kBc - 1) / kBc;
+  const int HD = p->head_dim, BC = p->block_kv, Tc = (Nk + BC - 1) / BC;
   CUtensorMap tmk, tmv;
   const CUtensorMapSwizzle swk = HD == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
-  if (!make_map_3d(&tmk, k1, HD, Nk, (uint64_t)B * Hkv, HD, (uint64_t)Nk * HD, HD, kBc, swk))
+  if (!make_map_3d(&tmk, k1, HD, Nk, (uint64_t)B * Hkv, HD, (uint64_t)Nk * HD, HD, BC, swk))
     return cudaErrorInvalidValue;
-  if (!make_map_3d(&tmv, v1t, kBc, HD, (uint64_t)B * Hkv * Tc, kBc * 2, (uint64_t)HD * kBc * 2, kBc, HD,
+  // V^T blocks [B_c][HD] of fp16 codes; boxes of 64 keys x HD channels (128-B rows)
+  if (!make_map_3d(&tmv, v1t, BC, HD, (uint64_t)B * Hkv * Tc, BC * 2, (uint64_t)HD * BC * 2, 64, HD,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16))
     return cudaErrorInvalidValue;
   PrefillArgs a;
@@ -574,13 +591,15 @@ cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Nk, int Hq
     a.unit_group = std::min(units, ug);
   }
   const bool prow = p->p_scale_rows != 0;
-#define TA_LAUNCH_T(HDV, TAPV, TPV, PRV)                                                                    \
-  {                                                                                                       \
-    const size_t smem = sizeof(PrefillSmem<HDV>) + 1024;                                                  \
-    cudaFuncSetAttribute(prefill_kernel<HDV, TAPV, TPV, PRV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                         (int)smem);                                                                      \
-    prefill_kernel<HDV, TAPV, TPV, PRV><<<grid, 384, smem, st>>>(tmk, tmv, a);                           \
+#define TA_LAUNCH_B(HDV, TAPV, TPV, PRV, BCV)                                                                    \
+  {                                                                                                            \
+    const size_t smem = sizeof(PrefillSmem<HDV, BCV>) + 1024;                                                 \
+    cudaFuncSetAttribute(prefill_kernel<HDV, TAPV, TPV, PRV, BCV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                         (int)smem);                                                                           \
+    prefill_kernel<HDV, TAPV, TPV, PRV, BCV><<<grid, 384, smem, st>>>(tmk, tmv, a);                           \
   }
+#define TA_LAUNCH_T(HDV, TAPV, TPV, PRV) \
+  if (BC == 64) TA_LAUNCH_B(HDV, TAPV, TPV, PRV, 64) else TA_LAUNCH_B(HDV, TAPV, TPV, PRV, 128)
 #define TA_LAUNCH_R(HDV, TAPV, TPV) \
   if (prow) TA_LAUNCH_T(HDV, TAPV, TPV, true) else TA_LAUNCH_T(HDV, TAPV, TPV, false)
 #define TA_LAUNCH_P(HDV, TAPV) \
@@ -592,6 +611,7 @@ cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Nk, int Hq
 #undef TA_LAUNCH_P
 #undef TA_LAUNCH_R
 #undef TA_LAUNCH_T
+#undef TA_LAUNCH_B
   return cudaGetLastError();
 }
 }  // namespace ta_host

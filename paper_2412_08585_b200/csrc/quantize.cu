@@ -9,13 +9,14 @@
 namespace ta {
 
 // ---------------------------------------------------------------------------
-// Stage 2 of one channel group held in shared memory (column c of a [64][ld]
+// Stage 2 of one channel group held in shared memory (column c of a [B_c][ld]
 // int8 tile): z = min, s = max(1, ceil((max-min)/(2^b-1))), code =
 // round_half_up((v - z)/s) (R-6).  Codes are written back in place as u8.
+template <int BC>
 TA_DEV void stage2_column(int8_t* tile, int ld, int c, int bits, uint8_t* s_out, int8_t* z_out) {
   int mn = 127, mx = -128;
 #pragma unroll 8
-  for (int t = 0; t < kBc; ++t) {
+  for (int t = 0; t < BC; ++t) {
     int v = tile[t * ld + c];
     mn = min(mn, v);
     mx = max(mx, v);
@@ -28,7 +29,7 @@ TA_DEV void stage2_column(int8_t* tile, int ld, int c, int bits, uint8_t* s_out,
   // (exhaustively verified, tests/test_quant_arith.py).
   const float inv2s = __fdiv_rn(1.0f, (float)(2 * s));
 #pragma unroll 8
-  for (int t = 0; t < kBc; ++t) {
+  for (int t = 0; t < BC; ++t) {
     const int v = tile[t * ld + c];
     const int code = __float2int_rz(__fmaf_rn((float)(2 * (v - mn) + s), inv2s, 0.0009765625f));
     tile[t * ld + c] = (int8_t)(uint8_t)code;
@@ -37,16 +38,16 @@ TA_DEV void stage2_column(int8_t* tile, int ld, int c, int bits, uint8_t* s_out,
   *z_out = (int8_t)mn;
 }
 
-// Pack one stage-2 block (codes in smem tile [64][HD], u8 in [0, 2^bits)) into
+// Pack one stage-2 block (codes in smem tile [B_c][HD], u8 in [0, 2^bits)) into
 // the record's code area, following layout.cuh.  All threads of the CTA.
-template <int HD>
+template <int HD, int BC>
 TA_DEV void pack_record(const int8_t* tile, int kind, int bits, uint8_t* rec_codes, int tid, int nthr) {
   const uint8_t* q = reinterpret_cast<const uint8_t*>(tile);
   uint32_t* out = reinterpret_cast<uint32_t*>(rec_codes);
   if (kind == 0) {
     // K: token-major, natural channel order, LSB-first within a byte.
     const int words_per_tok = HD * bits / 32;
-    for (int w = tid; w < kBc * words_per_tok; w += nthr) {
+    for (int w = tid; w < BC * words_per_tok; w += nthr) {
       const int t = w / words_per_tok, wi = w % words_per_tok;
       const int per = 32 / bits;  // channels per word
       uint32_t v = 0;
@@ -56,16 +57,16 @@ TA_DEV void pack_record(const int8_t* tile, int kind, int bits, uint8_t* rec_cod
       out[w] = v;
     }
   } else {
-    // V: channel-major; per channel the token order of layout.cuh (v_word).
-    const int words_per_ch = kBc * bits / 32;
-    for (int w = tid; w < HD * words_per_ch; w += nthr) {
-      const int c = w / words_per_ch, wi = w % words_per_ch;
+    // V: channel-major per 64-token sub-block; per channel the token order of layout.cuh.
+    const int words_per_ch = kSub * bits / 32;
+    for (int w = tid; w < (BC / kSub) * HD * words_per_ch; w += nthr) {
+      const int u = w / (HD * words_per_ch), c = (w / words_per_ch) % HD, wi = w % words_per_ch;
       uint32_t v = 0;
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         if (i < 32 / bits) {
           int e, sh;
-          const int t = v_token_of(bits, wi, i, &e, &sh);
+          const int t = kSub * u + v_token_of(bits, wi, i, &e, &sh);
           v |= (uint32_t)q[t * HD + c] << (8 * e + sh);
         }
       }
@@ -76,7 +77,7 @@ TA_DEV void pack_record(const int8_t* tile, int kind, int bits, uint8_t* rec_cod
 
 // ---------------------------------------------------------------------------
 // PREFILL: one CTA per (block j, kv_head h, batch b); thread = (kind, channel)
-// holds its channel's 64 tokens in registers, so the block max, stage-1 codes,
+// holds its channel's B_c tokens in registers, so the block max, stage-1 codes,
 // the stage-2 column statistics and the V record words need no shared-memory
 // round trips; only K's token-major outputs are transposed through smem.
 
@@ -95,8 +96,8 @@ TA_DEV uint32_t pack_crumb8(uint2 v) {
   return (uint32_t)(x | (x >> 24)) & 0xFFFFu;
 }
 
-template <int HD>
-__global__ void __launch_bounds__(HD, 6 * 128 / HD) quant_prefill_kernel(
+template <int HD, int BC>
+__global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefill_kernel(
     const __half* __restrict__ k, const __half* __restrict__ v, int N, int Hkv, int max_blocks, int j0, int Nk,
     const int32_t* __restrict__ bits_dev, uint8_t* __restrict__ block_rec, float* __restrict__ s_parent,
     float* __restrict__ a_univ, int8_t* __restrict__ k1, __half* __restrict__ v1t, float* __restrict__ k1s,
@@ -106,34 +107,34 @@ __global__ void __launch_bounds__(HD, 6 * 128 / HD) quant_prefill_kernel(
   // flight than 3 CTAs doing K and V together.  The block (FP16 [64][HD]) is staged with
   // coalesced 16-byte loads; after every thread has taken its column (the barrier of the
   // max reduction) the space is reused for K's token-major stage-1 / stage-2 code tiles.
-  __shared__ __align__(16) __half xs[kBc][HD];
+  __shared__ __align__(16) __half xs[BC][HD];
   __shared__ float red[NW];
   uint8_t* tile1 = reinterpret_cast<uint8_t*>(&xs[0][0]);            // K stage-1 codes [t][c]
-  uint8_t* tile2 = reinterpret_cast<uint8_t*>(&xs[0][0]) + kBc * HD;  // K stage-2 codes [t][c]
+  uint8_t* tile2 = reinterpret_cast<uint8_t*>(&xs[0][0]) + BC * HD;  // K stage-2 codes [t][c]
   const int j = blockIdx.x, h = blockIdx.y, b = blockIdx.z >> 1, kind = blockIdx.z & 1, tid = threadIdx.x;
   const int c = tid;
   // chunk block j is cache block j0 + j; the stage-1 outputs cover Nk tokens (Tc blocks)
-  const int Tc = (Nk + kBc - 1) / kBc;
-  const int rows = min(kBc, N - j * kBc);
+  const int Tc = (Nk + BC - 1) / BC;
+  const int rows = min(BC, N - j * BC);
   const size_t bh = (size_t)b * Hkv + h;
   {
     constexpr int C8 = HD / 8;  // 16-byte chunks per token row
     const __half* src = kind ? v : k;
 #pragma unroll
-    for (int i = tid; i < kBc * C8; i += HD) {
+    for (int i = tid; i < BC * C8; i += HD) {
       const int t = i / C8, c8 = i % C8;
       uint4 val = make_uint4(0, 0, 0, 0);
       if (t < rows)
-        val = __ldcs(reinterpret_cast<const uint4*>(src + (((size_t)b * N + (size_t)j * kBc + t) * Hkv + h) * HD) + c8);
+        val = __ldcs(reinterpret_cast<const uint4*>(src + (((size_t)b * N + (size_t)j * BC + t) * Hkv + h) * HD) + c8);
       *reinterpret_cast<uint4*>(&xs[t][8 * c8]) = val;
     }
   }
   __syncthreads();
-  // the channel's 64 tokens as 32 half2
-  __half2 xh[kBc / 2];
+  // the channel's B_c tokens as B_c / 2 half2
+  __half2 xh[BC / 2];
   __half2 amax2 = __float2half2_rn(0.f);
 #pragma unroll
-  for (int t = 0; t < kBc; t += 2) {
+  for (int t = 0; t < BC; t += 2) {
     xh[t / 2] = __halves2half2(xs[t][c], xs[t + 1][c]);
     amax2 = __hmax2(amax2, __habs2(xh[t / 2]));
   }
@@ -155,17 +156,17 @@ __global__ void __launch_bounds__(HD, 6 * 128 / HD) quant_prefill_kernel(
     (kind ? v1s : k1s)[bh * Tc + j0 + j] = sc;
     // universal max-abs per (b, h, K/V) (R-9): non-negative floats order as ints
     atomicMax(reinterpret_cast<int*>(a_univ + bh * 2 + kind), __float_as_int(a));
-    if (rows == kBc) s_parent[(bh * 2 + kind) * max_blocks + j0 + j] = sc;
+    if (rows == BC) s_parent[(bh * 2 + kind) * max_blocks + j0 + j] = sc;
   }
   if (kind == 0) {
 #pragma unroll
-    for (int t = 0; t < kBc; ++t) tile1[t * HD + c] = (uint8_t)q1(t);
+    for (int t = 0; t < BC; ++t) tile1[t * HD + c] = (uint8_t)q1(t);
   } else {
     // v1t: the block transposed, [d][B_c], codes as fp16 (exact) -- the B operand
     // of the prefill's kind::f16 P V MMA; tokens past N are 0.
-    uint4* dst = reinterpret_cast<uint4*>(v1t + ((bh * Tc + j0 + j) * HD + c) * kBc);
+    uint4* dst = reinterpret_cast<uint4*>(v1t + ((bh * Tc + j0 + j) * HD + c) * BC);
 #pragma unroll
-    for (int t8 = 0; t8 < kBc / 8; ++t8) {
+    for (int t8 = 0; t8 < BC / 8; ++t8) {
       uint32_t u[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -176,15 +177,15 @@ __global__ void __launch_bounds__(HD, 6 * 128 / HD) quant_prefill_kernel(
     }
   }
   const int bits = bits_dev[h * 2 + kind];
-  constexpr int REC = rec_bytes(HD);
+  constexpr int REC = rec_bytes(HD, BC);
   uint8_t* rec = block_rec + ((bh * 2 + kind) * (size_t)max_blocks + j0 + j) * REC;
-  if (rows == kBc) {
+  if (rows == BC) {
     // Stage 2 of this channel (integer only, R-6): z = min, s = max(1, ceil((max-min)/(2^b-1))),
     // code = floor((2 (v - z) + s) / (2 s)) = fl((2(v-z)+s) * fl(1/(2s)) + 2^-10) truncated
     // (exact for these ranges, tests/test_quant_arith.py).
     int mn = q1(0), mx = mn;
 #pragma unroll
-    for (int t = 1; t < kBc; ++t) {
+    for (int t = 1; t < BC; ++t) {
       mn = min(mn, q1(t));
       mx = max(mx, q1(t));
     }
@@ -198,54 +199,61 @@ __global__ void __launch_bounds__(HD, 6 * 128 / HD) quant_prefill_kernel(
     rec[HD + c] = (uint8_t)(int8_t)mn;
     if (kind == 0) {
 #pragma unroll
-      for (int t = 0; t < kBc; ++t) tile2[t * HD + c] = (uint8_t)q(t);
+      for (int t = 0; t < BC; ++t) tile2[t * HD + c] = (uint8_t)q(t);
     } else if (bits == 4) {
-      // V, 4-bit: word W = 4jj + qd, byte e: token 32jj + 4qd + e (lo), + 16 (hi) (layout.cuh)
-      uint32_t w[8];
+      // V, 4-bit, per 64-token sub-block u: word W = 4jj + qd, byte e: token 32jj + 4qd + e (lo),
+      // + 16 (hi) (layout.cuh)
 #pragma unroll
-      for (int W = 0; W < 8; ++W) {
-        const int jj = W >> 2, qd = W & 3;
-        uint32_t acc = 0;
+      for (int u = 0; u < BC / kSub; ++u) {
+        uint32_t w[8];
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          acc |= (q(32 * jj + 4 * qd + e) | (q(32 * jj + 16 + 4 * qd + e) << 4)) << (8 * e);
-        w[W] = acc;
+        for (int W = 0; W < 8; ++W) {
+          const int jj = W >> 2, qd = W & 3, t0 = kSub * u + 32 * jj + 4 * qd;
+          uint32_t acc = 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc |= (q(t0 + e) | (q(t0 + 16 + e) << 4)) << (8 * e);
+          w[W] = acc;
+        }
+        uint4* dst = reinterpret_cast<uint4*>(rec + 2 * HD + u * (HD * kSub / 2) + c * (kSub / 2));
+        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
       }
-      uint4* dst = reinterpret_cast<uint4*>(rec + 2 * HD + c * (kBc / 2));
-      dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-      dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
     } else {
-      // V, 2-bit: word qd, byte e, bits 2s: token 32(s>>1) + 16(s&1) + 4qd + e
-      uint32_t w[4];
+      // V, 2-bit, per sub-block u: word qd, byte e, bits 2s: token 32(s>>1) + 16(s&1) + 4qd + e
 #pragma unroll
-      for (int qd = 0; qd < 4; ++qd) {
-        uint32_t acc = 0;
+      for (int u = 0; u < BC / kSub; ++u) {
+        uint32_t w[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
+        for (int qd = 0; qd < 4; ++qd) {
+          uint32_t acc = 0;
 #pragma unroll
-          for (int s2 = 0; s2 < 4; ++s2)
-            acc |= q(32 * (s2 >> 1) + 16 * (s2 & 1) + 4 * qd + e) << (8 * e + 2 * s2);
-        w[qd] = acc;
+          for (int e = 0; e < 4; ++e)
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2)
+              acc |= q(kSub * u + 32 * (s2 >> 1) + 16 * (s2 & 1) + 4 * qd + e) << (8 * e + 2 * s2);
+          w[qd] = acc;
+        }
+        *reinterpret_cast<uint4*>(rec + 2 * HD + u * (HD * kSub / 4) + c * (kSub / 4)) =
+            make_uint4(w[0], w[1], w[2], w[3]);
       }
-      *reinterpret_cast<uint4*>(rec + 2 * HD + c * (kBc / 4)) = make_uint4(w[0], w[1], w[2], w[3]);
     }
   }
   if (kind == 1) return;  // V: done (its record words were written per channel)
   __syncthreads();
   // k1 rows (token-major, natural channel order) from tile1
-  constexpr int CH16 = kBc * HD / 16;
+  constexpr int CH16 = BC * HD / 16;
   for (int i = tid; i < CH16; i += HD) {
     const int t = i / (HD / 16), c16 = i % (HD / 16);
     if (t < rows)
-      *reinterpret_cast<uint4*>(k1 + (bh * Nk + (size_t)(j0 + j) * kBc + t) * HD + c16 * 16) =
+      *reinterpret_cast<uint4*>(k1 + (bh * Nk + (size_t)(j0 + j) * BC + t) * HD + c16 * 16) =
           *reinterpret_cast<const uint4*>(tile1 + t * HD + c16 * 16);
   }
-  if (rows < kBc) return;  // partial tail block: goes to the buffer (tail kernel)
+  if (rows < BC) return;  // partial tail block: goes to the buffer (tail kernel)
   // K record codes: token-major, natural channel order, LSB-first; one uint4 = 4 words per thread
   const int kbits = bits_dev[h * 2];
   uint8_t* krec = block_rec + ((bh * 2) * (size_t)max_blocks + j0 + j) * REC + 2 * HD;
   if (kbits == 4) {
-    for (int i = tid; i < kBc * HD / 32; i += HD) {  // 32 channels (16 B of codes) per item
+    for (int i = tid; i < BC * HD / 32; i += HD) {  // 32 channels (16 B of codes) per item
       const int t = i / (HD / 32), c32 = i % (HD / 32);
       const uint4 lo = *reinterpret_cast<const uint4*>(tile2 + t * HD + c32 * 32);
       const uint4 hi = *reinterpret_cast<const uint4*>(tile2 + t * HD + c32 * 32 + 16);
@@ -254,7 +262,7 @@ __global__ void __launch_bounds__(HD, 6 * 128 / HD) quant_prefill_kernel(
                      pack_nib8(make_uint2(hi.x, hi.y)), pack_nib8(make_uint2(hi.z, hi.w)));
     }
   } else {
-    for (int i = tid; i < kBc * HD / 64; i += HD) {  // 64 channels (16 B of codes) per item
+    for (int i = tid; i < BC * HD / 64; i += HD) {  // 64 channels (16 B of codes) per item
       const int t = i / (HD / 64), c64 = i % (HD / 64);
       uint32_t w[4];
 #pragma unroll
@@ -269,12 +277,12 @@ __global__ void __launch_bounds__(HD, 6 * 128 / HD) quant_prefill_kernel(
 
 // Tail (N mod B_c tokens) -> INT8 buffer with the universal scale (R-11);
 // sets the counters.  One CTA per (kv_head, batch), thread = channel x kind.
-template <int HD>
+template <int HD, int BC>
 __global__ void quant_tail_kernel(const __half* __restrict__ k, const __half* __restrict__ v, int N, int Hkv,
                                   const float* __restrict__ a_univ, int8_t* __restrict__ buf,
                                   int32_t* __restrict__ counters, int j0) {
   const int h = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
-  const int nfull = N / kBc, ntail = N - nfull * kBc;
+  const int nfull = N / BC, ntail = N - nfull * BC;
   const size_t bh = (size_t)b * Hkv + h;
   if (h == 0 && tid == 0) {
     counters[b * 2 + 0] = j0 + nfull;
@@ -285,44 +293,44 @@ __global__ void quant_tail_kernel(const __half* __restrict__ k, const __half* __
   const float a = a_univ[bh * 2 + kv];
   const float inv = a > 0.f ? div_119_by(a) : 0.f;
   const __half* src = kv == 0 ? k : v;
-  int8_t* bslot = buf + (bh * 2 + kv) * (size_t)(kBc * HD);
+  int8_t* bslot = buf + (bh * 2 + kv) * (size_t)(BC * HD);
   for (int t = 0; t < ntail; ++t) {
-    const float x = __half2float(src[(((size_t)b * N + (size_t)nfull * kBc + t) * Hkv + h) * HD + c]);
+    const float x = __half2float(src[(((size_t)b * N + (size_t)nfull * BC + t) * Hkv + h) * HD + c]);
     const int code = max(-119, min(119, rint_prod(x, inv)));
-    bslot[kv == 0 ? t * HD + c : c * kBc + t] = (int8_t)code;
+    bslot[kv == 0 ? t * HD + c : c * BC + t] = (int8_t)code;
   }
 }
 
 // APPEND one token per sequence (P:222-224 append-then-attend).
 // One CTA per (kv_head, batch); thread = (kind, channel).  Flushes a full buffer.
-template <int HD>
+template <int HD, int BC>
 __global__ void __launch_bounds__(256) quant_append_kernel(
     const __half* __restrict__ k, const __half* __restrict__ v, int Hkv, int max_blocks,
     const int32_t* __restrict__ bits_dev, const float* __restrict__ a_univ, int8_t* __restrict__ buf,
     uint8_t* __restrict__ block_rec, float* __restrict__ s_parent, const int32_t* __restrict__ counters,
     int scale_fp16) {
-  __shared__ __align__(16) int8_t tile[2][kBc * HD];
+  __shared__ __align__(16) int8_t tile[2][BC * HD];
   const int h = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
   const int n_blocks = counters[b * 2 + 0], n_buf = counters[b * 2 + 1];
   const size_t bh = (size_t)b * Hkv + h;
-  const bool flush = n_buf + 1 == kBc;
+  const bool flush = n_buf + 1 == BC;
   if (tid < 2 * HD) {
     const int kv = tid / HD, c = tid % HD;
     const float a = a_univ[bh * 2 + kv];
     const float inv = a > 0.f ? div_119_by(a) : 0.f;
     const float x = __half2float((kv == 0 ? k : v)[bh * HD + c]);
     const int code = max(-119, min(119, rint_prod(x, inv)));
-    int8_t* bslot = buf + (bh * 2 + kv) * (size_t)(kBc * HD);
-    bslot[kv == 0 ? n_buf * HD + c : c * kBc + n_buf] = (int8_t)code;
+    int8_t* bslot = buf + (bh * 2 + kv) * (size_t)(BC * HD);
+    bslot[kv == 0 ? n_buf * HD + c : c * BC + n_buf] = (int8_t)code;
     if (flush) {
-      for (int t = 0; t < kBc; ++t)
-        tile[kv][t * HD + c] = t == n_buf ? (int8_t)code : bslot[kv == 0 ? t * HD + c : c * kBc + t];
+      for (int t = 0; t < BC; ++t)
+        tile[kv][t * HD + c] = t == n_buf ? (int8_t)code : bslot[kv == 0 ? t * HD + c : c * BC + t];
     }
   }
   if (!flush) return;
   if (n_blocks >= max_blocks) return;  // host checks capacity first
   __syncthreads();
-  constexpr int REC = rec_bytes(HD);
+  constexpr int REC = rec_bytes(HD, BC);
   uint8_t* rec[2];
 #pragma unroll
   for (int kv = 0; kv < 2; ++kv) rec[kv] = block_rec + ((bh * 2 + kv) * (size_t)max_blocks + n_blocks) * REC;
@@ -330,21 +338,21 @@ __global__ void __launch_bounds__(256) quant_append_kernel(
     const int kv = tid / HD, c = tid % HD;
     uint8_t s;
     int8_t z;
-    stage2_column(tile[kv], HD, c, bits_dev[h * 2 + kv], &s, &z);
+    stage2_column<BC>(tile[kv], HD, c, bits_dev[h * 2 + kv], &s, &z);
     rec[kv][c] = s;
     rec[kv][HD + c] = (uint8_t)z;
   }
   __syncthreads();
 #pragma unroll
-  for (int kv = 0; kv < 2; ++kv) pack_record<HD>(tile[kv], kv, bits_dev[h * 2 + kv], rec[kv] + 2 * HD, tid, 256);
+  for (int kv = 0; kv < 2; ++kv) pack_record<HD, BC>(tile[kv], kv, bits_dev[h * 2 + kv], rec[kv] + 2 * HD, tid, 256);
   if (tid < 2) s_parent[(bh * 2 + tid) * max_blocks + n_blocks] = st1_scale(div_by_119(a_univ[bh * 2 + tid]), scale_fp16);
 }
 
-__global__ void append_counters_kernel(int32_t* counters, int B) {
+__global__ void append_counters_kernel(int32_t* counters, int B, int BC) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   int nb = counters[b * 2], nbuf = counters[b * 2 + 1] + 1;
-  if (nbuf == kBc) {
+  if (nbuf == BC) {
     nb += 1;
     nbuf = 0;
   }
@@ -354,11 +362,11 @@ __global__ void append_counters_kernel(int32_t* counters, int B) {
 
 // ---------------------------------------------------------------------------
 // Stage-1 reconstruction of cache blocks (chunked prefill, R-28): block j of
-// (b, kv head) -> k1 rows [64 j, 64 j + 64) and v1t block j of the prefill
+// (b, kv head) -> k1 rows [B_c j, B_c j + B_c) and v1t block j of the prefill
 // operand layout, values code s_int + z_int (Alg. 2; exact in int8,
 // R-6), scales = the blocks' parent scales.  One CTA per (block, kv head,
 // batch), thread = (K/V, channel).
-template <int HD>
+template <int HD, int BC>
 __global__ void __launch_bounds__(2 * HD) dequant_cache_kernel(
     int Hkv, int max_blocks, int blk_begin, int blk_end, int Nk, const int32_t* __restrict__ bits_dev,
     const uint8_t* __restrict__ block_rec, const float* __restrict__ s_parent, const int32_t* __restrict__ counters,
@@ -366,10 +374,10 @@ __global__ void __launch_bounds__(2 * HD) dequant_cache_kernel(
   const int j = blk_begin + blockIdx.x, h = blockIdx.y, b = blockIdx.z, tid = threadIdx.x;
   const int nb = counters[b * 2];
   if (j >= nb || (blk_end >= 0 && j >= blk_end)) return;
-  const int kind = tid / HD, c = tid % HD, Tk = (Nk + kBc - 1) / kBc;
+  const int kind = tid / HD, c = tid % HD, Tk = (Nk + BC - 1) / BC;
   const size_t bh = (size_t)b * Hkv + h;
   const int bits = bits_dev[h * 2 + kind];
-  constexpr int REC = rec_bytes(HD);
+  constexpr int REC = rec_bytes(HD, BC);
   const uint8_t* rec = block_rec + ((bh * 2 + kind) * (size_t)max_blocks + j) * REC;
   const int sc = rec[c], zc = (int)(int8_t)rec[HD + c];
   const uint8_t* codes = rec + 2 * HD;
@@ -379,21 +387,22 @@ __global__ void __launch_bounds__(2 * HD) dequant_cache_kernel(
     // K: token-major, channel c in byte c bits / 8 at bit (c bits) % 8 (layout.cuh)
     const int TB = HD * bits / 8, byte = c * bits / 8, sh = (c * bits) % 8;
 #pragma unroll 4
-    for (int t = 0; t < kBc; ++t)
-      k1[(bh * Nk + (size_t)j * kBc + t) * HD + c] = (int8_t)((int)((codes[t * TB + byte] >> sh) & mask) * sc + zc);
+    for (int t = 0; t < BC; ++t)
+      k1[(bh * Nk + (size_t)j * BC + t) * HD + c] = (int8_t)((int)((codes[t * TB + byte] >> sh) & mask) * sc + zc);
   } else {
-    // V: channel-major words in the IMMA token order (layout.cuh v_token_of)
-    const int CB = kBc * bits / 8;
-    __align__(16) __half row[kBc];  // read back as uint4 below
-    for (int wi = 0; wi < CB / 4; ++wi)
-      for (int i = 0; i < 32 / bits; ++i) {
-        int e, sh;
-        const int t = v_token_of(bits, wi, i, &e, &sh);
-        row[t] = __int2half_rn((int)((codes[c * CB + 4 * wi + e] >> sh) & mask) * sc + zc);
-      }
-    uint4* dst = reinterpret_cast<uint4*>(v1t + ((bh * Tk + j) * HD + c) * kBc);
+    // V: channel-major words per 64-token sub-block in the IMMA token order (layout.cuh v_token_of)
+    const int CB = kSub * bits / 8;
+    __align__(16) __half row[BC];  // read back as uint4 below
+    for (int u = 0; u < BC / kSub; ++u)
+      for (int wi = 0; wi < CB / 4; ++wi)
+        for (int i = 0; i < 32 / bits; ++i) {
+          int e, sh;
+          const int t = kSub * u + v_token_of(bits, wi, i, &e, &sh);
+          row[t] = __int2half_rn((int)((codes[u * HD * CB + c * CB + 4 * wi + e] >> sh) & mask) * sc + zc);
+        }
+    uint4* dst = reinterpret_cast<uint4*>(v1t + ((bh * Tk + j) * HD + c) * BC);
 #pragma unroll
-    for (int t8 = 0; t8 < kBc / 8; ++t8) dst[t8] = reinterpret_cast<const uint4*>(row)[t8];
+    for (int t8 = 0; t8 < BC / 8; ++t8) dst[t8] = reinterpret_cast<const uint4*>(row)[t8];
   }
 }
 
@@ -404,58 +413,82 @@ __global__ void __launch_bounds__(2 * HD) dequant_cache_kernel(
 namespace ta_host {
 using namespace ta;
 
+template <int HD, int BC>
+static void quant_prefill_hd(const turbo_kv_cache_t* c, const __half* k, const __half* v, int N, int8_t* k1,
+                             __half* v1t, float* k1s, float* v1s, cudaStream_t st, int j0, int Nk, int scale_fp16) {
+  const int B = c->batch, H = c->n_kv_heads, Tc = (N + BC - 1) / BC;
+  dim3 grid(Tc, H, 2 * B);  // z = 2 b + (K, V)
+  quant_prefill_kernel<HD, BC><<<grid, HD, 0, st>>>(k, v, N, H, c->max_blocks, j0, Nk, c->bits_dev, c->block_rec,
+                                                   c->s_parent, c->a_univ, k1, v1t, k1s, v1s, scale_fp16);
+  quant_tail_kernel<HD, BC><<<dim3(H, B), 256, 0, st>>>(k, v, N, H, c->a_univ, c->buf, c->counters, j0);
+}
+
 cudaError_t launch_quant_prefill(const turbo_kv_cache_t* c, const __half* k, const __half* v, int N, int8_t* k1,
                                  __half* v1t, float* k1s, float* v1s, cudaStream_t st, int j0, int Nk,
                                  int scale_fp16) {
   // j0 = 0, Nk = N: PREFILL (resets the universal scales and the buffer); j0 > 0: a
   // further prefill chunk appended at cache block j0 (R-28), stage-1 outputs over Nk tokens.
-  const int B = c->batch, H = c->n_kv_heads, HD = c->head_dim;
-  const int Tc = (N + kBc - 1) / kBc;
+  const int B = c->batch, H = c->n_kv_heads, HD = c->head_dim, BC = c->block_kv;
   cudaError_t e = cudaSuccess;
   if (j0 == 0) {
     e = cudaMemsetAsync(c->a_univ, 0, sizeof(float) * B * H * 2, st);
     if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(c->buf, 0, (size_t)B * H * 2 * kBc * HD, st);
+    e = cudaMemsetAsync(c->buf, 0, (size_t)B * H * 2 * BC * HD, st);
     if (e != cudaSuccess) return e;
   }
-  dim3 grid(Tc, H, 2 * B);  // z = 2 b + (K, V)
   if (HD == 128) {
-    quant_prefill_kernel<128><<<grid, 128, 0, st>>>(k, v, N, H, c->max_blocks, j0, Nk, c->bits_dev, c->block_rec,
-                                                    c->s_parent, c->a_univ, k1, v1t, k1s, v1s, scale_fp16);
-    quant_tail_kernel<128><<<dim3(H, B), 256, 0, st>>>(k, v, N, H, c->a_univ, c->buf, c->counters, j0);
+    if (BC == 64) quant_prefill_hd<128, 64>(c, k, v, N, k1, v1t, k1s, v1s, st, j0, Nk, scale_fp16);
+    else quant_prefill_hd<128, 128>(c, k, v, N, k1, v1t, k1s, v1s, st, j0, Nk, scale_fp16);
   } else {
-    quant_prefill_kernel<64><<<grid, 64, 0, st>>>(k, v, N, H, c->max_blocks, j0, Nk, c->bits_dev, c->block_rec,
-                                                   c->s_parent, c->a_univ, k1, v1t, k1s, v1s, scale_fp16);
-    quant_tail_kernel<64><<<dim3(H, B), 256, 0, st>>>(k, v, N, H, c->a_univ, c->buf, c->counters, j0);
+    if (BC == 64) quant_prefill_hd<64, 64>(c, k, v, N, k1, v1t, k1s, v1s, st, j0, Nk, scale_fp16);
+    else quant_prefill_hd<64, 128>(c, k, v, N, k1, v1t, k1s, v1s, st, j0, Nk, scale_fp16);
   }
   return cudaGetLastError();
+}
+
+template <int HD, int BC>
+static void dequant_cache_hd(const turbo_kv_cache_t* c, dim3 grid, int blk_begin, int blk_end, int Nk, int8_t* k1,
+                             __half* v1t, float* k1s, float* v1s, cudaStream_t st) {
+  dequant_cache_kernel<HD, BC><<<grid, 2 * HD, 0, st>>>(c->n_kv_heads, c->max_blocks, blk_begin, blk_end, Nk,
+                                                        c->bits_dev, c->block_rec, c->s_parent, c->counters, k1, v1t,
+                                                        k1s, v1s);
 }
 
 cudaError_t launch_dequant_cache(const turbo_kv_cache_t* c, int blk_begin, int blk_end, int Nk, int8_t* k1,
                                  __half* v1t, float* k1s, float* v1s, cudaStream_t st) {
-  const int B = c->batch, H = c->n_kv_heads, HD = c->head_dim;
+  const int B = c->batch, H = c->n_kv_heads, HD = c->head_dim, BC = c->block_kv;
   const int last = blk_end >= 0 ? std::min(blk_end, c->max_blocks) : c->max_blocks;
   if (last <= blk_begin) return cudaSuccess;
   dim3 grid(last - blk_begin, H, B);
-  if (HD == 128)
-    dequant_cache_kernel<128><<<grid, 256, 0, st>>>(H, c->max_blocks, blk_begin, blk_end, Nk, c->bits_dev,
-                                                    c->block_rec, c->s_parent, c->counters, k1, v1t, k1s, v1s);
-  else
-    dequant_cache_kernel<64><<<grid, 128, 0, st>>>(H, c->max_blocks, blk_begin, blk_end, Nk, c->bits_dev,
-                                                   c->block_rec, c->s_parent, c->counters, k1, v1t, k1s, v1s);
+  if (HD == 128) {
+    if (BC == 64) dequant_cache_hd<128, 64>(c, grid, blk_begin, blk_end, Nk, k1, v1t, k1s, v1s, st);
+    else dequant_cache_hd<128, 128>(c, grid, blk_begin, blk_end, Nk, k1, v1t, k1s, v1s, st);
+  } else {
+    if (BC == 64) dequant_cache_hd<64, 64>(c, grid, blk_begin, blk_end, Nk, k1, v1t, k1s, v1s, st);
+    else dequant_cache_hd<64, 128>(c, grid, blk_begin, blk_end, Nk, k1, v1t, k1s, v1s, st);
+  }
   return cudaGetLastError();
+}
+
+template <int HD, int BC>
+static void quant_append_hd(const turbo_kv_cache_t* c, const __half* k, const __half* v, cudaStream_t st,
+                            int scale_fp16) {
+  quant_append_kernel<HD, BC><<<dim3(c->n_kv_heads, c->batch), 256, 0, st>>>(
+      k, v, c->n_kv_heads, c->max_blocks, c->bits_dev, c->a_univ, c->buf, c->block_rec, c->s_parent, c->counters,
+      scale_fp16);
 }
 
 cudaError_t launch_quant_append(const turbo_kv_cache_t* c, const __half* k, const __half* v, cudaStream_t st,
                                 int scale_fp16) {
-  const int B = c->batch, H = c->n_kv_heads, HD = c->head_dim;
-  if (HD == 128)
-    quant_append_kernel<128><<<dim3(H, B), 256, 0, st>>>(k, v, H, c->max_blocks, c->bits_dev, c->a_univ, c->buf,
-                                                         c->block_rec, c->s_parent, c->counters, scale_fp16);
-  else
-    quant_append_kernel<64><<<dim3(H, B), 256, 0, st>>>(k, v, H, c->max_blocks, c->bits_dev, c->a_univ, c->buf,
-                                                        c->block_rec, c->s_parent, c->counters, scale_fp16);
-  append_counters_kernel<<<(B + 127) / 128, 128, 0, st>>>(c->counters, B);
+  const int B = c->batch, HD = c->head_dim, BC = c->block_kv;
+  if (HD == 128) {
+    if (BC == 64) quant_append_hd<128, 64>(c, k, v, st, scale_fp16);
+    else quant_append_hd<128, 128>(c, k, v, st, scale_fp16);
+  } else {
+    if (BC == 64) quant_append_hd<64, 64>(c, k, v, st, scale_fp16);
+    else quant_append_hd<64, 128>(c, k, v, st, scale_fp16);
+  }
+  append_counters_kernel<<<(B + 127) / 128, 128, 0, st>>>(c->counters, B, BC);
   return cudaGetLastError();
 }
 }  // namespace ta_host

@@ -60,8 +60,14 @@ def test_host_validation_without_gpu(L):
     assert L.turbo_attention_prefill(C.byref(p), 1, 64, 3, 2, 1, *[None] * 7, None) == b.TURBO_ERR_UNSUPPORTED
     assert L.turbo_attention_prefill(C.byref(p), 1, 64, 2, 2, 1, *[None] * 7, None) == b.TURBO_ERR_INVALID_ARG
     assert L.turbo_attention_prefill(None, 1, 64, 2, 2, 1, *[None] * 7, None) == b.TURBO_ERR_INVALID_ARG
-    bad = b.params(head_dim=128, block_kv=128)
+    bad = b.params(head_dim=128, block_kv=96)  # B_c in {64, 128}
     assert L.turbo_attention_prefill(C.byref(bad), 1, 64, 2, 2, 1, *[None] * 7, None) == b.TURBO_ERR_UNSUPPORTED
+    ok128 = b.params(head_dim=128, block_kv=128)
+    assert L.turbo_attention_prefill(C.byref(ok128), 1, 64, 2, 2, 1, *[None] * 7, None) == b.TURBO_ERR_INVALID_ARG
+    sz = C.c_size_t()
+    assert L.turbo_cache_sizes(1, 1, 128, 128, 3, C.byref(sz), None, None, None, None) == b.TURBO_OK
+    assert sz.value == 2 * 3 * (2 * 128 + 128 * 128 // 2)
+    assert L.turbo_cache_sizes(1, 1, 128, 32, 3, C.byref(sz), None, None, None, None) == b.TURBO_ERR_UNSUPPORTED
     bad = b.params(head_dim=128, sas_nr=0)
     assert L.turbo_attention_prefill(C.byref(bad), 1, 64, 2, 2, 1, *[None] * 7, None) == b.TURBO_ERR_UNSUPPORTED
     assert L.turbo_combine_lse(0, 1, 1, None, None, None, None, None, None) == b.TURBO_ERR_INVALID_ARG

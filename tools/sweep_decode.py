@@ -16,16 +16,17 @@ if os.environ.get("DEC_SHAPES"):  # "B,N,Hq,Hkv,d;..." with split list SPLX (e.g
     SPLX = tuple(int(x) for x in os.environ.get("SPLX", "0").split(","))
     SHAPES = [("G%d" % (int(t.split(",")[2]) // int(t.split(",")[3])), tuple(int(x) for x in t.split(",")), SPLX)
               for t in os.environ["DEC_SHAPES"].split(";")]
+BC = int(os.environ.get("TP_BC", "64"))  # block_kv
 for name, (B, N, Hq, Hkv, d), splits in SHAPES:
     bits = synth.head_bits_alternating(Hkv)
-    p = ta.params(head_dim=d)
-    cache = ta.KVCache(B, Hkv, d, max_blocks=N // 64 + 4, bits=bits)
+    p = ta.params(head_dim=d, block_kv=BC)
+    cache = ta.KVCache(B, Hkv, d, max_blocks=N // BC + 4, bits=bits, block_kv=BC)
     _, k, v = synth.qkv_torch(3003, B, N, Hkv, Hkv, d)
     ta.turbo_quantize_kv(p, cache, k, v)
     del k, v
     torch.cuda.empty_cache()
     qd = synth.qkv_torch(7, B, 1, Hq, Hkv, d)[0][:, 0].contiguous()
-    byt = bench.decode_bytes(B, Hkv, d, N // 64, 0, bits, Hq)
+    byt = bench.decode_bytes(B, Hkv, d, N // BC, 0, bits, Hq, BC)
     for S in splits:
         ws = torch.empty(max(ta.turbo_decode_workspace_bytes(B, Hq, Hkv, d, S), 16), dtype=torch.uint8, device="cuda")
         for _ in range(3):
@@ -37,6 +38,6 @@ for name, (B, N, Hq, Hkv, d), splits in SHAPES:
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 20
-        print(f"{name} B={B} N={N} S={S:3d} {ms * 1e3:8.1f} us  {byt / ms / 1e6:8.1f} GB/s", flush=True)
+        print(f"{name} BC={BC} B={B} N={N} S={S:3d} {ms * 1e3:8.1f} us  {byt / ms / 1e6:8.1f} GB/s", flush=True)
     del cache
     torch.cuda.empty_cache()

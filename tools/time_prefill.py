@@ -13,9 +13,11 @@ B, N, Hq, Hkv, d = (1, 32768, 64, 8, 128) if os.environ.get("TP_CFG") == "70b" e
 if os.environ.get("TP_SHAPE"):  # "B,N,Hq,Hkv,d" (e.g. MHA: 8,4096,32,32,128)
     B, N, Hq, Hkv, d = (int(x) for x in os.environ["TP_SHAPE"].split(","))
 p = ta.params(head_dim=d, p_scale_rows=int(os.environ.get("TP_PROW", "0")),
-              alpha_mode=int(os.environ.get("TP_ALPHA", "0")), block_q=int(os.environ.get("TP_BQ", "64")))
+              alpha_mode=int(os.environ.get("TP_ALPHA", "0")), block_q=int(os.environ.get("TP_BQ", "64")),
+              block_kv=int(os.environ.get("TP_BC", "64")))
 q, k, v = synth.qkv_torch(1002, B, N, Hq, Hkv, d)
-cache = ta.KVCache(B, Hkv, d, max_blocks=N // 64 + 2, bits=synth.head_bits_alternating(Hkv))
+cache = ta.KVCache(B, Hkv, d, max_blocks=N // p.block_kv + 2, bits=synth.head_bits_alternating(Hkv),
+                   block_kv=p.block_kv)
 k1, v1t, k1s, v1s = ta.turbo_quantize_kv(p, cache, k, v)
 o, lse = ta.turbo_attention_prefill(p, q, k1, v1t, k1s, v1s)
 for _ in range(3):
