@@ -61,7 +61,7 @@ class Params(C.Structure):
         ("d", C.c_int32), ("block_q", C.c_int32), ("block_kv", C.c_int32), ("sas_nr", C.c_int32),
         ("alpha_mode", C.c_int32), ("softmax_scale", C.c_float), ("quant", C.c_int32), ("sas", C.c_int32),
         ("p_row", C.c_int32),
-        ("scale_fp16", C.c_int32),
+        ("scale_fp16", C.c_int32), ("sas_fp16", C.c_int32),
     ]
 
 
@@ -96,6 +96,10 @@ def _declare(L):
     L.tq_sas_poly.restype = f32
     L.tq_sas.argtypes = [f32, i32]
     L.tq_sas.restype = f32
+    L.tq_sas_poly_fp16.argtypes = [f32]
+    L.tq_sas_poly_fp16.restype = f32
+    L.tq_sas_fp16.argtypes = [f32, i32]
+    L.tq_sas_fp16.restype = f32
     L.tq_sas_softmax_rows.argtypes = [i32, i32, vp, i32, vp]
     L.tq_quant_sym8.argtypes = [vp, i64, vp, vp]
     L.tq_quant_asym.argtypes = [vp, i32, i64, i32, vp, i64, vp, vp]
@@ -122,12 +126,13 @@ def _declare(L):
 
 
 def params(d=128, block_q=64, block_kv=64, sas_nr=-6, alpha_mode=0, softmax_scale=None, quant=1, sas=1, p_row=0,
-           scale_fp16=0):
+           scale_fp16=0, sas_fp16=0):
     """Paper defaults: B_r = B_c = n_b = 64, n_r = -6; p_row=1 is the
-    per-row prefill P scale (NEXT-2 variant)."""
+    per-row prefill P scale, scale_fp16=1 FP16 first-stage scales, sas_fp16=1 the FP16 SAS
+    polynomial (NEXT-2 variants)."""
     if softmax_scale is None:
         softmax_scale = float(np.float32(1.0) / np.sqrt(np.float32(d)))
-    return Params(d, block_q, block_kv, sas_nr, alpha_mode, softmax_scale, quant, sas, p_row, scale_fp16)
+    return Params(d, block_q, block_kv, sas_nr, alpha_mode, softmax_scale, quant, sas, p_row, scale_fp16, sas_fp16)
 
 
 def _f32(x):
@@ -147,6 +152,14 @@ def sas_poly(f: float) -> np.float32:
 
 def sas(dist: float, nr=-6) -> np.float32:
     return np.float32(lib().tq_sas(float(np.float32(dist)), nr))
+
+
+def sas_poly_fp16(f: float) -> np.float32:
+    return np.float32(lib().tq_sas_poly_fp16(float(np.float32(f))))
+
+
+def sas_fp16(dist: float, nr=-6) -> np.float32:
+    return np.float32(lib().tq_sas_fp16(float(np.float32(dist)), nr))
 
 
 def sas_softmax_rows(x: np.ndarray, nr=-6) -> np.ndarray:

@@ -21,6 +21,45 @@
 
 #define TQ_DIV 119.0f /* Alg. 1: s = max(abs(X)) / 119 */
 
+/* IEEE binary16 rounding (nearest, ties to even) of a float, returned as a float: the
+ * first-stage scales of the scale_fp16 variant (P:297 "FP16" scales; R-29).  Written out
+ * from the format's definition: 11 significant bits, quantum 2^(e-11) for |s| in
+ * [2^(e-1), 2^e), never finer than the subnormal quantum 2^-24, overflow past 65504. */
+static float round_fp16(float s) {
+  double a = fabs((double)s);
+  if (a == 0.0 || !isfinite(a)) return s;
+  int e;
+  frexp(a, &e);
+  int q = e - 11;
+  if (q < -24) q = -24;
+  double r = ldexp(rint(ldexp(a, -q)), q);  /* rint: round half to even (default mode) */
+  if (r > 65504.0) r = INFINITY;
+  return (float)(s < 0.0f ? -r : r);
+}
+
+/* binary16 fused multiply-add: the binary16 rounding (nearest even) of the EXACT a*b + c
+ * for binary16 values a, b, c (sas_fp16 variant, R-30).  Every binary16 value is an integer
+ * multiple of 2^-24, so a*b + c = K 2^-48 with |K| < 2^81: K is formed exactly in 128-bit
+ * integers and rounded once, with the quantum rule of round_fp16. */
+static float fma_fp16(float a, float b, float c) {
+  const __int128 ka = (__int128)ldexp((double)a, 24), kb = (__int128)ldexp((double)b, 24);
+  const __int128 kc = (__int128)ldexp((double)c, 24);
+  const __int128 K = ka * kb + kc * ((__int128)1 << 24);
+  if (K == 0) return 0.0f;
+  unsigned __int128 m = (unsigned __int128)(K < 0 ? -K : K);
+  int e = 0;                                   /* |K| in [2^(e-1), 2^e) */
+  while (e < 127 && (m >> e) != 0) ++e;
+  int q = (e - 48) - 11;                       /* quantum exponent of the result */
+  if (q < -24) q = -24;
+  const int sh = q + 48;                       /* >= 24: drop sh bits of K */
+  unsigned __int128 r = m >> sh;
+  const unsigned __int128 rem = m & (((unsigned __int128)1 << sh) - 1), half = (unsigned __int128)1 << (sh - 1);
+  if (rem > half || (rem == half && (r & 1))) ++r;
+  double v = ldexp((double)(uint64_t)r, q);
+  if (v > 65504.0) v = INFINITY;
+  return (float)(K < 0 ? -v : v);
+}
+
 /* ------------------------------------------------------------------------ */
 /* SAS: e^{-x} ~= LUT(x_int) * POLY(x_dec), 0 below the threshold n_r.       */
 /* ------------------------------------------------------------------------ */
@@ -50,6 +89,30 @@ float tq_sas(float dist, int32_t nr) {
   return lut_i * tq_sas_poly(f);
 }
 
+/* sas_fp16 variant (the polynomial "in FP16"; R-30): the same threshold, floor and
+ * exact fraction, then f and the four printed coefficients rounded to binary16 and POLY by
+ * Horner with binary16 fused multiply-adds; the LUT factor and the product stay binary32. */
+float tq_sas_poly_fp16(float f) {
+  const float c3 = round_fp16(-0.1025f), c2 = round_fp16(0.4626f), c1 = round_fp16(-0.9922f),
+              c0 = round_fp16(0.9996f);
+  const float fh = round_fp16(f);
+  return fma_fp16(fma_fp16(fma_fp16(c3, fh, c2), fh, c1), fh, c0);
+}
+
+float tq_sas_fp16(float dist, int32_t nr) {
+  if (dist > (float)(-nr)) return 0.0f;
+  float fi = floorf(dist);
+  int32_t i = (int32_t)fi;
+  float f = dist - fi;
+  float lut_i = (float)exp(-(double)i);
+  return lut_i * tq_sas_poly_fp16(f);
+}
+
+/* The SAS a parameter set selects (FP32 Horner, or the sas_fp16 variant). */
+static float sas_p(const tq_params* p, float dist) {
+  return p->sas_fp16 ? tq_sas_fp16(dist, p->sas_nr) : tq_sas(dist, p->sas_nr);
+}
+
 /* Appendix B: row-normalised SAS softmax.  Step 1 subtract the
  * row max, step 2 threshold, steps 3-4 LUT x POLY, step 5 divide by row sum. */
 void tq_sas_softmax_rows(int32_t rows, int32_t cols, const float* x, int32_t nr, float* out) {
@@ -67,21 +130,6 @@ void tq_sas_softmax_rows(int32_t rows, int32_t cols, const float* x, int32_t nr,
   }
 }
 
-/* IEEE binary16 rounding (nearest, ties to even) of a float, returned as a float: the
- * first-stage scales of the scale_fp16 variant (P:297 "FP16" scales; R-29).  Written out
- * from the format's definition: 11 significant bits, quantum 2^(e-11) for |s| in
- * [2^(e-1), 2^e), never finer than the subnormal quantum 2^-24, overflow past 65504. */
-static float round_fp16(float s) {
-  double a = fabs((double)s);
-  if (a == 0.0 || !isfinite(a)) return s;
-  int e;
-  frexp(a, &e);
-  int q = e - 11;
-  if (q < -24) q = -24;
-  double r = ldexp(rint(ldexp(a, -q)), q);  /* rint: round half to even (default mode) */
-  if (r > 65504.0) r = INFINITY;
-  return (float)(s < 0.0f ? -r : r);
-}
 
 /* A first-stage scale as used and stored: FP32, or its FP16 rounding (scale_fp16). */
 static float st1(const tq_params* p, float s) { return p->scale_fp16 ? round_fp16(s) : s; }
@@ -245,7 +293,7 @@ int32_t tq_cache_append_slot(const tq_params* p, const float* x, tq_slot* s) {
 
 static float expo(const tq_params* p, float dist) {
   /* P~ = SAS(x - m), or the exact exponential under the P5 switch. */
-  return p->sas ? tq_sas(dist, p->sas_nr) : (float)exp(-(double)dist);
+  return p->sas ? sas_p(p, dist) : (float)exp(-(double)dist);
 }
 
 /* One row of one tile.  x[c] = -inf marks masked keys.  Returns 0 when the row
@@ -261,7 +309,7 @@ static int32_t row_step(const tq_params* p, int32_t nc, const float* x, float* m
   if (m_prev == -INFINITY) alpha = 0.0;
   else if (!p->sas) alpha = exp((double)m_prev - (double)m_new);
   else if (p->alpha_mode == 1 && m_new == m_prev) alpha = 1.0;
-  else alpha = (double)tq_sas(m_new - m_prev, p->sas_nr);
+  else alpha = (double)sas_p(p, m_new - m_prev);
   double rowsum = 0.0;
   for (int32_t c = 0; c < nc; ++c) {
     pt[c] = x[c] == -INFINITY ? 0.0f : expo(p, m_new - x[c]);

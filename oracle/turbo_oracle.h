@@ -36,6 +36,8 @@ typedef struct {
   int32_t scale_fp16;    /* first-stage scales stored in FP16 (Eq. 8 text): every stage-1 scale
                             s = max|x|/119 (Q, K, V blocks, decode q, parent scales, s_univ) is rounded to
                             binary16 (nearest even) before use; codes unchanged (R-29) -- NEXT-2 variant */
+  int32_t sas_fp16;      /* SAS polynomial in FP16: f and the coefficients rounded to binary16,
+                            Horner with binary16 FMAs; LUT and product in binary32 (R-30) -- NEXT-2 variant */
 } tq_params;
 
 /* One cache "slot" = one (batch, kv_head, K-or-V) stream.  Logical layout
@@ -85,6 +87,8 @@ typedef struct {
 void tq_sas_lut(int32_t nr, float* lut /* [-nr + 1] */);
 float tq_sas_poly(float f);
 float tq_sas(float dist, int32_t nr);
+float tq_sas_poly_fp16(float f);
+float tq_sas_fp16(float dist, int32_t nr);
 void tq_sas_softmax_rows(int32_t rows, int32_t cols, const float* x, int32_t nr, float* out);
 
 /* --- FlashQ stage 1 / stage 2 (Eq. 9/10; Alg. 1) --- */

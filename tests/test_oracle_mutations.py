@@ -13,7 +13,8 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = os.path.join(ROOT, "oracle", "turbo_oracle.c")
-PINS = ["tests/test_oracle_decode_pins.py", "tests/test_oracle_pins.py", "tests/test_chunked_oracle.py"]
+PINS = ["tests/test_oracle_decode_pins.py", "tests/test_oracle_pins.py", "tests/test_chunked_oracle.py",
+        "tests/test_oracle_sas_fp16.py"]
 
 # (name, original text, mutated text) -- each original must occur in the source
 MUTATIONS = [
@@ -52,6 +53,18 @@ MUTATIONS = [
     ("FP16 scale variant: binary16 ties rounded away from zero (R-29)",
      "double r = ldexp(rint(ldexp(a, -q)), q);",
      "double r = ldexp(round(ldexp(a, -q)), q);"),
+    ("FP16 SAS: fraction left in binary32 (R-30)",
+     "const float fh = round_fp16(f);",
+     "const float fh = f;"),
+    ("FP16 SAS: binary16 FMA double-rounded through binary32 (R-30)",
+     "  return fma_fp16(fma_fp16(fma_fp16(c3, fh, c2), fh, c1), fh, c0);",
+     "  return round_fp16(fmaf(round_fp16(fmaf(round_fp16(fmaf(c3, fh, c2)), fh, c1)), fh, c0));"),
+    ("FP16 SAS: Horner in binary32, rounded to binary16 once (R-30)",
+     "  return fma_fp16(fma_fp16(fma_fp16(c3, fh, c2), fh, c1), fh, c0);",
+     "  return round_fp16(fmaf(fmaf(fmaf(c3, fh, c2), fh, c1), fh, c0));"),
+    ("FP16 SAS not used for alpha (R-30)",
+     "  else alpha = (double)sas_p(p, m_new - m_prev);",
+     "  else alpha = (double)tq_sas(m_new - m_prev, p->sas_nr);"),
     ("universal scale from the last block only (R-9)",
      "float a_univ = 0.0f;\n  for (int64_t i = 0; i < (int64_t)n * d; ++i) a_univ = fmaxf(a_univ, fabsf(x[i]));",
      "float a_univ = 0.0f;\n  for (int64_t i = (int64_t)(n - 1) / bc * bc * d; i < (int64_t)n * d; ++i)"

@@ -15,3 +15,15 @@ def test_division_free_round_half_up_is_exact():
             a = 2 * diff + s
             fused = (a.astype(np.float64) * np.float64(inv) + 2.0 ** -10).astype(np.float32)
             np.testing.assert_array_equal(np.trunc(fused).astype(np.int64), a // (2 * s))
+
+
+def test_mulhi_round_half_up_is_exact():
+    """quantize.cu:quant_prefill_kernel: code = umulhi(a, M), M = floor((2^32 - 1) / 2s) + 1
+    = ceil(2^32 / 2s), equals floor(a / (2s)) for every a = 2(v - z) + s a stage-2 group can
+    produce (v - z <= 238, s <= 80) -- the multiply-high form of R-6's round half up."""
+    for s in range(1, 81):
+        D = 2 * s
+        M = (0xFFFFFFFF // D) + 1
+        assert M < 2 ** 32
+        a = np.arange(0, 2 * 238 + 80 + 1, dtype=np.uint64)
+        np.testing.assert_array_equal((a * np.uint64(M)) >> np.uint64(32), a // np.uint64(D))

@@ -1,2 +1,5 @@
-TURBO_LIB=variants/qL3.so timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "quantize or append" 2>&1 | tail -1
-bash tools/ab.sh tools/time_quant.py variants/head.so variants/qL3.so variants/qL4.so
+#!/bin/bash
+# quantize_kv A/B: parity of the candidate library, then interleaved timings (tools/time_quant.py)
+cand=${1:-variants/qv2.so}
+TURBO_LIB=$cand timeout 900 python -m pytest tests -m gpu -x -q -k "quantize or append or bc128 or chunk" 2>&1 | tail -1
+for rep in 1 2 3; do for lib in variants/head.so $cand; do TURBO_LIB=$lib timeout 300 python tools/time_quant.py; done; done
