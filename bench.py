@@ -357,37 +357,35 @@ def run_ours(args, rank, world, device):
         deviation = {"prefill_configs1": dict(
             units=f"(b, q head) {units}, {len(rows)} query rows each (every 29th + the last)",
             **deviation_prefill(p, q, k, v, {0: o0, 1: o1}, units, rows))}
-        # NEXT-2 variant: prefill P scale per row x B_c block (Alg. 2's granularity) instead of
-        # per B_r x B_c tile (Alg. 1): kernel speed and deviation on the same units
-        pr = ta.params(head_dim=d, block_q=64, alpha_mode=0, p_scale_rows=1)
-        k1_, v1t_, k1s_, v1s_ = ta.turbo_quantize_kv(pr, cache, k, v)
-        orow, lrow = ta.turbo_attention_prefill(pr, q, k1_, v1t_, k1s_, v1s_, causal=True)
+        # NEXT-2 variants, each with its kernel speed and its deviation on the same units:
+        #  * prefill P scale per row x B_c block (Alg. 2's granularity) instead of per B_r x B_c
+        #    tile (Alg. 1);
+        #  * first-stage scales stored in FP16 (R-29);
+        #  * the SAS polynomial in FP16 (R-30);
+        #  * B_c = 128 (the block-size ablation, Table 3): its own cache and prefill operands.
+        variants = {}
         g0, g1 = ev(), ev()
-        g0.record(st)
-        for _ in range(10):
-            ta.turbo_attention_prefill(pr, q, k1_, v1t_, k1s_, v1s_, causal=True, o=orow, lse=lrow)
-        g1.record(st)
-        torch.cuda.synchronize()
-        row_ms = g0.elapsed_time(g1) / 10
-        variants = {"prefill_p_scale_per_row": {
-            "kernel_ms": round(row_ms, 4), "tops": round(ops / (row_ms * 1e-3) / 1e12, 1),
-            "deviation_alpha_mode_0": deviation_prefill(pr, q, k, v, {0: orow}, units, rows)["alpha_mode_0"]}}
-        # NEXT-2 variant: first-stage scales stored in FP16 (R-29)
-        pf = ta.params(head_dim=d, block_q=64, alpha_mode=0, scale_fp16=1)
-        k1_, v1t_, k1s_, v1s_ = ta.turbo_quantize_kv(pf, cache, k, v)
-        of, lf = ta.turbo_attention_prefill(pf, q, k1_, v1t_, k1s_, v1s_, causal=True)
-        g0.record(st)
-        for _ in range(10):
-            ta.turbo_attention_prefill(pf, q, k1_, v1t_, k1s_, v1s_, causal=True, o=of, lse=lf)
-        g1.record(st)
-        torch.cuda.synchronize()
-        f_ms = g0.elapsed_time(g1) / 10
-        variants["first_stage_scales_fp16"] = {
-            "kernel_ms": round(f_ms, 4), "tops": round(ops / (f_ms * 1e-3) / 1e12, 1),
-            "deviation_alpha_mode_0": deviation_prefill(pf, q, k, v, {0: of}, units, rows)["alpha_mode_0"]}
-        del of, lf
+        for name, kw in (("prefill_p_scale_per_row", dict(p_scale_rows=1)),
+                         ("first_stage_scales_fp16", dict(scale_fp16=1)),
+                         ("sas_polynomial_fp16", dict(sas_fp16=1)),
+                         ("block_kv_128", dict(block_kv=128))):
+            pv = ta.params(head_dim=d, block_q=64, alpha_mode=0, **kw)
+            cv = cache if pv.block_kv == 64 else ta.KVCache(B, Hkv, d, max_blocks=N // pv.block_kv + 2, bits=bits,
+                                                             block_kv=pv.block_kv, device=device)
+            k1_, v1t_, k1s_, v1s_ = ta.turbo_quantize_kv(pv, cv, k, v)
+            ov, lv = ta.turbo_attention_prefill(pv, q, k1_, v1t_, k1s_, v1s_, causal=True)
+            g0.record(st)
+            for _ in range(10):
+                ta.turbo_attention_prefill(pv, q, k1_, v1t_, k1s_, v1s_, causal=True, o=ov, lse=lv)
+            g1.record(st)
+            torch.cuda.synchronize()
+            v_ms = g0.elapsed_time(g1) / 10
+            variants[name] = {
+                "kernel_ms": round(v_ms, 4), "tops": round(ops / (v_ms * 1e-3) / 1e12, 1),
+                "deviation_alpha_mode_0": deviation_prefill(pv, q, k, v, {0: ov}, units, rows)["alpha_mode_0"]}
+            del ov, lv, k1_, v1t_, k1s_, v1s_, cv
         deviation["variants"] = variants
-        del o0, o1, orow, lrow, k1_, v1t_, k1s_, v1s_
+        del o0, o1
     result = dict(value=value, ms_step=ms_step, e2e=e2e, roofline=roof, clocks=clocks, quantize_kv=quant,
                   deviation=deviation,
                   planner=planner,

@@ -69,6 +69,11 @@ typedef struct {
                             before it is stored or used, as the paper stores them; codes unchanged
                             (R-29) -- NEXT-2 variant, oracle flag scale_fp16.  Must match the value the
                             cache was built with. */
+  int32_t sas_fp16;      /* 0 (default): SAS polynomial in binary32 (R-13); 1: the fraction and the
+                            coefficients rounded to binary16 and Horner with binary16 FMAs, as the paper
+                            evaluates it "in FP16"; LUT factor and product in binary32; used for
+                            P~ and alpha in prefill and decode (R-30) -- NEXT-2 variant, oracle flag
+                            sas_fp16. */
   void* debug_tap;       /* NULL, or a turbo_debug_tap_t* (see below) */
 } turbo_params_t;
 

@@ -34,7 +34,7 @@ class TurboError(RuntimeError):
 class TurboParams(C.Structure):
     _fields_ = [("head_dim", C.c_int32), ("block_q", C.c_int32), ("block_kv", C.c_int32), ("sas_nr", C.c_int32),
                 ("alpha_mode", C.c_int32), ("softmax_scale", C.c_float), ("p_scale_rows", C.c_int32),
-                ("scale_fp16", C.c_int32), ("debug_tap", C.c_void_p)]
+                ("scale_fp16", C.c_int32), ("sas_fp16", C.c_int32), ("debug_tap", C.c_void_p)]
 
 
 class TurboKVCache(C.Structure):
@@ -109,13 +109,14 @@ def _stream(stream=None):
 
 
 def params(head_dim=128, block_q=64, block_kv=64, sas_nr=-6, alpha_mode=0, softmax_scale=None, debug_tap=None,
-           p_scale_rows=0, scale_fp16=0):
+           p_scale_rows=0, scale_fp16=0, sas_fp16=0):
     """turbo_params_t with the paper's defaults.  p_scale_rows=1 selects the
-    per-row prefill P scale, scale_fp16=1 the FP16 first-stage scales (NEXT-2 variants,
-    include/turbo_attention.h)."""
+    per-row prefill P scale, scale_fp16=1 the FP16 first-stage scales, sas_fp16=1 the FP16 SAS
+    polynomial (NEXT-2 variants, include/turbo_attention.h)."""
     if softmax_scale is None:
         softmax_scale = 1.0 / math.sqrt(head_dim)
-    p = TurboParams(head_dim, block_q, block_kv, sas_nr, alpha_mode, softmax_scale, p_scale_rows, scale_fp16, None)
+    p = TurboParams(head_dim, block_q, block_kv, sas_nr, alpha_mode, softmax_scale, p_scale_rows, scale_fp16,
+                    sas_fp16, None)
     if debug_tap is not None:
         p._tap = debug_tap  # keep alive
         p.debug_tap = C.cast(C.pointer(debug_tap.c), C.c_void_p)

@@ -53,6 +53,7 @@ turbo_status_t check_params(const turbo_params_t* p) {
   if (!(p->softmax_scale > 0.0f) || !std::isfinite(p->softmax_scale)) return TURBO_ERR_INVALID_ARG;
   if (p->p_scale_rows != 0 && p->p_scale_rows != 1) return TURBO_ERR_INVALID_ARG;
   if (p->scale_fp16 != 0 && p->scale_fp16 != 1) return TURBO_ERR_INVALID_ARG;
+  if (p->sas_fp16 != 0 && p->sas_fp16 != 1) return TURBO_ERR_INVALID_ARG;
   return TURBO_OK;
 }
 

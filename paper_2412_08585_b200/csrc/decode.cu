@@ -55,7 +55,7 @@ struct DecodeArgs {
   __half* fin_o16;  // balanced schedule: final fp16 output (or NULL)
   float* fin_o32;   // balanced schedule: final f32 output (or NULL)
   float* fin_lse;   // balanced schedule: final L
-  int B, Hq, Hkv, G, max_blocks, blk_begin, blk_end, with_buffer, n_splits, alpha_mode, scale_fp16;
+  int B, Hq, Hkv, G, max_blocks, blk_begin, blk_end, with_buffer, n_splits, alpha_mode, scale_fp16, sas_fp16;
   float scale;
   SasConst sas;
   turbo_debug_tap_t tap;
@@ -309,7 +309,7 @@ struct RowState {
 
 // One tile of Alg. 2 on the thread's score values: running max,
 // alpha, SAS, row sum, per-row P scale and codes (to smem rows).
-template <int HD, bool PACK, bool TAP, bool FULL, int BC>
+template <int HD, bool PACK, bool TAP, bool FULL, int BC, bool SF = false>
 TA_DEV void softmax_tile(const DecodeArgs& a, RowState<HD, PACK>& st, int (&sv)[Map<HD, PACK>::NT * BC / 64][2], int nvalid,
                          const float (&cqk)[2], uint32_t pbuf, float lut_lane, float (&alpha)[2], float (&s_p)[2],
                          int (&sum_p)[2], bool tap, int tap_row, int g, int q) {
@@ -326,7 +326,7 @@ TA_DEV void softmax_tile(const DecodeArgs& a, RowState<HD, PACK>& st, int (&sv)[
     const float m_prev = st.m[e];
     const float m_new = fmaxf(m_prev, __fmul_rn((float)smax, cqk[e]));
     // alpha = SAS(m_prev - m_new) (R-15); every lane evaluates (shuffle LUT)
-    const float al_s = sas_eval(__fsub_rn(m_new, m_prev), lut_lane, a.sas.nr_abs);
+    const float al_s = sas_eval_v<SF>(__fsub_rn(m_new, m_prev), lut_lane, a.sas.nr_abs);
     const float al = m_prev == -INFINITY ? 0.f : (a.alpha_mode == 1 && m_new == m_prev) ? 1.f : al_s;
     float pt[NT], rs = 0.f, pm = 0.f;
     const f32x2 m2 = pk2(m_new, m_new);
@@ -335,7 +335,7 @@ TA_DEV void softmax_tile(const DecodeArgs& a, RowState<HD, PACK>& st, int (&sv)[
       // x rounded on its own (scalar __fmul_rn: a packed multiply feeding the
       // subtraction would be contracted into an FFMA2)
       const f32x2 x2 = pk2(__fmul_rn((float)sv[t][e], cqk[e]), __fmul_rn((float)sv[t + 1][e], cqk[e]));
-      const f32x2 p2 = sas_eval2(sub2(m2, x2), lut_lane, a.sas.nr_abs);
+      const f32x2 p2 = sas_eval2_v<SF>(sub2(m2, x2), lut_lane, a.sas.nr_abs);  // R-13 / R-30
       float p0 = lo2(p2), p1 = hi2(p2);
       if (!FULL) {
         p0 = M::tok(t, g, q) < nvalid ? p0 : 0.f;
@@ -580,7 +580,10 @@ TA_DEV void decode_segment(const DecodeArgs& a, DecodeSmem<HD, PACK, BC>& sm, in
     const bool tap = TAP && tap_row >= 0 && a.tap.j_block == j;
     float alpha[2], s_p[2];
     int sum_p[2];
-    softmax_tile<HD, PACK, TAP, true, BC>(a, st, sv, BC, cqk, pbuf, lut_lane, alpha, s_p, sum_p, tap, tap_row, g, q);
+    if (a.sas_fp16)
+      softmax_tile<HD, PACK, TAP, true, BC, true>(a, st, sv, BC, cqk, pbuf, lut_lane, alpha, s_p, sum_p, tap, tap_row, g, q);
+    else
+      softmax_tile<HD, PACK, TAP, true, BC>(a, st, sv, BC, cqk, pbuf, lut_lane, alpha, s_p, sum_p, tap, tap_row, g, q);
     int acc[M::NC][2];
     if (bitsV == 4) pv_block<HD, 4, PACK, false, BC>(recV, nullptr, pbuf, sum_p, acc, g, q);
     else pv_block<HD, 2, PACK, false, BC>(recV, nullptr, pbuf, sum_p, acc, g, q);
@@ -604,7 +607,11 @@ TA_DEV void decode_segment(const DecodeArgs& a, DecodeSmem<HD, PACK, BC>& sm, in
     const bool tap = TAP && tap_row >= 0 && a.tap.j_block == -1;
     float alpha[2], s_p[2];
     int sum_p[2];
-    softmax_tile<HD, PACK, TAP, false, BC>(a, st, sv, nbuf, cqk, pbuf, lut_lane, alpha, s_p, sum_p, tap, tap_row, g, q);
+    if (a.sas_fp16)
+      softmax_tile<HD, PACK, TAP, false, BC, true>(a, st, sv, nbuf, cqk, pbuf, lut_lane, alpha, s_p, sum_p, tap, tap_row, g,
+                                                    q);
+    else
+      softmax_tile<HD, PACK, TAP, false, BC>(a, st, sv, nbuf, cqk, pbuf, lut_lane, alpha, s_p, sum_p, tap, tap_row, g, q);
     int acc[M::NC][2];
     pv_block<HD, 4, PACK, true, BC>(0, vb, pbuf, sum_p, acc, g, q);
     const float cpv[2] = {__fmul_rn(s_p[0], sV), __fmul_rn(s_p[1], sV)};
@@ -923,6 +930,7 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
   a.n_splits = S;
   a.alpha_mode = p->alpha_mode;
   a.scale_fp16 = p->scale_fp16;
+  a.sas_fp16 = p->sas_fp16;
   a.scale = p->softmax_scale;
   fill_sas_const(&a.sas, p->sas_nr);
   const bool has_tap = p->debug_tap != nullptr;

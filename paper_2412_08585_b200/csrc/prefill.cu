@@ -85,7 +85,7 @@ constexpr float kFmin = 0.00006103515625f;  // 2^-14
 // F = 2^e m, m in [1, 2): 2^-e (exact power of two; F normal and positive)
 TA_DEV float inv_pow2_of(float F) { return __uint_as_float((uint32_t)(254 - (__float_as_uint(F) >> 23)) << 23); }
 
-template <int HD, bool TAP, bool TP, bool PROW, int BC>
+template <int HD, bool TAP, bool TP, bool PROW, int BC, bool SF>
 __global__ void __launch_bounds__(384, 1)
     prefill_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                    const __grid_constant__ PrefillArgs args) {
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(384, 1)
       }
       // m_new, alpha = SAS(m_prev - m_new) (R-15)
       const float m_new = fmaxf(m, mt);
-      float alpha = sas_eval(__fsub_rn(m_new, m), lut_lane, nr_abs);
+      float alpha = sas_eval_v<SF>(__fsub_rn(m_new, m), lut_lane, nr_abs);
       if (m == -INFINITY) alpha = 0.f;
       else if (args.alpha_mode == 1 && m_new == m) alpha = 1.f;
       const float m_use = active ? m_new : 0.f;  // inactive row: every x = -inf -> P~ = 0
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(384, 1)
           const f32x2 f2 = sub2(d2, sub2(t2, mg2));  // d - floor(d), exact
           const float l0 = lut_shfl(lut_lane, __float_as_uint(lo2(t2)));
           const float l1 = lut_shfl(lut_lane, __float_as_uint(hi2(t2)));
-          const f32x2 p2 = fma2(fma2(fma2(c3, f2, c2), f2, c1), f2, c0);
+          const f32x2 p2 = SF ? sas_poly2_h(f2) : fma2(fma2(fma2(c3, f2, c2), f2, c1), f2, c0);  // R-30 / R-13
           const f32x2 lp = mul2(pk2(l0, l1), p2);
           const float pt0 = lo2(d2) > nr_abs ? 0.f : lo2(lp);
           const float pt1 = hi2(d2) > nr_abs ? 0.f : hi2(lp);
@@ -591,13 +591,15 @@ cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Nk, int Hq
     a.unit_group = std::min(units, ug);
   }
   const bool prow = p->p_scale_rows != 0;
-#define TA_LAUNCH_B(HDV, TAPV, TPV, PRV, BCV)                                                                    \
+#define TA_LAUNCH_S(HDV, TAPV, TPV, PRV, BCV, SFV)                                                              \
   {                                                                                                            \
     const size_t smem = sizeof(PrefillSmem<HDV, BCV>) + 1024;                                                 \
-    cudaFuncSetAttribute(prefill_kernel<HDV, TAPV, TPV, PRV, BCV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                         (int)smem);                                                                           \
-    prefill_kernel<HDV, TAPV, TPV, PRV, BCV><<<grid, 384, smem, st>>>(tmk, tmv, a);                           \
+    cudaFuncSetAttribute(prefill_kernel<HDV, TAPV, TPV, PRV, BCV, SFV>,                                       \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                              \
+    prefill_kernel<HDV, TAPV, TPV, PRV, BCV, SFV><<<grid, 384, smem, st>>>(tmk, tmv, a);                      \
   }
+#define TA_LAUNCH_B(HDV, TAPV, TPV, PRV, BCV) \
+  if (p->sas_fp16) TA_LAUNCH_S(HDV, TAPV, TPV, PRV, BCV, true) else TA_LAUNCH_S(HDV, TAPV, TPV, PRV, BCV, false)
 #define TA_LAUNCH_T(HDV, TAPV, TPV, PRV) \
   if (BC == 64) TA_LAUNCH_B(HDV, TAPV, TPV, PRV, 64) else TA_LAUNCH_B(HDV, TAPV, TPV, PRV, 128)
 #define TA_LAUNCH_R(HDV, TAPV, TPV) \
@@ -612,6 +614,7 @@ cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Nk, int Hq
 #undef TA_LAUNCH_R
 #undef TA_LAUNCH_T
 #undef TA_LAUNCH_B
+#undef TA_LAUNCH_S
   return cudaGetLastError();
 }
 }  // namespace ta_host

@@ -181,8 +181,8 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefi
   uint8_t* rec = block_rec + ((bh * 2 + kind) * (size_t)max_blocks + j0 + j) * REC;
   if (rows == BC) {
     // Stage 2 of this channel (integer only, R-6): z = min, s = max(1, ceil((max-min)/(2^b-1))),
-    // code = floor((2 (v - z) + s) / (2 s)) = fl((2(v-z)+s) * fl(1/(2s)) + 2^-10) truncated
-    // (exact for these ranges, tests/test_quant_arith.py).
+    // code = floor((2 (v - z) + s) / (2 s)) = umulhi(2 (v - z) + s, ceil(2^32 / 2s)) (exact for these
+    // ranges, tests/test_quant_arith.py; integer multiply-high instead of the XU-pipe float->int path).
     int mn = q1(0), mx = mn;
 #pragma unroll
     for (int t = 1; t < BC; ++t) {
@@ -191,10 +191,8 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefi
     }
     const int range = mx - mn;
     const int sint = max(1, bits == 4 ? (range + 14) / 15 : (range + 2) / 3);
-    const float inv2s = __fdiv_rn(1.0f, (float)(2 * sint));
-    auto q = [&](int t) -> uint32_t {
-      return (uint32_t)__float2int_rz(__fmaf_rn((float)(2 * (q1(t) - mn) + sint), inv2s, 0.0009765625f));
-    };
+    const uint32_t M = 0xFFFFFFFFu / (uint32_t)(2 * sint) + 1u;  // ceil(2^32 / 2s)
+    auto q = [&](int t) -> uint32_t { return __umulhi((uint32_t)(2 * (q1(t) - mn) + sint), M); };
     rec[c] = (uint8_t)sint;
     rec[HD + c] = (uint8_t)(int8_t)mn;
     if (kind == 0) {

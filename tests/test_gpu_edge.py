@@ -260,3 +260,87 @@ def test_scale_fp16_variant_decode_with_flush(ta):
     qd, _, _ = synth.decode_token(5600, B, Hq, Hkv, d)
     _check_decode(ta, p, op, cache, ref, qd, Hq // Hkv, S=1)
     _check_decode(ta, p, op, cache, ref, qd, Hq // Hkv, S=3)
+
+
+SF_CASES = [  # (B, N, Hq, Hkv, d, causal, block_q, alpha_mode, block_kv)
+    (2, 200, 8, 2, 128, True, 64, 0, 64),
+    (1, 333, 4, 4, 128, False, 64, 1, 64),
+    (1, 256, 2, 1, 64, True, 128, 0, 64),
+    (2, 700, 3, 3, 128, True, 64, 0, 64),
+    (1, 300, 8, 2, 128, True, 64, 1, 128),
+]
+
+
+@pytest.mark.parametrize("case", SF_CASES)
+def test_sas_fp16_variant_prefill(ta, case):
+    """NEXT-2 variant sas_fp16 (R-30): the SAS polynomial with binary16 FMAs in the
+    prefill (P~ and alpha), O / LSE against the oracle run with the same flag."""
+    B, N, Hq, Hkv, d, causal, bq, am, bc = case
+    q, k, v = synth.qkv(5700 + N, B, N, Hq, Hkv, d)
+    bits = synth.head_bits_alternating(Hkv)
+    p = ta.params(head_dim=d, block_q=bq, block_kv=bc, alpha_mode=am, sas_fp16=1)
+    cache = ta.KVCache(B, Hkv, d, max_blocks=N // bc + 2, bits=bits, block_kv=bc)
+    qt, kt, vt = (torch.from_numpy(x).cuda() for x in (q, k, v))
+    k1, v1t, k1s, v1s = ta.turbo_quantize_kv(p, cache, kt, vt)
+    o, lse = ta.turbo_attention_prefill(p, qt, k1, v1t, k1s, v1s, causal=causal)
+    torch.cuda.synchronize()
+    op = O.params(d=d, block_q=bq, block_kv=bc, alpha_mode=am, sas_fp16=1)
+    _check_prefill_heads(op, q, k, v, o.cpu().numpy(), lse.cpu().numpy(),
+                         [(b, h) for b in range(B) for h in range(Hq)], causal=causal)
+
+
+@pytest.mark.parametrize("ij", [(3, 2), (4, 4)])
+def test_sas_fp16_variant_prefill_tap(ta, ij):
+    """Bit-exact P codes, s_P, m and PV_int under sas_fp16 (P~ from binary16 Horner)."""
+    B, N, Hq, Hkv, d = 1, 300, 4, 2, 128
+    q, k, v = synth.qkv(5800, B, N, Hq, Hkv, d)
+    bits = synth.head_bits_alternating(Hkv)
+    b, h = 0, 3
+    i, j = ij
+    tap = ta.DebugTap(b, h, i, j, d)
+    p = ta.params(head_dim=d, debug_tap=tap, sas_fp16=1)
+    _prefill(ta, p, q, k, v, bits)
+    _, _, rt = O.prefill_head(O.params(d=d, sas_fp16=1), q[b, :, h], k[b, :, h // 2], v[b, :, h // 2], causal=True,
+                              tap=(i, j))
+    rows = min(64, N - 64 * i)
+    np.testing.assert_array_equal(tap.m_new.cpu().numpy()[:rows], rt["m_new"][:rows])
+    np.testing.assert_array_equal(tap.p_codes.cpu().numpy()[:rows], rt["p_codes"][:rows])
+    np.testing.assert_array_equal(tap.pv_int.cpu().numpy()[:rows], rt["pv_int"][:rows])
+    assert tap.s_p.item() == rt["s_p"][0]
+
+
+@pytest.mark.parametrize("Hq,S", [(8, 1), (8, 3), (16, 2), (16, 1)])
+def test_sas_fp16_variant_decode(ta, Hq, S):
+    """sas_fp16 in the decode (packed G = 4 and general G = 8 paths, equal splits),
+    through appends that flush the buffer."""
+    B, N, Hkv, d = 2, 64 * 4 + 50, 2, 128
+    q, k, v = synth.qkv(5900, B, N, Hq, Hkv, d)
+    bits = synth.head_bits_alternating(Hkv)
+    p, op = ta.params(head_dim=d, sas_fp16=1), O.params(d=d, sas_fp16=1)
+    apps = [synth.decode_token(6000 + t, B, Hq, Hkv, d)[1:] for t in range(20)]
+    cache, ref = _decode_setup(ta, p, op, q, k, v, bits, apps)
+    qd, _, _ = synth.decode_token(6100, B, Hq, Hkv, d)
+    _check_decode(ta, p, op, cache, ref, qd, Hq // Hkv, S=S)
+
+
+def test_sas_fp16_variant_decode_tap(ta):
+    B, N, Hq, Hkv, d = 2, 64 * 5 + 37, 8, 2, 128
+    q, k, v = synth.qkv(6200, B, N, Hq, Hkv, d)
+    bits = synth.head_bits_alternating(Hkv)
+    b, h, jb = 1, 5, 3
+    tap = ta.DebugTap(b, h, 0, jb, d, decode=True)
+    p = ta.params(head_dim=d, debug_tap=tap, sas_fp16=1)
+    cache = ta.KVCache(B, Hkv, d, max_blocks=8, bits=bits)
+    ta.turbo_quantize_kv(p, cache, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    qd, _, _ = synth.decode_token(6300, B, Hq, Hkv, d)
+    ta.turbo_attention_decode(p, cache, torch.from_numpy(qd).cuda(), n_splits=1)
+    torch.cuda.synchronize()
+    op = O.params(d=d, sas_fp16=1)
+    ref = O.build_cache(op, k.astype(np.float32), v.astype(np.float32), bits, 8)
+    ks, vs = ref["slots"][b][h // (Hq // Hkv)]
+    _, _, rt = O.decode_head(op, qd[b, h].astype(np.float32), ks, vs, 0, ks.n_blocks, True, tap=jb)
+    assert rt["hit"]
+    assert tap.m_new.item() == rt["m_new"][0]
+    np.testing.assert_array_equal(tap.p_codes.cpu().numpy()[0], rt["p_codes"])
+    assert tap.s_p.item() == rt["s_p"][0]
+    np.testing.assert_array_equal(tap.pv_int.cpu().numpy()[0], rt["pv_int"])

@@ -14,7 +14,7 @@ if os.environ.get("TP_SHAPE"):  # "B,N,Hq,Hkv,d" (e.g. MHA: 8,4096,32,32,128)
     B, N, Hq, Hkv, d = (int(x) for x in os.environ["TP_SHAPE"].split(","))
 p = ta.params(head_dim=d, p_scale_rows=int(os.environ.get("TP_PROW", "0")),
               alpha_mode=int(os.environ.get("TP_ALPHA", "0")), block_q=int(os.environ.get("TP_BQ", "64")),
-              block_kv=int(os.environ.get("TP_BC", "64")))
+              block_kv=int(os.environ.get("TP_BC", "64")), sas_fp16=int(os.environ.get("TP_SF16", "0")))
 q, k, v = synth.qkv_torch(1002, B, N, Hq, Hkv, d)
 cache = ta.KVCache(B, Hkv, d, max_blocks=N // p.block_kv + 2, bits=synth.head_bits_alternating(Hkv),
                    block_kv=p.block_kv)
@@ -31,5 +31,5 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / ITERS
 ops = 4.0 * d * N * (N + 1) / 2 * B * Hq
-print(f"{os.environ.get('TURBO_LIB', 'in-tree')} {B},{N},{Hq},{Hkv},{d}: {ms * 1e3:8.1f} us  {ops / ms / 1e9:7.1f} TOPS  "
+print(f"{os.environ.get('TURBO_LIB', 'in-tree')} sf16={p.sas_fp16} bc={p.block_kv} {B},{N},{Hq},{Hkv},{d}: {ms * 1e3:8.1f} us  {ops / ms / 1e9:7.1f} TOPS  "
       f"checksum {o.float().abs().sum().item():.6e}")

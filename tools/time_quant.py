@@ -10,9 +10,10 @@ from paper_2412_08585_b200 import binding as ta  # noqa: E402
 from paper_2412_08585_b200 import synth  # noqa: E402
 
 B, N, Hq, Hkv, d = 8, 4096, 32, 8, 128
-p = ta.params(head_dim=d)
+BC = int(os.environ.get("TP_BC", "64"))
+p = ta.params(head_dim=d, block_kv=BC)
 q, k, v = synth.qkv_torch(1002, B, N, Hq, Hkv, d)
-cache = ta.KVCache(B, Hkv, d, max_blocks=N // 64 + 2, bits=synth.head_bits_alternating(Hkv))
+cache = ta.KVCache(B, Hkv, d, max_blocks=N // BC + 2, bits=synth.head_bits_alternating(Hkv), block_kv=BC)
 outs = ta.turbo_quantize_kv(p, cache, k, v)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 ts = []
