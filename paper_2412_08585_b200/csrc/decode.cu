@@ -655,6 +655,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   DecodeSmem<HD, PACK, BC>& sm = reinterpret_cast<DecodeSmem<HD, PACK, BC>*>(smem_raw)[warp];
+  pdl_trigger();  // the combine grid may launch once every decode CTA has started
+  pdl_wait();     // (launched with PDL after the append kernels: their counters / buffer)
   if (lane == 0) {
     mbar_init(&sm.bar[0], 1);
     mbar_init(&sm.bar[1], 1);
@@ -814,6 +816,7 @@ __global__ void __launch_bounds__(32 * kCombWarps) combine_balanced_kernel(const
                                                                              int d) {
   extern __shared__ float w[];  // [n + 1]
   __shared__ float part[kCombWarps][128];
+  pdl_wait();  // the decode grid's partials
   const int r = blockIdx.x, b = r / a.Hq, h = r % a.Hq, kvh = h / a.G, row = h % a.G, lane = threadIdx.x & 31;
   int tot = 0, before = 0;
   for (int b0 = 0; b0 < a.B; b0 += 32) {
@@ -848,6 +851,7 @@ __global__ void __launch_bounds__(32 * kCombWarps) combine_kernel(int n_parts, i
                                                                     float* __restrict__ lse) {
   extern __shared__ float w[];  // [n_parts + 1]
   __shared__ float part[kCombWarps][128];
+  pdl_wait();  // the decode grid's partials
   const int r = blockIdx.x;
   combine_row<VEC>(n_parts, lse_parts + r, rows, o_parts + (size_t)r * d, (size_t)rows * d, d, w, part,
                    o16 ? o16 + (size_t)r * d : nullptr, o32 ? o32 + (size_t)r * d : nullptr,
@@ -862,10 +866,12 @@ static void launch_combine_kernel(int n_parts, int rows, int d, const float* o_p
   const int thr = 32 * comb_warps(n_parts);
   if (d == 128) {
     cudaFuncSetAttribute(combine_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    combine_kernel<4><<<rows, thr, smem, st>>>(n_parts, rows, d, o_parts, lse_parts, o16, o32, lse);
+    ta_host::launch_pdl(combine_kernel<4>, dim3(rows), dim3(thr), smem, st, n_parts, rows, d, o_parts, lse_parts, o16,
+                        o32, lse);
   } else {
     cudaFuncSetAttribute(combine_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    combine_kernel<2><<<rows, thr, smem, st>>>(n_parts, rows, d, o_parts, lse_parts, o16, o32, lse);
+    ta_host::launch_pdl(combine_kernel<2>, dim3(rows), dim3(thr), smem, st, n_parts, rows, d, o_parts, lse_parts, o16,
+                        o32, lse);
   }
 }
 
@@ -956,7 +962,7 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
   {                                                                                                         \
     const size_t smem = sizeof(DecodeSmem<HDV, PK, BCV>) * kWarpsPerCta;                                    \
     cudaFuncSetAttribute(decode_kernel<HDV, PK, TP, BCV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    decode_kernel<HDV, PK, TP, BCV><<<grid, 32 * kWarpsPerCta, smem, st>>>(a);                             \
+    launch_pdl(decode_kernel<HDV, PK, TP, BCV>, grid, dim3(32 * kWarpsPerCta), smem, st, a);                \
   }
 #define TA_DEC(HDV, PK, TP) \
   if (c->block_kv == 64) TA_DEC_B(HDV, PK, TP, 64) else TA_DEC_B(HDV, PK, TP, 128)
@@ -982,10 +988,10 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
     const int thr = 32 * comb_warps(W / (B * H) + 1);
     if (HD == 128) {
       cudaFuncSetAttribute(combine_balanced_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      combine_balanced_kernel<4><<<B * Hq, thr, smem, st>>>(a, W, HD);
+      launch_pdl(combine_balanced_kernel<4>, dim3(B * Hq), dim3(thr), smem, st, a, W, HD);
     } else {
       cudaFuncSetAttribute(combine_balanced_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      combine_balanced_kernel<2><<<B * Hq, thr, smem, st>>>(a, W, HD);
+      launch_pdl(combine_balanced_kernel<2>, dim3(B * Hq), dim3(thr), smem, st, a, W, HD);
     }
   } else {
     const int rows = B * Hq;

@@ -309,6 +309,7 @@ __global__ void __launch_bounds__(256) quant_append_kernel(
     int scale_fp16) {
   __shared__ __align__(16) int8_t tile[2][BC * HD];
   const int h = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+  pdl_wait();  // (launched with PDL: the previous step's counters / buffer)
   const int n_blocks = counters[b * 2 + 0], n_buf = counters[b * 2 + 1];
   const size_t bh = (size_t)b * Hkv + h;
   const bool flush = n_buf + 1 == BC;
@@ -347,6 +348,7 @@ __global__ void __launch_bounds__(256) quant_append_kernel(
 }
 
 __global__ void append_counters_kernel(int32_t* counters, int B, int BC) {
+  pdl_wait();  // after quant_append_kernel has read the counters
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   int nb = counters[b * 2], nbuf = counters[b * 2 + 1] + 1;
@@ -471,9 +473,9 @@ cudaError_t launch_dequant_cache(const turbo_kv_cache_t* c, int blk_begin, int b
 template <int HD, int BC>
 static void quant_append_hd(const turbo_kv_cache_t* c, const __half* k, const __half* v, cudaStream_t st,
                             int scale_fp16) {
-  quant_append_kernel<HD, BC><<<dim3(c->n_kv_heads, c->batch), 256, 0, st>>>(
-      k, v, c->n_kv_heads, c->max_blocks, c->bits_dev, c->a_univ, c->buf, c->block_rec, c->s_parent, c->counters,
-      scale_fp16);
+  launch_pdl(quant_append_kernel<HD, BC>, dim3(c->n_kv_heads, c->batch), dim3(256), 0, st, k, v, c->n_kv_heads,
+             c->max_blocks, (const int32_t*)c->bits_dev, (const float*)c->a_univ, c->buf, c->block_rec, c->s_parent,
+             (const int32_t*)c->counters, scale_fp16);
 }
 
 cudaError_t launch_quant_append(const turbo_kv_cache_t* c, const __half* k, const __half* v, cudaStream_t st,
@@ -486,7 +488,7 @@ cudaError_t launch_quant_append(const turbo_kv_cache_t* c, const __half* k, cons
     if (BC == 64) quant_append_hd<64, 64>(c, k, v, st, scale_fp16);
     else quant_append_hd<64, 128>(c, k, v, st, scale_fp16);
   }
-  append_counters_kernel<<<(B + 127) / 128, 128, 0, st>>>(c->counters, B, BC);
+  launch_pdl(append_counters_kernel, dim3((B + 127) / 128), dim3(128), 0, st, c->counters, B, BC);
   return cudaGetLastError();
 }
 }  // namespace ta_host
