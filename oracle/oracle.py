@@ -123,6 +123,8 @@ def _declare(L):
     L.tq_combine.argtypes = [i32, i32, vp, vp, vp, vp]
     L.tq_reference_attention.argtypes = [i32, i32, i32, vp, vp, vp, i32, i32, C.c_double, vp, vp]
     L.tq_head_priority.argtypes = [i32, i32, vp, vp]
+    L.tq_slot_univ_scale.argtypes = [vp, vp]
+    L.tq_slot_univ_scale.restype = f32
 
 
 def params(d=128, block_q=64, block_kv=64, sas_nr=-6, alpha_mode=0, softmax_scale=None, quant=1, sas=1, p_row=0,
@@ -240,11 +242,14 @@ class Slot:
         return x1, sc
 
     def prefill_append(self, x: np.ndarray):
-        """A further prefill chunk (R-28; needs n_buf == 0): returns the chunk's
-        stage-1 operands (x1 [n][d] int8, x1_scale [ceil(n / B_c)] f32)."""
+        """A further prefill chunk (R-28; R-31 when the cache ends inside a block): returns the
+        chunk's stage-1 operands (x1 [n][d] int8, x1_scale f32 of the chunk's own blocks -- the
+        boundary block's scale s_univ belongs to stage1_prefix(with_buffer=True))."""
         x = _f32(x)
         n = x.shape[0]
-        tc = -(-n // self.p.block_kv)
+        bc = self.p.block_kv
+        r = min(n, bc - self.n_buf) if self.n_buf else 0
+        tc = -(-(n - r) // bc)
         x1 = np.zeros((n, self.p.d), np.int8)
         sc = np.zeros(tc, np.float32)
         rc = lib().tq_cache_prefill_append_slot(C.byref(self.p), n, _p(x), C.byref(self.c), _p(x1), _p(sc))
@@ -252,12 +257,17 @@ class Slot:
             raise ValueError(f"tq_cache_prefill_append_slot -> {rc}")
         return x1, sc
 
-    def stage1_prefix(self, n_blocks: int):
+    def stage1_prefix(self, n_blocks: int, with_buffer: bool = False):
         """Stage-1 reconstruction of blocks [0, n_blocks): int8 [n_blocks B_c][d] codes
-        code s^int + z^int (Alg. 2) with the blocks' parent scales."""
+        code s^int + z^int (Alg. 2) with the blocks' parent scales; with_buffer: then
+        the n_buf buffered tokens' codes and the boundary block's scale s_univ (R-31)."""
         x1 = np.concatenate([self.dequant_block(j) for j in range(n_blocks)], 0) if n_blocks else \
             np.zeros((0, self.p.d), np.int32)
-        return x1.astype(np.int8), self.s_parent[:n_blocks].copy()
+        sc = self.s_parent[:n_blocks].copy()
+        if with_buffer and self.n_buf:
+            x1 = np.concatenate([x1, self.buf[:self.n_buf].astype(np.int32)], 0)
+            sc = np.concatenate([sc, [np.float32(lib().tq_slot_univ_scale(C.byref(self.p), C.byref(self.c)))]])
+        return x1.astype(np.int8), sc.astype(np.float32)
 
     def append(self, x: np.ndarray):
         x = _f32(x)

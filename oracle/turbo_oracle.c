@@ -247,7 +247,22 @@ int32_t tq_cache_prefill_slot(const tq_params* p, int32_t n, const float* x, tq_
 int32_t tq_cache_prefill_append_slot(const tq_params* p, int32_t n, const float* x, tq_slot* s,
                                      int8_t* x1, float* x1_scale) {
   int32_t d = p->d, bc = p->block_kv;
-  if (n < 1 || s->n_buf != 0) return -1;
+  if (n < 1) return -1;
+  if (s->n_buf != 0) {
+    /* R-31: a chunk that starts inside a block first completes that block exactly as decode
+     * appends do (universal scale, clamp +-119, flushed at B_c with parent s_univ);
+     * those tokens' stage-1 operands are their buffer codes, at the boundary block's scale
+     * s_univ (listed with the prefix, stage1_prefix); the rest of the chunk is block-aligned. */
+    int32_t r = bc - s->n_buf < n ? bc - s->n_buf : n;
+    for (int32_t t = 0; t < r; ++t) {
+      if (x1)
+        for (int32_t c = 0; c < d; ++c) x1[(int64_t)t * d + c] = quant_univ(x[(int64_t)t * d + c], s->a_univ);
+      int32_t rc = tq_cache_append_slot(p, x + (int64_t)t * d, s);
+      if (rc != 0) return rc;
+    }
+    if (r == n) return 0;
+    return tq_cache_prefill_append_slot(p, n - r, x + (int64_t)r * d, s, x1 ? x1 + (int64_t)r * d : x1, x1_scale);
+  }
   int32_t tc = (n + bc - 1) / bc, nfull = n / bc;
   if (s->n_blocks + nfull > s->max_blocks) return -3;
   int8_t* blk = (int8_t*)malloc((size_t)bc * d);
@@ -270,6 +285,10 @@ int32_t tq_cache_prefill_append_slot(const tq_params* p, int32_t n, const float*
   free(blk);
   return 0;
 }
+
+/* The universal scale s_univ = a_univ / 119 as used (the buffer block's and a flushed buffer's
+ * scale; FP16 variant: R-29). */
+float tq_slot_univ_scale(const tq_params* p, const tq_slot* s) { return st1(p, s->a_univ / TQ_DIV); }
 
 /* APPEND one decode token (append, then attend).  When the buffer
  * reaches n_b = B_c tokens it is progressively quantised with the universal

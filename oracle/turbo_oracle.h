@@ -102,6 +102,7 @@ int32_t tq_cache_prefill_slot(const tq_params* p, int32_t n_tokens, const float*
                               tq_slot* slot, int8_t* x1 /*[N][d] or NULL*/,
                               float* x1_scale /*[T_c] or NULL*/);
 int32_t tq_cache_append_slot(const tq_params* p, const float* x /*[d]*/, tq_slot* slot);
+float tq_slot_univ_scale(const tq_params* p, const tq_slot* slot);
 
 /* --- Attention --- */
 int32_t tq_prefill_head(const tq_params* p, int32_t n, int32_t causal, const float* q,
