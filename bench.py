@@ -337,6 +337,18 @@ def run_ours(args, rank, world, device):
             "share_of_step": round(pre_ms / statistics.mean(t_step), 3),
             "int8_gemm_tops_measured": int8_gemm,
             "tensor_ceiling_of_mma_mix": round(2.0 / (1.0 / int8_peak + 2.0 / int8_peak), 1)}
+    # The bound that actually binds: the FP32 (FMA) pipe running the bit-exact SAS mix.
+    # Unit counts: 4 SMSPs x 32 lanes x 2 elements per packed FMA-pipe instruction at 0.5 instr / clk
+    # = 128 element-operations / clk / SM; the pinned arithmetic needs 13 per score element (x, d,
+    # floor, floor - magic, fraction, Horner x 3, LUT product, row sum, P code, P' hi, P' lo), and a
+    # score element carries 4 d = 512 ops.  Clock: the median SM clock under load.
+    sm_hz = (clocks or {}).get("sm_mhz") or 1965.0
+    alu_peak = 148 * 128 / 13 * sm_hz * 1e6 * 4 * d / 1e12
+    roof["alu_bound"] = {"bound": "alu", "achieved": round(achieved, 1), "peak": round(alu_peak, 1), "unit": "TOPS",
+                         "frac": round(achieved / alu_peak, 4),
+                         "peak_source": f"148 SMs x 128 FP32-pipe element-ops/clk / 13 per score element x "
+                                        f"{sm_hz:.0f} MHz x 512 ops per element (DESIGN.md 7)",
+                         "measured_mix_ceiling_tops": 745.0}
     # quantize_kv (a1/a2) as its own HBM-bound kernel: FP16 K, V in; k1 (INT8), v1t (FP16 codes), records,
     # scales out
     q_ms = statistics.mean(t_quant)

@@ -155,11 +155,15 @@ TURBO_API turbo_status_t turbo_cache_sizes(int32_t batch, int32_t n_kv_heads, in
  *     +-119 into the buffer; a full buffer (n_b = B_c tokens) is flushed to a
  *     stage-2 block with parent scale a_univ/119.  The *_out pointers must be
  *     NULL.  Updates cache->n_tokens (host) and the device counters.
- *   mode 2 = PREFILL_CHUNK (R-28, NEXT-3): k, v FP16 [B][n_tokens][Hkv][d], a
- *     further prefill chunk after the P = cache->n_tokens cached tokens, which
- *     must be a whole number of blocks (else TURBO_ERR_INVALID_ARG).  The
- *     universal scales become the running max over all chunks; the chunk's
- *     full blocks are appended at block P / B_c, its tail goes to the buffer.
+ *   mode 2 = PREFILL_CHUNK (R-28, R-31, NEXT-3): k, v FP16 [B][n_tokens][Hkv][d],
+ *     a further prefill chunk after the P = cache->n_tokens cached tokens.  When
+ *     P is not a whole number of blocks (R-31) the chunk's first
+ *     min(n_tokens, B_c - P % B_c) tokens complete the buffered block exactly
+ *     as APPEND does (universal scale, clamp, flush with parent a_univ/119);
+ *     their stage-1 outputs are those codes (the block's scale comes from
+ *     turbo_dequantize_cache).  The rest of the chunk is block-aligned: the
+ *     universal scales become the running max over it and the previous value,
+ *     its full blocks are appended, its tail goes to the buffer.
  *     The stage-1 outputs cover Nk = P + n_tokens tokens (k1_out
  *     [B][Hkv][Nk][d], v1t_out [B][Hkv][ceil(Nk/B_c)][d][B_c], scales
  *     [B][Hkv][ceil(Nk/B_c)]); the chunk's are written at token P / block
@@ -186,10 +190,12 @@ TURBO_API turbo_status_t turbo_attention_prefill(const turbo_params_t* params, i
 /* Stage-1 reconstruction of flushed cache blocks [blk_begin, blk_end)
  * (blk_end = -1: all; blocks past a sequence's count are skipped), the
  * prefix operands of a chunked prefill (R-28): k1_out [B][Hkv][Nk][d] rows
- * [64 j, 64 j + 64) and v1t_out [B][Hkv][ceil(Nk/B_c)][d][B_c] block j get
+ * [B_c j, B_c j + B_c) and v1t_out [B][Hkv][ceil(Nk/B_c)][d][B_c] block j get
  * code s_int + z_int (Alg. 2), the scales the blocks' parent
- * scales.  Nk = token capacity of k1_out (>= B_c x the last block).  The
- * cache is not modified. */
+ * scales.  With blk_end = -1 and buffered tokens (R-31) these follow as block
+ * n_blocks: their INT8 codes, scale a_univ/119, the block's later v1t columns
+ * zero.  Nk = token capacity of k1_out (>= B_c x the last block, and >= the
+ * cached length when the buffer is written).  The cache is not modified. */
 TURBO_API turbo_status_t turbo_dequantize_cache(const turbo_params_t* params, const turbo_kv_cache_t* cache,
                                                 int32_t blk_begin, int32_t blk_end, int8_t* k1_out, void* v1t_out,
                                                 float* k1_scale_out, float* v1_scale_out, int32_t Nk,

@@ -14,7 +14,7 @@ cudaError_t launch_quant_prefill(const turbo_kv_cache_t* c, const __half* k, con
                                  __half* v1t, float* k1s, float* v1s, cudaStream_t st, int j0, int Nk,
                                  int scale_fp16);
 cudaError_t launch_dequant_cache(const turbo_kv_cache_t* c, int blk_begin, int blk_end, int Nk, int8_t* k1,
-                                 __half* v1t, float* k1s, float* v1s, cudaStream_t st);
+                                 __half* v1t, float* k1s, float* v1s, cudaStream_t st, int scale_fp16);
 cudaError_t launch_quant_append(const turbo_kv_cache_t* c, const __half* k, const __half* v, cudaStream_t st,
                                 int scale_fp16);
 cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Nk, int Hq, int Hkv, int causal, const __half* q,
@@ -109,9 +109,9 @@ turbo_status_t turbo_quantize_kv(const turbo_params_t* params, turbo_kv_cache_t*
     if (s == TURBO_OK) cache->n_tokens = n_tokens;
     return s;
   }
-  if (mode == 2) {  // a further prefill chunk (R-28): the cache must hold whole blocks
+  if (mode == 2) {  // a further prefill chunk (R-28; R-31 when the cache ends inside a block)
     if (n_tokens < 1 || !k1_out || !v1t_out || !k1_scale_out || !v1_scale_out) return TURBO_ERR_INVALID_ARG;
-    if (cache->n_tokens < 1 || cache->n_tokens % params->block_kv != 0) return TURBO_ERR_INVALID_ARG;
+    if (cache->n_tokens < 1) return TURBO_ERR_INVALID_ARG;
     const int64_t nk = cache->n_tokens + n_tokens;
     if (nk / params->block_kv > cache->max_blocks || nk > INT32_MAX) return TURBO_ERR_CAPACITY;
     s = cuda_status(ta_host::launch_quant_prefill(cache, reinterpret_cast<const __half*>(k),
@@ -145,9 +145,11 @@ turbo_status_t turbo_dequantize_cache(const turbo_params_t* params, const turbo_
   const int64_t last = blk_end < 0 ? flushed : std::min<int64_t>(blk_end, flushed);
   if (blk_end >= 0 && blk_end < blk_begin) return TURBO_ERR_INVALID_ARG;
   if (Nk < 1 || last * params->block_kv > Nk) return TURBO_ERR_INVALID_ARG;
+  // blk_end < 0 with buffered tokens: they are written too, as the boundary block (R-31)
+  if (blk_end < 0 && cache->n_tokens % params->block_kv != 0 && cache->n_tokens > Nk) return TURBO_ERR_INVALID_ARG;
   return cuda_status(ta_host::launch_dequant_cache(cache, blk_begin, blk_end, Nk, k1_out,
                                                    reinterpret_cast<__half*>(v1t_out), k1_scale_out, v1_scale_out,
-                                                   reinterpret_cast<cudaStream_t>(stream)));
+                                                   reinterpret_cast<cudaStream_t>(stream), params->scale_fp16));
 }
 
 turbo_status_t turbo_attention_prefill_chunk(const turbo_params_t* params, int32_t B, int32_t Nq, int32_t Nk,

@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefi
     const __half* __restrict__ k, const __half* __restrict__ v, int N, int Hkv, int max_blocks, int j0, int Nk,
     const int32_t* __restrict__ bits_dev, uint8_t* __restrict__ block_rec, float* __restrict__ s_parent,
     float* __restrict__ a_univ, int8_t* __restrict__ k1, __half* __restrict__ v1t, float* __restrict__ k1s,
-    float* __restrict__ v1s, int scale_fp16) {
+    float* __restrict__ v1s, int scale_fp16, int t0, int Nin) {
   constexpr int NW = HD / 32;  // warps
   // One CTA per (block, kv head, batch, K or V): 6 small CTAs per SM keep more loads in
   // flight than 3 CTAs doing K and V together.  The block (FP16 [64][HD]) is staged with
@@ -125,7 +125,8 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefi
       const int t = i / C8, c8 = i % C8;
       uint4 val = make_uint4(0, 0, 0, 0);
       if (t < rows)
-        val = __ldcs(reinterpret_cast<const uint4*>(src + (((size_t)b * N + (size_t)j * BC + t) * Hkv + h) * HD) + c8);
+        val = __ldcs(reinterpret_cast<const uint4*>(src + (((size_t)b * Nin + t0 + (size_t)j * BC + t) * Hkv + h) * HD) +
+                     c8);
       *reinterpret_cast<uint4*>(&xs[t][8 * c8]) = val;
     }
   }
@@ -278,7 +279,7 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefi
 template <int HD, int BC>
 __global__ void quant_tail_kernel(const __half* __restrict__ k, const __half* __restrict__ v, int N, int Hkv,
                                   const float* __restrict__ a_univ, int8_t* __restrict__ buf,
-                                  int32_t* __restrict__ counters, int j0) {
+                                  int32_t* __restrict__ counters, int j0, int t0, int Nin) {
   const int h = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
   const int nfull = N / BC, ntail = N - nfull * BC;
   const size_t bh = (size_t)b * Hkv + h;
@@ -293,7 +294,7 @@ __global__ void quant_tail_kernel(const __half* __restrict__ k, const __half* __
   const __half* src = kv == 0 ? k : v;
   int8_t* bslot = buf + (bh * 2 + kv) * (size_t)(BC * HD);
   for (int t = 0; t < ntail; ++t) {
-    const float x = __half2float(src[(((size_t)b * N + (size_t)nfull * BC + t) * Hkv + h) * HD + c]);
+    const float x = __half2float(src[(((size_t)b * Nin + t0 + (size_t)nfull * BC + t) * Hkv + h) * HD + c]);
     const int code = max(-119, min(119, rint_prod(x, inv)));
     bslot[kv == 0 ? t * HD + c : c * BC + t] = (int8_t)code;
   }
@@ -406,6 +407,97 @@ __global__ void __launch_bounds__(2 * HD) dequant_cache_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// R-31: a prefill chunk into a cache that ends inside a block (cache block j0 holds nbuf buffered
+// tokens): its first r tokens complete that block exactly as APPEND does -- universal-scale codes,
+// clamped to +-119, into buffer rows nbuf .. nbuf + r - 1 -- and, as the chunk's stage-1 operands,
+// into k1 rows B_c j0 + nbuf + t and v1t block j0 columns nbuf + t; a full block is flushed
+// (stage 2, parent s_univ).  One CTA per (kv head, batch); thread = (K/V, channel).
+template <int HD, int BC>
+__global__ void __launch_bounds__(256) quant_boundary_kernel(
+    const __half* __restrict__ k, const __half* __restrict__ v, int N, int r, int Hkv, int max_blocks, int j0, int nbuf,
+    int Nk, const int32_t* __restrict__ bits_dev, const float* __restrict__ a_univ, int8_t* __restrict__ buf,
+    uint8_t* __restrict__ block_rec, float* __restrict__ s_parent, int8_t* __restrict__ k1, __half* __restrict__ v1t,
+    int scale_fp16) {
+  __shared__ __align__(16) int8_t tile[2][BC * HD];
+  const int h = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+  const size_t bh = (size_t)b * Hkv + h;
+  const int Tk = (Nk + BC - 1) / BC;
+  const bool flush = nbuf + r == BC;
+  if (tid < 2 * HD) {
+    const int kv = tid / HD, c = tid % HD;
+    const float a = a_univ[bh * 2 + kv];
+    const float inv = a > 0.f ? div_119_by(a) : 0.f;
+    const __half* src = kv == 0 ? k : v;
+    int8_t* bslot = buf + (bh * 2 + kv) * (size_t)(BC * HD);
+    for (int t = 0; t < r; ++t) {
+      const float x = __half2float(src[(((size_t)b * N + t) * Hkv + h) * HD + c]);
+      const int code = max(-119, min(119, rint_prod(x, inv)));
+      const int row = nbuf + t;
+      bslot[kv == 0 ? row * HD + c : c * BC + row] = (int8_t)code;
+      if (kv == 0) k1[(bh * Nk + (size_t)j0 * BC + row) * HD + c] = (int8_t)code;
+      else v1t[((bh * Tk + j0) * HD + c) * BC + row] = __int2half_rn(code);
+    }
+    if (flush)
+      for (int t = 0; t < BC; ++t) tile[kv][t * HD + c] = bslot[kv == 0 ? t * HD + c : c * BC + t];
+  }
+  if (!flush || j0 >= max_blocks) return;  // (the host checks capacity first)
+  __syncthreads();
+  constexpr int REC = rec_bytes(HD, BC);
+  uint8_t* rec[2];
+#pragma unroll
+  for (int kv = 0; kv < 2; ++kv) rec[kv] = block_rec + ((bh * 2 + kv) * (size_t)max_blocks + j0) * REC;
+  if (tid < 2 * HD) {
+    const int kv = tid / HD, c = tid % HD;
+    uint8_t s;
+    int8_t z;
+    stage2_column<BC>(tile[kv], HD, c, bits_dev[h * 2 + kv], &s, &z);
+    rec[kv][c] = s;
+    rec[kv][HD + c] = (uint8_t)z;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int kv = 0; kv < 2; ++kv) pack_record<HD, BC>(tile[kv], kv, bits_dev[h * 2 + kv], rec[kv] + 2 * HD, tid, 256);
+  if (tid < 2) s_parent[(bh * 2 + tid) * max_blocks + j0] = st1_scale(div_by_119(a_univ[bh * 2 + tid]), scale_fp16);
+}
+
+__global__ void boundary_counters_kernel(int32_t* counters, int B, int BC, int r) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  int nb = counters[b * 2], nbuf = counters[b * 2 + 1] + r;
+  if (nbuf == BC) {
+    nb += 1;
+    nbuf = 0;
+  }
+  counters[b * 2] = nb;
+  counters[b * 2 + 1] = nbuf;
+}
+
+// The buffered tokens as the prefill operands of the boundary block (R-31): k1 rows B_c nb + t and
+// v1t block nb columns t < n_buf (the rest of the block's columns 0), scales s_univ.  One CTA per
+// (kv head, batch); thread = (K/V, channel).
+template <int HD, int BC>
+__global__ void __launch_bounds__(2 * HD) dequant_buffer_kernel(int Hkv, int Nk, const int8_t* __restrict__ buf,
+                                                               const float* __restrict__ a_univ,
+                                                               const int32_t* __restrict__ counters,
+                                                               int8_t* __restrict__ k1, __half* __restrict__ v1t,
+                                                               float* __restrict__ k1s, float* __restrict__ v1s,
+                                                               int scale_fp16) {
+  const int h = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+  const int nb = counters[b * 2], nbuf = counters[b * 2 + 1];
+  if (nbuf == 0) return;
+  const int kind = tid / HD, c = tid % HD, Tk = (Nk + BC - 1) / BC;
+  const size_t bh = (size_t)b * Hkv + h;
+  const int8_t* bslot = buf + (bh * 2 + kind) * (size_t)(BC * HD);
+  if (c == 0) (kind ? v1s : k1s)[bh * Tk + nb] = st1_scale(div_by_119(a_univ[bh * 2 + kind]), scale_fp16);
+  if (kind == 0) {
+    for (int t = 0; t < nbuf; ++t) k1[(bh * Nk + (size_t)nb * BC + t) * HD + c] = bslot[t * HD + c];
+  } else {
+    for (int t = 0; t < BC; ++t)
+      v1t[((bh * Tk + nb) * HD + c) * BC + t] = __int2half_rn(t < nbuf ? (int)bslot[c * BC + t] : 0);
+  }
+}
+
 }  // namespace ta
 
 // ---------------------------------------------------------------------------
@@ -414,13 +506,23 @@ namespace ta_host {
 using namespace ta;
 
 template <int HD, int BC>
+static void quant_boundary_hd(const turbo_kv_cache_t* c, const __half* k, const __half* v, int N, int r, int j0,
+                              int nbuf, int Nk, int8_t* k1, __half* v1t, cudaStream_t st, int scale_fp16) {
+  quant_boundary_kernel<HD, BC><<<dim3(c->n_kv_heads, c->batch), 256, 0, st>>>(
+      k, v, N, r, c->n_kv_heads, c->max_blocks, j0, nbuf, Nk, c->bits_dev, c->a_univ, c->buf, c->block_rec,
+      c->s_parent, k1, v1t, scale_fp16);
+  boundary_counters_kernel<<<(c->batch + 127) / 128, 128, 0, st>>>(c->counters, c->batch, BC, r);
+}
+
+template <int HD, int BC>
 static void quant_prefill_hd(const turbo_kv_cache_t* c, const __half* k, const __half* v, int N, int8_t* k1,
-                             __half* v1t, float* k1s, float* v1s, cudaStream_t st, int j0, int Nk, int scale_fp16) {
+                             __half* v1t, float* k1s, float* v1s, cudaStream_t st, int j0, int Nk, int scale_fp16,
+                             int t0, int Nin) {
   const int B = c->batch, H = c->n_kv_heads, Tc = (N + BC - 1) / BC;
   dim3 grid(Tc, H, 2 * B);  // z = 2 b + (K, V)
   quant_prefill_kernel<HD, BC><<<grid, HD, 0, st>>>(k, v, N, H, c->max_blocks, j0, Nk, c->bits_dev, c->block_rec,
-                                                   c->s_parent, c->a_univ, k1, v1t, k1s, v1s, scale_fp16);
-  quant_tail_kernel<HD, BC><<<dim3(H, B), 256, 0, st>>>(k, v, N, H, c->a_univ, c->buf, c->counters, j0);
+                                                   c->s_parent, c->a_univ, k1, v1t, k1s, v1s, scale_fp16, t0, Nin);
+  quant_tail_kernel<HD, BC><<<dim3(H, B), 256, 0, st>>>(k, v, N, H, c->a_univ, c->buf, c->counters, j0, t0, Nin);
 }
 
 cudaError_t launch_quant_prefill(const turbo_kv_cache_t* c, const __half* k, const __half* v, int N, int8_t* k1,
@@ -428,20 +530,38 @@ cudaError_t launch_quant_prefill(const turbo_kv_cache_t* c, const __half* k, con
                                  int scale_fp16) {
   // j0 = 0, Nk = N: PREFILL (resets the universal scales and the buffer); j0 > 0: a
   // further prefill chunk appended at cache block j0 (R-28), stage-1 outputs over Nk tokens.
+  // A chunk into a cache that ends inside a block (n_buf = Nk - N - B_c j0 > 0, R-31) first
+  // completes that block as appends do (quant_boundary_kernel), the rest is block-aligned.
   const int B = c->batch, H = c->n_kv_heads, HD = c->head_dim, BC = c->block_kv;
   cudaError_t e = cudaSuccess;
-  if (j0 == 0) {
+  if (Nk == N) {  // PREFILL (no cached tokens before)
     e = cudaMemsetAsync(c->a_univ, 0, sizeof(float) * B * H * 2, st);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(c->buf, 0, (size_t)B * H * 2 * BC * HD, st);
     if (e != cudaSuccess) return e;
   }
+  int t0 = 0;
+  const int nbuf = (Nk - N) - j0 * BC;  // buffered tokens before the chunk (R-31)
+  if (nbuf > 0) {
+    const int r = std::min(N, BC - nbuf);
+    if (HD == 128) {
+      if (BC == 64) quant_boundary_hd<128, 64>(c, k, v, N, r, j0, nbuf, Nk, k1, v1t, st, scale_fp16);
+      else quant_boundary_hd<128, 128>(c, k, v, N, r, j0, nbuf, Nk, k1, v1t, st, scale_fp16);
+    } else {
+      if (BC == 64) quant_boundary_hd<64, 64>(c, k, v, N, r, j0, nbuf, Nk, k1, v1t, st, scale_fp16);
+      else quant_boundary_hd<64, 128>(c, k, v, N, r, j0, nbuf, Nk, k1, v1t, st, scale_fp16);
+    }
+    if (r == N) return cudaGetLastError();
+    t0 = r;  // the rest starts the next block
+    j0 += 1;
+  }
+  const int n = N - t0;
   if (HD == 128) {
-    if (BC == 64) quant_prefill_hd<128, 64>(c, k, v, N, k1, v1t, k1s, v1s, st, j0, Nk, scale_fp16);
-    else quant_prefill_hd<128, 128>(c, k, v, N, k1, v1t, k1s, v1s, st, j0, Nk, scale_fp16);
+    if (BC == 64) quant_prefill_hd<128, 64>(c, k, v, n, k1, v1t, k1s, v1s, st, j0, Nk, scale_fp16, t0, N);
+    else quant_prefill_hd<128, 128>(c, k, v, n, k1, v1t, k1s, v1s, st, j0, Nk, scale_fp16, t0, N);
   } else {
-    if (BC == 64) quant_prefill_hd<64, 64>(c, k, v, N, k1, v1t, k1s, v1s, st, j0, Nk, scale_fp16);
-    else quant_prefill_hd<64, 128>(c, k, v, N, k1, v1t, k1s, v1s, st, j0, Nk, scale_fp16);
+    if (BC == 64) quant_prefill_hd<64, 64>(c, k, v, n, k1, v1t, k1s, v1s, st, j0, Nk, scale_fp16, t0, N);
+    else quant_prefill_hd<64, 128>(c, k, v, n, k1, v1t, k1s, v1s, st, j0, Nk, scale_fp16, t0, N);
   }
   return cudaGetLastError();
 }
@@ -455,17 +575,32 @@ static void dequant_cache_hd(const turbo_kv_cache_t* c, dim3 grid, int blk_begin
 }
 
 cudaError_t launch_dequant_cache(const turbo_kv_cache_t* c, int blk_begin, int blk_end, int Nk, int8_t* k1,
-                                 __half* v1t, float* k1s, float* v1s, cudaStream_t st) {
+                                 __half* v1t, float* k1s, float* v1s, cudaStream_t st, int scale_fp16) {
   const int B = c->batch, H = c->n_kv_heads, HD = c->head_dim, BC = c->block_kv;
   const int last = blk_end >= 0 ? std::min(blk_end, c->max_blocks) : c->max_blocks;
-  if (last <= blk_begin) return cudaSuccess;
-  dim3 grid(last - blk_begin, H, B);
-  if (HD == 128) {
-    if (BC == 64) dequant_cache_hd<128, 64>(c, grid, blk_begin, blk_end, Nk, k1, v1t, k1s, v1s, st);
-    else dequant_cache_hd<128, 128>(c, grid, blk_begin, blk_end, Nk, k1, v1t, k1s, v1s, st);
-  } else {
-    if (BC == 64) dequant_cache_hd<64, 64>(c, grid, blk_begin, blk_end, Nk, k1, v1t, k1s, v1s, st);
-    else dequant_cache_hd<64, 128>(c, grid, blk_begin, blk_end, Nk, k1, v1t, k1s, v1s, st);
+  dim3 grid(std::max(0, last - blk_begin), H, B);
+  if (last > blk_begin) {
+    if (HD == 128) {
+      if (BC == 64) dequant_cache_hd<128, 64>(c, grid, blk_begin, blk_end, Nk, k1, v1t, k1s, v1s, st);
+      else dequant_cache_hd<128, 128>(c, grid, blk_begin, blk_end, Nk, k1, v1t, k1s, v1s, st);
+    } else {
+      if (BC == 64) dequant_cache_hd<64, 64>(c, grid, blk_begin, blk_end, Nk, k1, v1t, k1s, v1s, st);
+      else dequant_cache_hd<64, 128>(c, grid, blk_begin, blk_end, Nk, k1, v1t, k1s, v1s, st);
+    }
+  }
+  if (blk_end < 0 && c->n_tokens % BC != 0) {  // the buffered tail as the boundary block (R-31)
+    const dim3 g2(H, B);
+    if (HD == 128) {
+      if (BC == 64)
+        dequant_buffer_kernel<128, 64><<<g2, 256, 0, st>>>(H, Nk, c->buf, c->a_univ, c->counters, k1, v1t, k1s, v1s, scale_fp16);
+      else
+        dequant_buffer_kernel<128, 128><<<g2, 256, 0, st>>>(H, Nk, c->buf, c->a_univ, c->counters, k1, v1t, k1s, v1s, scale_fp16);
+    } else {
+      if (BC == 64)
+        dequant_buffer_kernel<64, 64><<<g2, 128, 0, st>>>(H, Nk, c->buf, c->a_univ, c->counters, k1, v1t, k1s, v1s, scale_fp16);
+      else
+        dequant_buffer_kernel<64, 128><<<g2, 128, 0, st>>>(H, Nk, c->buf, c->a_univ, c->counters, k1, v1t, k1s, v1s, scale_fp16);
+    }
   }
   return cudaGetLastError();
 }
