@@ -482,7 +482,7 @@ TA_DEV SeqUnits seq_units(const DecodeArgs& a, int b) {
 // part*G .. part*G+G-1 of o_parts / lse_parts; the final [B][Hq] layout when
 // part == b*Hkv + kvh).  `it` counts the ring iterations of this warp across
 // segments (stage = it & 1, mbarrier parity = (it >> 1) & 1).
-template <int HD, bool PACK, bool TAP, int BC>
+template <int HD, bool PACK, bool TAP, int BC, bool SF>
 TA_DEV void decode_segment(const DecodeArgs& a, DecodeSmem<HD, PACK, BC>& sm, int b, int kvh, int j0, int j1, bool use_buf,
                            int nbuf, size_t part, bool tap_ok, uint32_t& it, int lane) {
   using M = Map<HD, PACK>;
@@ -581,10 +581,7 @@ TA_DEV void decode_segment(const DecodeArgs& a, DecodeSmem<HD, PACK, BC>& sm, in
     const bool tap = TAP && tap_row >= 0 && a.tap.j_block == j;
     float alpha[2], s_p[2];
     int sum_p[2];
-    if (a.sas_fp16)
-      softmax_tile<HD, PACK, TAP, true, BC, true>(a, st, sv, BC, cqk, pbuf, lut_lane, alpha, s_p, sum_p, tap, tap_row, g, q);
-    else
-      softmax_tile<HD, PACK, TAP, true, BC>(a, st, sv, BC, cqk, pbuf, lut_lane, alpha, s_p, sum_p, tap, tap_row, g, q);
+    softmax_tile<HD, PACK, TAP, true, BC, SF>(a, st, sv, BC, cqk, pbuf, lut_lane, alpha, s_p, sum_p, tap, tap_row, g, q);
     int acc[M::NC][2];
     if (bitsV == 4) pv_block<HD, 4, PACK, false, BC>(recV, nullptr, pbuf, sum_p, acc, g, q);
     else pv_block<HD, 2, PACK, false, BC>(recV, nullptr, pbuf, sum_p, acc, g, q);
@@ -608,11 +605,8 @@ TA_DEV void decode_segment(const DecodeArgs& a, DecodeSmem<HD, PACK, BC>& sm, in
     const bool tap = TAP && tap_row >= 0 && a.tap.j_block == -1;
     float alpha[2], s_p[2];
     int sum_p[2];
-    if (a.sas_fp16)
-      softmax_tile<HD, PACK, TAP, false, BC, true>(a, st, sv, nbuf, cqk, pbuf, lut_lane, alpha, s_p, sum_p, tap, tap_row, g,
-                                                    q);
-    else
-      softmax_tile<HD, PACK, TAP, false, BC>(a, st, sv, nbuf, cqk, pbuf, lut_lane, alpha, s_p, sum_p, tap, tap_row, g, q);
+    softmax_tile<HD, PACK, TAP, false, BC, SF>(a, st, sv, nbuf, cqk, pbuf, lut_lane, alpha, s_p, sum_p, tap, tap_row, g,
+                                              q);
     int acc[M::NC][2];
     pv_block<HD, 4, PACK, true, BC>(0, vb, pbuf, sum_p, acc, g, q);
     const float cpv[2] = {__fmul_rn(s_p[0], sV), __fmul_rn(s_p[1], sV)};
@@ -651,7 +645,7 @@ TA_DEV void decode_segment(const DecodeArgs& a, DecodeSmem<HD, PACK, BC>& sm, in
 //    W contiguous chunks of C = max(kMinUnits, ceil(total / W)) units; a warp
 //    runs one pass per (b, kv head) piece of its chunk; piece (bh, w) writes
 //    part bh + w (unique: pieces of a later bh belong to no earlier warp).
-template <int HD, bool PACK, bool TAP, int BC>
+template <int HD, bool PACK, bool TAP, int BC, bool SF>
 __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_constant__ DecodeArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -673,7 +667,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
     const int je = su.jb + su.nblk, per = (su.nblk + a.n_splits - 1) / a.n_splits;
     const int j0 = min(su.jb + split * per, je), j1 = min(j0 + per, je);
     const bool use_buf = a.with_buffer && split == a.n_splits - 1 && su.nbuf > 0;
-    decode_segment<HD, PACK, TAP, BC>(a, sm, b, kvh, j0, j1, use_buf, su.nbuf, (size_t)split * a.B * a.Hkv + bh,
+    decode_segment<HD, PACK, TAP, BC, SF>(a, sm, b, kvh, j0, j1, use_buf, su.nbuf, (size_t)split * a.B * a.Hkv + bh,
                                   split == 0, it, lane);
     return;
   }
@@ -713,7 +707,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) decode_kernel(const __grid_
   while (pos < end) {
     const int U = su.units, kvh = (pos - base) / U, u0 = (pos - base) % U;
     const int seg_end = min(end, base + (kvh + 1) * U), u1 = seg_end - (base + kvh * U);
-    decode_segment<HD, PACK, TAP, BC>(a, sm, b, kvh, su.jb + u0, su.jb + min(u1, su.nblk), u1 > su.nblk, su.nbuf,
+    decode_segment<HD, PACK, TAP, BC, SF>(a, sm, b, kvh, su.jb + u0, su.jb + min(u1, su.nblk), u1 > su.nblk, su.nbuf,
                                   (size_t)b * a.Hkv + kvh + w, true, it, lane);
     pos = seg_end;
     while (pos < end && pos >= base + su.units * a.Hkv) {
@@ -887,8 +881,8 @@ template <int HD, bool PK, bool TP>
 static int decode_ctas_per_sm() {
   int n = 0;
   const size_t smem = sizeof(DecodeSmem<HD, PK, 64>) * kWarpsPerCta;
-  cudaFuncSetAttribute(decode_kernel<HD, PK, TP, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_kernel<HD, PK, TP, 64>, 32 * kWarpsPerCta, smem) !=
+  cudaFuncSetAttribute(decode_kernel<HD, PK, TP, 64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_kernel<HD, PK, TP, 64, false>, 32 * kWarpsPerCta, smem) !=
       cudaSuccess)
     n = 0;
   return n;
@@ -961,12 +955,15 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
   const int tasks = S > 0 ? B * H * S : W;
   const dim3 grid((tasks + kWarpsPerCta - 1) / kWarpsPerCta);
   const bool pack = a.G <= 4;
-#define TA_DEC_B(HDV, PK, TP, BCV)                                                                        \
+#define TA_DEC_S(HDV, PK, TP, BCV, SFV)                                                                   \
   {                                                                                                         \
     const size_t smem = sizeof(DecodeSmem<HDV, PK, BCV>) * kWarpsPerCta;                                    \
-    cudaFuncSetAttribute(decode_kernel<HDV, PK, TP, BCV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    launch_pdl(decode_kernel<HDV, PK, TP, BCV>, grid, dim3(32 * kWarpsPerCta), smem, st, a);                \
+    cudaFuncSetAttribute(decode_kernel<HDV, PK, TP, BCV, SFV>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                         (int)smem);                                                                        \
+    launch_pdl(decode_kernel<HDV, PK, TP, BCV, SFV>, grid, dim3(32 * kWarpsPerCta), smem, st, a);           \
   }
+#define TA_DEC_B(HDV, PK, TP, BCV) \
+  if (a.sas_fp16) TA_DEC_S(HDV, PK, TP, BCV, true) else TA_DEC_S(HDV, PK, TP, BCV, false)
 #define TA_DEC(HDV, PK, TP) \
   if (c->block_kv == 64) TA_DEC_B(HDV, PK, TP, 64) else TA_DEC_B(HDV, PK, TP, 128)
 #define TA_DEC2(HDV)                                                  \
@@ -983,6 +980,7 @@ cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, in
 #undef TA_DEC2
 #undef TA_DEC
 #undef TA_DEC_B
+#undef TA_DEC_S
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || S == 1) return e;
   if (S <= 0) {

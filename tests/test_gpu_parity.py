@@ -402,6 +402,42 @@ def test_head_priority_planner_parity(ta, shape):
     np.testing.assert_array_equal(bits.reshape(-1), O.plan_bits(ref.reshape(-1), n2))
 
 
+def test_planner_drives_the_cache_end_to_end(ta):
+    """NEXT-1 end to end: the on-device plan (turbo_head_priority -> turbo_plan_bits, half of the
+    slots at 2 bits) configures the cache that turbo_quantize_kv fills; records and the
+    decode match the oracle run with the oracle's own plan over the same K/V."""
+    B, N, Hq, Hkv, d = 2, 64 * 6 + 21, 16, 4, 128
+    q, k, v = synth.qkv(808, B, N, Hq, Hkv, d)
+    kt, vt = torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda()
+    bits = ta.turbo_plan_bits(ta.turbo_head_priority(kt, vt), Hkv).numpy().reshape(Hkv, 2)
+    ref_pr = np.array([[O.head_priority(x[:, :, h].reshape(B * N, d).astype(np.float32)) for x in (k, v)]
+                       for h in range(Hkv)])
+    ref_bits = O.plan_bits(ref_pr.reshape(-1), Hkv).reshape(Hkv, 2)
+    np.testing.assert_array_equal(bits, ref_bits)
+    assert (bits == 2).sum() == Hkv and len(set(bits.reshape(-1))) == 2
+    p = ta.params(head_dim=d)
+    maxb = N // 64 + 2
+    cache = ta.KVCache(B, Hkv, d, max_blocks=maxb, bits=bits)
+    ta.turbo_quantize_kv(p, cache, kt, vt)
+    qd, _, _ = synth.decode_token(809, B, Hq, Hkv, d)
+    o, _, lse = ta.turbo_attention_decode(p, cache, torch.from_numpy(qd).cuda(), n_splits=1)
+    torch.cuda.synchronize()
+    op = O.params(d=d)
+    ref = O.build_cache(op, k.astype(np.float32), v.astype(np.float32), ref_bits, maxb)
+    recs = cache.records().cpu().numpy()
+    for b in range(B):
+        for h in range(Hkv):
+            for kind, sl in enumerate(ref["slots"][b][h]):
+                for j in range(sl.n_blocks):
+                    codes, s_int, z_int = cache_layout.unpack_record(recs[b, h, kind, j], d, int(ref_bits[h][kind]),
+                                                                     kind)
+                    np.testing.assert_array_equal(codes, sl.codes[j])
+                    np.testing.assert_array_equal(s_int, sl.s_int[j])
+        ro, rl = _oracle_decode(op, qd[b].astype(np.float32), ref["slots"][b], Hq // Hkv, [(0, N // 64)])
+        assert_out_close(o[b].cpu().numpy(), ro, f"b{b}")
+        np.testing.assert_allclose(lse[b].cpu().numpy(), rl, atol=1e-4, rtol=1e-5)
+
+
 @pytest.mark.parametrize("which,lo,hi", [(0, 0x04000000, 0x7F7FFFFF), (1, 0x03800000, 0x7E800000)])
 def test_fast_division_exhaustive(ta, which, lo, hi):
     """The fast correctly rounded a/119 and 119/a used for the stage-1 and P
