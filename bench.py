@@ -778,6 +778,64 @@ def run_prefill_chunk(args, rank, world, device):
                        "parallelism": f"{world} rank(s), each its own batch, no collective"}}
 
 
+def run_q_projection(args, rank, world, device):
+    """NEXT-3: the Q projection with the stage-1 Q quantisation fused into its epilogue on the
+    configs[1] shape (Llama-3-8B: B = 8, N = 4096, D = 4096 -> 32 heads x d = 128), then the prefill on
+    the quantised query (turbo_attention_prefill_q1).  Value: projection TFLOP/s (2 T D Hq d), its
+    roofline against the fp16 tensor peak (the measured bf16 burst; fp16 and bf16 share the rate)."""
+    import torch
+
+    from paper_2412_08585_b200 import binding as ta
+    from paper_2412_08585_b200 import synth
+
+    c = CFG_PREFILL
+    B, N, Hq, Hkv, d = c["B"], c["N"], c["Hq"], c["Hkv"], c["d"]
+    D = Hq * d
+    p = ta.params(head_dim=d)
+    gen = torch.Generator(device=device)
+    gen.manual_seed(5150 + rank)
+    x = (0.5 * torch.randn((B, N, D), generator=gen, device=device)).half()
+    wq = (torch.randn((Hq * d, D), generator=gen, device=device) / math.sqrt(D)).half()
+    _, k, v = synth.qkv_torch(5151 + rank, B, N, Hq, Hkv, d, device=device)
+    cache = ta.KVCache(B, Hkv, d, max_blocks=N // 64 + 2, bits=synth.head_bits_alternating(Hkv), device=device)
+    ops_kv = ta.turbo_quantize_kv(p, cache, k, v)
+    q1, sq, _ = ta.turbo_q_projection(p, x, wq, Hq)
+    o, lse = ta.turbo_attention_prefill_q1(p, q1, sq, *ops_kv)
+    st = torch.cuda.current_stream()
+    t_proj = t_pre = 0.0
+    clk = None
+    for i in range(args.warmup + args.steps):
+        if i == args.warmup:
+            clk = Clocks(device) if rank == 0 else None
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(st)
+        ta.turbo_q_projection(p, x, wq, Hq)
+        e1.record(st)
+        ta.turbo_attention_prefill_q1(p, q1, sq, *ops_kv, o=o, lse=lse)
+        e2.record(st)
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            t_proj += e0.elapsed_time(e1)
+            t_pre += e1.elapsed_time(e2)
+    clocks = clk.stop() if clk else None
+    ms_p = _max_over_ranks(t_proj, world, device) / args.steps
+    ms_a = _max_over_ranks(t_pre, world, device) / args.steps
+    flops = 2.0 * B * N * D * Hq * d * world
+    ops_attn = 4.0 * d * N * (N + 1) / 2 * B * Hq * world
+    pk = peaks()
+    ach = flops / world / (ms_p * 1e-3) / 1e12
+    return {"value": flops / (ms_p * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_step": ms_p + ms_a, "scaling": "weak",
+            "clocks": clocks, "dtype": "fp16",
+            "roofline": {"bound": "tensor", "kernel": "q_projection_kernel<128> (turbo_q_projection)",
+                         "achieved": round(ach, 1), "peak": round(pk["bf16"], 1), "unit": "TFLOP/s",
+                         "frac": round(ach / pk["bf16"], 4), "traffic": None,
+                         "peak_source": f"measured bf16 burst {pk['bf16']} TF/s ({pk['src']}), fp16 = bf16 rate"},
+            "prefill_q1": {"ms": round(ms_a, 4), "tops": round(ops_attn / (ms_a * 1e-3) / 1e12, 1)},
+            "config": {"workload": "NEXT-3 fused Q projection + stage-1 Q quantisation (P:660), configs[1] shape "
+                                   "(B=8, N=4096, D=4096 -> 32 heads x d=128), then the prefill on the INT8 query",
+                       "parallelism": f"{world} rank(s), each its own batch, no collective"}}
+
+
 def run_decode_long(args, rank, world, device):
     """configs[4]: 128k-context decode, batch 16 (Llama-3-8B attention shape,
     32/8 heads, mixed INT4/INT2), cache sequence-sharded over the ranks; per
@@ -888,7 +946,8 @@ def main():
                     help="decode split count (default: binding.auto_splits; 0: the balanced schedule)")
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-deviation", action="store_true", help="skip the deviation-from-exact report")
-    ap.add_argument("--workload", default="step", choices=["step", "prefill_70b", "decode_long", "prefill_chunk"],
+    ap.add_argument("--workload", default="step",
+                    choices=["step", "prefill_70b", "decode_long", "prefill_chunk", "q_projection"],
                     help="step = the default hot-path step (configs[1] + configs[2] decode)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -917,16 +976,16 @@ def main():
     build.build()
     if args.workload != "step":
         fn = {"prefill_70b": run_prefill_70b, "decode_long": run_decode_long,
-              "prefill_chunk": run_prefill_chunk}[args.workload]
+              "prefill_chunk": run_prefill_chunk, "q_projection": run_q_projection}[args.workload]
         res = fn(args, rank, world, local)
         if rank == 0:
             line = {"metric": BASE_METRIC, "value": round(res["value"], 2), "unit": res["unit"], "n_gpus": world,
                     "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["ms_step"], 4),
-                    "higher_is_better": True, "scaling": res["scaling"], "vs_baseline": None, "dtype": "int8",
-                    "data": "synthetic", "config": res["config"]}
+                    "higher_is_better": True, "scaling": res["scaling"], "vs_baseline": None,
+                    "dtype": res.get("dtype", "int8"), "data": "synthetic", "config": res["config"]}
             if "tokens_per_s" in res:
                 line["tokens_per_s"] = round(res["tokens_per_s"], 1)
-            for key in ("clocks", "roofline"):
+            for key in ("clocks", "roofline", "prefill_q1"):
                 if key in res:
                     line[key] = res[key]
             print(json.dumps(line), flush=True)

@@ -187,6 +187,30 @@ TURBO_API turbo_status_t turbo_attention_prefill(const turbo_params_t* params, i
                                        const void* v1t, const float* k1_scale, const float* v1_scale,
                                        void* o, float* lse, turbo_stream_t stream);
 
+/* The Q projection with the stage-1 Q quantisation fused into its epilogue (Sec. 5: "we
+ * fused the QKV projection with quantization"; NEXT-3), tcgen05 kind::f16 GEMM:
+ *   x       FP16 [B][N][D] (the layer input, token-major), D % 64 == 0.
+ *   wq      FP16 [Hq * d][D] (one row per output feature); (Hq * d) % 256 == 0.
+ *   q1_out  INT8 [B][N][Hq][d]: Q^q1 of Q = fp16(x wq^T) (the projection's FP16 output, rounded to
+ *           nearest even), stage 1 per (b, head, B_r-row block) exactly as turbo_attention_prefill
+ *           does it (Alg. 1; R-2, R-3; scale_fp16: R-29).
+ *   sq_out  f32 [B][Hq][ceil(N / B_r)] the blocks' scales.
+ *   q16_out FP16 [B][N][Hq][d] (the unquantised projection, for checking) or NULL.
+ * Errors: TURBO_ERR_UNSUPPORTED for D % 64 != 0 or (Hq d) % 256 != 0. */
+TURBO_API turbo_status_t turbo_q_projection(const turbo_params_t* params, int32_t B, int32_t N, int32_t D, int32_t Hq,
+                                            const void* x, const void* wq, int8_t* q1_out, float* sq_out,
+                                            void* q16_out, turbo_stream_t stream);
+
+/* turbo_attention_prefill with the query already quantised (q1 INT8 [B][N][Hq][d] and q1_scale
+ * f32 [B][Hq][ceil(N / B_r)], e.g. from turbo_q_projection): identical results to
+ * turbo_attention_prefill on the FP16 Q those codes came from; the kernel reads d instead of 2d
+ * bytes per query row. */
+TURBO_API turbo_status_t turbo_attention_prefill_q1(const turbo_params_t* params, int32_t B, int32_t N, int32_t Hq,
+                                                    int32_t Hkv, int32_t causal, const int8_t* q1,
+                                                    const float* q1_scale, const int8_t* k1, const void* v1t,
+                                                    const float* k1_scale, const float* v1_scale, void* o, float* lse,
+                                                    turbo_stream_t stream);
+
 /* Stage-1 reconstruction of flushed cache blocks [blk_begin, blk_end)
  * (blk_end = -1: all; blocks past a sequence's count are skipped), the
  * prefix operands of a chunked prefill (R-28): k1_out [B][Hkv][Nk][d] rows

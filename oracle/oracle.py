@@ -405,6 +405,13 @@ def plan_bits(priorities, n_2bit: int) -> np.ndarray:
 
 
 # ---------------------------------------------------------------- whole-tensor helpers
+def project_q(x, wq):
+    """The FP16 output of the Q projection: Q = fp16(x wq^T) with the product
+    formed in float64 and rounded once to binary16 (nearest even) -- a library matmul as one
+    step.  x [..., D], wq [Hq d][D] -> [..., Hq d] float16."""
+    return (np.asarray(x, np.float64) @ np.asarray(wq, np.float64).T).astype(np.float16)
+
+
 def build_cache(p: Params, k, v, bits, max_blocks):
     """Cache for a [B][N][Hkv][d] K/V pair: returns dict with slots[b][h] = (Kslot, Vslot),
     and the stage-1 prefill operands k1/v1 [B][Hkv][N][d], k1s/v1s [B][Hkv][T_c]."""

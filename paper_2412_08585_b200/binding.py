@@ -20,7 +20,8 @@ TURBO_OK, TURBO_ERR_INVALID_ARG, TURBO_ERR_UNSUPPORTED, TURBO_ERR_CAPACITY, TURB
 _ERR = {1: "TURBO_ERR_INVALID_ARG", 2: "TURBO_ERR_UNSUPPORTED", 3: "TURBO_ERR_CAPACITY", 4: "TURBO_ERR_CUDA"}
 
 EXPORTS = ("turbo_version", "turbo_cache_sizes", "turbo_quantize_kv", "turbo_attention_prefill",
-           "turbo_attention_prefill_chunk", "turbo_dequantize_cache",
+           "turbo_attention_prefill_chunk", "turbo_dequantize_cache", "turbo_q_projection",
+           "turbo_attention_prefill_q1",
            "turbo_decode_workspace_bytes", "turbo_decode_workers", "turbo_attention_decode", "turbo_combine_lse",
            "turbo_priority_workspace_bytes", "turbo_head_priority", "turbo_plan_bits", "turbo_selftest_div")
 
@@ -72,6 +73,10 @@ def lib() -> C.CDLL:
                                                         vp, vp, vp, vp, vp, vp]
             L.turbo_dequantize_cache.argtypes = [C.POINTER(TurboParams), C.POINTER(TurboKVCache), i32, i32, vp, vp,
                                                  vp, vp, i32, vp]
+        if hasattr(L, "turbo_q_projection"):  # (older A/B builds lack it)
+            L.turbo_q_projection.argtypes = [C.POINTER(TurboParams), i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]
+            L.turbo_attention_prefill_q1.argtypes = [C.POINTER(TurboParams), i32, i32, i32, i32, i32, vp, vp, vp, vp,
+                                                     vp, vp, vp, vp, vp]
         L.turbo_decode_workspace_bytes.argtypes = [i32, i32, i32, i32, i32]
         L.turbo_decode_workspace_bytes.restype = sz
         if hasattr(L, "turbo_decode_workers"):  # (older A/B builds lack it)
@@ -206,6 +211,40 @@ def turbo_attention_prefill(p, q, k1, v1t, k1_scale, v1_scale, causal=True, o=No
     _check("turbo_attention_prefill", lib().turbo_attention_prefill(
         C.byref(p), B, N, Hq, Hkv, int(causal), _ptr(q), _ptr(k1), _ptr(v1t), _ptr(k1_scale), _ptr(v1_scale),
         _ptr(o), _ptr(lse), _stream(stream)))
+    return o, lse
+
+
+def turbo_q_projection(p, x, wq, n_q_heads, want_q16=False, stream=None):
+    """Q = x wq^T with the stage-1 Q quantisation fused into the GEMM epilogue:
+    x fp16 [B,N,D], wq fp16 [Hq*d, D] -> (q1 int8 [B,N,Hq,d], q1_scale f32 [B,Hq,ceil(N/B_r)],
+    q16 fp16 [B,N,Hq,d] or None)."""
+    assert x.dtype == torch.float16 and wq.dtype == torch.float16 and x.is_contiguous() and wq.is_contiguous()
+    B, N, D = x.shape
+    d = p.head_dim
+    assert wq.shape == (n_q_heads * d, D)
+    dev = x.device
+    q1 = torch.empty((B, N, n_q_heads, d), dtype=torch.int8, device=dev)
+    sq = torch.empty((B, n_q_heads, -(-N // p.block_q)), dtype=torch.float32, device=dev)
+    q16 = torch.empty((B, N, n_q_heads, d), dtype=torch.float16, device=dev) if want_q16 else None
+    _check("turbo_q_projection", lib().turbo_q_projection(C.byref(p), B, N, D, n_q_heads, _ptr(x), _ptr(wq), _ptr(q1),
+                                                          _ptr(sq), _ptr(q16), _stream(stream)))
+    return q1, sq, q16
+
+
+def turbo_attention_prefill_q1(p, q1, q1_scale, k1, v1t, k1_scale, v1_scale, causal=True, o=None, lse=None,
+                               stream=None):
+    """Prefill with a pre-quantised query: q1 int8 [B,N,Hq,d], q1_scale [B,Hq,ceil(N/B_r)]
+    -> (o fp16 [B,N,Hq,d], lse f32 [B,Hq,N])."""
+    assert q1.dtype == torch.int8 and q1.is_contiguous()
+    B, N, Hq, d = q1.shape
+    Hkv = k1.shape[1]
+    if o is None:
+        o = torch.empty((B, N, Hq, d), dtype=torch.float16, device=q1.device)
+    if lse is None:
+        lse = torch.empty((B, Hq, N), dtype=torch.float32, device=q1.device)
+    _check("turbo_attention_prefill_q1", lib().turbo_attention_prefill_q1(
+        C.byref(p), B, N, Hq, Hkv, int(causal), _ptr(q1), _ptr(q1_scale), _ptr(k1), _ptr(v1t), _ptr(k1_scale),
+        _ptr(v1_scale), _ptr(o), _ptr(lse), _stream(stream)))
     return o, lse
 
 

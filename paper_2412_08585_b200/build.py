@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libturboattn.so")
-SOURCES = ["api.cu", "quantize.cu", "prefill.cu", "decode.cu", "planner.cu", "selftest.cu"]
+SOURCES = ["api.cu", "quantize.cu", "prefill.cu", "decode.cu", "projection.cu", "planner.cu", "selftest.cu"]
 HEADERS = ["common.cuh", "layout.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

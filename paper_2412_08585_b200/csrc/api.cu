@@ -19,7 +19,9 @@ cudaError_t launch_quant_append(const turbo_kv_cache_t* c, const __half* k, cons
                                 int scale_fp16);
 cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Nk, int Hq, int Hkv, int causal, const __half* q,
                            const int8_t* k1, const __half* v1t, const float* k1s, const float* v1s, __half* o,
-                           float* lse, cudaStream_t st);
+                           float* lse, cudaStream_t st, const int8_t* q1_in = nullptr, const float* sq_in = nullptr);
+cudaError_t launch_q_projection(const turbo_params_t* p, int B, int N, int D, int Hq, const __half* x, const __half* wq,
+                                int8_t* q1, float* sq, __half* q16, cudaStream_t st);
 size_t decode_workspace(int B, int Hq, int Hkv, int HD, int S);
 int decode_workers(int Hq, int Hkv, int HD);
 cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, int Hq, const __half* q, int blk_begin,
@@ -164,6 +166,35 @@ turbo_status_t turbo_attention_prefill_chunk(const turbo_params_t* params, int32
   return cuda_status(ta_host::launch_prefill(params, B, Nq, Nk, Hq, Hkv, causal, reinterpret_cast<const __half*>(q),
                                              k1, reinterpret_cast<const __half*>(v1t), k1_scale, v1_scale,
                                              reinterpret_cast<__half*>(o), lse, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+turbo_status_t turbo_q_projection(const turbo_params_t* params, int32_t B, int32_t N, int32_t D, int32_t Hq,
+                                  const void* x, const void* wq, int8_t* q1_out, float* sq_out, void* q16_out,
+                                  turbo_stream_t stream) {
+  turbo_status_t s = check_params(params);
+  if (s != TURBO_OK) return s;
+  if (B < 1 || N < 1 || D < 64 || Hq < 1) return TURBO_ERR_INVALID_ARG;
+  if (D % 64 != 0 || (Hq * params->head_dim) % 256 != 0) return TURBO_ERR_UNSUPPORTED;
+  if (!x || !wq || !q1_out || !sq_out) return TURBO_ERR_INVALID_ARG;
+  return cuda_status(ta_host::launch_q_projection(params, B, N, D, Hq, reinterpret_cast<const __half*>(x),
+                                                  reinterpret_cast<const __half*>(wq), q1_out, sq_out,
+                                                  reinterpret_cast<__half*>(q16_out),
+                                                  reinterpret_cast<cudaStream_t>(stream)));
+}
+
+turbo_status_t turbo_attention_prefill_q1(const turbo_params_t* params, int32_t B, int32_t N, int32_t Hq,
+                                          int32_t Hkv, int32_t causal, const int8_t* q1, const float* q1_scale,
+                                          const int8_t* k1, const void* v1t, const float* k1_scale,
+                                          const float* v1_scale, void* o, float* lse, turbo_stream_t stream) {
+  turbo_status_t s = check_params(params);
+  if (s != TURBO_OK) return s;
+  if (B < 1 || N < 1 || Hq < 1 || Hkv < 1 || (causal != 0 && causal != 1)) return TURBO_ERR_INVALID_ARG;
+  if (Hq % Hkv != 0) return TURBO_ERR_UNSUPPORTED;
+  if (!q1 || !q1_scale || !k1 || !v1t || !k1_scale || !v1_scale || !o || !lse) return TURBO_ERR_INVALID_ARG;
+  return cuda_status(ta_host::launch_prefill(params, B, N, N, Hq, Hkv, causal, nullptr, k1,
+                                             reinterpret_cast<const __half*>(v1t), k1_scale, v1_scale,
+                                             reinterpret_cast<__half*>(o), lse, reinterpret_cast<cudaStream_t>(stream),
+                                             q1, q1_scale));
 }
 
 turbo_status_t turbo_attention_prefill(const turbo_params_t* params, int32_t B, int32_t N, int32_t Hq, int32_t Hkv,

@@ -54,6 +54,8 @@ struct PrefillSmem {
 
 struct PrefillArgs {
   const __half* q;
+  const int8_t* q1_in;  // pre-quantised Q^q1 [B][N][Hq][d] (turbo_q_projection) or NULL
+  const float* sq_in;   // its scales [B][Hq][ceil(N / B_r)]
   __half* o;
   float* lse;
   const float* k1s;
@@ -225,9 +227,21 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t bar_grp = args.block_q == 64 ? 3 + slot * 2 + half : 1 + slot;  // the P-scale group
     const uint32_t grp_threads = args.block_q;
 
-    // Q stage-1 quantisation (Alg. 1; per B_r x d block)
+    // Q stage-1 quantisation (Alg. 1; per B_r x d block) -- or, with q1_in, the codes and
+    // scales the Q projection's epilogue produced (turbo_q_projection)
     float s_q;
-    {
+    if (args.q1_in) {
+      const int nbq = (N + args.block_q - 1) / args.block_q;
+      s_q = row_ok ? args.sq_in[((size_t)b * args.Hq + h) * nbq + row / args.block_q] : 0.f;
+      const uint4* src = reinterpret_cast<const uint4*>(args.q1_in + (((size_t)b * N + row) * args.Hq + h) * HD);
+#pragma unroll
+      for (int c = 0; c < HD / 16; ++c) {
+        const uint4 w = row_ok ? src[c] : make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(sm.q1[slot] + q1_swz<HD>(r, c)) = w;
+        if (tap_row) *reinterpret_cast<uint4*>(args.tap.q1 + (r & 63) * HD + c * 16) = w;
+      }
+      if (tap_row && (r & 63) == 0) args.tap.s_q[0] = s_q;
+    } else {
       uint4 qraw[HD / 8];
       float qa = 0.f;
       const __half* qrow = args.q + (((size_t)b * N + row) * args.Hq + h) * HD;
@@ -549,7 +563,7 @@ static bool make_map_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t 
 
 cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Nk, int Hq, int Hkv, int causal, const __half* q,
                            const int8_t* k1, const __half* v1t, const float* k1s, const float* v1s, __half* o,
-                           float* lse, cudaStream_t st) {
+                           float* lse, cudaStream_t st, const int8_t* q1_in, const float* sq_in) {
   const int HD = p->head_dim, BC = p->block_kv, Tc = (Nk + BC - 1) / BC;
   CUtensorMap tmk, tmv;
   const CUtensorMapSwizzle swk = HD == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
@@ -561,6 +575,8 @@ cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Nk, int Hq
     return cudaErrorInvalidValue;
   PrefillArgs a;
   a.q = q;
+  a.q1_in = q1_in;
+  a.sq_in = sq_in;
   a.o = o;
   a.lse = lse;
   a.k1s = k1s;
