@@ -9,7 +9,9 @@
 // so that turbo_attention_prefill_q1 reads INT8 Q^q1 (d bytes per row) instead of FP16 Q (2d bytes)
 // and Q is never written or re-read in FP16.
 //
-// One CTA per (128-token tile of one sequence, 256 output features = 256 / d heads); 192 threads:
+// One CTA per (128-token tile of one sequence, 256 output features = 256 / d heads); 192 threads;
+// CL = 2: clusters of two CTAs on consecutive token tiles share the W tile -- each loads one half
+// and multicasts it to both (TMA .multicast::cluster), halving the W stream from L2:
 //   warp 0      TMA producer: X [128 x 64] and W [256 x 64] fp16 tiles (128B swizzle), 4-stage ring;
 //   warp 1      single-thread tcgen05.mma.kind::f16 issuer, M = 128, N = 256, K = 16, fp32 accumulator
 //               in 256 TMEM columns (warp 1 also owns TMEM);
@@ -40,7 +42,30 @@ struct ProjArgs {
   int B, N, D, Hq, HD, block_q, m_tiles, scale_fp16;
 };
 
-template <int HD>
+TA_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+TA_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+TA_DEV void tma_load_2d_mc(void* smem_dst, const void* desc, uint64_t* bar, int c0, int c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(desc), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+TA_DEV void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+template <int HD, int CL>
 __global__ void __launch_bounds__(192, 1)
     q_projection_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
                         const __grid_constant__ ProjArgs args) {
@@ -51,10 +76,11 @@ __global__ void __launch_bounds__(192, 1)
   const int row0 = mt * kPM;                     // first token of the tile inside sequence b
   const int n0 = nt * kPN;                       // first output feature
   const int ksteps = args.D / kPK;
+  const uint32_t crank = CL > 1 ? cluster_rank() : 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kPStages; ++s) {
       mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], 1);
+      mbar_init(&sm.empty[s], CL);  // one MMA commit per CTA of the cluster (both read the shared W)
     }
     mbar_init(&sm.acc_full, 1);
     fence_barrier_init();
@@ -62,6 +88,7 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_alloc(&sm.tmem_base, kPN);
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync_all();  // the peer's barriers are initialised before any multicast
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
 
@@ -75,7 +102,13 @@ __global__ void __launch_bounds__(192, 1)
         if (n > 0) mbar_wait(&sm.empty[st], (n - 1) & 1);
         mbar_expect_tx(&sm.full[st], (kPM + kPN) * kPK * 2);
         tma_load_2d(sm.a[st], &tm_x, &sm.full[st], k * kPK, xrow);
-        tma_load_2d(sm.b[st], &tm_w, &sm.full[st], k * kPK, n0);
+        if (CL == 1) {
+          tma_load_2d(sm.b[st], &tm_w, &sm.full[st], k * kPK, n0);
+        } else {  // this CTA's half of the W tile, into both CTAs' stage (same offsets)
+          constexpr int HALF = kPN / 2;
+          tma_load_2d_mc(sm.b[st] + crank * HALF * kPK, &tm_w, &sm.full[st], k * kPK, n0 + (int)crank * HALF,
+                         (uint16_t)0x3);
+        }
       }
     }
   } else if (warp == 1) {
@@ -90,7 +123,8 @@ __global__ void __launch_bounds__(192, 1)
         for (int ks = 0; ks < kPK / 16; ++ks)
           mma_f16_ss(tmem, smem_desc(aa + ks * 32, 1024, kSw128), smem_desc(ba + ks * 32, 1024, kSw128), idesc,
                      (k | ks) != 0);
-        mma_commit(&sm.empty[st]);
+        if (CL == 1) mma_commit(&sm.empty[st]);
+        else mma_commit_mc(&sm.empty[st], (uint16_t)0x3);  // frees the stage in both CTAs
         if (k == ksteps - 1) mma_commit(&sm.acc_full);
       }
       __syncwarp();
@@ -160,6 +194,7 @@ __global__ void __launch_bounds__(192, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync_all();  // no CTA leaves while its peer may still multicast into it
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, kPN);
@@ -197,7 +232,9 @@ cudaError_t launch_q_projection(const turbo_params_t* p, int B, int N, int D, in
   const int HD = p->head_dim;
   CUtensorMap tmx, tmw;
   if (!make_map_2d_f16(&tmx, x, D, (uint64_t)B * N, kPK, kPM)) return cudaErrorInvalidValue;
-  if (!make_map_2d_f16(&tmw, wq, D, (uint64_t)Hq * HD, kPK, kPN)) return cudaErrorInvalidValue;
+  const bool pair = ((N + kPM - 1) / kPM * B) % 2 == 0;  // clusters of two token tiles sharing the W tile
+  // W boxes: the whole 256-feature tile, or (pair) the half each CTA of the cluster multicasts
+  if (!make_map_2d_f16(&tmw, wq, D, (uint64_t)Hq * HD, kPK, pair ? kPN / 2 : kPN)) return cudaErrorInvalidValue;
   ProjArgs a;
   a.q1 = q1;
   a.sq = sq;
@@ -212,13 +249,29 @@ cudaError_t launch_q_projection(const turbo_params_t* p, int B, int N, int D, in
   a.scale_fp16 = p->scale_fp16;
   const dim3 grid((unsigned)(a.m_tiles * B), (unsigned)(Hq * HD / kPN));
   const size_t smem = sizeof(ProjSmem) + 1024;
-  if (HD == 128) {
-    cudaFuncSetAttribute(q_projection_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    q_projection_kernel<128><<<grid, 192, smem, st>>>(tmx, tmw, a);
-  } else {
-    cudaFuncSetAttribute(q_projection_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    q_projection_kernel<64><<<grid, 192, smem, st>>>(tmx, tmw, a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = pair ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+#define TA_PROJ(HDV, CLV)                                                                                  \
+  {                                                                                                        \
+    cudaFuncSetAttribute(q_projection_kernel<HDV, CLV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    cudaError_t e = cudaLaunchKernelEx(&cfg, q_projection_kernel<HDV, CLV>, tmx, tmw, a);                  \
+    return e != cudaSuccess ? e : cudaGetLastError();                                                      \
   }
-  return cudaGetLastError();
+  if (HD == 128) {
+    if (pair) TA_PROJ(128, 2) else TA_PROJ(128, 1)
+  } else {
+    if (pair) TA_PROJ(64, 2) else TA_PROJ(64, 1)
+  }
+#undef TA_PROJ
 }
 }  // namespace ta_host
