@@ -30,7 +30,7 @@ constexpr int kPM = 128, kPN = 256, kPK = 64, kPStages = 4;
 struct ProjSmem {
   __half a[kPStages][kPM * kPK];  // X tile, K-major, 128-B rows (SW128)
   __half b[kPStages][kPN * kPK];  // W tile, K-major, 128-B rows (SW128)
-  uint64_t full[kPStages], empty[kPStages], acc_full;
+  uint64_t full[kPStages], empty[kPStages], acc_full[2], acc_empty[2];
   uint32_t tmem_base;
   float red[kPN / 64][4];  // [head][quadrant] row-block maxima
 };
@@ -65,6 +65,10 @@ TA_DEV void mma_commit_mc(uint64_t* bar, uint16_t mask) {
       : "memory");
 }
 
+// Persistent: the grid (a multiple of the cluster size, at most one CTA per SM) walks the tiles --
+// (128-token tile, 256-feature tile) pairs of CL consecutive token tiles sharing a feature tile, feature
+// tiles outermost -- and keeps two accumulators in TMEM (2 x 256 columns), so the producer and the MMA
+// issuer run ahead into the next tile while the epilogue drains the previous one.
 template <int HD, int CL>
 __global__ void __launch_bounds__(192, 1)
     q_projection_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
@@ -72,20 +76,29 @@ __global__ void __launch_bounds__(192, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   ProjSmem& sm = *reinterpret_cast<ProjSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int mt = blockIdx.x % args.m_tiles, b = (blockIdx.x / args.m_tiles), nt = blockIdx.y;
-  const int row0 = mt * kPM;                     // first token of the tile inside sequence b
-  const int n0 = nt * kPN;                       // first output feature
   const int ksteps = args.D / kPK;
   const uint32_t crank = CL > 1 ? cluster_rank() : 0;
+  const int mtot = args.m_tiles * args.B;               // token tiles over all sequences
+  const int groups = (mtot / CL) * (args.Hq * HD / kPN);  // cluster work units
+  const int g0 = blockIdx.x / CL, gstep = gridDim.x / CL;
+  auto tile_of = [&](int g, int& b, int& row0, int& n0) {
+    const int mx = (g % (mtot / CL)) * CL + (int)crank, ny = g / (mtot / CL);
+    b = mx / args.m_tiles;
+    row0 = (mx % args.m_tiles) * kPM;
+    n0 = ny * kPN;
+  };
   if (threadIdx.x == 0) {
     for (int s = 0; s < kPStages; ++s) {
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.empty[s], CL);  // one MMA commit per CTA of the cluster (both read the shared W)
     }
-    mbar_init(&sm.acc_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.acc_full[i], 1);
+      mbar_init(&sm.acc_empty[i], 4);  // one arrival per epilogue warp
+    }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(&sm.tmem_base, kPN);
+  if (warp == 1) tmem_alloc(&sm.tmem_base, 2 * kPN);
   tc_fence_before();
   __syncthreads();
   if (CL > 1) cluster_sync_all();  // the peer's barriers are initialised before any multicast
@@ -96,100 +109,136 @@ __global__ void __launch_bounds__(192, 1)
     if (elect_one()) {
       tma_prefetch_desc(&tm_x);
       tma_prefetch_desc(&tm_w);
-      const int xrow = b * args.N + row0;
-      for (int k = 0; k < ksteps; ++k) {
-        const int st = k % kPStages, n = k / kPStages;
-        if (n > 0) mbar_wait(&sm.empty[st], (n - 1) & 1);
-        mbar_expect_tx(&sm.full[st], (kPM + kPN) * kPK * 2);
-        tma_load_2d(sm.a[st], &tm_x, &sm.full[st], k * kPK, xrow);
-        if (CL == 1) {
-          tma_load_2d(sm.b[st], &tm_w, &sm.full[st], k * kPK, n0);
-        } else {  // this CTA's half of the W tile, into both CTAs' stage (same offsets)
-          constexpr int HALF = kPN / 2;
-          tma_load_2d_mc(sm.b[st] + crank * HALF * kPK, &tm_w, &sm.full[st], k * kPK, n0 + (int)crank * HALF,
-                         (uint16_t)0x3);
+      int kk = 0;  // k-steps issued by this CTA over all its tiles (ring position)
+      for (int g = g0; g < groups; g += gstep) {
+        int b, row0, n0;
+        tile_of(g, b, row0, n0);
+        const int xrow = b * args.N + row0;
+        for (int k = 0; k < ksteps; ++k, ++kk) {
+          const int st = kk % kPStages, n = kk / kPStages;
+          if (n > 0) mbar_wait(&sm.empty[st], (n - 1) & 1);
+          mbar_expect_tx(&sm.full[st], (kPM + kPN) * kPK * 2);
+          tma_load_2d(sm.a[st], &tm_x, &sm.full[st], k * kPK, xrow);
+          if (CL == 1) {
+            tma_load_2d(sm.b[st], &tm_w, &sm.full[st], k * kPK, n0);
+          } else {  // this CTA's half of the W tile, into both CTAs' stage (same offsets)
+            constexpr int HALF = kPN / 2;
+            tma_load_2d_mc(sm.b[st] + crank * HALF * kPK, &tm_w, &sm.full[st], k * kPK, n0 + (int)crank * HALF,
+                           (uint16_t)0x3);
+          }
         }
       }
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc = idesc_f16(kPM, kPN);
-    for (int k = 0; k < ksteps; ++k) {
-      const int st = k % kPStages;
-      mbar_wait(&sm.full[st], (k / kPStages) & 1);
+    int kk = 0, it = 0;
+    for (int g = g0; g < groups; g += gstep, ++it) {
+      const int ab = it & 1;
+      if (it >= 2) mbar_wait(&sm.acc_empty[ab], ((it >> 1) - 1) & 1);  // the epilogue drained this buffer
       tc_fence_after();
-      if (elect_one()) {
-        const uint32_t aa = smem_u32(sm.a[st]), ba = smem_u32(sm.b[st]);
+      const uint32_t tacc = tmem + ab * kPN;
+      for (int k = 0; k < ksteps; ++k, ++kk) {
+        const int st = kk % kPStages;
+        mbar_wait(&sm.full[st], (kk / kPStages) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t aa = smem_u32(sm.a[st]), ba = smem_u32(sm.b[st]);
 #pragma unroll
-        for (int ks = 0; ks < kPK / 16; ++ks)
-          mma_f16_ss(tmem, smem_desc(aa + ks * 32, 1024, kSw128), smem_desc(ba + ks * 32, 1024, kSw128), idesc,
-                     (k | ks) != 0);
-        if (CL == 1) mma_commit(&sm.empty[st]);
-        else mma_commit_mc(&sm.empty[st], (uint16_t)0x3);  // frees the stage in both CTAs
-        if (k == ksteps - 1) mma_commit(&sm.acc_full);
+          for (int ks = 0; ks < kPK / 16; ++ks)
+            mma_f16_ss(tacc, smem_desc(aa + ks * 32, 1024, kSw128), smem_desc(ba + ks * 32, 1024, kSw128), idesc,
+                       (k | ks) != 0);
+          if (CL == 1) mma_commit(&sm.empty[st]);
+          else mma_commit_mc(&sm.empty[st], (uint16_t)0x3);  // frees the stage in both CTAs
+          if (k == ksteps - 1) mma_commit(&sm.acc_full[ab]);
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
   } else {
     // ---------------------------------------------------------------- epilogue (warps 2-5)
-    const int qd = warp & 3, r = qd * 32 + lane, row = row0 + r;
-    const bool row_ok = row < args.N;
-    const uint32_t tq = tmem + ((uint32_t)(qd * 32) << 16);
+    const int qd = warp & 3, r = qd * 32 + lane;
     const int nbq = (args.N + args.block_q - 1) / args.block_q;
-    mbar_wait(&sm.acc_full, 0);
-    tc_fence_after();
-    constexpr int NH = kPN / HD;  // heads of this CTA
+    constexpr int NH = kPN / HD;  // heads of a tile
+    int it = 0;
+    for (int g = g0; g < groups; g += gstep, ++it) {
+      int b, row0, n0;
+      tile_of(g, b, row0, n0);
+      const int ab = it & 1, row = row0 + r;
+      const bool row_ok = row < args.N;
+      const uint32_t tq = tmem + ((uint32_t)(qd * 32) << 16) + ab * kPN;
+      mbar_wait(&sm.acc_full[ab], (it >> 1) & 1);
+      tc_fence_after();
 #pragma unroll 1
-    for (int hh = 0; hh < NH; ++hh) {
-      const int head = (n0 / HD) + hh;
-      uint32_t hq[HD / 2];  // the row's d outputs as fp16 pairs (RNE)
-      float qa = 0.f;
+      for (int hh = 0; hh < NH; ++hh) {
+        const int head = (n0 / HD) + hh;
+        // pass 1: the row's |max| over its d fp16 outputs (RNE of the fp32 accumulators)
+        float qa = 0.f;
 #pragma unroll
-      for (int cc = 0; cc < HD / 32; ++cc) {
-        uint32_t acc[32];
-        TA_TMEM_LD32(tq + hh * HD + cc * 32, acc);
-        tmem_ld_wait();
+        for (int cc = 0; cc < HD / 32; ++cc) {
+          uint32_t acc[32];
+          TA_TMEM_LD32(tq + hh * HD + cc * 32, acc);
+          tmem_ld_wait();
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const __half2 h2 = __floats2half2_rn(__uint_as_float(acc[2 * e]), __uint_as_float(acc[2 * e + 1]));
-          hq[cc * 16 + e] = *reinterpret_cast<const uint32_t*>(&h2);
-          const float2 f = __half22float2(h2);
-          qa = fmaxf(qa, fmaxf(fabsf(f.x), fabsf(f.y)));
-        }
-      }
-      if (!row_ok) qa = 0.f;
-      qa = warp_max_nonneg(qa);
-      if (lane == 0) sm.red[hh][qd] = qa;
-      named_bar_sync(1, 128);
-      const int half = args.block_q == 64 ? (r >> 6) : 0;
-      const float a_q = args.block_q == 64 ? fmaxf(sm.red[hh][2 * half], sm.red[hh][2 * half + 1])
-                                           : fmaxf(fmaxf(sm.red[hh][0], sm.red[hh][1]), fmaxf(sm.red[hh][2], sm.red[hh][3]));
-      const float inv_q = a_q > 0.f ? div_119_by(a_q) : 0.f;
-      const float s_q = st1_scale(div_by_119(a_q), args.scale_fp16);  // (FP16 variant: R-29)
-      const int rb = (row0 + (args.block_q == 64 ? 64 * half : 0)) / args.block_q;  // row block in the sequence
-      if ((r & (args.block_q - 1)) == 0 && rb < nbq) args.sq[((size_t)b * args.Hq + head) * nbq + rb] = s_q;
-      if (row_ok) {
-        const size_t base = (((size_t)b * args.N + row) * args.Hq + head) * HD;
-        uint4* dst = reinterpret_cast<uint4*>(args.q1 + base);
-#pragma unroll
-        for (int c16 = 0; c16 < HD / 16; ++c16) {
-          uint32_t w[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&hq[c16 * 8 + 2 * e]));
-            const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&hq[c16 * 8 + 2 * e + 1]));
-            w[e] = pack4_lo(rint_prod_bits(f0.x, inv_q), rint_prod_bits(f0.y, inv_q), rint_prod_bits(f1.x, inv_q),
-                            rint_prod_bits(f1.y, inv_q));
+          for (int e = 0; e < 16; ++e) {
+            const float2 f =
+                __half22float2(__floats2half2_rn(__uint_as_float(acc[2 * e]), __uint_as_float(acc[2 * e + 1])));
+            qa = fmaxf(qa, fmaxf(fabsf(f.x), fabsf(f.y)));
           }
-          dst[c16] = make_uint4(w[0], w[1], w[2], w[3]);
         }
-        if (args.q16) {
-          uint4* d16 = reinterpret_cast<uint4*>(args.q16 + base);
+        if (!row_ok) qa = 0.f;
+        qa = warp_max_nonneg(qa);
+        if (lane == 0) sm.red[hh][qd] = qa;
+        named_bar_sync(1, 128);
+        const int half = args.block_q == 64 ? (r >> 6) : 0;
+        const float a_q = args.block_q == 64
+                              ? fmaxf(sm.red[hh][2 * half], sm.red[hh][2 * half + 1])
+                              : fmaxf(fmaxf(sm.red[hh][0], sm.red[hh][1]), fmaxf(sm.red[hh][2], sm.red[hh][3]));
+        const float inv_q = a_q > 0.f ? div_119_by(a_q) : 0.f;
+        const float s_q = st1_scale(div_by_119(a_q), args.scale_fp16);  // (FP16 variant: R-29)
+        const int rb = (row0 + (args.block_q == 64 ? 64 * half : 0)) / args.block_q;  // row block in the sequence
+        if ((r & (args.block_q - 1)) == 0 && rb < nbq) args.sq[((size_t)b * args.Hq + head) * nbq + rb] = s_q;
+        // pass 2: the same accumulators again -> fp16 -> codes (and the fp16 Q if asked), row-contiguous
+        const size_t base = (((size_t)b * args.N + row) * args.Hq + head) * HD;
 #pragma unroll
-          for (int c8 = 0; c8 < HD / 8; ++c8)
-            d16[c8] = make_uint4(hq[4 * c8], hq[4 * c8 + 1], hq[4 * c8 + 2], hq[4 * c8 + 3]);
+        for (int cc = 0; cc < HD / 32; ++cc) {
+          uint32_t acc[32];
+          TA_TMEM_LD32(tq + hh * HD + cc * 32, acc);
+          tmem_ld_wait();
+          uint32_t hq[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const __half2 h2 = __floats2half2_rn(__uint_as_float(acc[2 * e]), __uint_as_float(acc[2 * e + 1]));
+            hq[e] = *reinterpret_cast<const uint32_t*>(&h2);
+          }
+          if (row_ok) {
+            uint4* dst = reinterpret_cast<uint4*>(args.q1 + base + cc * 32);
+#pragma unroll
+            for (int c16 = 0; c16 < 2; ++c16) {
+              uint32_t w[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&hq[c16 * 8 + 2 * e]));
+                const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&hq[c16 * 8 + 2 * e + 1]));
+                w[e] = pack4_lo(rint_prod_bits(f0.x, inv_q), rint_prod_bits(f0.y, inv_q),
+                                rint_prod_bits(f1.x, inv_q), rint_prod_bits(f1.y, inv_q));
+              }
+              dst[c16] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+            if (args.q16) {
+              uint4* d16 = reinterpret_cast<uint4*>(args.q16 + base + cc * 32);
+#pragma unroll
+              for (int c8 = 0; c8 < 4; ++c8)
+                d16[c8] = make_uint4(hq[4 * c8], hq[4 * c8 + 1], hq[4 * c8 + 2], hq[4 * c8 + 3]);
+            }
+          }
         }
+        if (hh == NH - 1) {  // every TMEM read of this buffer is done: hand it back to the MMA issuer
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.acc_empty[ab]);
+        }
+        named_bar_sync(1, 128);  // sm.red is rewritten by the next head
       }
-      named_bar_sync(1, 128);  // sm.red is rewritten by the next head
     }
   }
   tc_fence_before();
@@ -197,7 +246,7 @@ __global__ void __launch_bounds__(192, 1)
   if (CL > 1) cluster_sync_all();  // no CTA leaves while its peer may still multicast into it
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, kPN);
+    tmem_dealloc(tmem, 2 * kPN);
   }
 }
 
@@ -247,10 +296,14 @@ cudaError_t launch_q_projection(const turbo_params_t* p, int B, int N, int D, in
   a.block_q = p->block_q;
   a.m_tiles = (N + kPM - 1) / kPM;
   a.scale_fp16 = p->scale_fp16;
-  const dim3 grid((unsigned)(a.m_tiles * B), (unsigned)(Hq * HD / kPN));
   const size_t smem = sizeof(ProjSmem) + 1024;
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int cl = pair ? 2 : 1;
+  const int groups = (a.m_tiles * B / cl) * (Hq * HD / kPN);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
+  cfg.gridDim = dim3((unsigned)(std::max(1, sms / cl) * cl));
   cfg.blockDim = dim3(192);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -261,9 +314,14 @@ cudaError_t launch_q_projection(const turbo_params_t* p, int B, int N, int D, in
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // persistent grid: as many clusters as can be resident at once (never a second wave), at most the tiles
 #define TA_PROJ(HDV, CLV)                                                                                  \
   {                                                                                                        \
     cudaFuncSetAttribute(q_projection_kernel<HDV, CLV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    int ncl = 0;                                                                                           \
+    if (cudaOccupancyMaxActiveClusters(&ncl, q_projection_kernel<HDV, CLV>, &cfg) != cudaSuccess || ncl < 1) \
+      ncl = std::max(1, sms / CLV);                                                                        \
+    cfg.gridDim = dim3((unsigned)(std::min(groups, ncl) * CLV));                                           \
     cudaError_t e = cudaLaunchKernelEx(&cfg, q_projection_kernel<HDV, CLV>, tmx, tmw, a);                  \
     return e != cudaSuccess ? e : cudaGetLastError();                                                      \
   }
