@@ -242,3 +242,36 @@ def test_bc128_chunked_prefill(ta):
             oref, lref = O.prefill_chunk_head(op, q[0, P:, hq], k1r, skr, v1r, svr, causal=True)
             assert_out_close(o[0, :, hq], oref, f"h{hq}")
             np.testing.assert_allclose(lse[0, hq], lref, atol=1e-4, rtol=1e-5)
+
+
+def test_bc128_with_fp16_scales_and_fp16_sas(ta):
+    """B_c = 128 together with both NEXT-2 arithmetic variants (scale_fp16: R-29, sas_fp16: R-30):
+    records / parent scales bit-exact, prefill and decode against the oracle run with the same flags."""
+    B, N, Hq, Hkv, d = 2, 128 * 3 + 40, 8, 2, 128
+    q, k, v = synth.qkv(7777, B, N, Hq, Hkv, d)
+    bits = synth.head_bits_alternating(Hkv)
+    p = ta.params(head_dim=d, block_kv=BC, scale_fp16=1, sas_fp16=1)
+    op = O.params(d=d, block_kv=BC, scale_fp16=1, sas_fp16=1)
+    mb = N // BC + 2
+    cache = ta.KVCache(B, Hkv, d, max_blocks=mb, bits=bits, block_kv=BC)
+    qt, kt, vt = (torch.from_numpy(x).cuda() for x in (q, k, v))
+    k1, v1t, k1s, v1s = ta.turbo_quantize_kv(p, cache, kt, vt)
+    o, lse = ta.turbo_attention_prefill(p, qt, k1, v1t, k1s, v1s)
+    qd, _, _ = synth.decode_token(7778, B, Hq, Hkv, d)
+    od, _, ld = ta.turbo_attention_decode(p, cache, torch.from_numpy(qd).cuda(), n_splits=2)
+    torch.cuda.synchronize()
+    ref = O.build_cache(op, k.astype(np.float32), v.astype(np.float32), bits, mb)
+    _check_cache(ta, cache, ref, B, Hkv, d, bits)
+    o, lse, od, ld = (x.cpu().numpy() for x in (o, lse, od, ld))
+    G = Hq // Hkv
+    for b in range(B):
+        for h in range(Hq):
+            oref, lref = O.prefill_head(op, q[b, :, h], k[b, :, h // G], v[b, :, h // G])
+            assert_out_close(o[b, :, h], oref, f"b{b} h{h}")
+            np.testing.assert_allclose(lse[b, h], lref, atol=1e-4, rtol=1e-5)
+        nb = ref["slots"][b][0][0].n_blocks
+        per = -(-nb // 2)
+        ro, rl = _oracle_decode(op, qd[b].astype(np.float32), ref["slots"][b], G,
+                                [(0, min(per, nb)), (min(per, nb), nb)])
+        assert_out_close(od[b], ro, f"decode b{b}")
+        np.testing.assert_allclose(ld[b], rl, atol=1e-4, rtol=1e-5)

@@ -117,3 +117,17 @@ def test_q_projection_validation(ta):  # noqa: F811
     with pytest.raises(ta.TurboError) as e:
         ta.turbo_q_projection(p, x, w, 2)
     assert e.value.code == ta.TURBO_ERR_UNSUPPORTED
+
+
+def test_q_projection_fp16_scales(ta):  # noqa: F811
+    """scale_fp16 (R-29) in the projection epilogue: the block scales are the binary16 roundings."""
+    B, N, D, Hq, d, bq = 2, 128, 256, 2, 128, 64
+    rng = np.random.default_rng(99)
+    x = rng.integers(-3, 4, (B, N, D)).astype(np.float16)
+    w = (rng.integers(-2, 3, (Hq * d, D)) * 0.03125).astype(np.float16)
+    p = ta.params(head_dim=d, block_q=bq, scale_fp16=1)
+    q1, sq, _ = ta.turbo_q_projection(p, torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda(), Hq)
+    torch.cuda.synchronize()
+    codes, sc = _oracle_q1(O.project_q(x, w), Hq, d, bq)
+    np.testing.assert_array_equal(q1.cpu().numpy(), codes)  # codes do not depend on the scale's format
+    np.testing.assert_array_equal(sq.cpu().numpy(), sc.astype(np.float16).astype(np.float32))
