@@ -145,7 +145,8 @@ TURBO_API turbo_status_t turbo_cache_sizes(int32_t batch, int32_t n_kv_heads, in
  *     stage-1 scale as parent scale; the n_tokens mod B_c tail is re-quantised
  *     with the universal scale into the INT8 buffer.  The stage-1 operands of
  *     turbo_attention_prefill are written to
- *       k1_out   int8 [B][Hkv][n_tokens][d]
+ *       k1_out   FP16 [B][Hkv][n_tokens][d]: K's stage-1 codes (integers in [-119,119], exact
+ *                in FP16 -- the B operand of the prefill's kind::f16 Q K^T MMA)
  *       v1t_out  FP16 [B][Hkv][T_c][d][B_c]  the stage-1 V codes (integers in
  *                [-119,119], exact in FP16), each block transposed; tokens past
  *                n_tokens are 0; T_c = ceil(n_tokens / B_c)
@@ -170,7 +171,7 @@ TURBO_API turbo_status_t turbo_cache_sizes(int32_t batch, int32_t n_kv_heads, in
  *     P / B_c (the prefix part comes from turbo_dequantize_cache).  Updates
  *     cache->n_tokens to Nk. */
 TURBO_API turbo_status_t turbo_quantize_kv(const turbo_params_t* params, turbo_kv_cache_t* cache, const void* k,
-                                 const void* v, int32_t n_tokens, int32_t mode, int8_t* k1_out,
+                                 const void* v, int32_t n_tokens, int32_t mode, void* k1_out,
                                  void* v1t_out, float* k1_scale_out, float* v1_scale_out,
                                  turbo_stream_t stream);
 
@@ -183,7 +184,7 @@ TURBO_API turbo_status_t turbo_quantize_kv(const turbo_params_t* params, turbo_k
  *   lse     f32 [B][Hq][N] = m + ln l.
  * Query head h reads kv head h / (Hq/Hkv) (GQA, R-22). */
 TURBO_API turbo_status_t turbo_attention_prefill(const turbo_params_t* params, int32_t B, int32_t N, int32_t Hq,
-                                       int32_t Hkv, int32_t causal, const void* q, const int8_t* k1,
+                                       int32_t Hkv, int32_t causal, const void* q, const void* k1,
                                        const void* v1t, const float* k1_scale, const float* v1_scale,
                                        void* o, float* lse, turbo_stream_t stream);
 
@@ -207,13 +208,13 @@ TURBO_API turbo_status_t turbo_q_projection(const turbo_params_t* params, int32_
  * bytes per query row. */
 TURBO_API turbo_status_t turbo_attention_prefill_q1(const turbo_params_t* params, int32_t B, int32_t N, int32_t Hq,
                                                     int32_t Hkv, int32_t causal, const int8_t* q1,
-                                                    const float* q1_scale, const int8_t* k1, const void* v1t,
+                                                    const float* q1_scale, const void* k1, const void* v1t,
                                                     const float* k1_scale, const float* v1_scale, void* o, float* lse,
                                                     turbo_stream_t stream);
 
 /* Stage-1 reconstruction of flushed cache blocks [blk_begin, blk_end)
  * (blk_end = -1: all; blocks past a sequence's count are skipped), the
- * prefix operands of a chunked prefill (R-28): k1_out [B][Hkv][Nk][d] rows
+ * prefix operands of a chunked prefill (R-28): k1_out FP16 [B][Hkv][Nk][d] rows
  * [B_c j, B_c j + B_c) and v1t_out [B][Hkv][ceil(Nk/B_c)][d][B_c] block j get
  * code s_int + z_int (Alg. 2), the scales the blocks' parent
  * scales.  With blk_end = -1 and buffered tokens (R-31) these follow as block
@@ -221,7 +222,7 @@ TURBO_API turbo_status_t turbo_attention_prefill_q1(const turbo_params_t* params
  * zero.  Nk = token capacity of k1_out (>= B_c x the last block, and >= the
  * cached length when the buffer is written).  The cache is not modified. */
 TURBO_API turbo_status_t turbo_dequantize_cache(const turbo_params_t* params, const turbo_kv_cache_t* cache,
-                                                int32_t blk_begin, int32_t blk_end, int8_t* k1_out, void* v1t_out,
+                                                int32_t blk_begin, int32_t blk_end, void* k1_out, void* v1t_out,
                                                 float* k1_scale_out, float* v1_scale_out, int32_t Nk,
                                                 turbo_stream_t stream);
 
@@ -230,7 +231,7 @@ TURBO_API turbo_status_t turbo_dequantize_cache(const turbo_params_t* params, co
  * prefix of Nk - Nq tokens (its stage-1 reconstruction from
  * turbo_dequantize_cache) followed by the chunk's own keys (turbo_quantize_kv
  * mode 2).  turbo_attention_prefill is the case Nq = Nk.
- *   q       FP16 [B][Nq][Hq][d];  k1 int8 [B][Hkv][Nk][d];
+ *   q       FP16 [B][Nq][Hq][d];  k1 FP16 codes [B][Hkv][Nk][d];
  *   v1t     FP16 codes [B][Hkv][T_k][d][B_c], T_k = ceil(Nk / B_c);
  *   k1_scale, v1_scale  f32 [B][Hkv][T_k];
  *   causal  1 = key <= Nk - Nq + query row, 0 = all Nk keys;
@@ -238,7 +239,7 @@ TURBO_API turbo_status_t turbo_dequantize_cache(const turbo_params_t* params, co
  * Errors: TURBO_ERR_INVALID_ARG if Nq < 1 or Nk < Nq. */
 TURBO_API turbo_status_t turbo_attention_prefill_chunk(const turbo_params_t* params, int32_t B, int32_t Nq,
                                                        int32_t Nk, int32_t Hq, int32_t Hkv, int32_t causal,
-                                                       const void* q, const int8_t* k1, const void* v1t,
+                                                       const void* q, const void* k1, const void* v1t,
                                                        const float* k1_scale, const float* v1_scale, void* o,
                                                        float* lse, turbo_stream_t stream);
 

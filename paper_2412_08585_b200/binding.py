@@ -186,7 +186,7 @@ def turbo_quantize_kv(p, cache: KVCache, k, v, mode=0, stream=None, out=None):
             assert k1.shape == (B, H, Nk, d) and v1t.shape == (B, H, tc, d, p.block_kv)
             assert k1s.shape == (B, H, tc) and v1s.shape == (B, H, tc)
         else:
-            k1 = torch.empty((B, H, Nk, d), dtype=torch.int8, device=dev)
+            k1 = torch.empty((B, H, Nk, d), dtype=torch.float16, device=dev)  # stage-1 codes, exact in fp16
             v1t = torch.empty((B, H, tc, d, p.block_kv), dtype=torch.float16, device=dev)
             k1s = torch.empty((B, H, tc), dtype=torch.float32, device=dev)
             v1s = torch.empty((B, H, tc), dtype=torch.float32, device=dev)
@@ -250,12 +250,12 @@ def turbo_attention_prefill_q1(p, q1, q1_scale, k1, v1t, k1_scale, v1_scale, cau
 
 def turbo_dequantize_cache(p, cache: KVCache, Nk, blk_begin=0, blk_end=-1, out=None, stream=None):
     """Stage-1 reconstruction of cache blocks [blk_begin, blk_end) into prefill operands over
-    Nk tokens -> (k1 int8 [B,Hkv,Nk,d], v1t fp16 [B,Hkv,Tk,d,B_c], k1_scale, v1_scale [B,Hkv,Tk])."""
+    Nk tokens -> (k1 fp16 codes [B,Hkv,Nk,d], v1t fp16 [B,Hkv,Tk,d,B_c], k1_scale, v1_scale [B,Hkv,Tk])."""
     B, H, d = cache.batch, cache.n_kv_heads, cache.head_dim
     tk = -(-Nk // p.block_kv)
     if out is None:
         dev = cache.counters.device
-        out = (torch.zeros((B, H, Nk, d), dtype=torch.int8, device=dev),
+        out = (torch.zeros((B, H, Nk, d), dtype=torch.float16, device=dev),
                torch.zeros((B, H, tk, d, p.block_kv), dtype=torch.float16, device=dev),
                torch.zeros((B, H, tk), dtype=torch.float32, device=dev),
                torch.zeros((B, H, tk), dtype=torch.float32, device=dev))

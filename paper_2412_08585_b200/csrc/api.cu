@@ -10,15 +10,15 @@
 #include "layout.cuh"
 
 namespace ta_host {
-cudaError_t launch_quant_prefill(const turbo_kv_cache_t* c, const __half* k, const __half* v, int N, int8_t* k1,
+cudaError_t launch_quant_prefill(const turbo_kv_cache_t* c, const __half* k, const __half* v, int N, __half* k1,
                                  __half* v1t, float* k1s, float* v1s, cudaStream_t st, int j0, int Nk,
                                  int scale_fp16);
-cudaError_t launch_dequant_cache(const turbo_kv_cache_t* c, int blk_begin, int blk_end, int Nk, int8_t* k1,
+cudaError_t launch_dequant_cache(const turbo_kv_cache_t* c, int blk_begin, int blk_end, int Nk, __half* k1,
                                  __half* v1t, float* k1s, float* v1s, cudaStream_t st, int scale_fp16);
 cudaError_t launch_quant_append(const turbo_kv_cache_t* c, const __half* k, const __half* v, cudaStream_t st,
                                 int scale_fp16);
 cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Nk, int Hq, int Hkv, int causal, const __half* q,
-                           const int8_t* k1, const __half* v1t, const float* k1s, const float* v1s, __half* o,
+                           const __half* k1, const __half* v1t, const float* k1s, const float* v1s, __half* o,
                            float* lse, cudaStream_t st, const int8_t* q1_in = nullptr, const float* sq_in = nullptr);
 cudaError_t launch_q_projection(const turbo_params_t* p, int B, int N, int D, int Hq, const __half* x, const __half* wq,
                                 int8_t* q1, float* sq, __half* q16, cudaStream_t st);
@@ -93,7 +93,7 @@ turbo_status_t turbo_cache_sizes(int32_t batch, int32_t n_kv_heads, int32_t head
 }
 
 turbo_status_t turbo_quantize_kv(const turbo_params_t* params, turbo_kv_cache_t* cache, const void* k,
-                                 const void* v, int32_t n_tokens, int32_t mode, int8_t* k1_out, void* v1t_out,
+                                 const void* v, int32_t n_tokens, int32_t mode, void* k1_out, void* v1t_out,
                                  float* k1_scale_out, float* v1_scale_out, turbo_stream_t stream) {
   turbo_status_t s = check_params(params);
   if (s != TURBO_OK) return s;
@@ -104,7 +104,7 @@ turbo_status_t turbo_quantize_kv(const turbo_params_t* params, turbo_kv_cache_t*
     if (n_tokens < 1 || !k1_out || !v1t_out || !k1_scale_out || !v1_scale_out) return TURBO_ERR_INVALID_ARG;
     if (n_tokens / params->block_kv > cache->max_blocks) return TURBO_ERR_CAPACITY;
     s = cuda_status(ta_host::launch_quant_prefill(cache, reinterpret_cast<const __half*>(k),
-                                                  reinterpret_cast<const __half*>(v), n_tokens, k1_out,
+                                                  reinterpret_cast<const __half*>(v), n_tokens, reinterpret_cast<__half*>(k1_out),
                                                   reinterpret_cast<__half*>(v1t_out),
                                                   k1_scale_out, v1_scale_out, st, 0, n_tokens,
                                                   params->scale_fp16));
@@ -117,7 +117,7 @@ turbo_status_t turbo_quantize_kv(const turbo_params_t* params, turbo_kv_cache_t*
     const int64_t nk = cache->n_tokens + n_tokens;
     if (nk / params->block_kv > cache->max_blocks || nk > INT32_MAX) return TURBO_ERR_CAPACITY;
     s = cuda_status(ta_host::launch_quant_prefill(cache, reinterpret_cast<const __half*>(k),
-                                                  reinterpret_cast<const __half*>(v), n_tokens, k1_out,
+                                                  reinterpret_cast<const __half*>(v), n_tokens, reinterpret_cast<__half*>(k1_out),
                                                   reinterpret_cast<__half*>(v1t_out), k1_scale_out, v1_scale_out,
                                                   st, (int)(cache->n_tokens / params->block_kv), (int)nk,
                                                   params->scale_fp16));
@@ -137,7 +137,7 @@ turbo_status_t turbo_quantize_kv(const turbo_params_t* params, turbo_kv_cache_t*
 }
 
 turbo_status_t turbo_dequantize_cache(const turbo_params_t* params, const turbo_kv_cache_t* cache,
-                                      int32_t blk_begin, int32_t blk_end, int8_t* k1_out, void* v1t_out,
+                                      int32_t blk_begin, int32_t blk_end, void* k1_out, void* v1t_out,
                                       float* k1_scale_out, float* v1_scale_out, int32_t Nk, turbo_stream_t stream) {
   turbo_status_t s = check_params(params);
   if (s != TURBO_OK) return s;
@@ -149,13 +149,13 @@ turbo_status_t turbo_dequantize_cache(const turbo_params_t* params, const turbo_
   if (Nk < 1 || last * params->block_kv > Nk) return TURBO_ERR_INVALID_ARG;
   // blk_end < 0 with buffered tokens: they are written too, as the boundary block (R-31)
   if (blk_end < 0 && cache->n_tokens % params->block_kv != 0 && cache->n_tokens > Nk) return TURBO_ERR_INVALID_ARG;
-  return cuda_status(ta_host::launch_dequant_cache(cache, blk_begin, blk_end, Nk, k1_out,
+  return cuda_status(ta_host::launch_dequant_cache(cache, blk_begin, blk_end, Nk, reinterpret_cast<__half*>(k1_out),
                                                    reinterpret_cast<__half*>(v1t_out), k1_scale_out, v1_scale_out,
                                                    reinterpret_cast<cudaStream_t>(stream), params->scale_fp16));
 }
 
 turbo_status_t turbo_attention_prefill_chunk(const turbo_params_t* params, int32_t B, int32_t Nq, int32_t Nk,
-                                             int32_t Hq, int32_t Hkv, int32_t causal, const void* q, const int8_t* k1,
+                                             int32_t Hq, int32_t Hkv, int32_t causal, const void* q, const void* k1,
                                              const void* v1t, const float* k1_scale, const float* v1_scale, void* o,
                                              float* lse, turbo_stream_t stream) {
   turbo_status_t s = check_params(params);
@@ -164,7 +164,8 @@ turbo_status_t turbo_attention_prefill_chunk(const turbo_params_t* params, int32
   if (Hq % Hkv != 0) return TURBO_ERR_UNSUPPORTED;
   if (!q || !k1 || !v1t || !k1_scale || !v1_scale || !o || !lse) return TURBO_ERR_INVALID_ARG;
   return cuda_status(ta_host::launch_prefill(params, B, Nq, Nk, Hq, Hkv, causal, reinterpret_cast<const __half*>(q),
-                                             k1, reinterpret_cast<const __half*>(v1t), k1_scale, v1_scale,
+                                             reinterpret_cast<const __half*>(k1), reinterpret_cast<const __half*>(v1t),
+                                             k1_scale, v1_scale,
                                              reinterpret_cast<__half*>(o), lse, reinterpret_cast<cudaStream_t>(stream)));
 }
 
@@ -184,21 +185,22 @@ turbo_status_t turbo_q_projection(const turbo_params_t* params, int32_t B, int32
 
 turbo_status_t turbo_attention_prefill_q1(const turbo_params_t* params, int32_t B, int32_t N, int32_t Hq,
                                           int32_t Hkv, int32_t causal, const int8_t* q1, const float* q1_scale,
-                                          const int8_t* k1, const void* v1t, const float* k1_scale,
+                                          const void* k1, const void* v1t, const float* k1_scale,
                                           const float* v1_scale, void* o, float* lse, turbo_stream_t stream) {
   turbo_status_t s = check_params(params);
   if (s != TURBO_OK) return s;
   if (B < 1 || N < 1 || Hq < 1 || Hkv < 1 || (causal != 0 && causal != 1)) return TURBO_ERR_INVALID_ARG;
   if (Hq % Hkv != 0) return TURBO_ERR_UNSUPPORTED;
   if (!q1 || !q1_scale || !k1 || !v1t || !k1_scale || !v1_scale || !o || !lse) return TURBO_ERR_INVALID_ARG;
-  return cuda_status(ta_host::launch_prefill(params, B, N, N, Hq, Hkv, causal, nullptr, k1,
+  return cuda_status(ta_host::launch_prefill(params, B, N, N, Hq, Hkv, causal, nullptr,
+                                             reinterpret_cast<const __half*>(k1),
                                              reinterpret_cast<const __half*>(v1t), k1_scale, v1_scale,
                                              reinterpret_cast<__half*>(o), lse, reinterpret_cast<cudaStream_t>(stream),
                                              q1, q1_scale));
 }
 
 turbo_status_t turbo_attention_prefill(const turbo_params_t* params, int32_t B, int32_t N, int32_t Hq, int32_t Hkv,
-                                       int32_t causal, const void* q, const int8_t* k1, const void* v1t,
+                                       int32_t causal, const void* q, const void* k1, const void* v1t,
                                        const float* k1_scale, const float* v1_scale, void* o, float* lse,
                                        turbo_stream_t stream) {
   return turbo_attention_prefill_chunk(params, B, N, N, Hq, Hkv, causal, q, k1, v1t, k1_scale, v1_scale, o, lse,

@@ -4,10 +4,13 @@
 // query tile) -- or, for odd G, two adjacent 128-row tiles of one head; each
 // tile ("slot") holds two B_r = 64 quantisation blocks (or one B_r = 128 block).
 // One CTA per SM (all 512 TMEM columns: per slot S_0 | S_1 | O).  Warp roles:
-//   warp 0      TMA producer: K_j [64 x d] INT8 and V_j^T [d x 64] FP16-code
-//               tiles into a 3-stage smem ring shared by both slots.
+//   warp 0      TMA producer: K_j [64 x d] and V_j^T [d x 64] tiles of stage-1 codes
+//               carried exactly in FP16, into a 3-stage smem ring shared by both slots.
 //   warps 1, 2  one single-thread tcgen05.mma issuer per slot (warp 1 also owns
-//               TMEM): S_j = Q^q1 K_j^q1^T (kind::i8, int32, double-buffered) and
+//               TMEM): S_j = Q^q1 K_j^q1^T (kind::f16 on the integer codes: every
+//               product and partial sum is an integer below 2^24, so the fp32
+//               accumulator holds S_int exactly and pass 1 needs no int->float
+//               conversion; double-buffered) and
 //               O^ += P'_j V_j^q1 (kind::f16, A = P' from TMEM, B = V codes from
 //               smem, fp32 accumulator in TMEM across all key tiles).
 //   warps 4-11  one softmax warpgroup per slot, thread = query row = TMEM lane:
@@ -41,10 +44,11 @@ constexpr int stages_of() { return BC == 64 ? 3 : 2; }
 template <int HD, int BC>
 struct PrefillSmem {
   static constexpr int kStages = stages_of<BC>();
-  int8_t q1[2][kTileM * HD];   // Q^q1, K-major, swizzled rows of HD bytes
-  int8_t k[kStages][BC * HD];  // K_j^q1 [B_c][HD]
+  // Q^q1 codes as fp16 (exact), K-major SW128: HD / 64 atoms of [128 rows][64 channels] (128-B rows).  Once
+  // the slot's last QK^T MMA has completed, its buffer stages the epilogue's O rows.
+  __half q1[2][kTileM * HD];
+  __half k[kStages][BC * HD];  // K_j^q1 codes as fp16, HD / 64 atoms of [B_c keys][64 channels] (SW128)
   __half v[kStages][HD * BC];  // V_j^q1 codes as fp16, transposed, B_c / 64 tiles [HD][64] (128-B rows, SW128)
-  __half stg[2][kTileM * HD];  // epilogue staging of O rows (per slot)
   uint64_t kv_full[kStages], kv_empty[kStages];
   uint64_t s_full[2][2], p_full[2][2], pv_done[2], q_ready;
   uint32_t tmem_base;
@@ -68,13 +72,24 @@ struct PrefillArgs {
   turbo_debug_tap_t tap;
 };
 
-template <int HD>
-TA_DEV uint32_t q1_swz(int r, int chunk) {
-  // 128B swizzle for 128-B rows, 64B swizzle for 64-B rows (matches the TMA
-  // swizzle of the K tile and the UMMA descriptor layout type).
-  if (HD == 128) return r * 128 + ((chunk ^ (r & 7)) << 4);
-  return r * 64 + ((chunk ^ ((r >> 1) & 3)) << 4);
+// Byte offset of the 16-byte chunk c8 (channels 8 c8 .. 8 c8 + 7, fp16) of row r in a K-major SW128
+// operand of `rows` rows split into 64-channel atoms of 128-B rows.
+TA_DEV uint32_t f16_swz(int rows, int r, int c8) {
+  return (uint32_t)((c8 >> 3) * rows * 128 + r * 128 + (((c8 & 7) ^ (r & 7)) << 4));
 }
+// fp16 pair of two stage-1 codes given as magic-float bits (rint_prod_bits: magic + code, exact)
+TA_DEV uint32_t codes_h2(uint32_t b0, uint32_t b1) {
+  const __half2 h = __floats2half2_rn(__uint_as_float(b0) - kMagic, __uint_as_float(b1) - kMagic);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+// fp16 pairs of the four signed bytes of w (exact)
+TA_DEV void bytes_h2(uint32_t w, uint32_t& lo, uint32_t& hi) {
+  const __half2 a = __floats2half2_rn((float)(int8_t)(w & 0xFF), (float)(int8_t)((w >> 8) & 0xFF));
+  const __half2 b = __floats2half2_rn((float)(int8_t)((w >> 16) & 0xFF), (float)(int8_t)(w >> 24));
+  lo = *reinterpret_cast<const uint32_t*>(&a);
+  hi = *reinterpret_cast<const uint32_t*>(&b);
+}
+
 
 // Window of F = s_P s_V R outside which the row of O^ is rescaled by a power of two.
 // Upper: fp16(-1024 F_hi) must be finite (F_hi <= 63.97) for the P' hi/lo split.
@@ -151,8 +166,10 @@ __global__ void __launch_bounds__(384, 1)
         for (int j = 0; j < nkv; ++j) {
           const int st = j % kStages, n = j / kStages;
           if (n > 0) mbar_wait(&sm.kv_empty[st], (n - 1) & 1);
-          mbar_expect_tx(&sm.kv_full[st], 3 * BC * HD);  // K int8 + V fp16
-          tma_load_3d(sm.k[st], &tm_k, &sm.kv_full[st], 0, j * BC, (int)bkv);
+          mbar_expect_tx(&sm.kv_full[st], 4 * BC * HD);  // K and V fp16
+#pragma unroll
+          for (int a = 0; a < HD / 64; ++a)  // K^T: one [B_c][64] fp16 box per 64 channels
+            tma_load_3d(sm.k[st] + a * BC * 64, &tm_k, &sm.kv_full[st], 64 * a, j * BC, (int)bkv);
 #pragma unroll
           for (int u = 0; u < BC / 64; ++u)  // V^T: one [HD][64] box per 64 keys
             tma_load_3d(sm.v[st] + u * HD * 64, &tm_v, &sm.kv_full[st], 64 * u, 0, (int)(bkv * Tc + j));
@@ -164,8 +181,7 @@ __global__ void __launch_bounds__(384, 1)
       // P'_{j-1}, which PV_{j-1} (issued before it) has consumed -- tcgen05.mma of one
       // thread executes in order.
       const int t = warp - 1;
-      constexpr uint32_t kLayQK = HD == 128 ? kSw128 : kSw64;
-      constexpr uint32_t idesc_qk = idesc_i8(kTileM, BC, true, true);
+      constexpr uint32_t idesc_qk = idesc_f16(kTileM, BC);  // fp16 codes, fp32 S: exact integers
       constexpr uint32_t idesc_pv = idesc_f16(kTileM, HD);
       const uint32_t tslot = tmem + t * kSlotCols;
       mbar_wait(&sm.q_ready, 0);
@@ -181,9 +197,9 @@ __global__ void __launch_bounds__(384, 1)
           if (elect_one()) {
             const uint32_t q1a = smem_u32(sm.q1[t]), ka = smem_u32(sm.k[st]);
 #pragma unroll
-            for (int ks = 0; ks < HD / 32; ++ks)
-              mma_i8_ss(tslot + sb * 64, smem_desc(q1a + ks * 32, 8 * HD, kLayQK),
-                        smem_desc(ka + ks * 32, 8 * HD, kLayQK), idesc_qk, ks > 0);
+            for (int ks = 0; ks < HD / 16; ++ks)  // K = 16 channels: atom ks / 4, 32 B into its 128-B rows
+              mma_f16_ss(tslot + sb * 64, smem_desc(q1a + (ks >> 2) * kTileM * 128 + (ks & 3) * 32, 1024, kSw128),
+                         smem_desc(ka + (ks >> 2) * BC * 128 + (ks & 3) * 32, 1024, kSw128), idesc_qk, ks > 0);
             mma_commit(&sm.s_full[t][sb]);
           }
           __syncwarp();
@@ -237,7 +253,14 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
       for (int c = 0; c < HD / 16; ++c) {
         const uint4 w = row_ok ? src[c] : make_uint4(0, 0, 0, 0);
-        *reinterpret_cast<uint4*>(sm.q1[slot] + q1_swz<HD>(r, c)) = w;
+        uint32_t h[8];
+        bytes_h2(w.x, h[0], h[1]);
+        bytes_h2(w.y, h[2], h[3]);
+        bytes_h2(w.z, h[4], h[5]);
+        bytes_h2(w.w, h[6], h[7]);
+        uint8_t* qb = reinterpret_cast<uint8_t*>(sm.q1[slot]);
+        *reinterpret_cast<uint4*>(qb + f16_swz(kTileM, r, 2 * c)) = make_uint4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<uint4*>(qb + f16_swz(kTileM, r, 2 * c + 1)) = make_uint4(h[4], h[5], h[6], h[7]);
         if (tap_row) *reinterpret_cast<uint4*>(args.tap.q1 + (r & 63) * HD + c * 16) = w;
       }
       if (tap_row && (r & 63) == 0) args.tap.s_q[0] = s_q;
@@ -264,21 +287,21 @@ __global__ void __launch_bounds__(384, 1)
       const float inv_q = a_q > 0.f ? div_119_by(a_q) : 0.f;
       s_q = st1_scale(div_by_119(a_q), args.scale_fp16);  // (FP16 variant: R-29)
 #pragma unroll
-      for (int c = 0; c < HD / 16; ++c) {
-        uint32_t w[4];
+      for (int c = 0; c < HD / 8; ++c) {  // 8 channels: one 16-B chunk of fp16 codes
+        const __half2* hp = reinterpret_cast<const __half2*>(&qraw[c]);
+        uint32_t bq[8], h[4];
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const __half2* hp = reinterpret_cast<const __half2*>(&qraw[2 * c + hh]);
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            float2 f0 = __half22float2(hp[2 * e]), f1 = __half22float2(hp[2 * e + 1]);
-            w[hh * 2 + e] = pack4_lo(rint_prod_bits(f0.x, inv_q), rint_prod_bits(f0.y, inv_q),
-                                     rint_prod_bits(f1.x, inv_q), rint_prod_bits(f1.y, inv_q));
-          }
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __half22float2(hp[e]);
+          bq[2 * e] = rint_prod_bits(f.x, inv_q);
+          bq[2 * e + 1] = rint_prod_bits(f.y, inv_q);
+          h[e] = codes_h2(bq[2 * e], bq[2 * e + 1]);
         }
-        *reinterpret_cast<uint4*>(sm.q1[slot] + q1_swz<HD>(r, c)) = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.q1[slot]) + f16_swz(kTileM, r, c)) =
+            make_uint4(h[0], h[1], h[2], h[3]);
         if (tap_row)
-          *reinterpret_cast<uint4*>(args.tap.q1 + (r & 63) * HD + c * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+          *reinterpret_cast<uint2*>(args.tap.q1 + (r & 63) * HD + c * 8) =
+              make_uint2(pack4_lo(bq[0], bq[1], bq[2], bq[3]), pack4_lo(bq[4], bq[5], bq[6], bq[7]));
       }
       if (tap_row && (r & 63) == 0) args.tap.s_q[0] = s_q;
     }
@@ -302,7 +325,7 @@ __global__ void __launch_bounds__(384, 1)
       for (int c = 0; c < BC; c += 32) TA_TMEM_LD32(tS + c, (v + c));
       tmem_ld_wait();
       if (TAP && tap_row && j == tap_j)
-        for (int c = 0; c < BC; ++c) args.tap.s_int[(r & 63) * BC + c] = c < nvalid ? (int)v[c] : 0;
+        for (int c = 0; c < BC; ++c) args.tap.s_int[(r & 63) * BC + c] = c < nvalid ? (int)__uint_as_float(v[c]) : 0;
       // x = S s_Q s_K / sqrt(d) (R-18); masked keys -> -inf
       const float cqk = __fmul_rn(__fmul_rn(s_q, args.k1s[bkv * Tc + j]), args.scale);
       const float s_v = args.v1s[bkv * Tc + j];
@@ -312,8 +335,8 @@ __global__ void __launch_bounds__(384, 1)
         if (full) {
 #pragma unroll
           for (int c = 0; c < BC; c += 4) {  // two independent max chains
-            const f32x2 x2 = mul2(pk2((float)(int)v[c], (float)(int)v[c + 1]), cq2);
-            const f32x2 y2 = mul2(pk2((float)(int)v[c + 2], (float)(int)v[c + 3]), cq2);
+            const f32x2 x2 = mul2(pk2(__uint_as_float(v[c]), __uint_as_float(v[c + 1])), cq2);  // S: exact fp32
+            const f32x2 y2 = mul2(pk2(__uint_as_float(v[c + 2]), __uint_as_float(v[c + 3])), cq2);
             mt = fmaxf(mt, fmaxf(lo2(x2), hi2(x2)));
             mt1 = fmaxf(mt1, fmaxf(lo2(y2), hi2(y2)));
             v[c] = __float_as_uint(lo2(x2));
@@ -324,7 +347,7 @@ __global__ void __launch_bounds__(384, 1)
         } else {
 #pragma unroll
           for (int c = 0; c < BC; c += 2) {
-            const f32x2 x2 = mul2(pk2((float)(int)v[c], (float)(int)v[c + 1]), cq2);
+            const f32x2 x2 = mul2(pk2(__uint_as_float(v[c]), __uint_as_float(v[c + 1])), cq2);
             const float x0 = c < nvalid ? lo2(x2) : -INFINITY;
             const float x1 = c + 1 < nvalid ? hi2(x2) : -INFINITY;
             mt = fmaxf(mt, fmaxf(x0, x1));
@@ -493,7 +516,8 @@ __global__ void __launch_bounds__(384, 1)
       // O rows go through shared memory (this warp's 32 rows, XOR-swizzled 16-byte chunks)
       // so that the global stores are row-contiguous.
       constexpr int CH = HD / 8;  // 16-byte chunks per row
-      uint8_t* stg = reinterpret_cast<uint8_t*>(sm.stg[slot]) + qd * (32 * HD * 2);
+      // (the slot's Q buffer: its last QK^T MMA completed before the last tile's S was read)
+      uint8_t* stg = reinterpret_cast<uint8_t*>(sm.q1[slot]) + qd * (32 * HD * 2);
       const float f = (row_ok && R > 0.f) ? 1.f / (R * l) : 0.f;
 #pragma unroll
       for (int cc = 0; cc < HD / 32; ++cc) {
@@ -562,12 +586,13 @@ static bool make_map_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t 
 }
 
 cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Nk, int Hq, int Hkv, int causal, const __half* q,
-                           const int8_t* k1, const __half* v1t, const float* k1s, const float* v1s, __half* o,
+                           const __half* k1, const __half* v1t, const float* k1s, const float* v1s, __half* o,
                            float* lse, cudaStream_t st, const int8_t* q1_in, const float* sq_in) {
   const int HD = p->head_dim, BC = p->block_kv, Tc = (Nk + BC - 1) / BC;
   CUtensorMap tmk, tmv;
-  const CUtensorMapSwizzle swk = HD == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
-  if (!make_map_3d(&tmk, k1, HD, Nk, (uint64_t)B * Hkv, HD, (uint64_t)Nk * HD, HD, BC, swk))
+  // K [Nk][HD] fp16 codes; boxes of 64 channels x B_c keys (128-B rows, SW128)
+  if (!make_map_3d(&tmk, k1, HD, Nk, (uint64_t)B * Hkv, HD * 2, (uint64_t)Nk * HD * 2, 64, BC,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16))
     return cudaErrorInvalidValue;
   // V^T blocks [B_c][HD] of fp16 codes; boxes of 64 keys x HD channels (128-B rows)
   if (!make_map_3d(&tmv, v1t, BC, HD, (uint64_t)B * Hkv * Tc, BC * 2, (uint64_t)HD * BC * 2, 64, HD,

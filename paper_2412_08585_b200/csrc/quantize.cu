@@ -100,7 +100,7 @@ template <int HD, int BC>
 __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefill_kernel(
     const __half* __restrict__ k, const __half* __restrict__ v, int N, int Hkv, int max_blocks, int j0, int Nk,
     const int32_t* __restrict__ bits_dev, uint8_t* __restrict__ block_rec, float* __restrict__ s_parent,
-    float* __restrict__ a_univ, int8_t* __restrict__ k1, __half* __restrict__ v1t, float* __restrict__ k1s,
+    float* __restrict__ a_univ, __half* __restrict__ k1, __half* __restrict__ v1t, float* __restrict__ k1s,
     float* __restrict__ v1s, int scale_fp16, int t0, int Nin) {
   constexpr int NW = HD / 32;  // warps
   // One CTA per (block, kv head, batch, K or V): 6 small CTAs per SM keep more loads in
@@ -109,8 +109,11 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefi
   // max reduction) the space is reused for K's token-major stage-1 / stage-2 code tiles.
   __shared__ __align__(16) __half xs[BC][HD];
   __shared__ float red[NW];
-  uint8_t* tile1 = reinterpret_cast<uint8_t*>(&xs[0][0]);            // K stage-1 codes [t][c]
-  uint8_t* tile2 = reinterpret_cast<uint8_t*>(&xs[0][0]) + BC * HD;  // K stage-2 codes [t][c]
+  // K: B_c = 64 transposes the fp16 stage-1 codes through xs (then a coalesced copy-out) and keeps the
+  // stage-2 codes in t2s; B_c = 128 (48 KB static limit) writes k1 directly and keeps the stage-2 codes
+  // in the second half of xs.
+  __shared__ __align__(16) uint8_t t2s[BC == 64 ? BC * HD : 16];
+  uint8_t* tile2 = BC == 64 ? t2s : reinterpret_cast<uint8_t*>(&xs[0][0]) + BC * HD;  // K stage-2 codes [t][c]
   const int j = blockIdx.x, h = blockIdx.y, b = blockIdx.z >> 1, kind = blockIdx.z & 1, tid = threadIdx.x;
   const int c = tid;
   // chunk block j is cache block j0 + j; the stage-1 outputs cover Nk tokens (Tc blocks)
@@ -160,8 +163,17 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefi
     if (rows == BC) s_parent[(bh * 2 + kind) * max_blocks + j0 + j] = sc;
   }
   if (kind == 0) {
+    // k1: token-major [N][d] stage-1 codes as fp16 (exact) -- the B operand of the prefill's
+    // kind::f16 Q K^T MMA
+    if (BC == 64) {
 #pragma unroll
-    for (int t = 0; t < BC; ++t) tile1[t * HD + c] = (uint8_t)q1(t);
+      for (int t = 0; t < BC; ++t) xs[t][c] = __int2half_rn(q1(t));
+    } else {  // the CTA's threads write d contiguous halves per token
+      __half* krow = k1 + (bh * Nk + (size_t)(j0 + j) * BC) * HD + c;
+#pragma unroll
+      for (int t = 0; t < BC; ++t)
+        if (t < rows) krow[(size_t)t * HD] = __int2half_rn(q1(t));
+    }
   } else {
     // v1t: the block transposed, [d][B_c], codes as fp16 (exact) -- the B operand
     // of the prefill's kind::f16 P V MMA; tokens past N are 0.
@@ -239,13 +251,14 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefi
   }
   if (kind == 1) return;  // V: done (its record words were written per channel)
   __syncthreads();
-  // k1 rows (token-major, natural channel order) from tile1
-  constexpr int CH16 = BC * HD / 16;
-  for (int i = tid; i < CH16; i += HD) {
-    const int t = i / (HD / 16), c16 = i % (HD / 16);
-    if (t < rows)
-      *reinterpret_cast<uint4*>(k1 + (bh * Nk + (size_t)(j0 + j) * BC + t) * HD + c16 * 16) =
-          *reinterpret_cast<const uint4*>(tile1 + t * HD + c16 * 16);
+  if (BC == 64) {  // k1 rows (token-major, natural channel order) from xs, 16-byte chunks
+    constexpr int CH8 = BC * HD / 8;
+    for (int i = tid; i < CH8; i += HD) {
+      const int t = i / (HD / 8), c8 = i % (HD / 8);
+      if (t < rows)
+        *reinterpret_cast<uint4*>(k1 + (bh * Nk + (size_t)(j0 + j) * BC + t) * HD + c8 * 8) =
+            *reinterpret_cast<const uint4*>(&xs[t][8 * c8]);
+    }
   }
   if (rows < BC) return;  // partial tail block: goes to the buffer (tail kernel)
   // K record codes: token-major, natural channel order, LSB-first; one uint4 = 4 words per thread
@@ -371,7 +384,7 @@ template <int HD, int BC>
 __global__ void __launch_bounds__(2 * HD) dequant_cache_kernel(
     int Hkv, int max_blocks, int blk_begin, int blk_end, int Nk, const int32_t* __restrict__ bits_dev,
     const uint8_t* __restrict__ block_rec, const float* __restrict__ s_parent, const int32_t* __restrict__ counters,
-    int8_t* __restrict__ k1, __half* __restrict__ v1t, float* __restrict__ k1s, float* __restrict__ v1s) {
+    __half* __restrict__ k1, __half* __restrict__ v1t, float* __restrict__ k1s, float* __restrict__ v1s) {
   const int j = blk_begin + blockIdx.x, h = blockIdx.y, b = blockIdx.z, tid = threadIdx.x;
   const int nb = counters[b * 2];
   if (j >= nb || (blk_end >= 0 && j >= blk_end)) return;
@@ -389,7 +402,7 @@ __global__ void __launch_bounds__(2 * HD) dequant_cache_kernel(
     const int TB = HD * bits / 8, byte = c * bits / 8, sh = (c * bits) % 8;
 #pragma unroll 4
     for (int t = 0; t < BC; ++t)
-      k1[(bh * Nk + (size_t)j * BC + t) * HD + c] = (int8_t)((int)((codes[t * TB + byte] >> sh) & mask) * sc + zc);
+      k1[(bh * Nk + (size_t)j * BC + t) * HD + c] = __int2half_rn((int)((codes[t * TB + byte] >> sh) & mask) * sc + zc);
   } else {
     // V: channel-major words per 64-token sub-block in the IMMA token order (layout.cuh v_token_of)
     const int CB = kSub * bits / 8;
@@ -417,7 +430,7 @@ template <int HD, int BC>
 __global__ void __launch_bounds__(256) quant_boundary_kernel(
     const __half* __restrict__ k, const __half* __restrict__ v, int N, int r, int Hkv, int max_blocks, int j0, int nbuf,
     int Nk, const int32_t* __restrict__ bits_dev, const float* __restrict__ a_univ, int8_t* __restrict__ buf,
-    uint8_t* __restrict__ block_rec, float* __restrict__ s_parent, int8_t* __restrict__ k1, __half* __restrict__ v1t,
+    uint8_t* __restrict__ block_rec, float* __restrict__ s_parent, __half* __restrict__ k1, __half* __restrict__ v1t,
     int scale_fp16) {
   __shared__ __align__(16) int8_t tile[2][BC * HD];
   const int h = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
@@ -435,7 +448,7 @@ __global__ void __launch_bounds__(256) quant_boundary_kernel(
       const int code = max(-119, min(119, rint_prod(x, inv)));
       const int row = nbuf + t;
       bslot[kv == 0 ? row * HD + c : c * BC + row] = (int8_t)code;
-      if (kv == 0) k1[(bh * Nk + (size_t)j0 * BC + row) * HD + c] = (int8_t)code;
+      if (kv == 0) k1[(bh * Nk + (size_t)j0 * BC + row) * HD + c] = __int2half_rn(code);
       else v1t[((bh * Tk + j0) * HD + c) * BC + row] = __int2half_rn(code);
     }
     if (flush)
@@ -480,7 +493,7 @@ template <int HD, int BC>
 __global__ void __launch_bounds__(2 * HD) dequant_buffer_kernel(int Hkv, int Nk, const int8_t* __restrict__ buf,
                                                                const float* __restrict__ a_univ,
                                                                const int32_t* __restrict__ counters,
-                                                               int8_t* __restrict__ k1, __half* __restrict__ v1t,
+                                                               __half* __restrict__ k1, __half* __restrict__ v1t,
                                                                float* __restrict__ k1s, float* __restrict__ v1s,
                                                                int scale_fp16) {
   const int h = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
@@ -491,7 +504,7 @@ __global__ void __launch_bounds__(2 * HD) dequant_buffer_kernel(int Hkv, int Nk,
   const int8_t* bslot = buf + (bh * 2 + kind) * (size_t)(BC * HD);
   if (c == 0) (kind ? v1s : k1s)[bh * Tk + nb] = st1_scale(div_by_119(a_univ[bh * 2 + kind]), scale_fp16);
   if (kind == 0) {
-    for (int t = 0; t < nbuf; ++t) k1[(bh * Nk + (size_t)nb * BC + t) * HD + c] = bslot[t * HD + c];
+    for (int t = 0; t < nbuf; ++t) k1[(bh * Nk + (size_t)nb * BC + t) * HD + c] = __int2half_rn((int)bslot[t * HD + c]);
   } else {
     for (int t = 0; t < BC; ++t)
       v1t[((bh * Tk + nb) * HD + c) * BC + t] = __int2half_rn(t < nbuf ? (int)bslot[c * BC + t] : 0);
@@ -507,7 +520,7 @@ using namespace ta;
 
 template <int HD, int BC>
 static void quant_boundary_hd(const turbo_kv_cache_t* c, const __half* k, const __half* v, int N, int r, int j0,
-                              int nbuf, int Nk, int8_t* k1, __half* v1t, cudaStream_t st, int scale_fp16) {
+                              int nbuf, int Nk, __half* k1, __half* v1t, cudaStream_t st, int scale_fp16) {
   quant_boundary_kernel<HD, BC><<<dim3(c->n_kv_heads, c->batch), 256, 0, st>>>(
       k, v, N, r, c->n_kv_heads, c->max_blocks, j0, nbuf, Nk, c->bits_dev, c->a_univ, c->buf, c->block_rec,
       c->s_parent, k1, v1t, scale_fp16);
@@ -515,7 +528,7 @@ static void quant_boundary_hd(const turbo_kv_cache_t* c, const __half* k, const 
 }
 
 template <int HD, int BC>
-static void quant_prefill_hd(const turbo_kv_cache_t* c, const __half* k, const __half* v, int N, int8_t* k1,
+static void quant_prefill_hd(const turbo_kv_cache_t* c, const __half* k, const __half* v, int N, __half* k1,
                              __half* v1t, float* k1s, float* v1s, cudaStream_t st, int j0, int Nk, int scale_fp16,
                              int t0, int Nin) {
   const int B = c->batch, H = c->n_kv_heads, Tc = (N + BC - 1) / BC;
@@ -525,7 +538,7 @@ static void quant_prefill_hd(const turbo_kv_cache_t* c, const __half* k, const _
   quant_tail_kernel<HD, BC><<<dim3(H, B), 256, 0, st>>>(k, v, N, H, c->a_univ, c->buf, c->counters, j0, t0, Nin);
 }
 
-cudaError_t launch_quant_prefill(const turbo_kv_cache_t* c, const __half* k, const __half* v, int N, int8_t* k1,
+cudaError_t launch_quant_prefill(const turbo_kv_cache_t* c, const __half* k, const __half* v, int N, __half* k1,
                                  __half* v1t, float* k1s, float* v1s, cudaStream_t st, int j0, int Nk,
                                  int scale_fp16) {
   // j0 = 0, Nk = N: PREFILL (resets the universal scales and the buffer); j0 > 0: a
@@ -567,14 +580,14 @@ cudaError_t launch_quant_prefill(const turbo_kv_cache_t* c, const __half* k, con
 }
 
 template <int HD, int BC>
-static void dequant_cache_hd(const turbo_kv_cache_t* c, dim3 grid, int blk_begin, int blk_end, int Nk, int8_t* k1,
+static void dequant_cache_hd(const turbo_kv_cache_t* c, dim3 grid, int blk_begin, int blk_end, int Nk, __half* k1,
                              __half* v1t, float* k1s, float* v1s, cudaStream_t st) {
   dequant_cache_kernel<HD, BC><<<grid, 2 * HD, 0, st>>>(c->n_kv_heads, c->max_blocks, blk_begin, blk_end, Nk,
                                                         c->bits_dev, c->block_rec, c->s_parent, c->counters, k1, v1t,
                                                         k1s, v1s);
 }
 
-cudaError_t launch_dequant_cache(const turbo_kv_cache_t* c, int blk_begin, int blk_end, int Nk, int8_t* k1,
+cudaError_t launch_dequant_cache(const turbo_kv_cache_t* c, int blk_begin, int blk_end, int Nk, __half* k1,
                                  __half* v1t, float* k1s, float* v1s, cudaStream_t st, int scale_fp16) {
   const int B = c->batch, H = c->n_kv_heads, HD = c->head_dim, BC = c->block_kv;
   const int last = blk_end >= 0 ? std::min(blk_end, c->max_blocks) : c->max_blocks;

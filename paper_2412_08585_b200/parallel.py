@@ -138,7 +138,7 @@ def prefill_shard_tail(p, cache, k, v, a_global):
         B, _, H, d = k.shape
         nk = n + (k.shape[1] - n)
         tc = -(-nk // BC)
-        out = (torch.empty((B, H, nk, d), dtype=torch.int8, device=k.device),
+        out = (torch.empty((B, H, nk, d), dtype=torch.float16, device=k.device),
                torch.empty((B, H, tc, d, BC), dtype=torch.float16, device=k.device),
                torch.empty((B, H, tc), dtype=torch.float32, device=k.device),
                torch.empty((B, H, tc), dtype=torch.float32, device=k.device))  # prefill operands: unused
