@@ -15,7 +15,7 @@
  *       TURBO_ERR_INVALID_ARG  null pointer, non-positive size, bad enum value;
  *       TURBO_ERR_UNSUPPORTED  head_dim not in {64,128}, block_kv not in {64,128},
  *                              block_q not in {64,128}, Hq % Hkv != 0,
- *                              Hq/Hkv > 8 (decode), sas_nr not in [-30,-1];
+ *                              sas_nr not in [-30,-1];
  *       TURBO_ERR_CAPACITY     an append/prefill would exceed cache->max_blocks;
  *       TURBO_ERR_CUDA         a CUDA launch failed (cudaGetLastError).
  *     On error nothing has been enqueued (except TURBO_ERR_CUDA, where earlier
@@ -246,8 +246,8 @@ TURBO_API turbo_status_t turbo_attention_prefill_chunk(const turbo_params_t* par
 /* Workspace for turbo_attention_decode with n_splits on the current device
  * (HOST result; 0 = none needed, or invalid arguments).
  *   n_splits >= 2: S * B * Hq * (d + 1) floats;  n_splits <= 0 (balanced):
- *   (B * Hkv + W) * (Hq / Hkv) * (d + 1) floats, W = -n_splits, or
- *   turbo_decode_workers() for n_splits == 0. */
+ *   (B * Hkv' + W) * (Hq / Hkv') * (d + 1) floats, W = -n_splits, or
+ *   turbo_decode_workers() for n_splits == 0; Hkv' = Hkv * r (see below). */
 TURBO_API size_t turbo_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t head_dim,
                                               int32_t n_splits);
 
@@ -267,7 +267,9 @@ TURBO_API int32_t turbo_decode_workers(int32_t Hq, int32_t Hkv, int32_t head_dim
  *     joins the last one).
  *   n_splits in [-12000, 0] (balanced): the units of every (b, kv head) --
  *     its blocks in order, then the buffer block if used (with_buffer and
- *     n_buf > 0) -- are laid end to end in (b, kv head) order; the sequence
+ *     n_buf > 0) -- are laid end to end in (b, kv head) order (GQA groups of
+ *     G > 8 query rows: each KV head counts as r virtual heads of G / r rows,
+ *     r the least divisor of G with G / r <= 8, in (kv head, row group) order); the sequence
  *     of all `total` units is cut into chunks of C = max(8, ceil(total / W))
  *     units, W = -n_splits workers, or W = turbo_decode_workers(Hq, Hkv, d)
  *     (the current device's resident decode warps) for n_splits == 0, and

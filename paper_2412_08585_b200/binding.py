@@ -309,13 +309,24 @@ def balanced_ranges(unit_counts, Hkv, workers, min_units=8):
 B200_SMS = 148
 
 
+def decode_row_groups(G):
+    """Row groups per KV head in the decode (include/turbo_attention.h): the least r with G / r <= 8
+    query rows that divides G; the schedule then sees Hkv * r (virtual) KV heads of G / r rows."""
+    return next(r for r in range(-(-G // 8), G + 1) if G % r == 0)
+
+
 def reference_workers(Hq, Hkv, head_dim):
     """Resident decode warps of ONE B200 (148 SMs x the decode kernel's warps per SM: 12 for the
-    packed G <= 4 path and for d = 64, 8 for the general d = 128 path at 239 registers).  The default
+    packed G <= 4 path at d = 128, 16 at d = 64, 12 for the general d = 64 path, 8 for the general
+    d = 128 path at 250 registers).  The default
     decode schedule uses this fixed count on every device, so that its split partition -- and hence
     its numbers (turbo_attention.h, SPLIT DEPENDENCE) -- never depend on the GPU it runs on; on a
     B200 it equals turbo_decode_workers() (tests/test_gpu_parity.py checks it)."""
-    per_sm = 12 if (Hq // Hkv <= 4 or head_dim == 64) else 8
+    Gv = Hq // Hkv // decode_row_groups(Hq // Hkv)  # rows per (virtual) KV head
+    if head_dim == 64:
+        per_sm = 16 if Gv <= 4 else 12  # 128 / 165 registers
+    else:
+        per_sm = 12 if Gv <= 4 else 8   # 168 / 250 registers
     return B200_SMS * per_sm
 
 

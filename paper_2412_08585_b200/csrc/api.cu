@@ -24,6 +24,7 @@ cudaError_t launch_q_projection(const turbo_params_t* p, int B, int N, int D, in
                                 int8_t* q1, float* sq, __half* q16, cudaStream_t st);
 size_t decode_workspace(int B, int Hq, int Hkv, int HD, int S);
 int decode_workers(int Hq, int Hkv, int HD);
+int decode_row_groups(int G);
 cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, int Hq, const __half* q, int blk_begin,
                           int blk_end, int with_buffer, int S, void* ws, __half* o, float* o_part, float* lse,
                           cudaStream_t st);
@@ -215,7 +216,7 @@ size_t turbo_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t 
 
 int32_t turbo_decode_workers(int32_t Hq, int32_t Hkv, int32_t head_dim) {
   if (Hq < 1 || Hkv < 1 || Hq % Hkv != 0 || (head_dim != 64 && head_dim != 128)) return 0;
-  return ta_host::decode_workers(Hq, Hkv, head_dim);
+  return ta_host::decode_workers(Hq, Hkv * ta_host::decode_row_groups(Hq / Hkv), head_dim);  // (virtual heads, G > 8)
 }
 
 turbo_status_t turbo_attention_decode(const turbo_params_t* params, const turbo_kv_cache_t* cache, int32_t Hq,
@@ -227,7 +228,6 @@ turbo_status_t turbo_attention_decode(const turbo_params_t* params, const turbo_
   if ((s = check_cache(params, cache)) != TURBO_OK) return s;
   if (Hq < 1 || !q || !lse || (!o && !o_part)) return TURBO_ERR_INVALID_ARG;
   if (Hq % cache->n_kv_heads != 0) return TURBO_ERR_UNSUPPORTED;
-  if (Hq / cache->n_kv_heads > 8) return TURBO_ERR_UNSUPPORTED;
   if (n_splits < -12000 || n_splits > 12000 || blk_begin < 0 || (blk_end >= 0 && blk_end < blk_begin))
     return TURBO_ERR_INVALID_ARG;
   if (with_buffer != 0 && with_buffer != 1) return TURBO_ERR_INVALID_ARG;

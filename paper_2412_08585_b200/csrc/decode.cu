@@ -56,7 +56,10 @@ struct DecodeArgs {
   __half* fin_o16;  // balanced schedule: final fp16 output (or NULL)
   float* fin_o32;   // balanced schedule: final f32 output (or NULL)
   float* fin_lse;   // balanced schedule: final L
-  int B, Hq, Hkv, G, max_blocks, blk_begin, blk_end, with_buffer, n_splits, alpha_mode, scale_fp16, sas_fp16;
+  // Hkv and G are VIRTUAL when the group has more than 8 query rows: each KV head's G_real rows are cut into RG
+  // row groups of G = G_real / RG rows (virtual KV head vk = kvh RG + rg, query head vk G + row as before), so a
+  // task holds at most 8 rows; the cache slot is (b, vk / RG).
+  int B, Hq, Hkv, G, RG, max_blocks, blk_begin, blk_end, with_buffer, n_splits, alpha_mode, scale_fp16, sas_fp16;
   float scale;
   SasConst sas;
   turbo_debug_tap_t tap;
@@ -488,8 +491,9 @@ TA_DEV void decode_segment(const DecodeArgs& a, DecodeSmem<HD, PACK, BC>& sm, in
   using M = Map<HD, PACK>;
   const int g = lane >> 2, q = lane & 3;
   const int G = a.G;
-  const int bitsK = a.bits[kvh * 2], bitsV = a.bits[kvh * 2 + 1];
-  const size_t slotK = ((size_t)b * a.Hkv + kvh) * 2, slotV = slotK + 1;
+  const int kvr = kvh / a.RG;  // the real KV head of this (virtual) head
+  const int bitsK = a.bits[kvr * 2], bitsV = a.bits[kvr * 2 + 1];
+  const size_t slotK = ((size_t)b * (a.Hkv / a.RG) + kvr) * 2, slotV = slotK + 1;
   constexpr int REC = rec_bytes(HD, BC);
   constexpr int NT = M::NT * BC / 64;
   const uint32_t bytesK = 2 * HD + BC * HD * bitsK / 8, bytesV = 2 * HD + BC * HD * bitsV / 8;
@@ -901,20 +905,31 @@ int decode_workers(int Hq, int Hkv, int HD) {
   return sms * per_sm * kWarpsPerCta;
 }
 
+// Row groups per KV head: the least RG with G / RG <= 8 rows that divides G (G <= 8: 1).
+int decode_row_groups(int G) {
+  for (int r = (G + 7) / 8; r <= G; ++r)
+    if (G % r == 0) return r;
+  return G;
+}
+
 size_t decode_workspace(int B, int Hq, int Hkv, int HD, int S) {
   if (S == 1) return 0;
   if (S > 1) return (size_t)S * B * Hq * (HD + 1) * sizeof(float);
-  // balanced: parts bh + w < B * Hkv + W, G rows of d + 1 floats each (S < 0: W = -S workers)
-  const int W = S < 0 ? -S : decode_workers(Hq, Hkv, HD);
-  return W <= 0 ? 0 : ((size_t)B * Hkv + W) * (Hq / Hkv) * (HD + 1) * sizeof(float);
+  // balanced: parts bh + w < B * Hkv' + W (Hkv' = Hkv x row groups), G' rows of d + 1 floats each
+  // (S < 0: W = -S workers)
+  const int RG = decode_row_groups(Hq / Hkv), Hv = Hkv * RG;
+  const int W = S < 0 ? -S : decode_workers(Hq, Hv, HD);
+  return W <= 0 ? 0 : ((size_t)B * Hv + W) * (Hq / Hv) * (HD + 1) * sizeof(float);
 }
 
 cudaError_t launch_decode(const turbo_params_t* p, const turbo_kv_cache_t* c, int Hq, const __half* q, int blk_begin,
                           int blk_end, int with_buffer, int S, void* ws, __half* o, float* o_part, float* lse,
                           cudaStream_t st) {
-  const int B = c->batch, H = c->n_kv_heads, HD = c->head_dim;
+  const int RG = decode_row_groups(Hq / c->n_kv_heads);
+  const int B = c->batch, H = c->n_kv_heads * RG, HD = c->head_dim;  // H: virtual KV heads (G > 8)
   DecodeArgs a;
   memset(&a, 0, sizeof(a));
+  a.RG = RG;
   a.q = q;
   a.block_rec = c->block_rec;
   a.s_parent = c->s_parent;

@@ -510,3 +510,51 @@ def test_seq_sharded_prefill_global_universal_scale(ta):
     for c, t0, t1 in caches:
         nb = (t1 - t0) // 64
         np.testing.assert_array_equal(c.records().cpu().numpy()[:, :, :, :nb], rw[:, :, :, t0 // 64:t0 // 64 + nb])
+
+
+@pytest.mark.parametrize("Hq,Hkv,d,S", [(32, 2, 128, 1), (32, 2, 128, 3), (24, 2, 128, 2), (18, 2, 64, 1),
+                                        (32, 2, 128, 0)])
+def test_decode_large_gqa_groups(ta, Hq, Hkv, d, S):
+    """G > 8 query rows per KV head (G = 16, 12, 9): each KV head runs as r virtual heads of G / r <= 8
+    rows (include/turbo_attention.h) over the same cache; equal splits and the balanced schedule."""
+    B, N, n_app = 2, 64 * 5 + 21, 3
+    G = Hq // Hkv
+    q, k, v = synth.qkv(8800 + Hq, B, N, Hq, Hkv, d)
+    bits = synth.head_bits_alternating(Hkv)
+    p, op = ta.params(head_dim=d), O.params(d=d)
+    maxb = (N + n_app) // 64 + 2
+    cache = ta.KVCache(B, Hkv, d, max_blocks=maxb, bits=bits)
+    ta.turbo_quantize_kv(p, cache, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    ref = O.build_cache(op, k.astype(np.float32), v.astype(np.float32), bits, maxb)
+    for t in range(n_app):
+        _, kt, vt = synth.decode_token(8900 + t, B, Hq, Hkv, d)
+        ta.turbo_quantize_kv(p, cache, torch.from_numpy(kt).cuda(), torch.from_numpy(vt).cuda(), mode=1)
+        for b in range(B):
+            for h in range(Hkv):
+                ref["slots"][b][h][0].append(kt[b, h].astype(np.float32))
+                ref["slots"][b][h][1].append(vt[b, h].astype(np.float32))
+    qd, _, _ = synth.decode_token(8999, B, Hq, Hkv, d)
+    o, _, lse = ta.turbo_attention_decode(p, cache, torch.from_numpy(qd).cuda(), n_splits=S)
+    torch.cuda.synchronize()
+    o, lse = o.cpu().numpy(), lse.cpu().numpy()
+    nb = ref["slots"][0][0][0].n_blocks
+    r = ta.decode_row_groups(G)
+    Gv, Hv = G // r, Hkv * r
+    if S > 0:
+        per = -(-nb // S)
+        bounds = [(min(s * per, nb), min(s * per + per, nb)) for s in range(S)]
+    else:  # the balanced partition over the virtual heads
+        units = [ref["slots"][b][0][0].n_blocks + (1 if ref["slots"][b][0][0].n_buf > 0 else 0) for b in range(B)]
+        rng = ta.balanced_ranges(units, Hv, ta.turbo_decode_workers(Hq, Hkv, d))
+    for b in range(B):
+        for hq in range(Hq):
+            ks, vs = ref["slots"][b][hq // G]
+            pieces = ([(a_, e_, s == len(bounds) - 1) for s, (a_, e_) in enumerate(bounds)] if S > 0 else
+                      [(u0, min(u1, nb), u1 > nb) for u0, u1 in rng[(b, hq // Gv)]])
+            parts = [O.decode_head(op, qd[b, hq].astype(np.float32), ks, vs, a_, e_, wb) for a_, e_, wb in pieces]
+            if len(parts) == 1:
+                ro, rl = parts[0]
+            else:
+                ro, rl = O.combine(np.stack([x[0] for x in parts]), np.array([x[1] for x in parts]))
+            assert_out_close(o[b, hq], ro, f"b{b} h{hq}")
+            np.testing.assert_allclose(lse[b, hq], rl, atol=1e-4, rtol=1e-5)

@@ -10,6 +10,8 @@ from paper_2412_08585_b200 import binding as ta  # noqa: E402
 from paper_2412_08585_b200 import synth  # noqa: E402
 
 B, N, Hq, Hkv, d = 64, 32768, 40, 10, 128
+if os.environ.get("DEC_SHAPE"):  # "B,N,Hq,Hkv,d" (e.g. the G = 8 shape 16,32768,64,8,128)
+    B, N, Hq, Hkv, d = (int(x) for x in os.environ["DEC_SHAPE"].split(","))
 S = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 p = ta.params(head_dim=d)
