@@ -237,10 +237,14 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t tbase = tmem + ((uint32_t)(qd * 32) << 16) + slot * kSlotCols;
     const float lut_lane = sas_lut_lane(args.sas, lane);
     const float nr_abs = args.sas.nr_abs;
+    const float p_top = sas_eval_v<SF>(0.f, lut_lane, nr_abs);  // SAS(0): the largest possible P~
+    const float inv_top = div_119_by(p_top), s_top = div_by_119(p_top);
     const bool tap_cta = TAP && args.tap.batch == b && args.tap.head == h && (args.tap.i_block >> 1) == its;
     const bool tap_row = tap_cta && (args.tap.i_block & 1) == (r >> 6);
     const uint32_t bar_slot = 1 + slot;                                  // the slot's 128 threads
-    const uint32_t bar_grp = args.block_q == 64 ? 3 + slot * 2 + half : 1 + slot;  // the P-scale group
+    // the P-scale group's two named barriers (alternating by tile parity: a warp that only arrives may
+    // reach the next tile's exchange before its partner has waited on this one)
+    const uint32_t bar_grp = args.block_q == 64 ? 3 + (slot * 2 + half) * 2 : 11 + slot * 2;
     const uint32_t grp_threads = args.block_q;
 
     // Q stage-1 quantisation (Alg. 1; per B_r x d block) -- or, with q1_in, the codes and
@@ -400,15 +404,26 @@ __global__ void __launch_bounds__(384, 1)
       // P scale: max P~ over the B_r x B_c tile (or, PROW, over the row)
       float a_p = pmax;
       if (!PROW) {
+        // Every P~ <= SAS(0) (LUT <= 1, POLY decreasing on [0, 1], the rounding of c0 - |.| f never
+        // exceeds c0), so a warp whose maximum is SAS(0) knows the tile's maximum: it publishes and only
+        // arrives; warps without it publish, wait and combine.
         const float wmax = warp_max_nonneg(pmax);
         if (lane == 0) sm.red_p[slot][rb][qd] = wmax;
-        named_bar_sync(bar_grp, grp_threads);
-        a_p = args.block_q == 64 ? fmaxf(sm.red_p[slot][rb][2 * half], sm.red_p[slot][rb][2 * half + 1])
-                                 : fmaxf(fmaxf(sm.red_p[slot][rb][0], sm.red_p[slot][rb][1]),
-                                         fmaxf(sm.red_p[slot][rb][2], sm.red_p[slot][rb][3]));
+        if (wmax == p_top) {
+          named_bar_arrive(bar_grp + rb, grp_threads);
+          a_p = p_top;
+        } else {
+          named_bar_sync(bar_grp + rb, grp_threads);
+          a_p = args.block_q == 64 ? fmaxf(sm.red_p[slot][rb][2 * half], sm.red_p[slot][rb][2 * half + 1])
+                                   : fmaxf(fmaxf(sm.red_p[slot][rb][0], sm.red_p[slot][rb][1]),
+                                           fmaxf(sm.red_p[slot][rb][2], sm.red_p[slot][rb][3]));
+        }
       }
-      const float inv_p = a_p > 0.f ? div_119_by(a_p) : 0.f;
-      const float s_p = div_by_119(a_p);
+      float inv_p = inv_top, s_p = s_top;  // the common case a_P = SAS(0): its scale and reciprocal, once
+      if (a_p != p_top) {
+        inv_p = a_p > 0.f ? div_119_by(a_p) : 0.f;
+        s_p = div_by_119(a_p);
+      }
       // Scale bookkeeping: O^ row *= fix (fix = 0: alpha = 0 discards the history;
       // power of two: keeps F = s_P s_V R in [2^-8, 2^5]).
       float F = 0.f, fix = 1.f;
