@@ -81,6 +81,13 @@ TA_DEV void pack_record(const int8_t* tile, int kind, int bits, uint8_t* rec_cod
 // the stage-2 column statistics and the V record words need no shared-memory
 // round trips; only K's token-major outputs are transposed through smem.
 
+// One 32-byte global store (STG.256) of 8 words; p 32-byte aligned.
+TA_DEV void st_global_v8(void* p, const uint32_t (&w)[8]) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+               "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+               : "memory");
+}
+
 // 8 bytes, each < 16, -> one LSB-first 4-bit word.
 TA_DEV uint32_t pack_nib8(uint2 v) {
   unsigned long long x = (unsigned long long)v.x | ((unsigned long long)v.y << 32);
@@ -176,8 +183,11 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefi
     }
   } else {
     // v1t: the block transposed, [d][B_c], codes as fp16 (exact) -- the B operand
-    // of the prefill's kind::f16 P V MMA; tokens past N are 0.
-    uint4* dst = reinterpret_cast<uint4*>(v1t + ((bh * Tc + j0 + j) * HD + c) * BC);
+    // of the prefill's kind::f16 P V MMA; tokens past N are 0.  Staged in xs as rows of B_c
+    // halves with the 16-byte chunks XOR-swizzled by (c & 7) (conflict-free 16-byte stores),
+    // then copied out as one contiguous, coalesced [d][B_c] tile (a thread's own row would be
+    // B_c / 8 half-sector stores 2 B_c bytes apart).
+    uint4* row = reinterpret_cast<uint4*>(&xs[0][0]) + c * (BC / 8);
 #pragma unroll
     for (int t8 = 0; t8 < BC / 8; ++t8) {
       uint32_t u[4];
@@ -186,7 +196,7 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefi
         const __half2 hv = __halves2half2(__int2half_rn(q1(8 * t8 + 2 * e)), __int2half_rn(q1(8 * t8 + 2 * e + 1)));
         u[e] = *reinterpret_cast<const uint32_t*>(&hv);
       }
-      dst[t8] = make_uint4(u[0], u[1], u[2], u[3]);
+      row[t8 ^ (c & 7)] = make_uint4(u[0], u[1], u[2], u[3]);
     }
   }
   const int bits = bits_dev[h * 2 + kind];
@@ -225,9 +235,7 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefi
           for (int e = 0; e < 4; ++e) acc |= (q(t0 + e) | (q(t0 + 16 + e) << 4)) << (8 * e);
           w[W] = acc;
         }
-        uint4* dst = reinterpret_cast<uint4*>(rec + 2 * HD + u * (HD * kSub / 2) + c * (kSub / 2));
-        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        st_global_v8(rec + 2 * HD + u * (HD * kSub / 2) + c * (kSub / 2), w);  // one full 32-byte sector
       }
     } else {
       // V, 2-bit, per sub-block u: word qd, byte e, bits 2s: token 32(s>>1) + 16(s&1) + 4qd + e
@@ -249,8 +257,17 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefi
       }
     }
   }
-  if (kind == 1) return;  // V: done (its record words were written per channel)
   __syncthreads();
+  if (kind == 1) {  // V: copy the staged v1t tile out (its record words were written per channel)
+    const uint4* tile = reinterpret_cast<const uint4*>(&xs[0][0]);
+    uint4* dst = reinterpret_cast<uint4*>(v1t + (bh * Tc + j0 + j) * HD * BC);
+#pragma unroll
+    for (int i = tid; i < HD * BC / 8; i += HD) {
+      const int r = i / (BC / 8), k8 = i % (BC / 8);
+      dst[i] = tile[r * (BC / 8) + (k8 ^ (r & 7))];
+    }
+    return;
+  }
   if (BC == 64) {  // k1 rows (token-major, natural channel order) from xs, 16-byte chunks
     constexpr int CH8 = BC * HD / 8;
     for (int i = tid; i < CH8; i += HD) {
