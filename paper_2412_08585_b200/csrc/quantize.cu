@@ -141,16 +141,18 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefi
     }
   }
   __syncthreads();
-  // the channel's B_c tokens as B_c / 2 half2
+  // the channel's B_c tokens as B_c / 2 half2, and the channel's min / max x (HMNMX2)
   __half2 xh[BC / 2];
-  __half2 amax2 = __float2half2_rn(0.f);
+  __half2 mn2 = __halves2half2(xs[0][c], xs[1][c]), mx2 = mn2;
 #pragma unroll
   for (int t = 0; t < BC; t += 2) {
     xh[t / 2] = __halves2half2(xs[t][c], xs[t + 1][c]);
-    amax2 = __hmax2(amax2, __habs2(xh[t / 2]));
+    mn2 = __hmin2(mn2, xh[t / 2]);
+    mx2 = __hmax2(mx2, xh[t / 2]);
   }
-  float amax = fmaxf(__low2float(amax2), __high2float(amax2));  // exact: max of fp16 magnitudes
-  amax = warp_max(amax);
+  const float xmin = fminf(__low2float(mn2), __high2float(mn2)), xmax = fmaxf(__low2float(mx2), __high2float(mx2));
+  // max |x| of the channel (exact: negation and fp16 -> fp32 are exact), then of the block
+  float amax = warp_max_nonneg(fmaxf(fmaxf(-xmin, xmax), 0.f));
   if ((tid & 31) == 0) red[c >> 5] = amax;
   __syncthreads();
   float a = red[0];
@@ -159,9 +161,21 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefi
   // s = max|x| / 119, codes = round_half_even(x * (119 / max|x|)) (Alg. 1; R-2, R-3, R-5)
   const float inv = a > 0.f ? div_119_by(a) : 0.f;
   const float sc = st1_scale(div_by_119(a), scale_fp16);  // (FP16 variant: R-29; codes unchanged)
-  // stage-1 code of token t, recomputed where needed (2 instructions) instead of held
-  auto q1 = [&](int t) -> int {
-    return rint_prod((t & 1) ? __high2float(xh[t >> 1]) : __low2float(xh[t >> 1]), inv);
+  // Stage-1 codes of a token pair as one FFMA2 against C1 = 1.5 2^23 + 0x6480: the exact product is
+  // rounded half-even to an integer once (C1 is even), and the low 16 bits of the result are
+  // 0x6480 + code = the binary16 pattern of 1152 + code.
+  constexpr float kC1 = 12582912.0f + 25728.0f;
+  const f32x2 inv2 = pk2(inv, inv), c12 = pk2(kC1, kC1);
+  auto F = [&](int pr) -> f32x2 {
+    const float2 xf = __half22float2(xh[pr]);
+    return fma2(pk2(xf.x, xf.y), inv2, c12);
+  };
+  // the pair's codes as exact fp16 values (one PRMT + one HSUB2)
+  auto code16 = [&](f32x2 f) -> uint32_t {
+    const __half2 h = __hsub2(__halves2half2(__ushort_as_half((unsigned short)(uint32_t)f),
+                                             __ushort_as_half((unsigned short)(uint32_t)(f >> 32))),
+                              __float2half2_rn(1152.f));
+    return *reinterpret_cast<const uint32_t*>(&h);
   };
   if (c == 0) {
     (kind ? v1s : k1s)[bh * Tc + j0 + j] = sc;
@@ -174,12 +188,19 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefi
     // kind::f16 Q K^T MMA
     if (BC == 64) {
 #pragma unroll
-      for (int t = 0; t < BC; ++t) xs[t][c] = __int2half_rn(q1(t));
+      for (int pr = 0; pr < BC / 2; ++pr) {
+        const uint32_t h = code16(F(pr));
+        *reinterpret_cast<uint16_t*>(&xs[2 * pr][c]) = (uint16_t)h;
+        *reinterpret_cast<uint16_t*>(&xs[2 * pr + 1][c]) = (uint16_t)(h >> 16);
+      }
     } else {  // the CTA's threads write d contiguous halves per token
-      __half* krow = k1 + (bh * Nk + (size_t)(j0 + j) * BC) * HD + c;
+      uint16_t* krow = reinterpret_cast<uint16_t*>(k1 + (bh * Nk + (size_t)(j0 + j) * BC) * HD + c);
 #pragma unroll
-      for (int t = 0; t < BC; ++t)
-        if (t < rows) krow[(size_t)t * HD] = __int2half_rn(q1(t));
+      for (int pr = 0; pr < BC / 2; ++pr) {
+        const uint32_t h = code16(F(pr));
+        if (2 * pr < rows) krow[(size_t)(2 * pr) * HD] = (uint16_t)h;
+        if (2 * pr + 1 < rows) krow[(size_t)(2 * pr + 1) * HD] = (uint16_t)(h >> 16);
+      }
     }
   } else {
     // v1t: the block transposed, [d][B_c], codes as fp16 (exact) -- the B operand
@@ -189,51 +210,54 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefi
     // B_c / 8 half-sector stores 2 B_c bytes apart).
     uint4* row = reinterpret_cast<uint4*>(&xs[0][0]) + c * (BC / 8);
 #pragma unroll
-    for (int t8 = 0; t8 < BC / 8; ++t8) {
-      uint32_t u[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const __half2 hv = __halves2half2(__int2half_rn(q1(8 * t8 + 2 * e)), __int2half_rn(q1(8 * t8 + 2 * e + 1)));
-        u[e] = *reinterpret_cast<const uint32_t*>(&hv);
-      }
-      row[t8 ^ (c & 7)] = make_uint4(u[0], u[1], u[2], u[3]);
-    }
+    for (int t8 = 0; t8 < BC / 8; ++t8)
+      row[t8 ^ (c & 7)] = make_uint4(code16(F(4 * t8)), code16(F(4 * t8 + 1)), code16(F(4 * t8 + 2)),
+                                     code16(F(4 * t8 + 3)));
   }
   const int bits = bits_dev[h * 2 + kind];
   constexpr int REC = rec_bytes(HD, BC);
   uint8_t* rec = block_rec + ((bh * 2 + kind) * (size_t)max_blocks + j0 + j) * REC;
   if (rows == BC) {
-    // Stage 2 of this channel (integer only, R-6): z = min, s = max(1, ceil((max-min)/(2^b-1))),
-    // code = floor((2 (v - z) + s) / (2 s)) = umulhi(2 (v - z) + s, ceil(2^32 / 2s)) (exact for these
-    // ranges, tests/test_quant_arith.py; integer multiply-high instead of the XU-pipe float->int path).
-    int mn = q1(0), mx = mn;
-#pragma unroll
-    for (int t = 1; t < BC; ++t) {
-      mn = min(mn, q1(t));
-      mx = max(mx, q1(t));
-    }
+    // Stage 2 of this channel (R-6): z = min code, s = max(1, ceil((max - min) / (2^b - 1))), code2 =
+    // floor((2 (v - z) + s) / (2 s)).  Stage-1 rounding is monotone, so z and the max code are the codes
+    // of the channel's min / max x.  Per token pair, packed: y = F - (C1 + z) = v - z (exact), then
+    // floor(fl(y fl(1/s) + 0.5 + 2^-10)) = code2 (exact for v - z <= 238, s <= 80: tests/test_quant_arith.py),
+    // the floor by add.rm against 2^23: the low byte of the result's bits is code2.
+    const int mn = rint_prod(xmin, inv), mx = rint_prod(xmax, inv);
     const int range = mx - mn;
     const int sint = max(1, bits == 4 ? (range + 14) / 15 : (range + 2) / 3);
-    const uint32_t M = 0xFFFFFFFFu / (uint32_t)(2 * sint) + 1u;  // ceil(2^32 / 2s)
-    auto q = [&](int t) -> uint32_t { return __umulhi((uint32_t)(2 * (q1(t) - mn) + sint), M); };
+    const float zf = kC1 + (float)mn, invs = __frcp_rn((float)sint);
+    const f32x2 nz2 = pk2(-zf, -zf), invs2 = pk2(invs, invs), half2c = pk2(0.5f + 0.0009765625f, 0.5f + 0.0009765625f),
+                two23 = pk2(8388608.f, 8388608.f);
+    // stage-2 code bits of a token pair (low byte of each 32-bit half = the code)
+    // (F recomputed here with a volatile FFMA2: keeping the output pass's F values alive would spill)
+    auto Q = [&](int pr) -> f32x2 {
+      const float2 xf = __half22float2(xh[pr]);
+      f32x2 f;
+      asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(f) : "l"(pk2(xf.x, xf.y)), "l"(inv2), "l"(c12));
+      return add2_rd(fma2(add2(f, nz2), invs2, half2c), two23);
+    };
     rec[c] = (uint8_t)sint;
     rec[HD + c] = (uint8_t)(int8_t)mn;
     if (kind == 0) {
 #pragma unroll
-      for (int t = 0; t < BC; ++t) tile2[t * HD + c] = (uint8_t)q(t);
+      for (int pr = 0; pr < BC / 2; ++pr) {
+        const f32x2 qq = Q(pr);
+        tile2[(2 * pr) * HD + c] = (uint8_t)(uint32_t)qq;
+        tile2[(2 * pr + 1) * HD + c] = (uint8_t)(uint32_t)(qq >> 32);
+      }
     } else if (bits == 4) {
       // V, 4-bit, per 64-token sub-block u: word W = 4jj + qd, byte e: token 32jj + 4qd + e (lo),
-      // + 16 (hi) (layout.cuh)
+      // + 16 (hi) (layout.cuh); byte = lo + 16 hi by one LEA on the code bits
 #pragma unroll
       for (int u = 0; u < BC / kSub; ++u) {
         uint32_t w[8];
 #pragma unroll
         for (int W = 0; W < 8; ++W) {
-          const int jj = W >> 2, qd = W & 3, t0 = kSub * u + 32 * jj + 4 * qd;
-          uint32_t acc = 0;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) acc |= (q(t0 + e) | (q(t0 + 16 + e) << 4)) << (8 * e);
-          w[W] = acc;
+          const int jj = W >> 2, qd = W & 3, p0 = (kSub * u + 32 * jj + 4 * qd) / 2;
+          const f32x2 A = Q(p0), B = Q(p0 + 1), C = Q(p0 + 8), D = Q(p0 + 9);
+          w[W] = pack4_lo(((uint32_t)C << 4) + (uint32_t)A, ((uint32_t)(C >> 32) << 4) + (uint32_t)(A >> 32),
+                          ((uint32_t)D << 4) + (uint32_t)B, ((uint32_t)(D >> 32) << 4) + (uint32_t)(B >> 32));
         }
         st_global_v8(rec + 2 * HD + u * (HD * kSub / 2) + c * (kSub / 2), w);  // one full 32-byte sector
       }
@@ -244,13 +268,19 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefi
         uint32_t w[4];
 #pragma unroll
         for (int qd = 0; qd < 4; ++qd) {
-          uint32_t acc = 0;
+          uint32_t by[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
+          for (int hp = 0; hp < 2; ++hp) {  // tokens 4qd + 2hp + {0, 1} at offsets 0 / 16 / 32 / 48
+            const int p0 = (kSub * u + 4 * qd + 2 * hp) / 2;
+            const f32x2 c0 = Q(p0), c1 = Q(p0 + 8), c2 = Q(p0 + 16), c3 = Q(p0 + 24);
 #pragma unroll
-            for (int s2 = 0; s2 < 4; ++s2)
-              acc |= q(kSub * u + 32 * (s2 >> 1) + 16 * (s2 & 1) + 4 * qd + e) << (8 * e + 2 * s2);
-          w[qd] = acc;
+            for (int e = 0; e < 2; ++e) {
+              const uint32_t v0 = (uint32_t)(c0 >> (32 * e)), v1 = (uint32_t)(c1 >> (32 * e)),
+                             v2 = (uint32_t)(c2 >> (32 * e)), v3 = (uint32_t)(c3 >> (32 * e));
+              by[2 * hp + e] = (((((v3 << 2) + v2) << 2) + v1) << 2) + v0;
+            }
+          }
+          w[qd] = pack4_lo(by[0], by[1], by[2], by[3]);
         }
         *reinterpret_cast<uint4*>(rec + 2 * HD + u * (HD * kSub / 4) + c * (kSub / 4)) =
             make_uint4(w[0], w[1], w[2], w[3]);

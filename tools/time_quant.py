@@ -16,10 +16,16 @@ q, k, v = synth.qkv_torch(1002, B, N, Hq, Hkv, d)
 cache = ta.KVCache(B, Hkv, d, max_blocks=N // BC + 2, bits=synth.head_bits_alternating(Hkv), block_kv=BC)
 outs = ta.turbo_quantize_kv(p, cache, k, v)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+rd = torch.ones(64 << 20, dtype=torch.float32, device="cuda")  # 256 MB read by the 'clean' flush
+FLUSH = os.environ.get("TQ_FLUSH", "write")  # write: zero 256 MB (L2 left dirty); clean: + read 256 MB; none
 ts = []
 for i in range(23):
-    flush.zero_()
+    if FLUSH != "none":
+        flush.zero_()
+    if FLUSH == "clean":
+        rd.sum()  # evicts the dirty flush lines (written back here, outside the timed region)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda._sleep(2_000_000)  # ~1 ms of GPU work: the host enqueues the timed launches before they run
     e0.record()
     ta.turbo_quantize_kv(p, cache, k, v)
     e1.record()
@@ -28,5 +34,5 @@ for i in range(23):
         ts.append(e0.elapsed_time(e1))
 ms = sorted(ts)[len(ts) // 2]
 nbytes = 2 * k.numel() * 2 + k.numel() + 2 * v.numel() + cache.records().numel()
-print(f"{os.environ.get('TURBO_LIB', 'in-tree')}: {ms * 1e3:8.1f} us  {nbytes / ms / 1e6:7.1f} GB/s  "
+print(f"{os.environ.get('TURBO_LIB', 'in-tree')} flush={FLUSH}: {ms * 1e3:8.1f} us  {nbytes / ms / 1e6:7.1f} GB/s  "
       f"checksum {sum(int(x.double().abs().sum().item()) for x in outs[:2])} {int(cache.records().double().sum().item())}")
