@@ -108,7 +108,9 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefi
     const __half* __restrict__ k, const __half* __restrict__ v, int N, int Hkv, int max_blocks, int j0, int Nk,
     const int32_t* __restrict__ bits_dev, uint8_t* __restrict__ block_rec, float* __restrict__ s_parent,
     float* __restrict__ a_univ, __half* __restrict__ k1, __half* __restrict__ v1t, float* __restrict__ k1s,
-    float* __restrict__ v1s, int scale_fp16, int t0, int Nin) {
+    float* __restrict__ v1s, int scale_fp16, int t0, int Nin, int8_t* __restrict__ zbuf, int32_t* __restrict__ counters) {
+  // zbuf != NULL (PREFILL of a whole number of blocks): the slot's INT8 buffer is zeroed by its block-0 CTA and the
+  // counters are set here -- no buffer memset and no quant_tail_kernel launch (the tail is empty).
   constexpr int NW = HD / 32;  // warps
   // One CTA per (block, kv head, batch, K or V): 6 small CTAs per SM keep more loads in
   // flight than 3 CTAs doing K and V together.  The block (FP16 [64][HD]) is staged with
@@ -127,6 +129,14 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefi
   const int Tc = (Nk + BC - 1) / BC;
   const int rows = min(BC, N - j * BC);
   const size_t bh = (size_t)b * Hkv + h;
+  if (zbuf != nullptr && j == 0) {
+    uint4* z = reinterpret_cast<uint4*>(zbuf + (bh * 2 + kind) * (size_t)(BC * HD));
+    for (int i = tid; i < BC * HD / 16; i += HD) z[i] = make_uint4(0, 0, 0, 0);
+    if (h == 0 && kind == 0 && tid == 0) {
+      counters[b * 2 + 0] = j0 + N / BC;
+      counters[b * 2 + 1] = 0;
+    }
+  }
   {
     constexpr int C8 = HD / 8;  // 16-byte chunks per token row
     const __half* src = kind ? v : k;
@@ -580,9 +590,13 @@ static void quant_prefill_hd(const turbo_kv_cache_t* c, const __half* k, const _
                              int t0, int Nin) {
   const int B = c->batch, H = c->n_kv_heads, Tc = (N + BC - 1) / BC;
   dim3 grid(Tc, H, 2 * B);  // z = 2 b + (K, V)
+  // PREFILL of whole blocks (no tail): the kernel zeroes the buffer and sets the counters itself
+  const bool whole = Nk == N && j0 == 0 && t0 == 0 && N % BC == 0;
   quant_prefill_kernel<HD, BC><<<grid, HD, 0, st>>>(k, v, N, H, c->max_blocks, j0, Nk, c->bits_dev, c->block_rec,
-                                                   c->s_parent, c->a_univ, k1, v1t, k1s, v1s, scale_fp16, t0, Nin);
-  quant_tail_kernel<HD, BC><<<dim3(H, B), 256, 0, st>>>(k, v, N, H, c->a_univ, c->buf, c->counters, j0, t0, Nin);
+                                                   c->s_parent, c->a_univ, k1, v1t, k1s, v1s, scale_fp16, t0, Nin,
+                                                   whole ? c->buf : nullptr, c->counters);
+  if (!whole)
+    quant_tail_kernel<HD, BC><<<dim3(H, B), 256, 0, st>>>(k, v, N, H, c->a_univ, c->buf, c->counters, j0, t0, Nin);
 }
 
 cudaError_t launch_quant_prefill(const turbo_kv_cache_t* c, const __half* k, const __half* v, int N, __half* k1,
@@ -597,8 +611,10 @@ cudaError_t launch_quant_prefill(const turbo_kv_cache_t* c, const __half* k, con
   if (Nk == N) {  // PREFILL (no cached tokens before)
     e = cudaMemsetAsync(c->a_univ, 0, sizeof(float) * B * H * 2, st);
     if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(c->buf, 0, (size_t)B * H * 2 * BC * HD, st);
-    if (e != cudaSuccess) return e;
+    if (N % BC != 0) {  // (a whole number of blocks: quant_prefill_kernel zeroes the buffer)
+      e = cudaMemsetAsync(c->buf, 0, (size_t)B * H * 2 * BC * HD, st);
+      if (e != cudaSuccess) return e;
+    }
   }
   int t0 = 0;
   const int nbuf = (Nk - N) - j0 * BC;  // buffered tokens before the chunk (R-31)

@@ -558,3 +558,56 @@ def test_decode_large_gqa_groups(ta, Hq, Hkv, d, S):
                 ro, rl = O.combine(np.stack([x[0] for x in parts]), np.array([x[1] for x in parts]))
             assert_out_close(o[b, hq], ro, f"b{b} h{hq}")
             np.testing.assert_allclose(lse[b, hq], rl, atol=1e-4, rtol=1e-5)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_prefill_whole_blocks_resets_a_used_cache(ta, d):
+    """A PREFILL of a whole number of B_c blocks writes the buffer and the counters inside
+    quant_prefill_kernel (no memset, no tail launch): on a cache that already holds a buffered
+    tail and appended tokens, the buffer must come back all zero, the counters (N / B_c, 0), the
+    universal scales and records those of the new prefill, and an append + decode must match the
+    oracle (P:448-453, Alg. 2)."""
+    B, Hq, Hkv = 2, 8, 2
+    G = Hq // Hkv
+    bits = synth.head_bits_alternating(Hkv)
+    p = ta.params(head_dim=d)
+    op = O.params(d=d)
+    cache = ta.KVCache(B, Hkv, d, max_blocks=8, bits=bits)
+    _, k0, v0 = synth.qkv(41, B, 200, Hq, Hkv, d)  # 3 blocks + an 8-token buffered tail
+    ta.turbo_quantize_kv(p, cache, torch.from_numpy(k0).cuda(), torch.from_numpy(v0).cuda())
+    for t in range(5):
+        _, kt, vt = synth.decode_token(600 + t, B, Hq, Hkv, d)
+        ta.turbo_quantize_kv(p, cache, torch.from_numpy(kt).cuda(), torch.from_numpy(vt).cuda(), mode=1)
+    torch.cuda.synchronize()
+    assert cache.buf.abs().sum().item() > 0
+    N = 256
+    q, k, v = synth.qkv(43, B, N, Hq, Hkv, d)
+    ta.turbo_quantize_kv(p, cache, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    torch.cuda.synchronize()
+    assert not cache.buf.any().item()
+    np.testing.assert_array_equal(cache.counters.view(B, 2).cpu().numpy(), [[N // 64, 0]] * B)
+    ref = O.build_cache(op, k.astype(np.float32), v.astype(np.float32), bits, 8)
+    a_univ = cache.a_univ.view(B, Hkv, 2).cpu().numpy()
+    recs = cache.records().cpu().numpy()
+    for b in range(B):
+        for h in range(Hkv):
+            for kind, sl in enumerate(ref["slots"][b][h]):
+                assert a_univ[b, h, kind] == sl.a_univ and sl.n_buf == 0
+                for j in range(sl.n_blocks):
+                    codes, s_int, z_int = cache_layout.unpack_record(recs[b, h, kind, j], d, int(bits[h][kind]), kind)
+                    np.testing.assert_array_equal(codes, sl.codes[j])
+    _, kt, vt = synth.decode_token(700, B, Hq, Hkv, d)
+    ta.turbo_quantize_kv(p, cache, torch.from_numpy(kt).cuda(), torch.from_numpy(vt).cuda(), mode=1)
+    for b in range(B):
+        for h in range(Hkv):
+            ref["slots"][b][h][0].append(kt[b, h].astype(np.float32))
+            ref["slots"][b][h][1].append(vt[b, h].astype(np.float32))
+    qd, _, _ = synth.decode_token(701, B, Hq, Hkv, d)
+    o, _, lse = ta.turbo_attention_decode(p, cache, torch.from_numpy(qd).cuda(), n_splits=1)
+    torch.cuda.synchronize()
+    o, lse = o.cpu().numpy(), lse.cpu().numpy()
+    nb = ref["slots"][0][0][0].n_blocks
+    for b in range(B):
+        ro, rl = _oracle_decode(op, qd[b].astype(np.float32), ref["slots"][b], G, [(0, nb)])
+        assert_out_close(o[b], ro, f"decode b{b}")
+        np.testing.assert_allclose(lse[b], rl, atol=1e-4, rtol=1e-5)
