@@ -3,6 +3,7 @@
 // channelwise asymmetric INT4/INT2 (integer only) into packed block records,
 // the universal-scale INT8 decode buffer and its flush.
 #include <algorithm>
+#include <cstdlib>
 #include "common.cuh"
 #include "layout.cuh"
 
@@ -103,28 +104,18 @@ TA_DEV uint32_t pack_crumb8(uint2 v) {
   return (uint32_t)(x | (x >> 24)) & 0xFFFFu;
 }
 
+// One (block j, kv head h, batch b, K or V) item whose FP16 [B_c][HD] block is in xs (rows past N zero):
+// stage 1, stage 2 and every output.  All threads of the CTA (thread = channel); xs, t2s and red are reused
+// as staging, so the caller syncs before refilling them.
 template <int HD, int BC>
-__global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefill_kernel(
+TA_DEV void quant_block(__half (*xs)[HD], uint8_t* t2s, float* red, int j, int h, int b, int kind,
     const __half* __restrict__ k, const __half* __restrict__ v, int N, int Hkv, int max_blocks, int j0, int Nk,
     const int32_t* __restrict__ bits_dev, uint8_t* __restrict__ block_rec, float* __restrict__ s_parent,
     float* __restrict__ a_univ, __half* __restrict__ k1, __half* __restrict__ v1t, float* __restrict__ k1s,
     float* __restrict__ v1s, int scale_fp16, int t0, int Nin, int8_t* __restrict__ zbuf, int32_t* __restrict__ counters) {
-  // zbuf != NULL (PREFILL of a whole number of blocks): the slot's INT8 buffer is zeroed by its block-0 CTA and the
-  // counters are set here -- no buffer memset and no quant_tail_kernel launch (the tail is empty).
   constexpr int NW = HD / 32;  // warps
-  // One CTA per (block, kv head, batch, K or V): 6 small CTAs per SM keep more loads in
-  // flight than 3 CTAs doing K and V together.  The block (FP16 [64][HD]) is staged with
-  // coalesced 16-byte loads; after every thread has taken its column (the barrier of the
-  // max reduction) the space is reused for K's token-major stage-1 / stage-2 code tiles.
-  __shared__ __align__(16) __half xs[BC][HD];
-  __shared__ float red[NW];
-  // K: B_c = 64 transposes the fp16 stage-1 codes through xs (then a coalesced copy-out) and keeps the
-  // stage-2 codes in t2s; B_c = 128 (48 KB static limit) writes k1 directly and keeps the stage-2 codes
-  // in the second half of xs.
-  __shared__ __align__(16) uint8_t t2s[BC == 64 ? BC * HD : 16];
   uint8_t* tile2 = BC == 64 ? t2s : reinterpret_cast<uint8_t*>(&xs[0][0]) + BC * HD;  // K stage-2 codes [t][c]
-  const int j = blockIdx.x, h = blockIdx.y, b = blockIdx.z >> 1, kind = blockIdx.z & 1, tid = threadIdx.x;
-  const int c = tid;
+  const int tid = threadIdx.x, c = tid;
   // chunk block j is cache block j0 + j; the stage-1 outputs cover Nk tokens (Tc blocks)
   const int Tc = (Nk + BC - 1) / BC;
   const int rows = min(BC, N - j * BC);
@@ -137,20 +128,6 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefi
       counters[b * 2 + 1] = 0;
     }
   }
-  {
-    constexpr int C8 = HD / 8;  // 16-byte chunks per token row
-    const __half* src = kind ? v : k;
-#pragma unroll
-    for (int i = tid; i < BC * C8; i += HD) {
-      const int t = i / C8, c8 = i % C8;
-      uint4 val = make_uint4(0, 0, 0, 0);
-      if (t < rows)
-        val = __ldcs(reinterpret_cast<const uint4*>(src + (((size_t)b * Nin + t0 + (size_t)j * BC + t) * Hkv + h) * HD) +
-                     c8);
-      *reinterpret_cast<uint4*>(&xs[t][8 * c8]) = val;
-    }
-  }
-  __syncthreads();
   // the channel's B_c tokens as B_c / 2 half2, and the channel's min / max x (HMNMX2)
   __half2 xh[BC / 2];
   __half2 mn2 = __halves2half2(xs[0][c], xs[1][c]), mx2 = mn2;
@@ -343,6 +320,107 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefi
     }
   }
 }
+
+template <int HD, int BC>
+__global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefill_kernel(
+    const __half* __restrict__ k, const __half* __restrict__ v, int N, int Hkv, int max_blocks, int j0, int Nk,
+    const int32_t* __restrict__ bits_dev, uint8_t* __restrict__ block_rec, float* __restrict__ s_parent,
+    float* __restrict__ a_univ, __half* __restrict__ k1, __half* __restrict__ v1t, float* __restrict__ k1s,
+    float* __restrict__ v1s, int scale_fp16, int t0, int Nin, int8_t* __restrict__ zbuf, int32_t* __restrict__ counters) {
+  // zbuf != NULL (PREFILL of a whole number of blocks): the slot's INT8 buffer is zeroed by its block-0 CTA and the
+  // counters are set here -- no buffer memset and no quant_tail_kernel launch (the tail is empty).
+  constexpr int NW = HD / 32;  // warps
+  // One CTA per (block, kv head, batch, K or V): 6 small CTAs per SM keep more loads in
+  // flight than 3 CTAs doing K and V together.  The block (FP16 [64][HD]) is staged with
+  // coalesced 16-byte loads; after every thread has taken its column (the barrier of the
+  // max reduction) the space is reused for K's token-major stage-1 / stage-2 code tiles.
+  __shared__ __align__(16) __half xs[BC][HD];
+  __shared__ float red[NW];
+  // K: B_c = 64 transposes the fp16 stage-1 codes through xs (then a coalesced copy-out) and keeps the
+  // stage-2 codes in t2s; B_c = 128 (48 KB static limit) writes k1 directly and keeps the stage-2 codes
+  // in the second half of xs.
+  __shared__ __align__(16) uint8_t t2s[BC == 64 ? BC * HD : 16];
+  const int j = blockIdx.x, h = blockIdx.y, b = blockIdx.z >> 1, kind = blockIdx.z & 1, tid = threadIdx.x;
+  const int rows = min(BC, N - j * BC);
+  {
+    constexpr int C8 = HD / 8;  // 16-byte chunks per token row
+    const __half* src = kind ? v : k;
+#pragma unroll
+    for (int i = tid; i < BC * C8; i += HD) {
+      const int t = i / C8, c8 = i % C8;
+      uint4 val = make_uint4(0, 0, 0, 0);
+      if (t < rows)
+        val = __ldcs(reinterpret_cast<const uint4*>(src + (((size_t)b * Nin + t0 + (size_t)j * BC + t) * Hkv + h) * HD) +
+                     c8);
+      *reinterpret_cast<uint4*>(&xs[t][8 * c8]) = val;
+    }
+  }
+  __syncthreads();
+  quant_block<HD, BC>(xs, t2s, red, j, h, b, kind, k, v, N, Hkv, max_blocks, j0, Nk, bits_dev, block_rec, s_parent, a_univ, k1, v1t, k1s, v1s, scale_fp16, t0, Nin, zbuf, counters);
+}
+
+// Persistent: as many CTAs as fit (B_c = 64: 5 per SM, 128: 3) walk the items (kv head fastest) with the FP16
+// block of the next item already on its way -- one TMA tile load ([B_c tokens][HD], the rows of one head) into
+// the second buffer of a double buffer -- while the current item is quantised.
+template <int HD, int BC>
+constexpr size_t quant_tma_smem() { return 2 * BC * HD * 2 + (BC == 64 ? BC * HD : 0) + 64; }
+template <int HD, int BC>
+__global__ void __launch_bounds__(HD, (BC == 64 ? 5 : 3) * 128 / HD) quant_prefill_tma_kernel(
+    const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv, int n_items, int Tcn,
+    const __half* __restrict__ k, const __half* __restrict__ v, int N, int Hkv, int max_blocks, int j0, int Nk,
+    const int32_t* __restrict__ bits_dev, uint8_t* __restrict__ block_rec, float* __restrict__ s_parent,
+    float* __restrict__ a_univ, __half* __restrict__ k1, __half* __restrict__ v1t, float* __restrict__ k1s,
+    float* __restrict__ v1s, int scale_fp16, int t0, int Nin, int8_t* __restrict__ zbuf, int32_t* __restrict__ counters) {
+  extern __shared__ __align__(128) uint8_t qsm[];
+  __half(*xs2)[BC][HD] = reinterpret_cast<__half(*)[BC][HD]>(qsm);  // [2][B_c][HD]
+  uint8_t* t2s = qsm + 2 * BC * HD * 2;                                // B_c = 64: K stage-2 codes
+  float* red = reinterpret_cast<float*>(t2s + (BC == 64 ? BC * HD : 0));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 8);
+  const int tid = threadIdx.x;
+  auto item = [&](int it, int& j, int& h, int& b, int& kind) {
+    h = it % Hkv;
+    const int r = it / Hkv;
+    j = r % Tcn;
+    kind = (r / Tcn) & 1;
+    b = (r / Tcn) >> 1;
+  };
+  auto issue = [&](int it, int st) {
+    int j, h, b, kind;
+    item(it, j, h, b, kind);
+    mbar_expect_tx(&bar[st], BC * HD * 2);  // (rows past the input are zero-filled and counted)
+    tma_load_3d(&xs2[st][0][0], kind ? (const void*)&tmv : (const void*)&tmk, &bar[st], 0, h, b * Nin + t0 + j * BC);
+  };
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if ((int)blockIdx.x < n_items) issue(blockIdx.x, 0);
+    if ((int)(blockIdx.x + gridDim.x) < n_items) issue(blockIdx.x + gridDim.x, 1);
+  }
+  int i = 0;
+  for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++i) {
+    const int st = i & 1;
+    int j, h, b, kind;
+    item(it, j, h, b, kind);
+    mbar_wait(&bar[st], (i >> 1) & 1);
+    const int rows = min(BC, N - j * BC);
+    if (rows < BC) {  // the tile reaches past the sequence: zero those rows
+      for (int e = tid; e < (BC - rows) * HD / 8; e += HD)
+        reinterpret_cast<uint4*>(&xs2[st][rows][0])[e] = make_uint4(0, 0, 0, 0);
+      __syncthreads();
+    }
+    quant_block<HD, BC>(xs2[st], t2s, red, j, h, b, kind, k, v, N, Hkv, max_blocks, j0, Nk, bits_dev, block_rec, s_parent, a_univ, k1, v1t, k1s, v1s, scale_fp16, t0, Nin, zbuf, counters);
+    __syncthreads();  // xs2[st], t2s and red are free again
+    if (tid == 0 && it + 2 * (int)gridDim.x < n_items) {
+      fence_proxy_async();  // the generic-proxy staging writes precede the async-proxy refill
+      issue(it + 2 * gridDim.x, st);
+    }
+  }
+}
+
 
 // Tail (N mod B_c tokens) -> INT8 buffer with the universal scale (R-11);
 // sets the counters.  One CTA per (kv_head, batch), thread = channel x kind.
@@ -584,6 +662,29 @@ static void quant_boundary_hd(const turbo_kv_cache_t* c, const __half* k, const 
   boundary_counters_kernel<<<(c->batch + 127) / 128, 128, 0, st>>>(c->counters, c->batch, BC, r);
 }
 
+typedef CUresult (*EncodeTiledQFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+// FP16 K or V input [tokens][Hkv][HD] as a 3-D map (HD, Hkv, tokens); box = the B_c rows of one head.
+static bool make_rows_map(CUtensorMap* m, const __half* base, int HD, int H, uint64_t tokens, int BC) {
+  static EncodeTiledQFn enc = nullptr;
+  if (!enc) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return false;
+    enc = reinterpret_cast<EncodeTiledQFn>(fn);
+  }
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)HD, (cuuint64_t)H, tokens};
+  cuuint64_t strides[2] = {(cuuint64_t)HD * 2, (cuuint64_t)H * HD * 2};
+  cuuint32_t box[3] = {(cuuint32_t)HD, 1, (cuuint32_t)BC};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<__half*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int HD, int BC>
 static void quant_prefill_hd(const turbo_kv_cache_t* c, const __half* k, const __half* v, int N, __half* k1,
                              __half* v1t, float* k1s, float* v1s, cudaStream_t st, int j0, int Nk, int scale_fp16,
@@ -592,9 +693,30 @@ static void quant_prefill_hd(const turbo_kv_cache_t* c, const __half* k, const _
   dim3 grid(Tc, H, 2 * B);  // z = 2 b + (K, V)
   // PREFILL of whole blocks (no tail): the kernel zeroes the buffer and sets the counters itself
   const bool whole = Nk == N && j0 == 0 && t0 == 0 && N % BC == 0;
-  quant_prefill_kernel<HD, BC><<<grid, HD, 0, st>>>(k, v, N, H, c->max_blocks, j0, Nk, c->bits_dev, c->block_rec,
-                                                   c->s_parent, c->a_univ, k1, v1t, k1s, v1s, scale_fp16, t0, Nin,
-                                                   whole ? c->buf : nullptr, c->counters);
+  int8_t* zbuf = whole ? c->buf : nullptr;
+  CUtensorMap tmk, tmv;
+  if (!getenv("TURBO_QUANT_NOTMA") && make_rows_map(&tmk, k, HD, H, (uint64_t)B * Nin, BC) &&
+      make_rows_map(&tmv, v, HD, H, (uint64_t)B * Nin, BC)) {
+    constexpr size_t smem = quant_tma_smem<HD, BC>();
+    static int per_sm = -1, sms = 0;
+    if (per_sm < 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaFuncSetAttribute(quant_prefill_tma_kernel<HD, BC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, quant_prefill_tma_kernel<HD, BC>, HD, smem);
+    }
+    const int n_items = Tc * H * 2 * B;
+    const int ctas = std::max(1, std::min(n_items, sms * std::max(1, per_sm)));
+    quant_prefill_tma_kernel<HD, BC><<<ctas, HD, smem, st>>>(tmk, tmv, n_items, Tc, k, v, N, H, c->max_blocks, j0,
+                                                             Nk, c->bits_dev, c->block_rec, c->s_parent, c->a_univ,
+                                                             k1, v1t, k1s, v1s, scale_fp16, t0, Nin, zbuf,
+                                                             c->counters);
+  } else {
+    quant_prefill_kernel<HD, BC><<<grid, HD, 0, st>>>(k, v, N, H, c->max_blocks, j0, Nk, c->bits_dev, c->block_rec,
+                                                     c->s_parent, c->a_univ, k1, v1t, k1s, v1s, scale_fp16, t0, Nin,
+                                                     zbuf, c->counters);
+  }
   if (!whole)
     quant_tail_kernel<HD, BC><<<dim3(H, B), 256, 0, st>>>(k, v, N, H, c->a_univ, c->buf, c->counters, j0, t0, Nin);
 }
