@@ -1,5 +1,5 @@
 #!/bin/bash
-# A/B of decode variant libraries on the G = 8 (general-path) shapes: tools/gpu_abg8.sh lib1 lib2 ...
+# A/B of decode variant libraries on the G = 8 (general-path) shapes: tools/gpu_ab_g8.sh lib1 lib2 ...
 for lib in "$@"; do
   echo "== $lib"
   TURBO_LIB=$lib DEC_SHAPES="16,32768,64,8,128;8,32768,64,8,128;64,8192,64,8,128;1,131072,64,8,128" \
