@@ -233,9 +233,40 @@ TA_DEV void qk_block(uint32_t rec, const int (&qv)[HD / 4], const uint4 (&q1r)[H
     lds_words<U::NW>(t0, w0);  // one vector load per token region
     lds_words<U::NW>(t1, w1);
     int ch[4] = {0, 0, 0, 0}, cl[4] = {0, 0, 0, 0};
+    if (!PACK) {
+      // General path (G > 4, issue-bound): the IMMAs accumulate in place.  4-bit: the low-nibble units
+      // straight into ch / cl, the high-nibble units (codes x 16) into a second pair, shifted back once;
+      // 2-bit: the code words are shifted down first, so every unit has scale 1.
+      int ch16[4] = {0, 0, 0, 0}, cl16[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int u = 0; u < U::N; ++u) {
+        uint32_t af[4];
+        const int sh = BK == 4 ? 0 : U::shift(u);
+        const uint32_t mk = BK == 4 ? U::mask(u) : 0x03030303u;
+        af[0] = (w0[U::word(u, 0)] >> sh) & mk;
+        af[1] = (w1[U::word(u, 0)] >> sh) & mk;
+        af[2] = U::chan(u, 1, 0) < 0 ? 0u : (w0[U::word(u, 1) < U::NW ? U::word(u, 1) : 0] >> sh) & mk;
+        af[3] = U::chan(u, 1, 0) < 0 ? 0u : (w1[U::word(u, 1) < U::NW ? U::word(u, 1) : 0] >> sh) & mk;
+        const uint32_t bh[2] = {bhi[u][0], bhi[u][1]}, bl[2] = {blo[u][0], blo[u][1]};
+        if (BK == 4 && U::shift(u) != 0) {
+          imma_u8s8(ch16, af, bh);
+          imma_u8s8(cl16, af, bl);
+        } else {
+          imma_u8s8(ch, af, bh);
+          imma_u8s8(cl, af, bl);
+        }
+      }
+      if (BK == 4) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          ch[i] += ch16[i] >> 4;  // exact: a multiple of 16
+          cl[i] += cl16[i] >> 4;
+        }
+      }
+    } else {
 #pragma unroll
     for (int u = 0; u < U::N; ++u) {
-      int cu[4] = {0, 0, 0, 0}, cv[4] = {0, 0, 0, 0};
+      int cu[4] = {0, 0, 0, 0};
       uint32_t af[4];
       const uint32_t mk = U::mask(u);
       af[0] = w0[U::word(u, 0)] & mk;
@@ -244,15 +275,9 @@ TA_DEV void qk_block(uint32_t rec, const int (&qv)[HD / 4], const uint4 (&q1r)[H
       af[3] = U::chan(u, 1, 0) < 0 ? 0u : w1[U::word(u, 1) < U::NW ? U::word(u, 1) : 0] & mk;
       const uint32_t bh[2] = {bhi[u][0], bhi[u][1]};
       imma_u8s8(cu, af, bh);
-      if (!PACK) {
-        const uint32_t bl[2] = {blo[u][0], blo[u][1]};
-        imma_u8s8(cv, af, bl);
-      }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        ch[i] += cu[i] >> U::shift(u);  // exact: acc_u is a multiple of its scale
-        if (!PACK) cl[i] += cv[i] >> U::shift(u);
-      }
+      for (int i = 0; i < 4; ++i) ch[i] += cu[i] >> U::shift(u);  // exact: acc_u is a multiple of its scale
+    }
     }
     if (PACK) {
       // exchange hi / lo halves between lane quads q and q ^ 2
@@ -435,10 +460,14 @@ TA_DEV void pv_block(uint32_t rec, const int8_t* vb, uint32_t pbuf, const int (&
           for (int i = 0; i < 4; ++i) af[i] = wv[i] & mk;
           // B rows of unit j: tokens (16 j + 4q..) and (32 + 16 j + 4q..)
           const uint32_t b2[2] = {j ? bf[u][0][1] : bf[u][0][0], j ? bf[u][1][1] : bf[u][1][0]};
-          int cu[4] = {0, 0, 0, 0};
-          imma_u8u8(cu, af, b2);
+          if (j == 0) {  // low nibbles: scale 1, accumulated in place
+            imma_u8u8(c, af, b2);
+          } else {
+            int cu[4] = {0, 0, 0, 0};
+            imma_u8u8(cu, af, b2);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) c[i] += cu[i] >> (4 * j);
+            for (int i = 0; i < 4; ++i) c[i] += cu[i] >> 4;
+          }
         } else {
           const int sh = 4 * j;
           af[0] = (wv[0] >> sh) & 0x03030303u;
