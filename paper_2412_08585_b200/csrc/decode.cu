@@ -234,6 +234,9 @@ TA_DEV void qk_block(uint32_t rec, const int (&qv)[HD / 4], const uint4 (&q1r)[H
     lds_words<U::NW>(t1, w1);
     int ch[4] = {0, 0, 0, 0}, cl[4] = {0, 0, 0, 0};
     if (!PACK) {
+      // (the z term starts the lo accumulators: S = 256 hi + lo + sum q1 z)
+      cl[0] = cl[2] = z0;
+      cl[1] = cl[3] = z1;
       // General path (G > 4, issue-bound): the IMMAs accumulate in place.  4-bit: the low-nibble units
       // straight into ch / cl, the high-nibble units (codes x 16) into a second pair, shifted back once;
       // 2-bit: the code words are shifted down first, so every unit has scale 1.
@@ -291,10 +294,10 @@ TA_DEV void qk_block(uint32_t rec, const int (&qv)[HD / 4], const uint4 (&q1r)[H
         sv[mt][e] = 256 * hi + lo + (e ? z1 : z0);
       }
     } else {
-      sv[2 * mt][0] = 256 * ch[0] + cl[0] + z0;
-      sv[2 * mt][1] = 256 * ch[1] + cl[1] + z1;
-      sv[2 * mt + 1][0] = 256 * ch[2] + cl[2] + z0;
-      sv[2 * mt + 1][1] = 256 * ch[3] + cl[3] + z1;
+      sv[2 * mt][0] = 256 * ch[0] + cl[0];
+      sv[2 * mt][1] = 256 * ch[1] + cl[1];
+      sv[2 * mt + 1][0] = 256 * ch[2] + cl[2];
+      sv[2 * mt + 1][1] = 256 * ch[3] + cl[3];
     }
   }
 }
@@ -384,18 +387,25 @@ TA_DEV void softmax_tile(const DecodeArgs& a, RowState<HD, PACK>& st, int (&sv)[
     // per-row P scale (Alg. 2, R-17)
     const float inv_p = pm > 0.f ? div_119_by(pm) : 0.f;
     s_p[e] = div_by_119(pm);
-    int sp = 0;
+    // P codes rne(P~ 119 / max) (R-27): two per FFMA2 against 1.5 2^23; the low byte of each result's bits is
+    // the code (stored as is) and the sum of the codes is the sum of the bits less NT x the magic's bits
+    uint32_t spb = 0;
+    const f32x2 ip2 = pk2(inv_p, inv_p), mg2 = pk2(kMagic, kMagic);
 #pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      const int c = rint_prod(pt[t], inv_p);
-      sp += c;
-      sts_u8(pbuf + row * BC + M::tok(t, g, q), (uint32_t)c);
-      if (TAP && tap && row == tap_row) {
-        a.tap.p_codes[M::tok(t, g, q)] = (uint8_t)c;
-        a.tap.s_int[M::tok(t, g, q)] = M::tok(t, g, q) < nvalid ? sv[t][e] : 0;
+    for (int t = 0; t < NT; t += 2) {
+      const f32x2 cb = fma2(pk2(pt[t], pt[t + 1]), ip2, mg2);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t bits = h ? (uint32_t)(cb >> 32) : (uint32_t)cb;
+        spb += bits;
+        sts_u8(pbuf + row * BC + M::tok(t + h, g, q), bits);
+        if (TAP && tap && row == tap_row) {
+          a.tap.p_codes[M::tok(t + h, g, q)] = (uint8_t)bits;
+          a.tap.s_int[M::tok(t + h, g, q)] = M::tok(t + h, g, q) < nvalid ? sv[t + h][e] : 0;
+        }
       }
     }
-    sum_p[e] = grp_sumi<PACK>(sp);
+    sum_p[e] = grp_sumi<PACK>((int)(spb - (uint32_t)NT * kMagicBits));
     if (TAP && tap && row == tap_row && g == 0 && (!PACK || q < 2)) {
       a.tap.m_new[0] = m_new;
       a.tap.s_p[0] = s_p[e];
@@ -592,13 +602,17 @@ TA_DEV void decode_segment(const DecodeArgs& a, DecodeSmem<HD, PACK, BC>& sm, in
   for (int c = 0; c < M::NC; ++c) st.o[c][0] = st.o[c][1] = 0.f;
 
   auto update = [&](const int (&acc)[M::NC][2], const float (&alpha)[2], const float (&cpv)[2], bool tap) {
+    // o = alpha o + cpv acc for the lane's two rows at once (FMUL2 then FFMA2: the same two roundings)
+    const f32x2 al2 = pk2(alpha[0], alpha[1]), cp2 = pk2(cpv[0], cpv[1]);
 #pragma unroll
-    for (int c = 0; c < M::NC; ++c)
+    for (int c = 0; c < M::NC; ++c) {
+      const f32x2 o2 = fma2(al2, pk2(st.o[c][0], st.o[c][1]), mul2(cp2, pk2((float)acc[c][0], (float)acc[c][1])));
+      st.o[c][0] = lo2(o2);
+      st.o[c][1] = hi2(o2);
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        st.o[c][e] = __fmaf_rn(alpha[e], st.o[c][e], cpv[e] * (float)acc[c][e]);
+      for (int e = 0; e < 2; ++e)
         if (TAP && tap && M::row(q, e) == tap_row) a.tap.pv_int[M::chan(c, g, q)] = acc[c][e];
-      }
+    }
   };
 
   for (int j = j0; j < j1; ++j) {
