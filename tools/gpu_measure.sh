@@ -16,7 +16,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --c
 NCU="ncu --set full --import-source on --clock-control none"
 timeout 900 $NCU -k regex:^prefill_kernel -c 1 -o ${o}_prefill python tools/time_prefill.py > /dev/null 2>&1
 timeout 900 $NCU -k regex:^decode_kernel -s 1 -c 1 -o ${o}_decode python tools/run_decode.py 12 2 > /dev/null 2>&1
-timeout 900 $NCU -k regex:^quant_prefill_kernel -c 2 -o ${o}_quant python tools/time_prefill.py > /dev/null 2>&1
+timeout 900 $NCU -k regex:^quant_prefill -c 2 -o ${o}_quant python tools/time_prefill.py > /dev/null 2>&1
 # the reports themselves can exceed gpurun's 64 MiB copy-back: keep the summary and the raw pages only
 python tools/ncu_summary.py ${o}_launches.csv ${o}_prefill.ncu-rep ${o}_decode.ncu-rep ${o}_quant.ncu-rep \
   > ${o}_ncu_summary.txt 2>&1

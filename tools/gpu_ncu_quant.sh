@@ -2,7 +2,7 @@
 # one ncu --set full capture of quant_prefill_kernel (configs[1]) -> gpurun_out/<tag>_quant_{raw,source}.csv + summary
 tag=${1:?tag}
 python __graft_entry__.py build > /dev/null 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:^quant_prefill_kernel -s 3 -c 1 \
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:^quant_prefill -s 3 -c 1 \
   -o gpurun_out/${tag}_quant python tools/time_quant.py > /dev/null 2>&1
 python tools/ncu_summary.py /dev/null gpurun_out/${tag}_quant.ncu-rep > gpurun_out/${tag}_quant_summary.txt 2>&1
 ncu -i gpurun_out/${tag}_quant.ncu-rep --page raw --csv > gpurun_out/${tag}_quant_raw.csv 2>/dev/null

@@ -55,6 +55,7 @@ def report(path):
 
 
 if __name__ == "__main__":
-    launches(sys.argv[1])
+    if sys.argv[1] != "/dev/null":  # (no launch list: report captures only)
+        launches(sys.argv[1])
     for p in sys.argv[2:]:
         report(p)
