@@ -337,12 +337,14 @@ def auto_splits(batch, n_kv_heads, n_blocks, workers=None):
     batch * n_kv_heads * S is closest to 4.5 waves of the resident decode warps
     (`workers`, default turbo_decode_workers for G <= 4, d = 128).  On B200 this is
     the best of a sweep on configs[2] (S = 12) and within 0.1 % on configs[4] (S = 64;
-    tools/sweep_decode.py)."""
+    tools/sweep_decode.py).  At most 128 splits: the LSE combine runs one CTA per output row, and
+    few rows with hundreds of parts each serialise it (B = 1 x 128k: S = 256 39 us, S = 128 35.5 us;
+    profiles/r2_small_batch_decode.txt)."""
     if workers is None:
         workers = reference_workers(4, 1, 128)
     bh = max(1, batch * n_kv_heads)
     best, best_err = 1, None
-    for s in range(1, max(1, n_blocks // 8) + 1):
+    for s in range(1, min(128, max(1, n_blocks // 8)) + 1):
         per = -(-n_blocks // s)
         last = n_blocks - per * (s - 1)
         if s > 1 and (last <= 0 or 4 * last < 3 * per):

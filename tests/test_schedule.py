@@ -59,10 +59,11 @@ def test_auto_splits_rule():
     assert auto_splits(16, 8, 2048, 1776) == 64   # configs[4]
     assert auto_splits(8, 8, 64, 1776) == 8       # bench step decode (capped at 8 blocks per split)
     assert auto_splits(1, 1, 7, 1776) == 1
+    assert auto_splits(1, 8, 2048, 1776) == 128   # B = 1 x 128k: at most 128 parts per combine row
     r = random.Random(3)
     for _ in range(200):
         B, H, nb, W = r.randint(1, 64), r.randint(1, 16), r.randint(0, 4096), r.randint(100, 4000)
         s = auto_splits(B, H, nb, W)
-        assert s == 1 or nb // s >= 8
+        assert s == 1 or (nb // s >= 8 and s <= 128)
         per = -(-nb // s)
         assert s == 1 or 4 * (nb - per * (s - 1)) >= 3 * per

@@ -46,7 +46,8 @@ for B, N, Hq, Hkv, d, causal in ((32, 1024, 32, 8, 128, True), (16, 2048, 32, 8,
 
 print("# decode: B, context, Hq, Hkv -> splits, us, KV GB/s (algorithmic bytes), tokens/s per layer")
 for B, N, Hq, Hkv in ((64, 4096, 40, 10), (64, 16384, 40, 10), (64, 32768, 40, 10), (16, 65536, 32, 8),
-                      (16, 131072, 32, 8), (8, 32768, 64, 8), (128, 8192, 32, 8), (1, 131072, 32, 8)):
+                      (16, 131072, 32, 8), (8, 32768, 64, 8), (16, 32768, 64, 8), (128, 8192, 32, 8),
+                      (1, 131072, 32, 8), (1, 131072, 64, 8)):
     d = 128
     bits = synth.head_bits_alternating(Hkv)
     p = ta.params(head_dim=d)
@@ -56,13 +57,13 @@ for B, N, Hq, Hkv in ((64, 4096, 40, 10), (64, 16384, 40, 10), (64, 32768, 40, 1
     del k, v
     torch.cuda.empty_cache()
     qd = synth.qkv_torch(7, B, 1, Hq, Hkv, d)[0][:, 0].contiguous()
-    S = ta.auto_splits(B, Hkv, N // 64, ta.turbo_decode_workers(Hq, Hkv, d))
+    S = ta.resolve_splits(None, B, Hq, cache)  # the binding's deterministic default (balanced for G > 4)
     ws = torch.empty(max(ta.turbo_decode_workspace_bytes(B, Hq, Hkv, d, S), 16), dtype=torch.uint8, device="cuda")
     o = torch.empty_like(qd)
     lse = torch.empty((B, Hq), dtype=torch.float32, device="cuda")
     ms = timeit(lambda: ta.turbo_attention_decode(p, cache, qd, n_splits=S, workspace=ws, o=o, lse=lse), 20)
     byt = bench.decode_bytes(B, Hkv, d, N // 64, 0, bits, Hq)
-    print(f"decode B={B:3d} ctx={N:7d} Hq={Hq} Hkv={Hkv} (G={Hq // Hkv}) S={S:3d}  {ms * 1e3:8.1f} us  "
+    print(f"decode B={B:3d} ctx={N:7d} Hq={Hq} Hkv={Hkv} (G={Hq // Hkv}) S={S:5d}  {ms * 1e3:8.1f} us  "
           f"{byt / ms / 1e6:7.1f} GB/s  {B / ms * 1e3:9.0f} tok/s", flush=True)
     del cache, qd, ws
     torch.cuda.empty_cache()
