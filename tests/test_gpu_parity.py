@@ -611,3 +611,31 @@ def test_prefill_whole_blocks_resets_a_used_cache(ta, d):
         ro, rl = _oracle_decode(op, qd[b].astype(np.float32), ref["slots"][b], G, [(0, nb)])
         assert_out_close(o[b], ro, f"decode b{b}")
         np.testing.assert_allclose(lse[b], rl, atol=1e-4, rtol=1e-5)
+
+
+@pytest.mark.parametrize("bc", [64, 128])
+def test_quantize_kv_fallback_kernel_matches_tma_kernel(ta, bc):
+    """turbo_quantize_kv runs the persistent TMA kernel; the per-block kernel (16-byte LDG staging) is the
+    fallback for inputs a tensor map cannot describe (TURBO_QUANT_NOTMA=1 forces it).  Both must write the
+    same stage-1 operands, records, scales, universal scales, buffer and counters, bit for bit."""
+    import os
+
+    B, N, Hkv, d = 2, 64 * 5 + 17, 4, 128
+    _, k, v = synth.qkv(77, B, N, Hkv, Hkv, d)
+    bits = synth.head_bits_alternating(Hkv)
+    p = ta.params(head_dim=d, block_kv=bc)
+    kt, vt = torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda()
+    outs = []
+    for force in (False, True):
+        cache = ta.KVCache(B, Hkv, d, max_blocks=N // bc + 2, bits=bits, block_kv=bc)
+        if force:
+            os.environ["TURBO_QUANT_NOTMA"] = "1"
+        try:
+            ops = ta.turbo_quantize_kv(p, cache, kt, vt)
+            torch.cuda.synchronize()
+        finally:
+            os.environ.pop("TURBO_QUANT_NOTMA", None)
+        outs.append([x.cpu() for x in ops] + [t.cpu() for t in (cache.block_rec, cache.s_parent, cache.buf,
+                                                                 cache.a_univ, cache.counters)])
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
