@@ -29,6 +29,7 @@
 // of round 1 accumulated in fp32 registers).
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -65,6 +66,7 @@ struct PrefillArgs {
   const float* k1s;
   const float* v1s;
   int B, N, Hq, Hkv, causal, block_q, alpha_mode, n_qtiles, unit_group, scale_fp16;
+  int q_prefetch;  // > 0: warp 3 prefetches into L2 the FP16 Q rows of CTA blockIdx.x + q_prefetch (a wave later)
   int Nk, q0;  // keys per sequence; absolute position of query row 0 (chunked prefill: Nk - N)
   float scale;
   SasConst sas;
@@ -119,10 +121,18 @@ __global__ void __launch_bounds__(384, 1)
   const int G = args.Hq / args.Hkv, GS = TP ? G : G / 2;
   const int units = args.B * args.Hkv * GS;
   const int UG = args.unit_group;
-  const int grp_i = (int)blockIdx.x / (UG * args.n_qtiles), rem = (int)blockIdx.x % (UG * args.n_qtiles);
-  const int UGg = min(UG, units - grp_i * UG);
-  const int it = args.n_qtiles - 1 - rem / UGg;
-  const int u = grp_i * UG + rem % UGg, b = u / (args.Hkv * GS), kvh = (u / GS) % args.Hkv, hg = u % GS;
+  // (query tile, batch, kv head, head group) of CTA number cta
+  auto unit_of = [&](int cta, int& it_, int& b_, int& kvh_, int& hg_) {
+    const int gi = cta / (UG * args.n_qtiles), rm = cta % (UG * args.n_qtiles);
+    const int ug = min(UG, units - gi * UG);
+    it_ = args.n_qtiles - 1 - rm / ug;
+    const int uu = gi * UG + rm % ug;
+    b_ = uu / (args.Hkv * GS);
+    kvh_ = (uu / GS) % args.Hkv;
+    hg_ = uu % GS;
+  };
+  int it, b, kvh, hg;
+  unit_of((int)blockIdx.x, it, b, kvh, hg);
   const int h0 = kvh * G + hg * (TP ? 1 : 2);
   const int N = args.N, Tc = (args.Nk + BC - 1) / BC;  // N query rows, Tc key tiles (B_c keys each)
   auto tile_of = [&](int s) { return TP ? 2 * it + s : it; };
@@ -173,6 +183,25 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
           for (int u = 0; u < BC / 64; ++u)  // V^T: one [HD][64] box per 64 keys
             tma_load_3d(sm.v[st] + u * HD * 64, &tm_v, &sm.kv_full[st], 64 * u, 0, (int)(bkv * Tc + j));
+        }
+      }
+    } else if (warp == 3) {
+      // ---------------------------------------------------------- Q prefetch (otherwise idle warp)
+      // The FP16 Q rows (2 x 128 rows of 2 d bytes) of the CTA that starts about a wave later go to L2 now,
+      // so that CTA's prologue loads hit L2 instead of waiting on HBM.
+      const int nxt = (int)blockIdx.x + args.q_prefetch;
+      if (args.q_prefetch > 0 && args.q1_in == nullptr && nxt < (int)gridDim.x) {
+        int it2, b2, kvh2, hg2;
+        unit_of(nxt, it2, b2, kvh2, hg2);
+        const int hb = kvh2 * G + hg2 * (TP ? 1 : 2);
+        for (int i = lane; i < 2 * kTileM; i += 32) {
+          const int s2 = i / kTileM, rr = i % kTileM;
+          const int row2 = (TP ? 2 * it2 + s2 : it2) * kTileM + rr, h2 = TP ? hb : hb + s2;
+          if (row2 < N)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                             args.q + (((size_t)b2 * N + row2) * args.Hq + h2) * HD),
+                         "r"(HD * 2)
+                         : "memory");
         }
       }
     } else if (warp == 1 || warp == 2) {
@@ -634,6 +663,16 @@ cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Nk, int Hq
   const int G = Hq / Hkv;
   const bool pair = (G % 2) == 0;  // slots = two heads of a GQA group, else two adjacent query tiles
   a.n_qtiles = (N + kTileM - 1) / kTileM;
+  {
+    static int sms = 0;
+    if (sms == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    a.q_prefetch = sms;  // one CTA per SM: the CTA a wave later
+    if (const char* e = getenv("TURBO_PREFILL_QPF")) a.q_prefetch = atoi(e) * sms / 4;  // A/B: quarter waves
+  }
   if (!pair) a.n_qtiles = (a.n_qtiles + 1) / 2;
   a.scale = p->softmax_scale;
   fill_sas_const(&a.sas, p->sas_nr);
