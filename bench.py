@@ -351,7 +351,7 @@ def run_ours(args, rank, world, device):
                          "peak_source": f"148 SMs x 128 FP32-pipe element-ops/clk / 13 per score element x "
                                         f"{sm_hz:.0f} MHz x 512 ops per element (DESIGN.md 7)",
                          "measured_mix_ceiling_tops": 745.0}
-    # quantize_kv (a1/a2) as its own HBM-bound kernel: FP16 K, V in; k1 (INT8), v1t (FP16 codes), records,
+    # quantize_kv (a1/a2) as its own HBM-bound kernel: FP16 K, V in; k1 and v1t (stage-1 codes carried in FP16), records,
     # scales out
     q_ms = statistics.mean(t_quant)
     rec_b = B * Hkv * (N // 64) * sum(2 * d + 64 * d * int(bits[h][kd]) // 8 for h in range(Hkv) for kd in range(2)) // Hkv
