@@ -321,6 +321,228 @@ TA_DEV void quant_block(__half (*xs)[HD], uint8_t* t2s, float* red, int j, int h
   }
 }
 
+// B_c = 64 item body of the TMA kernel with thread = (channel pair p, token half hf): one 4-byte shared load gives
+// a token's two channels (a half2), so the per-token work (min / max, stage-1 FFMA2, stage 2) runs on channel
+// pairs, k^1 is stored straight from registers (4 bytes per token and thread) and the K stage-2 codes go to
+// shared memory two at a time.  Half 1 of a warp takes the pairs of the neighbouring warp, so the two
+// half-warps read disjoint banks.  The per-channel min / max of the two halves meet in `xch`; the 2-bit V record
+// words, whose bytes mix both halves, are OR-ed through the (then unused) K stage-2 tile.  Outputs are
+// bit-identical to quant_block (tests/test_gpu_parity.py::test_quantize_kv_fallback_kernel_matches_tma_kernel).
+template <int HD>
+TA_DEV void quant_block_cp(__half (*xs)[HD], uint8_t* t2s, uint32_t* xch, float* red, int j, int h, int b, int kind,
+    const __half* __restrict__ k, const __half* __restrict__ v, int N, int Hkv, int max_blocks, int j0, int Nk,
+    const int32_t* __restrict__ bits_dev, uint8_t* __restrict__ block_rec, float* __restrict__ s_parent,
+    float* __restrict__ a_univ, __half* __restrict__ k1, __half* __restrict__ v1t, float* __restrict__ k1s,
+    float* __restrict__ v1s, int scale_fp16, int t0, int Nin, int8_t* __restrict__ zbuf, int32_t* __restrict__ counters) {
+  constexpr int BC = 64, NW = HD / 32, NP = HD / 2;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, hf = lane >> 4;
+  const int p = 16 * (hf ? (w ^ 1) : w) + (lane & 15), c0 = 2 * p;
+  const int Tc = (Nk + BC - 1) / BC;
+  const int rows = min(BC, N - j * BC);
+  const size_t bh = (size_t)b * Hkv + h;
+  if (zbuf != nullptr && j == 0) {
+    uint4* z = reinterpret_cast<uint4*>(zbuf + (bh * 2 + kind) * (size_t)(BC * HD));
+    for (int i = tid; i < BC * HD / 16; i += HD) z[i] = make_uint4(0, 0, 0, 0);
+    if (h == 0 && kind == 0 && tid == 0) {
+      counters[b * 2 + 0] = j0 + N / BC;
+      counters[b * 2 + 1] = 0;
+    }
+  }
+  // my 32 tokens (32 hf + i) of channels c0, c0 + 1, and their min / max
+  __half2 x2[32];
+  x2[0] = *reinterpret_cast<const __half2*>(&xs[32 * hf][c0]);
+  __half2 mn2 = x2[0], mx2 = x2[0];
+#pragma unroll
+  for (int i = 1; i < 32; ++i) {
+    x2[i] = *reinterpret_cast<const __half2*>(&xs[32 * hf + i][c0]);
+    mn2 = __hmin2(mn2, x2[i]);
+    mx2 = __hmax2(mx2, x2[i]);
+  }
+  {
+    const float pmax = fmaxf(fmaxf(-fminf(__low2float(mn2), __high2float(mn2)), fmaxf(__low2float(mx2), __high2float(mx2))), 0.f);
+    const float wm = warp_max_nonneg(pmax);
+    if (lane == 0) red[w] = wm;
+    xch[(hf * NP + p) * 2 + 0] = *reinterpret_cast<const uint32_t*>(&mn2);
+    xch[(hf * NP + p) * 2 + 1] = *reinterpret_cast<const uint32_t*>(&mx2);
+  }
+  __syncthreads();
+  float a = red[0];
+#pragma unroll
+  for (int i = 1; i < NW; ++i) a = fmaxf(a, red[i]);
+  {
+    const uint32_t omn = xch[((hf ^ 1) * NP + p) * 2 + 0], omx = xch[((hf ^ 1) * NP + p) * 2 + 1];
+    mn2 = __hmin2(mn2, *reinterpret_cast<const __half2*>(&omn));
+    mx2 = __hmax2(mx2, *reinterpret_cast<const __half2*>(&omx));
+  }
+  // s = max|x| / 119, codes = round_half_even(x * (119 / max|x|)) (Alg. 1; R-2, R-3, R-5)
+  const float inv = a > 0.f ? div_119_by(a) : 0.f;
+  const float sc = st1_scale(div_by_119(a), scale_fp16);  // (FP16 variant: R-29; codes unchanged)
+  constexpr float kC1 = 12582912.0f + 25728.0f;  // low 16 bits of fl(x inv + C1) = binary16 of 1152 + code
+  const f32x2 inv2 = pk2(inv, inv), c12 = pk2(kC1, kC1);
+  auto F = [&](int i) -> f32x2 {
+    const float2 xf = __half22float2(x2[i]);
+    return fma2(pk2(xf.x, xf.y), inv2, c12);
+  };
+  // two stage-1 codes (magic-float bits) -> exact fp16 pair
+  auto h2of = [&](uint32_t lo, uint32_t hi) -> uint32_t {
+    const uint32_t bitsp = __byte_perm(lo, hi, 0x5410);
+    const __half2 h = __hsub2(*reinterpret_cast<const __half2*>(&bitsp), __float2half2_rn(1152.f));
+    return *reinterpret_cast<const uint32_t*>(&h);
+  };
+  if (tid == 0) {
+    (kind ? v1s : k1s)[bh * Tc + j0 + j] = sc;
+    // universal max-abs per (b, h, K/V) (R-9): non-negative floats order as ints
+    atomicMax(reinterpret_cast<int*>(a_univ + bh * 2 + kind), __float_as_int(a));
+    if (rows == BC) s_parent[(bh * 2 + kind) * max_blocks + j0 + j] = sc;
+  }
+  if (kind == 0) {
+    // k1 [N][d] fp16 codes: my two channels of each token, 4 bytes straight to global
+    uint32_t* krow = reinterpret_cast<uint32_t*>(k1 + (bh * Nk + (size_t)(j0 + j) * BC + 32 * hf) * HD + c0);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const f32x2 f = F(i);
+      if (32 * hf + i < rows) krow[(size_t)i * (HD / 2)] = h2of((uint32_t)f, (uint32_t)(f >> 32));
+    }
+  } else {
+    // v1t [d][B_c] staged in xs (every thread has taken its tokens: the barrier above) as rows of B_c halves,
+    // 16-byte chunks at position t8 ^ (p & 7) (conflict-free); copied out contiguously below
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) {
+      uint32_t lo[4], hi[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const f32x2 f0 = F(8 * q4 + 2 * m), f1 = F(8 * q4 + 2 * m + 1);
+        lo[m] = h2of((uint32_t)f0, (uint32_t)f1);
+        hi[m] = h2of((uint32_t)(f0 >> 32), (uint32_t)(f1 >> 32));
+      }
+      const int pos = (4 * hf + q4) ^ (p & 7);
+      reinterpret_cast<uint4*>(&xs[0][0])[c0 * (BC / 8) + pos] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      reinterpret_cast<uint4*>(&xs[0][0])[(c0 + 1) * (BC / 8) + pos] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    }
+  }
+  const int bits = bits_dev[h * 2 + kind];
+  constexpr int REC = rec_bytes(HD, BC);
+  uint8_t* rec = block_rec + ((bh * 2 + kind) * (size_t)max_blocks + j0 + j) * REC;
+  if (rows == BC) {
+    // Stage 2 (R-6) of both channels, as in quant_block: z / top code = the codes of min / max x,
+    // code2 = floor(fl((v - z) fl(1/s) + 0.5 + 2^-10)) by FADD2 / FFMA2 / FADD2.RM on the channel pair
+    const int mn0 = rint_prod(__low2float(mn2), inv), mx0 = rint_prod(__low2float(mx2), inv);
+    const int mn1 = rint_prod(__high2float(mn2), inv), mx1 = rint_prod(__high2float(mx2), inv);
+    const int s0 = max(1, bits == 4 ? (mx0 - mn0 + 14) / 15 : (mx0 - mn0 + 2) / 3);
+    const int s1 = max(1, bits == 4 ? (mx1 - mn1 + 14) / 15 : (mx1 - mn1 + 2) / 3);
+    const f32x2 nz2 = pk2(-(kC1 + (float)mn0), -(kC1 + (float)mn1)),
+                invs2 = pk2(__frcp_rn((float)s0), __frcp_rn((float)s1)),
+                half2c = pk2(0.5f + 0.0009765625f, 0.5f + 0.0009765625f), two23 = pk2(8388608.f, 8388608.f);
+    // (F recomputed with a volatile FFMA2: keeping the output pass's values alive would spill)
+    auto Q = [&](int i) -> f32x2 {
+      const float2 xf = __half22float2(x2[i]);
+      f32x2 f;
+      asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(f) : "l"(pk2(xf.x, xf.y)), "l"(inv2), "l"(c12));
+      return add2_rd(fma2(add2(f, nz2), invs2, half2c), two23);
+    };
+    if (hf == 0) {
+      rec[c0] = (uint8_t)s0;
+      rec[c0 + 1] = (uint8_t)s1;
+      rec[HD + c0] = (uint8_t)(int8_t)mn0;
+      rec[HD + c0 + 1] = (uint8_t)(int8_t)mn1;
+    }
+    if (kind == 0) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const f32x2 q = Q(i);
+        *reinterpret_cast<uint16_t*>(t2s + (32 * hf + i) * HD + c0) =
+            (uint16_t)__byte_perm((uint32_t)q, (uint32_t)(q >> 32), 0x0040);
+      }
+    } else if (bits == 4) {
+      // word W = 4 hf + qd, byte e: token 32 hf + 4 qd + e (lo nibble), + 16 (hi nibble) (layout.cuh)
+      uint32_t wl[4], wh[4];
+#pragma unroll
+      for (int qd = 0; qd < 4; ++qd) {
+        uint32_t bl[4], bhh[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const f32x2 qa = Q(4 * qd + e), qb = Q(4 * qd + 16 + e);
+          bl[e] = ((uint32_t)qb << 4) + (uint32_t)qa;
+          bhh[e] = ((uint32_t)(qb >> 32) << 4) + (uint32_t)(qa >> 32);
+        }
+        wl[qd] = pack4_lo(bl[0], bl[1], bl[2], bl[3]);
+        wh[qd] = pack4_lo(bhh[0], bhh[1], bhh[2], bhh[3]);
+      }
+      *reinterpret_cast<uint4*>(rec + 2 * HD + c0 * (kSub / 2) + 16 * hf) = make_uint4(wl[0], wl[1], wl[2], wl[3]);
+      *reinterpret_cast<uint4*>(rec + 2 * HD + (c0 + 1) * (kSub / 2) + 16 * hf) = make_uint4(wh[0], wh[1], wh[2], wh[3]);
+    } else {
+      // word qd, byte e, bits 2s: token 32 (s >> 1) + 16 (s & 1) + 4 qd + e -- half hf holds s = 2 hf, 2 hf + 1
+      uint32_t wl[4], wh[4];
+#pragma unroll
+      for (int qd = 0; qd < 4; ++qd) {
+        uint32_t bl[4], bhh[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const f32x2 qa = Q(4 * qd + e), qb = Q(16 + 4 * qd + e);
+          bl[e] = ((((uint32_t)qb << 2) + (uint32_t)qa) & 0xFu) << (4 * hf);
+          bhh[e] = ((((uint32_t)(qb >> 32) << 2) + (uint32_t)(qa >> 32)) & 0xFu) << (4 * hf);
+        }
+        wl[qd] = pack4_lo(bl[0], bl[1], bl[2], bl[3]);
+        wh[qd] = pack4_lo(bhh[0], bhh[1], bhh[2], bhh[3]);
+      }
+      uint32_t* xw = reinterpret_cast<uint32_t*>(t2s);  // [d][4] words of the upper half (unused by V otherwise)
+      if (hf == 1) {
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd) {
+          xw[c0 * 4 + qd] = wl[qd];
+          xw[(c0 + 1) * 4 + qd] = wh[qd];
+        }
+      }
+      __syncthreads();
+      if (hf == 0) {
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd) {
+          wl[qd] |= xw[c0 * 4 + qd];
+          wh[qd] |= xw[(c0 + 1) * 4 + qd];
+        }
+        *reinterpret_cast<uint4*>(rec + 2 * HD + c0 * (kSub / 4)) = make_uint4(wl[0], wl[1], wl[2], wl[3]);
+        *reinterpret_cast<uint4*>(rec + 2 * HD + (c0 + 1) * (kSub / 4)) = make_uint4(wh[0], wh[1], wh[2], wh[3]);
+      }
+    }
+  }
+  __syncthreads();
+  if (kind == 1) {  // V: copy the staged v1t tile out
+    const uint4* tile = reinterpret_cast<const uint4*>(&xs[0][0]);
+    uint4* dst = reinterpret_cast<uint4*>(v1t + (bh * Tc + j0 + j) * HD * BC);
+#pragma unroll
+    for (int i = tid; i < HD * BC / 8; i += HD) {
+      const int r = i / (BC / 8), k8 = i % (BC / 8);
+      dst[i] = tile[r * (BC / 8) + (k8 ^ ((r >> 1) & 7))];
+    }
+    return;
+  }
+  if (rows < BC) return;  // partial tail block: goes to the buffer (tail kernel)
+  // K record codes from the stage-2 tile t2s [t][c] (token-major, natural channel order, LSB-first)
+  const int kbits = bits_dev[h * 2];
+  uint8_t* krec = block_rec + ((bh * 2) * (size_t)max_blocks + j0 + j) * REC + 2 * HD;
+  if (kbits == 4) {
+    for (int i = tid; i < BC * HD / 32; i += HD) {  // 32 channels (16 B of codes) per item
+      const int t = i / (HD / 32), c32 = i % (HD / 32);
+      const uint4 lo = *reinterpret_cast<const uint4*>(t2s + t * HD + c32 * 32);
+      const uint4 hi = *reinterpret_cast<const uint4*>(t2s + t * HD + c32 * 32 + 16);
+      *reinterpret_cast<uint4*>(krec + t * (HD / 2) + c32 * 16) =
+          make_uint4(pack_nib8(make_uint2(lo.x, lo.y)), pack_nib8(make_uint2(lo.z, lo.w)),
+                     pack_nib8(make_uint2(hi.x, hi.y)), pack_nib8(make_uint2(hi.z, hi.w)));
+    }
+  } else {
+    for (int i = tid; i < BC * HD / 64; i += HD) {  // 64 channels (16 B of codes) per item
+      const int t = i / (HD / 64), c64 = i % (HD / 64);
+      uint32_t wv[4];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const uint4 u = *reinterpret_cast<const uint4*>(t2s + t * HD + c64 * 64 + g * 16);
+        wv[g] = pack_crumb8(make_uint2(u.x, u.y)) | (pack_crumb8(make_uint2(u.z, u.w)) << 16);
+      }
+      *reinterpret_cast<uint4*>(krec + t * (HD / 4) + c64 * 16) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+    }
+  }
+}
+
 template <int HD, int BC>
 __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefill_kernel(
     const __half* __restrict__ k, const __half* __restrict__ v, int N, int Hkv, int max_blocks, int j0, int Nk,
@@ -363,7 +585,7 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefi
 // block of the next item already on its way -- one TMA tile load ([B_c tokens][HD], the rows of one head) into
 // the second buffer of a double buffer -- while the current item is quantised.
 template <int HD, int BC>
-constexpr size_t quant_tma_smem() { return 2 * BC * HD * 2 + (BC == 64 ? BC * HD : 0) + 64; }
+constexpr size_t quant_tma_smem() { return 2 * BC * HD * 2 + (BC == 64 ? BC * HD + HD * 8 : 0) + 64; }
 template <int HD, int BC>
 __global__ void __launch_bounds__(HD, (BC == 64 ? 5 : 3) * 128 / HD) quant_prefill_tma_kernel(
     const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv, int n_items, int Tcn,
@@ -374,7 +596,8 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 5 : 3) * 128 / HD) quant_prefi
   extern __shared__ __align__(128) uint8_t qsm[];
   __half(*xs2)[BC][HD] = reinterpret_cast<__half(*)[BC][HD]>(qsm);  // [2][B_c][HD]
   uint8_t* t2s = qsm + 2 * BC * HD * 2;                                // B_c = 64: K stage-2 codes
-  float* red = reinterpret_cast<float*>(t2s + (BC == 64 ? BC * HD : 0));
+  uint32_t* xch = reinterpret_cast<uint32_t*>(t2s + (BC == 64 ? BC * HD : 0));  // B_c = 64: [2][HD / 2][2] min / max
+  float* red = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(xch) + (BC == 64 ? HD * 8 : 0));
   uint64_t* bar = reinterpret_cast<uint64_t*>(red + 8);
   const int tid = threadIdx.x;
   auto item = [&](int it, int& j, int& h, int& b, int& kind) {
@@ -412,8 +635,13 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 5 : 3) * 128 / HD) quant_prefi
         reinterpret_cast<uint4*>(&xs2[st][rows][0])[e] = make_uint4(0, 0, 0, 0);
       __syncthreads();
     }
-    quant_block<HD, BC>(xs2[st], t2s, red, j, h, b, kind, k, v, N, Hkv, max_blocks, j0, Nk, bits_dev, block_rec, s_parent, a_univ, k1, v1t, k1s, v1s, scale_fp16, t0, Nin, zbuf, counters);
-    __syncthreads();  // xs2[st], t2s and red are free again
+    if constexpr (BC == 64)
+      quant_block_cp<HD>(xs2[st], t2s, xch, red, j, h, b, kind, k, v, N, Hkv, max_blocks, j0, Nk, bits_dev, block_rec,
+                         s_parent, a_univ, k1, v1t, k1s, v1s, scale_fp16, t0, Nin, zbuf, counters);
+    else
+      quant_block<HD, BC>(xs2[st], t2s, red, j, h, b, kind, k, v, N, Hkv, max_blocks, j0, Nk, bits_dev, block_rec,
+                          s_parent, a_univ, k1, v1t, k1s, v1s, scale_fp16, t0, Nin, zbuf, counters);
+    __syncthreads();  // xs2[st], t2s, xch and red are free again
     if (tid == 0 && it + 2 * (int)gridDim.x < n_items) {
       fence_proxy_async();  // the generic-proxy staging writes precede the async-proxy refill
       issue(it + 2 * gridDim.x, st);
