@@ -395,17 +395,106 @@ TA_DEV void quant_block_cp(__half (*xs)[HD], uint8_t* t2s, uint32_t* xch, float*
     atomicMax(reinterpret_cast<int*>(a_univ + bh * 2 + kind), __float_as_int(a));
     if (rows == BC) s_parent[(bh * 2 + kind) * max_blocks + j0 + j] = sc;
   }
-  if (kind == 0) {
-    // k1 [N][d] fp16 codes: my two channels of each token, 4 bytes straight to global
-    uint32_t* krow = reinterpret_cast<uint32_t*>(k1 + (bh * Nk + (size_t)(j0 + j) * BC + 32 * hf) * HD + c0);
+  const int bits = bits_dev[h * 2 + kind];
+  constexpr int REC = rec_bytes(HD, BC);
+  uint8_t* rec = block_rec + ((bh * 2 + kind) * (size_t)max_blocks + j0 + j) * REC;
+  uint32_t* krow = reinterpret_cast<uint32_t*>(k1 + (bh * Nk + (size_t)(j0 + j) * BC + 32 * hf) * HD + c0);
+  uint4* vst = reinterpret_cast<uint4*>(&xs[0][0]);  // v1t staging: rows of B_c halves, chunk t8 at t8 ^ (p & 7)
+  if (rows == BC) {
+    // Full block: each token's stage-1 value F is computed once and feeds k1 / v1t and stage 2 (R-6):
+    // z / top code = the codes of min / max x, code2 = floor(fl((v - z) fl(1/s) + 0.5 + 2^-10)) by
+    // FADD2 / FFMA2 / FADD2.RM on the channel pair
+    const int mn0 = rint_prod(__low2float(mn2), inv), mx0 = rint_prod(__low2float(mx2), inv);
+    const int mn1 = rint_prod(__high2float(mn2), inv), mx1 = rint_prod(__high2float(mx2), inv);
+    const int s0 = max(1, bits == 4 ? (mx0 - mn0 + 14) / 15 : (mx0 - mn0 + 2) / 3);
+    const int s1 = max(1, bits == 4 ? (mx1 - mn1 + 14) / 15 : (mx1 - mn1 + 2) / 3);
+    const f32x2 nz2 = pk2(-(kC1 + (float)mn0), -(kC1 + (float)mn1)),
+                invs2 = pk2(__frcp_rn((float)s0), __frcp_rn((float)s1)),
+                half2c = pk2(0.5f + 0.0009765625f, 0.5f + 0.0009765625f), two23 = pk2(8388608.f, 8388608.f);
+    auto Qf = [&](f32x2 f) -> f32x2 { return add2_rd(fma2(add2(f, nz2), invs2, half2c), two23); };
+    if (hf == 0) {
+      rec[c0] = (uint8_t)s0;
+      rec[c0 + 1] = (uint8_t)s1;
+      rec[HD + c0] = (uint8_t)(int8_t)mn0;
+      rec[HD + c0 + 1] = (uint8_t)(int8_t)mn1;
+    }
+    if (kind == 0) {
+      // k1 [N][d] fp16 codes (my two channels of each token, 4 bytes straight to global) and the stage-2
+      // codes two per 2-byte store into the tile t2s [t][c]
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const f32x2 f = F(i), q = Qf(f);
+        krow[(size_t)i * (HD / 2)] = h2of((uint32_t)f, (uint32_t)(f >> 32));
+        *reinterpret_cast<uint16_t*>(t2s + (32 * hf + i) * HD + c0) =
+            (uint16_t)__byte_perm((uint32_t)q, (uint32_t)(q >> 32), 0x0040);
+      }
+    } else {
+      // per qd: tokens 4 qd + e and 16 + 4 qd + e (e < 4) of my half -- the V record word pair (layout.cuh)
+      // and two 8-byte pieces of v1t per channel
+      uint32_t wl[4], wh[4];
+#pragma unroll
+      for (int qd = 0; qd < 4; ++qd) {
+        f32x2 fa[4], fb[4];
+        uint32_t bl[4], bhh[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          fa[e] = F(4 * qd + e);
+          fb[e] = F(16 + 4 * qd + e);
+          const f32x2 qa = Qf(fa[e]), qb = Qf(fb[e]);
+          if (bits == 4) {  // byte e: token 4 qd + e (lo nibble), + 16 (hi nibble)
+            bl[e] = ((uint32_t)qb << 4) + (uint32_t)qa;
+            bhh[e] = ((uint32_t)(qb >> 32) << 4) + (uint32_t)(qa >> 32);
+          } else {  // bits 2s, s = 2 hf + s': token 32 hf + 16 s' + 4 qd + e
+            bl[e] = ((((uint32_t)qb << 2) + (uint32_t)qa) & 0xFu) << (4 * hf);
+            bhh[e] = ((((uint32_t)(qb >> 32) << 2) + (uint32_t)(qa >> 32)) & 0xFu) << (4 * hf);
+          }
+        }
+        wl[qd] = pack4_lo(bl[0], bl[1], bl[2], bl[3]);
+        wh[qd] = pack4_lo(bhh[0], bhh[1], bhh[2], bhh[3]);
+        // v1t: tokens 32 hf + 4 qd .. +3 (chunk 4 hf + qd / 2, half qd & 1) and + 16 (chunk 4 hf + 2 + qd / 2)
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          const f32x2* fg = g ? fb : fa;
+          const int pos = (4 * hf + 2 * g + (qd >> 1)) ^ (p & 7);
+          uint2* r0 = reinterpret_cast<uint2*>(vst + c0 * (BC / 8) + pos) + (qd & 1);
+          uint2* r1 = reinterpret_cast<uint2*>(vst + (c0 + 1) * (BC / 8) + pos) + (qd & 1);
+          *r0 = make_uint2(h2of((uint32_t)fg[0], (uint32_t)fg[1]), h2of((uint32_t)fg[2], (uint32_t)fg[3]));
+          *r1 = make_uint2(h2of((uint32_t)(fg[0] >> 32), (uint32_t)(fg[1] >> 32)),
+                           h2of((uint32_t)(fg[2] >> 32), (uint32_t)(fg[3] >> 32)));
+        }
+      }
+      if (bits == 4) {
+        *reinterpret_cast<uint4*>(rec + 2 * HD + c0 * (kSub / 2) + 16 * hf) = make_uint4(wl[0], wl[1], wl[2], wl[3]);
+        *reinterpret_cast<uint4*>(rec + 2 * HD + (c0 + 1) * (kSub / 2) + 16 * hf) =
+            make_uint4(wh[0], wh[1], wh[2], wh[3]);
+      } else {  // the two halves' bits meet in t2s (unused by V): [d][4] words of the upper half
+        uint32_t* xw = reinterpret_cast<uint32_t*>(t2s);
+        if (hf == 1) {
+#pragma unroll
+          for (int qd = 0; qd < 4; ++qd) {
+            xw[c0 * 4 + qd] = wl[qd];
+            xw[(c0 + 1) * 4 + qd] = wh[qd];
+          }
+        }
+        __syncthreads();
+        if (hf == 0) {
+#pragma unroll
+          for (int qd = 0; qd < 4; ++qd) {
+            wl[qd] |= xw[c0 * 4 + qd];
+            wh[qd] |= xw[(c0 + 1) * 4 + qd];
+          }
+          *reinterpret_cast<uint4*>(rec + 2 * HD + c0 * (kSub / 4)) = make_uint4(wl[0], wl[1], wl[2], wl[3]);
+          *reinterpret_cast<uint4*>(rec + 2 * HD + (c0 + 1) * (kSub / 4)) = make_uint4(wh[0], wh[1], wh[2], wh[3]);
+        }
+      }
+    }
+  } else if (kind == 0) {  // partial tail block: stage-1 outputs of its tokens only
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
       const f32x2 f = F(i);
       if (32 * hf + i < rows) krow[(size_t)i * (HD / 2)] = h2of((uint32_t)f, (uint32_t)(f >> 32));
     }
-  } else {
-    // v1t [d][B_c] staged in xs (every thread has taken its tokens: the barrier above) as rows of B_c halves,
-    // 16-byte chunks at position t8 ^ (p & 7) (conflict-free); copied out contiguously below
+  } else {  // (rows past N are zero in xs: their codes are 0)
 #pragma unroll
     for (int q4 = 0; q4 < 4; ++q4) {
       uint32_t lo[4], hi[4];
@@ -416,93 +505,8 @@ TA_DEV void quant_block_cp(__half (*xs)[HD], uint8_t* t2s, uint32_t* xch, float*
         hi[m] = h2of((uint32_t)(f0 >> 32), (uint32_t)(f1 >> 32));
       }
       const int pos = (4 * hf + q4) ^ (p & 7);
-      reinterpret_cast<uint4*>(&xs[0][0])[c0 * (BC / 8) + pos] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-      reinterpret_cast<uint4*>(&xs[0][0])[(c0 + 1) * (BC / 8) + pos] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-    }
-  }
-  const int bits = bits_dev[h * 2 + kind];
-  constexpr int REC = rec_bytes(HD, BC);
-  uint8_t* rec = block_rec + ((bh * 2 + kind) * (size_t)max_blocks + j0 + j) * REC;
-  if (rows == BC) {
-    // Stage 2 (R-6) of both channels, as in quant_block: z / top code = the codes of min / max x,
-    // code2 = floor(fl((v - z) fl(1/s) + 0.5 + 2^-10)) by FADD2 / FFMA2 / FADD2.RM on the channel pair
-    const int mn0 = rint_prod(__low2float(mn2), inv), mx0 = rint_prod(__low2float(mx2), inv);
-    const int mn1 = rint_prod(__high2float(mn2), inv), mx1 = rint_prod(__high2float(mx2), inv);
-    const int s0 = max(1, bits == 4 ? (mx0 - mn0 + 14) / 15 : (mx0 - mn0 + 2) / 3);
-    const int s1 = max(1, bits == 4 ? (mx1 - mn1 + 14) / 15 : (mx1 - mn1 + 2) / 3);
-    const f32x2 nz2 = pk2(-(kC1 + (float)mn0), -(kC1 + (float)mn1)),
-                invs2 = pk2(__frcp_rn((float)s0), __frcp_rn((float)s1)),
-                half2c = pk2(0.5f + 0.0009765625f, 0.5f + 0.0009765625f), two23 = pk2(8388608.f, 8388608.f);
-    // (F recomputed with a volatile FFMA2: keeping the output pass's values alive would spill)
-    auto Q = [&](int i) -> f32x2 {
-      const float2 xf = __half22float2(x2[i]);
-      f32x2 f;
-      asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(f) : "l"(pk2(xf.x, xf.y)), "l"(inv2), "l"(c12));
-      return add2_rd(fma2(add2(f, nz2), invs2, half2c), two23);
-    };
-    if (hf == 0) {
-      rec[c0] = (uint8_t)s0;
-      rec[c0 + 1] = (uint8_t)s1;
-      rec[HD + c0] = (uint8_t)(int8_t)mn0;
-      rec[HD + c0 + 1] = (uint8_t)(int8_t)mn1;
-    }
-    if (kind == 0) {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const f32x2 q = Q(i);
-        *reinterpret_cast<uint16_t*>(t2s + (32 * hf + i) * HD + c0) =
-            (uint16_t)__byte_perm((uint32_t)q, (uint32_t)(q >> 32), 0x0040);
-      }
-    } else if (bits == 4) {
-      // word W = 4 hf + qd, byte e: token 32 hf + 4 qd + e (lo nibble), + 16 (hi nibble) (layout.cuh)
-      uint32_t wl[4], wh[4];
-#pragma unroll
-      for (int qd = 0; qd < 4; ++qd) {
-        uint32_t bl[4], bhh[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const f32x2 qa = Q(4 * qd + e), qb = Q(4 * qd + 16 + e);
-          bl[e] = ((uint32_t)qb << 4) + (uint32_t)qa;
-          bhh[e] = ((uint32_t)(qb >> 32) << 4) + (uint32_t)(qa >> 32);
-        }
-        wl[qd] = pack4_lo(bl[0], bl[1], bl[2], bl[3]);
-        wh[qd] = pack4_lo(bhh[0], bhh[1], bhh[2], bhh[3]);
-      }
-      *reinterpret_cast<uint4*>(rec + 2 * HD + c0 * (kSub / 2) + 16 * hf) = make_uint4(wl[0], wl[1], wl[2], wl[3]);
-      *reinterpret_cast<uint4*>(rec + 2 * HD + (c0 + 1) * (kSub / 2) + 16 * hf) = make_uint4(wh[0], wh[1], wh[2], wh[3]);
-    } else {
-      // word qd, byte e, bits 2s: token 32 (s >> 1) + 16 (s & 1) + 4 qd + e -- half hf holds s = 2 hf, 2 hf + 1
-      uint32_t wl[4], wh[4];
-#pragma unroll
-      for (int qd = 0; qd < 4; ++qd) {
-        uint32_t bl[4], bhh[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const f32x2 qa = Q(4 * qd + e), qb = Q(16 + 4 * qd + e);
-          bl[e] = ((((uint32_t)qb << 2) + (uint32_t)qa) & 0xFu) << (4 * hf);
-          bhh[e] = ((((uint32_t)(qb >> 32) << 2) + (uint32_t)(qa >> 32)) & 0xFu) << (4 * hf);
-        }
-        wl[qd] = pack4_lo(bl[0], bl[1], bl[2], bl[3]);
-        wh[qd] = pack4_lo(bhh[0], bhh[1], bhh[2], bhh[3]);
-      }
-      uint32_t* xw = reinterpret_cast<uint32_t*>(t2s);  // [d][4] words of the upper half (unused by V otherwise)
-      if (hf == 1) {
-#pragma unroll
-        for (int qd = 0; qd < 4; ++qd) {
-          xw[c0 * 4 + qd] = wl[qd];
-          xw[(c0 + 1) * 4 + qd] = wh[qd];
-        }
-      }
-      __syncthreads();
-      if (hf == 0) {
-#pragma unroll
-        for (int qd = 0; qd < 4; ++qd) {
-          wl[qd] |= xw[c0 * 4 + qd];
-          wh[qd] |= xw[(c0 + 1) * 4 + qd];
-        }
-        *reinterpret_cast<uint4*>(rec + 2 * HD + c0 * (kSub / 4)) = make_uint4(wl[0], wl[1], wl[2], wl[3]);
-        *reinterpret_cast<uint4*>(rec + 2 * HD + (c0 + 1) * (kSub / 4)) = make_uint4(wh[0], wh[1], wh[2], wh[3]);
-      }
+      vst[c0 * (BC / 8) + pos] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      vst[(c0 + 1) * (BC / 8) + pos] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
     }
   }
   __syncthreads();
