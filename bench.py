@@ -169,6 +169,8 @@ def run_ours(args, rank, world, device):
         S = ta.auto_splits(B, Hkv, N // 64, ta.reference_workers(Hq, Hkv, d))
     ws = torch.empty(max(ta.turbo_decode_workspace_bytes(B, Hq, Hkv, d, S), 16), dtype=torch.uint8, device=device)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=device)  # > 126 MB L2
+    # read after the write: the flush's own dirty lines are written back before the step, not inside it
+    flush_rd = torch.ones(64 << 20, dtype=torch.float32, device=device)  # 256 MB
     st = torch.cuda.current_stream()
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
@@ -205,7 +207,8 @@ def run_ours(args, rank, world, device):
     torch.cuda.synchronize()
     evs = [[ev() for _ in range(4)] for _ in range(args.steps)]
     for i in range(args.steps):
-        flush.zero_()  # L2 flush between timed steps (outside the events)
+        flush.zero_()  # L2 flush between timed steps (outside the events): write 512 MB, then read 256 MB
+        flush_rd.sum()
         step(q, k, v, qd, kd, vd, evs[i])
     torch.cuda.synchronize()
     clocks = clk.stop() if clk else None
@@ -407,7 +410,7 @@ def run_ours(args, rank, world, device):
                   breakdown_ms={"quantize_kv_prefill": round(statistics.mean(t_quant), 4),
                                 "attention_prefill": round(pre_ms, 4),
                                 "append+decode": round(statistics.mean(t_dec), 4)})
-    del hq, hk, hv, ho, hlse, dins, douts, outs, q, k, v, flush, cache
+    del hq, hk, hv, ho, hlse, dins, douts, outs, q, k, v, flush, flush_rd, cache
     torch.cuda.empty_cache()
     if not args.no_decode:
         result["decode"] = bench_decode(args, rank, world, device, pk)
@@ -672,7 +675,7 @@ def workload_config(args):
             "kv_bits": "half of the (kv_head, K/V) slots 2-bit, rest 4-bit",
             "decode_splits": args.splits if args.splits is not None else "auto (binding.auto_splits)",
             "parallelism": f"(batch, kv-head) partition, {args.gpus} rank(s), no collective",
-            "l2": "flushed between timed steps (512 MB write)"}
+            "l2": "flushed between timed steps (512 MB write, then 256 MB read: L2 left clean)"}
 
 
 # --------------------------------------------------------------------------- secondary workloads
