@@ -321,20 +321,23 @@ TA_DEV void quant_block(__half (*xs)[HD], uint8_t* t2s, float* red, int j, int h
   }
 }
 
-// B_c = 64 item body of the TMA kernel with thread = (channel pair p, token half hf): one 4-byte shared load gives
+// Item body of the TMA kernel with thread = (channel pair p, token half hf): one 4-byte shared load gives
 // a token's two channels (a half2), so the per-token work (min / max, stage-1 FFMA2, stage 2) runs on channel
 // pairs, k^1 is stored straight from registers (4 bytes per token and thread) and the K stage-2 codes go to
 // shared memory two at a time.  Half 1 of a warp takes the pairs of the neighbouring warp, so the two
 // half-warps read disjoint banks.  The per-channel min / max of the two halves meet in `xch`; the 2-bit V record
-// words, whose bytes mix both halves, are OR-ed through the (then unused) K stage-2 tile.  Outputs are
+// words, whose bytes mix both halves at B_c = 64, are OR-ed through the (then unused) K stage-2 tile; at B_c = 128
+// a token half is one 64-token V sub-block, so every record word is the thread's own.  The K stage-2 tile is t2s
+// (B_c = 64) or the block buffer itself (B_c = 128: free once every thread has gathered its tokens).  Outputs are
 // bit-identical to quant_block (tests/test_gpu_parity.py::test_quantize_kv_fallback_kernel_matches_tma_kernel).
-template <int HD>
+template <int HD, int BC>
 TA_DEV void quant_block_cp(__half (*xs)[HD], uint8_t* t2s, uint32_t* xch, float* red, int j, int h, int b, int kind,
     const __half* __restrict__ k, const __half* __restrict__ v, int N, int Hkv, int max_blocks, int j0, int Nk,
     const int32_t* __restrict__ bits_dev, uint8_t* __restrict__ block_rec, float* __restrict__ s_parent,
     float* __restrict__ a_univ, __half* __restrict__ k1, __half* __restrict__ v1t, float* __restrict__ k1s,
     float* __restrict__ v1s, int scale_fp16, int t0, int Nin, int8_t* __restrict__ zbuf, int32_t* __restrict__ counters) {
-  constexpr int BC = 64, NW = HD / 32, NP = HD / 2;
+  constexpr int NW = HD / 32, NP = HD / 2, TH = BC / 2;  // TH tokens per thread
+  uint8_t* tile2 = BC == 64 ? t2s : reinterpret_cast<uint8_t*>(&xs[0][0]);  // K stage-2 codes [t][c]
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, hf = lane >> 4;
   const int p = 16 * (hf ? (w ^ 1) : w) + (lane & 15), c0 = 2 * p;
   const int Tc = (Nk + BC - 1) / BC;
@@ -348,13 +351,13 @@ TA_DEV void quant_block_cp(__half (*xs)[HD], uint8_t* t2s, uint32_t* xch, float*
       counters[b * 2 + 1] = 0;
     }
   }
-  // my 32 tokens (32 hf + i) of channels c0, c0 + 1, and their min / max
-  __half2 x2[32];
-  x2[0] = *reinterpret_cast<const __half2*>(&xs[32 * hf][c0]);
+  // my TH tokens (TH hf + i) of channels c0, c0 + 1, and their min / max
+  __half2 x2[TH];
+  x2[0] = *reinterpret_cast<const __half2*>(&xs[TH * hf][c0]);
   __half2 mn2 = x2[0], mx2 = x2[0];
 #pragma unroll
-  for (int i = 1; i < 32; ++i) {
-    x2[i] = *reinterpret_cast<const __half2*>(&xs[32 * hf + i][c0]);
+  for (int i = 1; i < TH; ++i) {
+    x2[i] = *reinterpret_cast<const __half2*>(&xs[TH * hf + i][c0]);
     mn2 = __hmin2(mn2, x2[i]);
     mx2 = __hmax2(mx2, x2[i]);
   }
@@ -398,7 +401,7 @@ TA_DEV void quant_block_cp(__half (*xs)[HD], uint8_t* t2s, uint32_t* xch, float*
   const int bits = bits_dev[h * 2 + kind];
   constexpr int REC = rec_bytes(HD, BC);
   uint8_t* rec = block_rec + ((bh * 2 + kind) * (size_t)max_blocks + j0 + j) * REC;
-  uint32_t* krow = reinterpret_cast<uint32_t*>(k1 + (bh * Nk + (size_t)(j0 + j) * BC + 32 * hf) * HD + c0);
+  uint32_t* krow = reinterpret_cast<uint32_t*>(k1 + (bh * Nk + (size_t)(j0 + j) * BC + TH * hf) * HD + c0);
   uint4* vst = reinterpret_cast<uint4*>(&xs[0][0]);  // v1t staging: rows of B_c halves, chunk t8 at t8 ^ (p & 7)
   if (rows == BC) {
     // Full block: each token's stage-1 value F is computed once and feeds k1 / v1t and stage 2 (R-6):
@@ -422,15 +425,20 @@ TA_DEV void quant_block_cp(__half (*xs)[HD], uint8_t* t2s, uint32_t* xch, float*
       // k1 [N][d] fp16 codes (my two channels of each token, 4 bytes straight to global) and the stage-2
       // codes two per 2-byte store into the tile t2s [t][c]
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
+      for (int i = 0; i < TH; ++i) {
         const f32x2 f = F(i), q = Qf(f);
         krow[(size_t)i * (HD / 2)] = h2of((uint32_t)f, (uint32_t)(f >> 32));
-        *reinterpret_cast<uint16_t*>(t2s + (32 * hf + i) * HD + c0) =
+        *reinterpret_cast<uint16_t*>(tile2 + (TH * hf + i) * HD + c0) =
             (uint16_t)__byte_perm((uint32_t)q, (uint32_t)(q >> 32), 0x0040);
       }
     } else {
-      // per qd: tokens 4 qd + e and 16 + 4 qd + e (e < 4) of my half -- the V record word pair (layout.cuh)
-      // and two 8-byte pieces of v1t per channel
+      // per 32-token group gi of my half (jj = its 32-token half of the 64-token V sub-block u) and qd: tokens
+      // 4 qd + e and 16 + 4 qd + e (e < 4) -- the V record word pair (layout.cuh) and two 8-byte pieces of v1t
+      // per channel
+      uint32_t wl2[4], wh2[4];  // B_c = 128, 2-bit: the first 32-token half's words
+#pragma unroll
+      for (int gi = 0; gi < BC / 64; ++gi) {
+      const int jj = BC == 64 ? hf : gi, u = BC == 64 ? 0 : hf, tb = TH * hf + 32 * gi;  // tb: first token
       uint32_t wl[4], wh[4];
 #pragma unroll
       for (int qd = 0; qd < 4; ++qd) {
@@ -438,24 +446,24 @@ TA_DEV void quant_block_cp(__half (*xs)[HD], uint8_t* t2s, uint32_t* xch, float*
         uint32_t bl[4], bhh[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          fa[e] = F(4 * qd + e);
-          fb[e] = F(16 + 4 * qd + e);
+          fa[e] = F(32 * gi + 4 * qd + e);
+          fb[e] = F(32 * gi + 16 + 4 * qd + e);
           const f32x2 qa = Qf(fa[e]), qb = Qf(fb[e]);
           if (bits == 4) {  // byte e: token 4 qd + e (lo nibble), + 16 (hi nibble)
             bl[e] = ((uint32_t)qb << 4) + (uint32_t)qa;
             bhh[e] = ((uint32_t)(qb >> 32) << 4) + (uint32_t)(qa >> 32);
-          } else {  // bits 2s, s = 2 hf + s': token 32 hf + 16 s' + 4 qd + e
-            bl[e] = ((((uint32_t)qb << 2) + (uint32_t)qa) & 0xFu) << (4 * hf);
-            bhh[e] = ((((uint32_t)(qb >> 32) << 2) + (uint32_t)(qa >> 32)) & 0xFu) << (4 * hf);
+          } else {  // bits 2s, s = 2 jj + s': token 32 jj + 16 s' + 4 qd + e of the sub-block
+            bl[e] = ((((uint32_t)qb << 2) + (uint32_t)qa) & 0xFu) << (4 * jj);
+            bhh[e] = ((((uint32_t)(qb >> 32) << 2) + (uint32_t)(qa >> 32)) & 0xFu) << (4 * jj);
           }
         }
         wl[qd] = pack4_lo(bl[0], bl[1], bl[2], bl[3]);
         wh[qd] = pack4_lo(bhh[0], bhh[1], bhh[2], bhh[3]);
-        // v1t: tokens 32 hf + 4 qd .. +3 (chunk 4 hf + qd / 2, half qd & 1) and + 16 (chunk 4 hf + 2 + qd / 2)
+        // v1t: tokens tb + 4 qd .. +3 (chunk tb / 8 + qd / 2, half qd & 1) and + 16 (chunk tb / 8 + 2 + qd / 2)
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
           const f32x2* fg = g ? fb : fa;
-          const int pos = (4 * hf + 2 * g + (qd >> 1)) ^ (p & 7);
+          const int pos = (tb / 8 + 2 * g + (qd >> 1)) ^ (p & 7);
           uint2* r0 = reinterpret_cast<uint2*>(vst + c0 * (BC / 8) + pos) + (qd & 1);
           uint2* r1 = reinterpret_cast<uint2*>(vst + (c0 + 1) * (BC / 8) + pos) + (qd & 1);
           *r0 = make_uint2(h2of((uint32_t)fg[0], (uint32_t)fg[1]), h2of((uint32_t)fg[2], (uint32_t)fg[3]));
@@ -464,9 +472,23 @@ TA_DEV void quant_block_cp(__half (*xs)[HD], uint8_t* t2s, uint32_t* xch, float*
         }
       }
       if (bits == 4) {
-        *reinterpret_cast<uint4*>(rec + 2 * HD + c0 * (kSub / 2) + 16 * hf) = make_uint4(wl[0], wl[1], wl[2], wl[3]);
-        *reinterpret_cast<uint4*>(rec + 2 * HD + (c0 + 1) * (kSub / 2) + 16 * hf) =
-            make_uint4(wh[0], wh[1], wh[2], wh[3]);
+        uint8_t* rv = rec + 2 * HD + u * (HD * kSub / 2) + 16 * jj;
+        *reinterpret_cast<uint4*>(rv + c0 * (kSub / 2)) = make_uint4(wl[0], wl[1], wl[2], wl[3]);
+        *reinterpret_cast<uint4*>(rv + (c0 + 1) * (kSub / 2)) = make_uint4(wh[0], wh[1], wh[2], wh[3]);
+      } else if (BC == 128) {  // both 32-token halves of the sub-block are mine: OR them in registers
+        if (gi == 0) {
+#pragma unroll
+          for (int qd = 0; qd < 4; ++qd) {
+            wl2[qd] = wl[qd];
+            wh2[qd] = wh[qd];
+          }
+        } else {
+          uint8_t* rv = rec + 2 * HD + u * (HD * kSub / 4);
+          *reinterpret_cast<uint4*>(rv + c0 * (kSub / 4)) =
+              make_uint4(wl[0] | wl2[0], wl[1] | wl2[1], wl[2] | wl2[2], wl[3] | wl2[3]);
+          *reinterpret_cast<uint4*>(rv + (c0 + 1) * (kSub / 4)) =
+              make_uint4(wh[0] | wh2[0], wh[1] | wh2[1], wh[2] | wh2[2], wh[3] | wh2[3]);
+        }
       } else {  // the two halves' bits meet in t2s (unused by V): [d][4] words of the upper half
         uint32_t* xw = reinterpret_cast<uint32_t*>(t2s);
         if (hf == 1) {
@@ -487,16 +509,17 @@ TA_DEV void quant_block_cp(__half (*xs)[HD], uint8_t* t2s, uint32_t* xch, float*
           *reinterpret_cast<uint4*>(rec + 2 * HD + (c0 + 1) * (kSub / 4)) = make_uint4(wh[0], wh[1], wh[2], wh[3]);
         }
       }
+      }  // gi
     }
   } else if (kind == 0) {  // partial tail block: stage-1 outputs of its tokens only
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
+    for (int i = 0; i < TH; ++i) {
       const f32x2 f = F(i);
-      if (32 * hf + i < rows) krow[(size_t)i * (HD / 2)] = h2of((uint32_t)f, (uint32_t)(f >> 32));
+      if (TH * hf + i < rows) krow[(size_t)i * (HD / 2)] = h2of((uint32_t)f, (uint32_t)(f >> 32));
     }
   } else {  // (rows past N are zero in xs: their codes are 0)
 #pragma unroll
-    for (int q4 = 0; q4 < 4; ++q4) {
+    for (int q4 = 0; q4 < TH / 8; ++q4) {
       uint32_t lo[4], hi[4];
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
@@ -504,7 +527,7 @@ TA_DEV void quant_block_cp(__half (*xs)[HD], uint8_t* t2s, uint32_t* xch, float*
         lo[m] = h2of((uint32_t)f0, (uint32_t)f1);
         hi[m] = h2of((uint32_t)(f0 >> 32), (uint32_t)(f1 >> 32));
       }
-      const int pos = (4 * hf + q4) ^ (p & 7);
+      const int pos = (TH / 8 * hf + q4) ^ (p & 7);
       vst[c0 * (BC / 8) + pos] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
       vst[(c0 + 1) * (BC / 8) + pos] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
     }
@@ -527,8 +550,8 @@ TA_DEV void quant_block_cp(__half (*xs)[HD], uint8_t* t2s, uint32_t* xch, float*
   if (kbits == 4) {
     for (int i = tid; i < BC * HD / 32; i += HD) {  // 32 channels (16 B of codes) per item
       const int t = i / (HD / 32), c32 = i % (HD / 32);
-      const uint4 lo = *reinterpret_cast<const uint4*>(t2s + t * HD + c32 * 32);
-      const uint4 hi = *reinterpret_cast<const uint4*>(t2s + t * HD + c32 * 32 + 16);
+      const uint4 lo = *reinterpret_cast<const uint4*>(tile2 + t * HD + c32 * 32);
+      const uint4 hi = *reinterpret_cast<const uint4*>(tile2 + t * HD + c32 * 32 + 16);
       *reinterpret_cast<uint4*>(krec + t * (HD / 2) + c32 * 16) =
           make_uint4(pack_nib8(make_uint2(lo.x, lo.y)), pack_nib8(make_uint2(lo.z, lo.w)),
                      pack_nib8(make_uint2(hi.x, hi.y)), pack_nib8(make_uint2(hi.z, hi.w)));
@@ -539,7 +562,7 @@ TA_DEV void quant_block_cp(__half (*xs)[HD], uint8_t* t2s, uint32_t* xch, float*
       uint32_t wv[4];
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
-        const uint4 u = *reinterpret_cast<const uint4*>(t2s + t * HD + c64 * 64 + g * 16);
+        const uint4 u = *reinterpret_cast<const uint4*>(tile2 + t * HD + c64 * 64 + g * 16);
         wv[g] = pack_crumb8(make_uint2(u.x, u.y)) | (pack_crumb8(make_uint2(u.z, u.w)) << 16);
       }
       *reinterpret_cast<uint4*>(krec + t * (HD / 4) + c64 * 16) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
@@ -589,7 +612,7 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 6 : 3) * 128 / HD) quant_prefi
 // block of the next item already on its way -- one TMA tile load ([B_c tokens][HD], the rows of one head) into
 // the second buffer of a double buffer -- while the current item is quantised.
 template <int HD, int BC>
-constexpr size_t quant_tma_smem() { return 2 * BC * HD * 2 + (BC == 64 ? BC * HD + HD * 8 : 0) + 64; }
+constexpr size_t quant_tma_smem() { return 2 * BC * HD * 2 + (BC == 64 ? BC * HD : 0) + HD * 8 + 64; }
 template <int HD, int BC>
 __global__ void __launch_bounds__(HD, (BC == 64 ? 5 : 3) * 128 / HD) quant_prefill_tma_kernel(
     const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv, int n_items, int Tcn,
@@ -600,8 +623,8 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 5 : 3) * 128 / HD) quant_prefi
   extern __shared__ __align__(128) uint8_t qsm[];
   __half(*xs2)[BC][HD] = reinterpret_cast<__half(*)[BC][HD]>(qsm);  // [2][B_c][HD]
   uint8_t* t2s = qsm + 2 * BC * HD * 2;                                // B_c = 64: K stage-2 codes
-  uint32_t* xch = reinterpret_cast<uint32_t*>(t2s + (BC == 64 ? BC * HD : 0));  // B_c = 64: [2][HD / 2][2] min / max
-  float* red = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(xch) + (BC == 64 ? HD * 8 : 0));
+  uint32_t* xch = reinterpret_cast<uint32_t*>(t2s + (BC == 64 ? BC * HD : 0));  // [2][HD / 2][2] min / max
+  float* red = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(xch) + HD * 8);
   uint64_t* bar = reinterpret_cast<uint64_t*>(red + 8);
   const int tid = threadIdx.x;
   auto item = [&](int it, int& j, int& h, int& b, int& kind) {
@@ -639,12 +662,8 @@ __global__ void __launch_bounds__(HD, (BC == 64 ? 5 : 3) * 128 / HD) quant_prefi
         reinterpret_cast<uint4*>(&xs2[st][rows][0])[e] = make_uint4(0, 0, 0, 0);
       __syncthreads();
     }
-    if constexpr (BC == 64)
-      quant_block_cp<HD>(xs2[st], t2s, xch, red, j, h, b, kind, k, v, N, Hkv, max_blocks, j0, Nk, bits_dev, block_rec,
-                         s_parent, a_univ, k1, v1t, k1s, v1s, scale_fp16, t0, Nin, zbuf, counters);
-    else
-      quant_block<HD, BC>(xs2[st], t2s, red, j, h, b, kind, k, v, N, Hkv, max_blocks, j0, Nk, bits_dev, block_rec,
-                          s_parent, a_univ, k1, v1t, k1s, v1s, scale_fp16, t0, Nin, zbuf, counters);
+    quant_block_cp<HD, BC>(xs2[st], t2s, xch, red, j, h, b, kind, k, v, N, Hkv, max_blocks, j0, Nk, bits_dev, block_rec,
+                           s_parent, a_univ, k1, v1t, k1s, v1s, scale_fp16, t0, Nin, zbuf, counters);
     __syncthreads();  // xs2[st], t2s, xch and red are free again
     if (tid == 0 && it + 2 * (int)gridDim.x < n_items) {
       fence_proxy_async();  // the generic-proxy staging writes precede the async-proxy refill
