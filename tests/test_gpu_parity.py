@@ -614,28 +614,38 @@ def test_prefill_whole_blocks_resets_a_used_cache(ta, d):
 
 
 @pytest.mark.parametrize("bc", [64, 128])
-def test_quantize_kv_fallback_kernel_matches_tma_kernel(ta, bc):
-    """turbo_quantize_kv runs the persistent TMA kernel; the per-block kernel (16-byte LDG staging) is the
-    fallback for inputs a tensor map cannot describe (TURBO_QUANT_NOTMA=1 forces it).  Both must write the
-    same stage-1 operands, records, scales, universal scales, buffer and counters, bit for bit."""
+@pytest.mark.parametrize("d", [64, 128])
+def test_quantize_kv_fallback_kernel_matches_tma_kernel(ta, bc, d):
+    """turbo_quantize_kv runs the persistent TMA kernel (channel-pair body); the per-block kernel (16-byte LDG
+    staging, thread = channel) is the fallback for inputs a tensor map cannot describe (TURBO_QUANT_NOTMA=1
+    forces it).  Both must write the same stage-1 operands, records, scales, universal scales, buffer and
+    counters, bit for bit -- for a PREFILL with a ragged tail and for a chunk that starts inside a block and
+    continues over whole blocks (mode 2 after appends, R-31)."""
     import os
 
-    B, N, Hkv, d = 2, 64 * 5 + 17, 4, 128
-    _, k, v = synth.qkv(77, B, N, Hkv, Hkv, d)
+    B, N, Hkv = 2, 64 * 5 + 17, 4
+    _, k, v = synth.qkv(77 + d, B, N, Hkv, Hkv, d)
+    _, kc, vc = synth.qkv(78 + d, B, 3 * bc + 9, Hkv, Hkv, d)
     bits = synth.head_bits_alternating(Hkv)
     p = ta.params(head_dim=d, block_kv=bc)
-    kt, vt = torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda()
+    kt, vt, kct, vct = (torch.from_numpy(x).cuda() for x in (k, v, kc, vc))
     outs = []
     for force in (False, True):
-        cache = ta.KVCache(B, Hkv, d, max_blocks=N // bc + 2, bits=bits, block_kv=bc)
+        cache = ta.KVCache(B, Hkv, d, max_blocks=(N + kc.shape[1]) // bc + 4, bits=bits, block_kv=bc)
         if force:
             os.environ["TURBO_QUANT_NOTMA"] = "1"
         try:
             ops = ta.turbo_quantize_kv(p, cache, kt, vt)
             torch.cuda.synchronize()
+            got = [x.cpu() for x in ops]
+            Nk = N + kc.shape[1]
+            buf = ta.turbo_dequantize_cache(p, cache, Nk)
+            ops2 = ta.turbo_quantize_kv(p, cache, kct, vct, mode=2, out=buf)
+            torch.cuda.synchronize()
+            got += [x.cpu() for x in ops2]
         finally:
             os.environ.pop("TURBO_QUANT_NOTMA", None)
-        outs.append([x.cpu() for x in ops] + [t.cpu() for t in (cache.block_rec, cache.s_parent, cache.buf,
-                                                                 cache.a_univ, cache.counters)])
+        outs.append(got + [t.cpu() for t in (cache.block_rec, cache.s_parent, cache.buf, cache.a_univ,
+                                             cache.counters)])
     for a, b in zip(*outs):
         assert torch.equal(a, b)
