@@ -9,8 +9,15 @@
  * Conventions for every entry point
  *   * All tensor pointers are caller-owned DEVICE memory (e.g. torch tensors)
  *     unless the argument says HOST.  The library never allocates or frees,
- *     keeps no mutable global state, and never synchronises: work is enqueued
- *     on `stream` (0 = legacy default stream) and completes asynchronously.
+ *     keeps no mutable global state (beyond one-time caches of device
+ *     attributes: SM count, kernel occupancy, the tensor-map encoder entry
+ *     point -- one device per process), and never synchronises: work is
+ *     enqueued on `stream` (0 = legacy default stream) and completes
+ *     asynchronously.
+ *   * Developer knobs (environment; results are unchanged): TURBO_QUANT_NOTMA=1
+ *     makes turbo_quantize_kv use its per-block fallback kernel instead of the
+ *     persistent TMA kernel; TURBO_PREFILL_QPF=n sets the prefill's L2 prefetch
+ *     of the next wave's Q rows to n quarter-waves ahead (0 = off).
  *   * Arguments are validated on the host before any launch.  Errors:
  *       TURBO_ERR_INVALID_ARG  null pointer, non-positive size, bad enum value;
  *       TURBO_ERR_UNSUPPORTED  head_dim not in {64,128}, block_kv not in {64,128},

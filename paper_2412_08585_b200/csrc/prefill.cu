@@ -668,12 +668,12 @@ cudaError_t launch_prefill(const turbo_params_t* p, int B, int N, int Nk, int Hq
   const bool pair = (G % 2) == 0;  // slots = two heads of a GQA group, else two adjacent query tiles
   a.n_qtiles = (N + kTileM - 1) / kTileM;
   {
-    static int sms = 0;
-    if (sms == 0) {
-      int dev = 0;
+    static const int sms = [] {  // (thread-safe one-time init; one device per process)
+      int dev = 0, n = 0;
       cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+      cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+      return n;
+    }();
     a.q_prefetch = sms;  // one CTA per SM: the CTA a wave later
     if (const char* e = getenv("TURBO_PREFILL_QPF")) a.q_prefetch = atoi(e) * sms / 4;  // A/B: quarter waves
   }

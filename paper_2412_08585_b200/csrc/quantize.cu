@@ -918,14 +918,13 @@ typedef CUresult (*EncodeTiledQFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 // FP16 K or V input [tokens][Hkv][HD] as a 3-D map (HD, Hkv, tokens); box = the B_c rows of one head.
 static bool make_rows_map(CUtensorMap* m, const __half* base, int HD, int H, uint64_t tokens, int BC) {
-  static EncodeTiledQFn enc = nullptr;
-  if (!enc) {
+  static const EncodeTiledQFn enc = [] {  // (thread-safe one-time init)
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
-      return false;
-    enc = reinterpret_cast<EncodeTiledQFn>(fn);
-  }
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess) fn = nullptr;
+    return reinterpret_cast<EncodeTiledQFn>(fn);
+  }();
+  if (!enc) return false;
   if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
   cuuint64_t dims[3] = {(cuuint64_t)HD, (cuuint64_t)H, tokens};
   cuuint64_t strides[2] = {(cuuint64_t)HD * 2, (cuuint64_t)H * HD * 2};
@@ -949,16 +948,17 @@ static void quant_prefill_hd(const turbo_kv_cache_t* c, const __half* k, const _
   if (!getenv("TURBO_QUANT_NOTMA") && make_rows_map(&tmk, k, HD, H, (uint64_t)B * Nin, BC) &&
       make_rows_map(&tmv, v, HD, H, (uint64_t)B * Nin, BC)) {
     constexpr size_t smem = quant_tma_smem<HD, BC>();
-    static int per_sm = -1, sms = 0;
-    if (per_sm < 0) {
-      int dev = 0;
+    // resident CTAs of this instantiation (thread-safe one-time init; one device per process)
+    static const int resident = [] {
+      int dev = 0, sms = 0, per_sm = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       cudaFuncSetAttribute(quant_prefill_tma_kernel<HD, BC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, quant_prefill_tma_kernel<HD, BC>, HD, smem);
-    }
+      return sms * std::max(1, per_sm);
+    }();
     const int n_items = Tc * H * 2 * B;
-    const int ctas = std::max(1, std::min(n_items, sms * std::max(1, per_sm)));
+    const int ctas = std::max(1, std::min(n_items, resident));
     quant_prefill_tma_kernel<HD, BC><<<ctas, HD, smem, st>>>(tmk, tmv, n_items, Tc, k, v, N, H, c->max_blocks, j0,
                                                              Nk, c->bits_dev, c->block_rec, c->s_parent, c->a_univ,
                                                              k1, v1t, k1s, v1s, scale_fp16, t0, Nin, zbuf,
