@@ -193,7 +193,9 @@ def run_ours(args, rank, world, device):
             evs[3].record(st)
         return o, lse, od, lsed
 
-    launches_per_step = 2 + 1 + 2 + (2 if S > 1 else 1)
+    # our kernels per step: quantize_kv PREFILL (the TMA kernel; + quant_tail_kernel when N is not a whole number of
+    # B_c blocks -- its a_univ reset is a cudaMemsetAsync), the prefill, APPEND (append + counters), decode (+ combine)
+    launches_per_step = (1 if N % 64 == 0 else 2) + 1 + 2 + (2 if S > 1 else 1)
     clk = Clocks(device) if rank == 0 else None  # sampler runs through the soak and the timed steps
     for _ in range(args.warmup):
         step(q, k, v, qd, kd, vd)
